@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py -- GraVAC per-iteration gradient-compression step on B200.
+
+Metric (BASELINE.json): gradient GB/s compressed + allgathered per step.
+One step = the fused GraVAC iteration of controller.run_iteration on a
+ResNet101-size fp32 gradient (BASELINE configs[1]): g_ef = g + r, ||g_ef||^2,
+Top-k selection with the gains of the whole CF search {10, 100, 1000} from one
+sweep, the controller's decision, the emit of the chosen (index, value) list
+with the residual update, the sparse allgather (NCCL, N > 1) and the fp64
+rank-ordered decompress-average.  value = N * 4 * M bytes / step time (max over
+ranks, CUDA events, L2 flushed between steps).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload resnet101|vgg16|resnet18]
+torchrun launches one rank per GPU (NCCL over NVLink).  --impl reference times
+the reference algorithm's CPU restatement (oracle/, the C port) on the host
+cores of rank 0 for the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gradient GB/s compressed+allgathered per step, 1/2/4/8 B200; % of HBM roofline"
+WORKLOADS = {
+    # name: (M, theta_min, theta_s (candidate = theta_s * theta_min), extra CFs, description)
+    "resnet101": (44_500_000, 10.0, 10.0, (1000.0,),
+                  "ResNet101-size 44.5M fp32 gradient, GraVAC CF search {10,100,1000} with Top-k + EF, "
+                  "sparse allgather + fp64 decompress-average (BASELINE configs[1])"),
+    "vgg16": (138_000_000, 10.0, 10.0, (1000.0,),
+              "VGG16-size 138M fp32 gradient, Top-k + EF + CF search {10,100,1000} (north-star size)"),
+    "resnet18": (11_700_000, 100.0, 1.0, (), "ResNet-18-size 11.7M fp32 gradient, Top-k CF100 + EF + gain"),
+}
+EPSILON = 0.4  # iid N(0,1) gradients give gain(CF10) ~= 0.42 -> the compressed CF10 branch is taken
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- CPU legs
+def oracle_step(O, g, r, M, theta_min, theta_s, extra, nworkers=1):
+    """One reference-algorithm step on the host: per worker EF, norm, Top-k at
+    theta_min, the ladder via compress_further (compressors.py:226-246), the
+    residual update, then aggregate() over the parts (simworkers.py:242-245)."""
+    parts = []
+    new_r = []
+    for w in range(nworkers):
+        ef = O.ef_add(g[w], r[w])
+        norm = O.sq_norm(ef)
+        idx, vals, _ = O.compress("topk", ef, theta_min)
+        gains = [O.sq_norm(vals) / norm]
+        for step in (theta_s, *[c / theta_min for c in extra]):
+            _, v2, _ = O.compress_further("topk", idx, vals, M, step)
+            gains.append(O.sq_norm(v2) / norm)
+        new_r.append(O.update_residual(ef, idx, vals))
+        parts.append((idx, vals))
+    O.aggregate(parts, M)
+    return new_r
+
+
+def run_reference(args, M, theta_min, theta_s, extra, desc):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.lib()
+    rng = np.random.default_rng(1234)
+    g = [rng.standard_normal(M, dtype=np.float32) for _ in range(world)]
+    r = [np.zeros(M, dtype=np.float32) for _ in range(world)]
+    warm, steps = min(args.warmup, 1), min(args.steps, 3)
+    for _ in range(warm):
+        r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world)
+    dt = (time.perf_counter() - t0) / steps
+    value = world * 4 * M / dt / 1e9
+    sample = (f"{steps} timed full steps ({warm} warm-up) of the {M}-element workload, {world} simulated "
+              f"worker(s) run sequentially as the reference does (controller.py:232-250)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) fp32 gradients",
+            "config": {"workload": desc, "M": M, "parallelism": f"dp{world} (simulated, host)"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- GPU leg
+def run_ours(args, M, theta_min, theta_s, extra, desc):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_12201_b200 as G
+    from paper_2305_12201_b200 import _native as nat
+    from paper_2305_12201_b200.compressors import aggregate_packed
+    from paper_2305_12201_b200.exchange import allgather_aggregate, allgather_dense_mean
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    nat.load()
+
+    gen = torch.Generator(device=dev)
+    pool = []
+    for p in range(3):
+        gen.manual_seed(1000 * rank + p)
+        pool.append(torch.randn(M, generator=gen, device=dev, dtype=torch.float32))
+    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=max(1000.0, theta_min), epsilon=EPSILON,
+                             window=1 << 30, compressor=G.CompressorKind("topk"))
+    state = G.ControllerState.fresh(cfg, world)
+    state.theta_s = theta_s
+    store = G.ResidualStore(M, device=dev)
+    cost = G.CostModelParams(workers=world)
+    rng = G.SeededRng(7)
+    avg = torch.empty(M, dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    chosen = {}
+
+    def step(g):
+        res = G.run_iteration(state, G.GradientVector._wrap(g), store, cost, rng, extra_cfs=extra, group=pg)
+        chosen[res.decision.cf] = chosen.get(res.decision.cf, 0) + 1
+        part = res.sent[0]
+        if res.decision.choice == "dense":
+            out = allgather_dense_mean(part, pg) if pg is not None else part
+        elif pg is not None:
+            out = allgather_aggregate(part, pg, out=avg)
+        else:
+            out = aggregate_packed(part.indices, part.vals, [part.kept], M, out=avg)
+        return res, out
+
+    for w in range(args.warmup):
+        step(pool[w % 3])
+    torch.cuda.synchronize()
+    if pg is not None:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    chosen.clear()
+    nat.prof_read()
+    nat.prof_enable(True)
+    launches0 = nat.launch_count()
+    with ClockSampler(local) as clocks:
+        for s in range(args.steps):
+            flush.fill_(float(s))  # evict g / r / candidates from L2 (outside the timed events)
+            ev[s][0].record()
+            res, _ = step(pool[s % 3])
+            ev[s][1].record()
+        torch.cuda.synchronize()
+    launches = nat.launch_count() - launches0
+    prof = nat.prof_read()
+    nat.prof_enable(False)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = world * 4 * M / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the public API: pinned host gradient -> H2D -> step -> D2H of the decision
+    g_host = pool[0].cpu().pin_memory()
+    g_dev = torch.empty_like(pool[0])
+    n_e2e = max(1, min(args.steps, 5))
+    e2e_ms = 0.0
+    for s in range(n_e2e):
+        flush.fill_(float(s))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g_dev.copy_(g_host, non_blocking=True)
+        step(g_dev)
+        b.record()
+        torch.cuda.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_step = float(t.item()) / n_e2e
+    e2e_value = world * 4 * M / (e2e_step * 1e-3) / 1e9
+
+    if rank != 0:
+        if pg is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peaks()
+    col_ms, col_n = prof["collect"]
+    col_launch = col_ms / max(col_n, 1)
+    col_bytes = 12 * M  # read g, read r, write g_ef: the algorithmic bytes of the fused EF pass
+    achieved = col_bytes / (col_launch * 1e-3) / 1e9
+    k1 = G.keep_count(M, theta_min)
+    sel_ms = prof["select"][0] / max(prof["select"][1], 1)
+    emit_ms = prof["emit"][0] / max(prof["emit"][1], 1)
+    agg_ms = prof["aggregate"][0] / max(prof["aggregate"][1], 1)
+    comp_bytes = 12 * M + 8 * k1
+    comp_achieved = comp_bytes / ((sel_ms + emit_ms) * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: N(0,1) fp32 gradients (torch.randn, 3 per rank, cycled), residual carried across steps",
+        "config": {"workload": desc, "M": M, "cf_ladder": [theta_min, theta_min * theta_s, *extra],
+                   "epsilon": EPSILON, "chosen_cf": {str(k): v for k, v in chosen.items()},
+                   "l2": "flushed (256 MiB write) before every timed step, outside the timed events",
+                   "parallelism": f"dp{world}"},
+        "roofline": {"bound": "hbm", "kernel": "k_collect (fused EF add + fp64 norm + candidate compaction)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "algorithmic_bytes_per_launch": col_bytes,
+                     "launch_ms": col_launch},
+        "compress_stage": {"what": "gvc_select (all kernels) + gvc_emit, algorithmic 12M + 8k bytes",
+                           "ms": sel_ms + emit_ms, "achieved": comp_achieved, "frac": comp_achieved / peak},
+        "breakdown_ms": {"collect": col_launch, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * M,
+                "d2h_bytes_per_step": nat.RESULT_BYTES, "ms_per_step": e2e_step},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.lib()
+        gh = pool[0].cpu().numpy()
+        rh = np.zeros(M, dtype=np.float32)
+        oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra)  # warm
+        t0 = time.perf_counter()
+        n_cpu = 2
+        for _ in range(n_cpu):
+            rh = oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra)[0]
+        dt = (time.perf_counter() - t0) / n_cpu
+        line["cpu_baseline"] = {"value": 4 * M / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+                                "sample": f"{n_cpu} full steps of the same workload (C oracle, single thread)",
+                                "ms_per_step": dt * 1e3}
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="resnet101")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    M, theta_min, theta_s, extra, desc = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, M, theta_min, theta_s, extra, desc)
+    else:
+        run_ours(args, M, theta_min, theta_s, extra, desc)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * gravac_b200.h -- C-ABI of the B200-native GraVAC gradient-compression step.
+ *
+ * The reference (arxiv 2305.12201, /root/reference/pkg/src/gravac) has no
+ * FFI: its boundary is the Python API re-exported by gravac/__init__.py:3-17.
+ * This header is the native layer UNDER those Python names; the package
+ * paper_2305_12201_b200 binds it with ctypes and keeps the reference's
+ * function names, argument meaning and ValueError behaviour.  Each entry point
+ * cites the reference function(s) it replaces.
+ *
+ * Conventions
+ *   - every pointer named *_dev is a device pointer (cudaMalloc / torch CUDA
+ *     storage); everything else is host memory;
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered,
+ *     allocation-free (the caller passes a workspace sized by
+ *     gvc_select_workspace_bytes) and deterministic: identical inputs give
+ *     bit-identical outputs, including fp64 reductions (fixed-order trees);
+ *   - every call returns an int status (GVC_OK or a negative gvc_status);
+ *     gvc_last_error() returns the message of the last failure on this thread.
+ *   - no call synchronises the stream.
+ */
+#ifndef GRAVAC_B200_H
+#define GRAVAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GVC_API __attribute__((visibility("default")))
+#else
+#define GVC_API
+#endif
+
+#define GVC_ABI_VERSION 1
+#define GVC_MAX_LADDER 16
+
+typedef enum {
+    GVC_OK = 0,
+    GVC_ERR_ARG = -1,       /* invalid argument (ValueError in the reference)          */
+    GVC_ERR_NAN = -2,       /* NaN in the gradient: selection order undefined           */
+    GVC_ERR_WORKSPACE = -3, /* workspace too small                                      */
+    GVC_ERR_CUDA = -4,      /* CUDA launch / runtime failure                            */
+    GVC_ERR_STATE = -5      /* call order violated (emit before select, ...)            */
+} gvc_status;
+
+/* Compressor kinds, compressors.py:21-25 */
+typedef enum { GVC_TOPK = 0, GVC_DGC = 1, GVC_REDSYNC = 2, GVC_RANDOMK = 3 } gvc_kind;
+
+/* Device-resident result of one gvc_select (read back by the host controller). */
+typedef struct {
+    double ef_norm_sq;                      /* ||values||^2 in fp64 (gradcore.py:61-70)        */
+    double kept_sq[GVC_MAX_LADDER];         /* ||C_j(values)||^2 of the values to SEND, fp64   */
+    double kept_abs[GVC_MAX_LADDER];        /* sum |v| over the kept support, fp64             */
+    uint32_t threshold_key[GVC_MAX_LADDER]; /* k_j-th largest selection key                    */
+    uint32_t pad0[GVC_MAX_LADDER];
+    uint64_t tie_quota[GVC_MAX_LADDER];     /* how many keys == threshold are kept             */
+    float redsync_mean[GVC_MAX_LADDER];     /* fl32(mean_f64 |v|) (compressors.py:188)         */
+    uint64_t candidates;                    /* size of the candidate superset                  */
+    int32_t status;                         /* GVC_OK or GVC_ERR_NAN                           */
+    int32_t fallback_used;                  /* 1 when the threshold estimate missed (exact re-scan ran) */
+    uint64_t kept_count[GVC_MAX_LADDER];    /* == ks[j] (sanity)                               */
+    uint64_t kept_nonzero[GVC_MAX_LADDER];  /* kept entries with |v| > 0                       */
+} gvc_select_result;
+
+/* Arguments of one selection over n values.  Two input modes:
+ *   EF mode   (g_dev != NULL, resid_dev != NULL): values = fl32(g + resid) is
+ *             computed on the fly (feedback.py:32-36) and written over
+ *             resid_dev, which then holds g_ef;
+ *   plain mode (values_dev != NULL): the values are read as given.            */
+typedef struct {
+    int32_t kind;                 /* gvc_kind                                               */
+    int32_t n_ks;                 /* ladder length, 1..GVC_MAX_LADDER                       */
+    uint64_t n;                   /* number of values (>= 1)                                */
+    const float *values_dev;      /* plain mode input                                       */
+    const float *g_dev;           /* EF mode raw gradient                                   */
+    float *resid_dev;             /* EF mode residual in, g_ef out                          */
+    uint64_t ks[GVC_MAX_LADDER];  /* keep counts, non-increasing, each in [1, n)            */
+    uint64_t seed;                /* SeededRng.seed   (gradcore.py:139-142)                 */
+    uint64_t rng_stream;          /* SeededRng.stream (after split)                         */
+    uint64_t pos_base;            /* hash counter offset (layerwise segments)               */
+    double dgc_sample_fraction;   /* CompressorKind.dgc_sample_fraction (compressors.py:36) */
+    int32_t force_exact;          /* 1: skip the threshold estimate (every value is a candidate) */
+    int32_t reserved;
+} gvc_select_args;
+
+GVC_API const char *gvc_last_error(void);
+GVC_API int gvc_abi_version(void);
+
+/* Workspace bytes for selections over up to n values of the given kind. */
+GVC_API size_t gvc_select_workspace_bytes(int kind, uint64_t n);
+
+/* Thresholds, tie quotas and kept energies for every ladder entry in one pass
+ * over HBM.  Replaces: feedback.apply_feedback (feedback.py:32-36),
+ * gradcore.squared_l2_norm (gradcore.py:61-70), compressors._select /
+ * _exact_topk / _redsync_pick / _dgc_pick / RandomK choice
+ * (compressors.py:86-190), compressors.compress_further for nested Top-k
+ * (compressors.py:226-246, every ladder entry at once) and
+ * metrics.compression_gain_raw numerators (metrics.py:18-32).
+ * Writes *result_dev (device memory). */
+GVC_API int gvc_select(const gvc_select_args *args, void *ws_dev, size_t ws_bytes,
+               gvc_select_result *result_dev, void *stream);
+
+/* Materialise ladder entry j of the last gvc_select on this workspace as an
+ * index-ascending (u32 index, f32 value) list of exactly ks[j] entries.
+ *   idx_map_dev: optional; output index = idx_map_dev[position] (second-level
+ *                compression maps local positions back, compressors.py:242-244);
+ *   resid_dev:   optional; resid[index] = fl32(value - sent_value) at every sent
+ *                position, i.e. update_residual (feedback.py:39-51) given that
+ *                resid_dev holds g_ef;
+ *   sent_stats_dev: optional double[2] = {sum sent^2, sum |sent|} (fp64, fixed order).
+ * Replaces compressors._select's sort+gather (compressors.py:185-190). */
+GVC_API int gvc_emit(void *ws_dev, size_t ws_bytes, int j, const uint32_t *idx_map_dev,
+             uint32_t *out_idx_dev, float *out_val_dev, float *resid_dev,
+             double *sent_stats_dev, void *stream);
+
+/* out = fl32(g + r) (feedback.py:32-36, non-mutating form). */
+GVC_API int gvc_ef_add(const float *g_dev, const float *r_dev, float *out_dev, uint64_t n, void *stream);
+
+/* *out_dev = sum x^2 in fp64, fixed-order (gradcore.py:61-70).
+ * Workspace: gvc_sq_norm_workspace_bytes(n). */
+GVC_API size_t gvc_sq_norm_workspace_bytes(uint64_t n);
+GVC_API int gvc_sq_norm(const float *x_dev, uint64_t n, double *out_dev, void *ws_dev, size_t ws_bytes,
+                void *stream);
+
+/* resid[idx[i]] = fl32(ef[idx[i]] - vals[i]) after resid = ef (feedback.py:39-51).
+ * ef_dev may equal resid_dev (in-place). */
+GVC_API int gvc_update_residual(const float *ef_dev, const uint32_t *idx_dev, const float *vals_dev,
+                        uint64_t k, uint64_t n, float *resid_dev, void *stream);
+
+/* Dense vector from one sparse part: zeros + scatter, -0.0 preserved
+ * (compressors.py:249-253).  Workspace: gvc_aggregate_workspace_bytes(1, n). */
+GVC_API int gvc_decompress(const uint32_t *idx_dev, const float *vals_dev, uint64_t k, uint64_t n,
+                   float *out_dev, void *ws_dev, size_t ws_bytes, void *stream);
+
+/* Mean of nparts index-ascending sparse parts, fp64 accumulation in part
+ * order, /nparts, -> fp32 (compressors.py:256-271).  Part p is
+ * (idx_dev + offs[p], vals_dev + offs[p]) with counts[p] entries; offs/counts are
+ * HOST arrays.  Shared-memory tiles of the dense output, one coalesced
+ * 128-bit store per 4 outputs.  This is the decompress-average half of the
+ * sparse allgather. */
+GVC_API int gvc_aggregate(const uint32_t *idx_dev, const float *vals_dev, const uint64_t *offs,
+                  const uint64_t *counts, int nparts, uint64_t n, float *out_dev,
+                  void *ws_dev, size_t ws_bytes, void *stream);
+GVC_API size_t gvc_aggregate_workspace_bytes(int nparts, uint64_t n);
+
+/* fp64 mean of nparts dense vectors laid out [nparts][n] (compressors.py:274-285). */
+GVC_API int gvc_aggregate_dense(const float *parts_dev, int nparts, uint64_t n, float *out_dev,
+                        void *stream);
+
+/* Measurement hooks (bench.py): when enabled, CUDA events bracket the
+ * collect kernel, the whole selection, the emit and the decompress-average on
+ * the launching stream; gvc_prof_read synchronises on them, returns per-category
+ * milliseconds and launch counts (categories: 0 collect, 1 select, 2 emit,
+ * 3 aggregate) and resets.  gvc_launch_count is a running count of every
+ * kernel this library launched. */
+GVC_API void gvc_prof_enable(int on);
+GVC_API int gvc_prof_read(double *ms, unsigned long long *counts, int ncat);
+GVC_API unsigned long long gvc_launch_count(void);
+
+/* Fill out[i] = i (identity support for k >= n, compressors.py:172-173). */
+GVC_API int gvc_iota(uint32_t *out_dev, uint64_t n, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,176 @@
+"""ctypes binding of libgravac_b200.so (include/gravac_b200.h).
+
+The product path has exactly one backend: the sm_100a kernels in this
+library.  There is no CPU fallback -- if the library is missing or no CUDA
+device is present, every compute call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgravac_b200.so")
+
+GVC_OK, GVC_ERR_ARG, GVC_ERR_NAN, GVC_ERR_WORKSPACE, GVC_ERR_CUDA, GVC_ERR_STATE = 0, -1, -2, -3, -4, -5
+GVC_TOPK, GVC_DGC, GVC_REDSYNC, GVC_RANDOMK = 0, 1, 2, 3
+KIND_IDS = {"topk": GVC_TOPK, "dgc": GVC_DGC, "redsync": GVC_REDSYNC, "randomk": GVC_RANDOMK}
+MAX_LADDER = 16
+
+# every symbol include/gravac_b200.h declares (tests assert the .so exports them)
+EXPORTS = (
+    "gvc_last_error", "gvc_abi_version", "gvc_select_workspace_bytes", "gvc_select", "gvc_emit",
+    "gvc_ef_add", "gvc_sq_norm_workspace_bytes", "gvc_sq_norm", "gvc_update_residual",
+    "gvc_decompress", "gvc_aggregate", "gvc_aggregate_workspace_bytes", "gvc_aggregate_dense",
+    "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count",
+)
+
+_u64, _i32, _f64, _vp, _sz = ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
+
+
+class SelectArgs(ctypes.Structure):
+    _fields_ = [
+        ("kind", _i32), ("n_ks", _i32), ("n", _u64),
+        ("values_dev", _vp), ("g_dev", _vp), ("resid_dev", _vp),
+        ("ks", _u64 * MAX_LADDER),
+        ("seed", _u64), ("rng_stream", _u64), ("pos_base", _u64),
+        ("dgc_sample_fraction", _f64),
+        ("force_exact", _i32), ("reserved", _i32),
+    ]
+
+
+class SelectResult(ctypes.Structure):
+    _fields_ = [
+        ("ef_norm_sq", _f64),
+        ("kept_sq", _f64 * MAX_LADDER),
+        ("kept_abs", _f64 * MAX_LADDER),
+        ("threshold_key", ctypes.c_uint32 * MAX_LADDER),
+        ("pad0", ctypes.c_uint32 * MAX_LADDER),
+        ("tie_quota", _u64 * MAX_LADDER),
+        ("redsync_mean", ctypes.c_float * MAX_LADDER),
+        ("candidates", _u64),
+        ("status", _i32),
+        ("fallback_used", _i32),
+        ("kept_count", _u64 * MAX_LADDER),
+        ("kept_nonzero", _u64 * MAX_LADDER),
+    ]
+
+
+RESULT_BYTES = ctypes.sizeof(SelectResult)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(build_if_missing: bool = False):
+    """Load the native library; raises ImportError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            if build_if_missing:
+                from . import build_ext
+                build_ext.build()
+            else:
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build the sm_100a extension first "
+                    "(python -m paper_2305_12201_b200.build_ext); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        L.gvc_last_error.restype = ctypes.c_char_p
+        L.gvc_abi_version.restype = ctypes.c_int
+        L.gvc_select_workspace_bytes.argtypes = [ctypes.c_int, _u64]
+        L.gvc_select_workspace_bytes.restype = _sz
+        L.gvc_select.argtypes = [ctypes.POINTER(SelectArgs), _vp, _sz, _vp, _vp]
+        L.gvc_emit.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.gvc_ef_add.argtypes = [_vp, _vp, _vp, _u64, _vp]
+        L.gvc_sq_norm_workspace_bytes.argtypes = [_u64]
+        L.gvc_sq_norm_workspace_bytes.restype = _sz
+        L.gvc_sq_norm.argtypes = [_vp, _u64, _vp, _vp, _sz, _vp]
+        L.gvc_update_residual.argtypes = [_vp, _vp, _vp, _u64, _u64, _vp, _vp]
+        L.gvc_decompress.argtypes = [_vp, _vp, _u64, _u64, _vp, _vp, _sz, _vp]
+        L.gvc_aggregate.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, _vp, _sz, _vp]
+        L.gvc_aggregate_workspace_bytes.argtypes = [ctypes.c_int, _u64]
+        L.gvc_aggregate_workspace_bytes.restype = _sz
+        L.gvc_aggregate_dense.argtypes = [_vp, ctypes.c_int, _u64, _vp, _vp]
+        L.gvc_iota.argtypes = [_vp, _u64, _vp]
+        L.gvc_prof_enable.argtypes = [ctypes.c_int]
+        L.gvc_prof_enable.restype = None
+        L.gvc_prof_read.argtypes = [_vp, _vp, ctypes.c_int]
+        L.gvc_launch_count.restype = ctypes.c_ulonglong
+        if L.gvc_abi_version() != 1:
+            raise ImportError("libgravac_b200 ABI version mismatch")
+        _lib = L
+        return L
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == GVC_OK:
+        return
+    msg = load().gvc_last_error().decode(errors="replace")
+    if rc in (GVC_ERR_ARG, GVC_ERR_NAN):
+        raise ValueError(msg or what)
+    raise RuntimeError(f"{what}: {msg} (status {rc})")
+
+
+def require_cuda(t: torch.Tensor) -> None:
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (the compression path runs on the GPU only)")
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Workspace:
+    """Grow-only device scratch buffers, one per (device, slot)."""
+
+    _bufs: dict = {}
+
+    @classmethod
+    def get(cls, device: torch.device, slot: str, nbytes: int) -> torch.Tensor:
+        key = (device.index if device.index is not None else torch.cuda.current_device(), slot)
+        buf = cls._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            cls._bufs[key] = buf
+        return buf
+
+
+def select_workspace(device, slot: str, kind: int, n: int) -> torch.Tensor:
+    return Workspace.get(device, slot, int(load().gvc_select_workspace_bytes(kind, n)))
+
+
+PROF_CATS = ("collect", "select", "emit", "aggregate")
+
+
+def prof_enable(on: bool) -> None:
+    load().gvc_prof_enable(1 if on else 0)
+
+
+def prof_read() -> dict:
+    """{category: (total_ms, launches)} since the last read (synchronises on the events)."""
+    ms = (ctypes.c_double * len(PROF_CATS))()
+    cnt = (ctypes.c_ulonglong * len(PROF_CATS))()
+    load().gvc_prof_read(ms, cnt, len(PROF_CATS))
+    return {c: (ms[i], cnt[i]) for i, c in enumerate(PROF_CATS)}
+
+
+def launch_count() -> int:
+    return int(load().gvc_launch_count())
+
+
+def read_result(res_dev: torch.Tensor) -> SelectResult:
+    """Device -> host copy of a gvc_select_result (synchronises the stream)."""
+    host = res_dev.cpu().numpy().tobytes()
+    return SelectResult.from_buffer_copy(host[:RESULT_BYTES])

@@ -1,0 +1,389 @@
+"""GraVAC adaptive-CF controller with the fused GPU compression step.
+
+Drop-in for ``gravac.controller`` (/root/reference/pkg/src/gravac/controller.py).
+The scalar state machine (select_cf, scaling_policy, check_gravac, EWMA
+observation order) is host logic kept arithmetic-identical to the reference,
+so the chosen CF is bit-exact.  The data plane of ``run_iteration`` is the
+hot path: per worker ONE fused selection pass computes g_ef = g + r (written
+over the residual), ||g_ef||^2 and the kept energy of every CF in the ladder;
+the host reads back 3 doubles per worker, decides, and a single emit kernel
+writes the chosen (index, value) list and leaves g_ef - sent in the residual.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+
+from . import _native as nat
+from .compressors import (TOPK, CompressorKind, Selection, SparseGradient, _iota, compress,
+                          compress_further, keep_count)
+from .costmodel import (CostModelParams, allreduce_time, dense_message_words, iteration_time,
+                        sparse_message_words)
+from .feedback import ResidualStore
+from .gradcore import GradientVector, SeededRng, ewma_lambda_from_workers
+from .metrics import GainTracker, ThroughputTable, update_step
+
+EXPONENTIAL = "exponential"
+GEOMETRIC = "geometric"
+POLICIES = (EXPONENTIAL, GEOMETRIC)
+
+CANDIDATE = "candidate"
+MINIMUM = "minimum"
+DENSE = "dense"
+
+_STAGE_MIN = 0   # rng substream tags (controller.py:33-35)
+_STAGE_STEP = 1
+
+
+@dataclass(frozen=True)
+class ControllerConfig:
+    theta_min: float = 10.0
+    theta_max: float = 1000.0
+    epsilon: float = 0.7
+    omega: float = 0.01
+    window: int = 500
+    policy: str = EXPONENTIAL
+    compressor: CompressorKind = CompressorKind("topk")
+
+    def __post_init__(self):
+        if self.theta_min < 1.0:
+            raise ValueError(f"theta_min must be >= 1, got {self.theta_min}")
+        if self.theta_max < self.theta_min:
+            raise ValueError(f"theta_max must be >= theta_min, got {self.theta_max}")
+        if not (0.0 < self.epsilon < 1.0):
+            raise ValueError(f"epsilon out of (0,1): {self.epsilon}")
+        if not (0.0 < self.omega < 1.0):
+            raise ValueError(f"omega out of (0,1): {self.omega}")
+        if self.window < 1:
+            raise ValueError(f"window must be >= 1, got {self.window}")
+        if self.policy not in POLICIES:
+            raise ValueError(f"unknown policy {self.policy!r}, expected one of {POLICIES}")
+
+
+@dataclass
+class CfDecision:
+    choice: str
+    cf: float
+    gain: float
+    delta_min: float
+    delta_c: float
+
+
+def select_cf(delta_c: float, delta_min: float, epsilon: float,
+              candidate_cf: float | None = None, minimum_cf: float | None = None) -> CfDecision:
+    """Candidate if its smoothed gain clears epsilon, else minimum, else dense (controller.py:74-82)."""
+    if delta_c >= epsilon:
+        return CfDecision(CANDIDATE, candidate_cf, delta_c, delta_min, delta_c)
+    if delta_min >= epsilon:
+        return CfDecision(MINIMUM, minimum_cf, delta_min, delta_min, delta_c)
+    return CfDecision(DENSE, 1.0, 1.0, delta_min, delta_c)
+
+
+def scaling_policy(policy: str, step: int, theta_min_initial: float, theta_max: float,
+                   theta_min_current: float | None = None) -> float:
+    """Step factor at policy step `step`, capped at theta_max / theta_min (controller.py:85-105).
+
+    Step 0 evaluates theta_min itself (factor 1).  Exponential: 2^(2^(step-1));
+    geometric: 2^step.
+    """
+    if step < 0:
+        raise ValueError(f"policy step must be >= 0, got {step}")
+    if policy not in POLICIES:
+        raise ValueError(f"unknown policy {policy!r}")
+    base = theta_min_initial if theta_min_current is None else theta_min_current
+    cap = theta_max / base
+    if step == 0:
+        return min(1.0, cap)
+    exponent = step if policy == GEOMETRIC else 2 ** (step - 1)
+    if exponent >= 1024:  # 2.0**exponent would overflow; the cap wins anyway
+        return cap
+    return min(2.0 ** exponent, cap)
+
+
+@dataclass
+class ControllerState:
+    config: ControllerConfig
+    gains: GainTracker
+    table: ThroughputTable
+    theta_min: float
+    theta_min_initial: float
+    theta_s: float = 1.0
+    step: int = 0
+    iteration: int = 0
+    frozen: bool = False
+    theta_ideal: float | None = None
+    saturation_picked_higher_cf: bool = False
+
+    @classmethod
+    def fresh(cls, config: ControllerConfig, workers: int) -> "ControllerState":
+        return cls(config=config, gains=GainTracker(ewma_lambda_from_workers(workers)),
+                   table=ThroughputTable(), theta_min=config.theta_min,
+                   theta_min_initial=config.theta_min)
+
+    @property
+    def candidate_cf(self) -> float:
+        return self.theta_s * self.theta_min
+
+
+def check_gravac(state: ControllerState, iteration: int, delta_min: float | None,
+                 delta_c: float | None) -> ControllerState:
+    """Window-boundary escalation / step advance / saturation freeze (controller.py:137-171)."""
+    cfg = state.config
+    if state.frozen or iteration % cfg.window != 0:
+        return state
+    if delta_min is not None and delta_c is not None and delta_min > 0:
+        if cfg.omega >= abs(delta_min - delta_c) / delta_min:
+            state.theta_min = min(cfg.theta_max, state.theta_s * state.theta_min)
+    state.step += 1
+    state.theta_s = scaling_policy(cfg.policy, state.step, state.theta_min_initial, cfg.theta_max,
+                                   state.theta_min)
+    top = state.table.top_two()
+    if top is not None:
+        (cf_first, v_first), (cf_second, v_second) = top
+        if v_second > 0 and abs(v_first - v_second) / v_second <= cfg.omega:
+            state.theta_ideal = cf_second
+            state.frozen = True
+            if cf_second > cf_first:
+                state.saturation_picked_higher_cf = True
+            state.theta_s = max(1.0, state.theta_ideal / state.theta_min)
+    return state
+
+
+@dataclass
+class IterationResult:
+    sent: Sequence[SparseGradient] | Sequence[GradientVector]
+    decision: CfDecision
+    t_compute: float
+    t_compress: float
+    t_sync: float
+    t_iter: float
+    floats_sent: int
+    words_sent: int
+    gain_min_raw: float
+    gain_c_raw: float
+    candidate_cf: float
+    theta_min: float
+    # beyond the reference: raw mean gain of every CF evaluated in the fused sweep
+    ladder_gains: dict = field(default_factory=dict)
+
+
+# ------------------------------------------------------------ fused step
+class _WorkerStep:
+    """Device-side work of one worker for one iteration (level 1 + level 2)."""
+
+    def __init__(self, kind: CompressorKind, g: torch.Tensor, resid: torch.Tensor, k1: int, k2: int,
+                 extra_ks: Sequence[int], rng: SeededRng, i: int, w: int):
+        self.kind, self.k1, self.k2 = kind, k1, k2
+        self.resid = resid
+        self.n = g.numel()
+        self.g_min: SparseGradient | None = None
+        self.sel2: Selection | None = None
+        self.identity1 = k1 >= self.n
+        rng0 = rng.split(i, w, _STAGE_MIN)
+        rng1 = rng.split(i, w, _STAGE_STEP)
+        slot = f"step{w}"
+        if self.identity1:
+            # theta_min == 1: level 1 keeps everything; g_ef by the EF kernel
+            nat.check(nat.load().gvc_ef_add(nat.ptr(g), nat.ptr(resid), nat.ptr(resid), self.n,
+                                            nat.stream_ptr(g.device)), "apply_feedback")
+            self.g_min = SparseGradient._wrap(_iota(self.n, g.device), resid.clone(), self.n, 1.0)
+            self.sel1 = None
+            self._norm_dev = None
+            self.ladder = [k2] + list(extra_ks)
+            if kind.name == TOPK:
+                ks = [k for k in self.ladder if k < self.n]
+                self.sel2 = Selection(kind, ks or [self.n - 1], values=resid, slot=slot + "b") if ks else None
+            else:
+                self.sel2 = (Selection(kind, [k2], values=self.g_min.vals, rng=rng1, slot=slot + "b")
+                             if k2 < self.n else None)
+            return
+        if kind.name == TOPK:
+            # F2: nested Top-k == exact top-k2 of the whole vector -> one sweep
+            self.ladder = [k1, k2] + list(extra_ks)
+            self.sel1 = Selection(kind, self.ladder, g=g, resid=resid, rng=rng0, slot=slot + "a")
+        else:
+            self.ladder = [k1]
+            self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a")
+            idx, vals = self.sel1.emit(0)
+            self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
+            if k2 < k1:
+                self.sel2 = Selection(kind, [k2], values=vals, rng=rng1, slot=slot + "b")
+
+    def stats_dev(self) -> list[torch.Tensor]:
+        """Device tensors whose bytes the host reads once per iteration."""
+        out = []
+        if self.sel1 is not None:
+            out.append(self.sel1.res_dev)
+        if self.sel2 is not None:
+            out.append(self.sel2.res_dev)
+        return out
+
+    def gains_from(self, results: list[nat.SelectResult], norm_host: float | None):
+        """(ef_norm, E_min, E_c, extra energies) from the read-back results."""
+        r1 = results[0] if self.sel1 is not None else None
+        r2 = results[-1] if self.sel2 is not None else None
+        for r in results:
+            if r.status == nat.GVC_ERR_NAN:
+                raise ValueError("NaN in gradient: compression order undefined")
+            if r.status != nat.GVC_OK:
+                raise RuntimeError(f"selection consistency failure (status {r.status})")
+        if self.identity1:
+            norm = norm_host
+            e_min = norm
+            if self.kind.name == TOPK:
+                extra_e = []
+                ks = [k for k in self.ladder if k < self.n]
+                e_by_k = {k: r2.kept_sq[j] for j, k in enumerate(ks)} if r2 is not None else {}
+                e_c = e_by_k.get(self.k2, norm)
+                extra_e = [e_by_k.get(k, norm) for k in self.ladder[1:]]
+                return norm, e_min, e_c, extra_e
+            e_c = r2.kept_sq[0] if r2 is not None else norm
+            return norm, e_min, e_c, []
+        norm = r1.ef_norm_sq
+        if self.kind.name == TOPK:
+            return norm, r1.kept_sq[0], r1.kept_sq[1], [r1.kept_sq[2 + j] for j in range(len(self.ladder) - 2)]
+        e_min = r1.kept_sq[0]
+        e_c = r2.kept_sq[0] if r2 is not None else e_min
+        return norm, e_min, e_c, []
+
+    def emit(self, candidate: bool) -> SparseGradient:
+        """Materialise the chosen view and leave g_ef - sent in the residual."""
+        lib = nat.load()
+        if self.kind.name == TOPK and not self.identity1:
+            j = 1 if candidate else 0
+            k = self.ladder[j]
+            idx, vals = self.sel1.emit(j, resid=self.resid)
+            return SparseGradient._wrap(idx, vals, self.n, self.n / k)
+        if candidate and self.sel2 is not None:
+            idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, resid=self.resid)
+            return SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
+        part = self.g_min
+        nat.check(lib.gvc_update_residual(nat.ptr(self.resid), nat.ptr(part.indices), nat.ptr(part.vals),
+                                          part.kept, self.n, nat.ptr(self.resid),
+                                          nat.stream_ptr(self.resid.device)), "update_residual")
+        return part
+
+
+def _read_results(tensors: list[torch.Tensor]) -> list[nat.SelectResult]:
+    if not tensors:
+        return []
+    raw = torch.stack(tensors).cpu().numpy()
+    return [nat.SelectResult.from_buffer_copy(row.tobytes()[:nat.RESULT_BYTES]) for row in raw]
+
+
+def _mean_raw_gain(energies: Sequence[float], ef_norms: Sequence[float]) -> float:
+    """Mean over non-zero-norm workers of min(1, E/||g_ef||^2), worker order (controller.py:284-288)."""
+    gains = [min(1.0, e / n) for e, n in zip(energies, ef_norms) if n > 0.0]
+    return sum(gains) / len(gains)
+
+
+def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelParams, rng: SeededRng,
+                  batch_size: int = 1, *, extra_cfs: Sequence[float] = (), group=None) -> IterationResult:
+    """One adaptive GraVAC step (controller.py:192-281) on the GPU.
+
+    ``gradients``/``residuals``: one object (one worker) or worker-ascending
+    sequences (workers simulated on this GPU), exactly as in the reference.
+    With ``group`` (a torch.distributed process group), this process is ONE
+    worker -- worker index = rank -- and the per-worker gain ratios are
+    all-gathered so every rank takes the same decision in the reference's
+    worker order.  ``extra_cfs``: more CFs (>= theta_min) whose gains the Top-k
+    sweep evaluates in the same pass; reported in ``ladder_gains`` but never
+    fed to the EWMA trackers.
+    """
+    cfg = state.config
+    grads = [gradients] if isinstance(gradients, GradientVector) else list(gradients)
+    stores = [residuals] if isinstance(residuals, ResidualStore) else list(residuals)
+    if len(grads) != len(stores):
+        raise ValueError(f"{len(grads)} gradients for {len(stores)} residual stores")
+    if group is not None and len(grads) != 1:
+        raise ValueError("with a process group each rank passes exactly one gradient")
+    kind = cfg.compressor
+    state.iteration += 1
+    i = state.iteration
+    theta_min = state.theta_min
+    candidate_cf = state.candidate_cf
+    length = grads[0].length
+    rank = 0
+    if group is not None:
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+    k1 = keep_count(length, theta_min)
+    k2 = keep_count(k1, state.theta_s)
+    extra = [float(c) for c in extra_cfs if kind.name == TOPK]
+    extra_ks = [keep_count(k1, c / theta_min) for c in extra]
+
+    steps = []
+    for w, (g, store) in enumerate(zip(grads, stores)):
+        if g.length != store.length:
+            raise ValueError(f"length mismatch: gradient {g.length}, residual {store.length}")
+        nat.require_cuda(g.values)
+        steps.append(_WorkerStep(kind, g.values, store.residual, k1, k2, extra_ks, rng, i, rank + w))
+
+    # ---- one device->host read per iteration: every worker's norms and energies
+    norm_host = None
+    if steps[0].identity1:
+        from .gradcore import squared_l2_norm_dev
+        norm_dev = [squared_l2_norm_dev(s.resid) for s in steps]
+        norm_host = [float(x) for x in torch.stack(norm_dev).cpu()]
+    results = _read_results([t for s in steps for t in s.stats_dev()])
+    local = []
+    pos = 0
+    for w, s in enumerate(steps):
+        cnt = len(s.stats_dev())
+        local.append(s.gains_from(results[pos:pos + cnt], norm_host[w] if norm_host else None))
+        pos += cnt
+    if group is not None:
+        from .exchange import allgather_gain_rows
+        local = allgather_gain_rows(local[0], group, grads[0].values.device)
+    ef_norms = [x[0] for x in local]
+
+    if all(nv == 0.0 for nv in ef_norms):
+        # vanished gradient: dense no-op (controller.py:217-230)
+        sent = []
+        for store in stores:
+            sent.append(GradientVector._wrap(store.residual, grads[0].layer_offsets))
+            store.residual = torch.zeros_like(store.residual)
+        t_sync = allreduce_time(dense_message_words(length), cost)
+        decision = CfDecision(DENSE, 1.0, 1.0, 1.0, 1.0)
+        t_iter = iteration_time(decision, cost.t_compute, 0.0, t_sync)
+        update_step(state.table, 1.0, 1.0, t_iter, cost.workers, batch_size)
+        d_min = state.gains.value(theta_min) if state.gains.has(theta_min) else None
+        d_c = state.gains.value(candidate_cf) if state.gains.has(candidate_cf) else None
+        check_gravac(state, i, d_min, d_c)
+        return IterationResult(sent, decision, cost.t_compute, 0.0, t_sync, t_iter, length,
+                               dense_message_words(length), 1.0, 1.0, candidate_cf, theta_min)
+
+    raw_min = _mean_raw_gain([x[1] for x in local], ef_norms)
+    delta_min = state.gains.observe(theta_min, raw_min)
+    raw_c = _mean_raw_gain([x[2] for x in local], ef_norms)
+    delta_c = state.gains.observe(candidate_cf, raw_c)
+    ladder = {theta_min: raw_min, candidate_cf: raw_c}
+    for j, c in enumerate(extra):
+        ladder[c] = _mean_raw_gain([x[3][j] for x in local], ef_norms)
+    t_min = cost.compression_latency(kind, length, k1)
+    t_step = cost.compression_latency(kind, k1, k2)
+    t_compress = t_min + t_step
+
+    decision = select_cf(delta_c, delta_min, cfg.epsilon, candidate_cf=candidate_cf, minimum_cf=theta_min)
+    if decision.choice == DENSE:
+        sent = []
+        for store in stores:
+            # the residual buffer holds g_ef: hand it over as the dense message
+            sent.append(GradientVector._wrap(store.residual, grads[0].layer_offsets))
+            store.residual = torch.zeros_like(store.residual)
+        floats = length
+        words = dense_message_words(length)
+    else:
+        sent = [s.emit(decision.choice == CANDIDATE) for s in steps]
+        floats = sent[0].kept
+        words = sparse_message_words(sent[0])
+
+    t_sync = allreduce_time(words, cost)
+    t_iter = iteration_time(decision, cost.t_compute, t_compress, t_sync)
+    update_step(state.table, decision.cf, decision.gain, t_iter, cost.workers, batch_size)
+    check_gravac(state, i, delta_min, delta_c)
+    return IterationResult(sent, decision, cost.t_compute, 0.0 if decision.choice == DENSE else t_compress,
+                           t_sync, t_iter, floats, words, raw_min, raw_c, candidate_cf, theta_min, ladder)

@@ -1,0 +1,219 @@
+// gvc_capi.cu -- extern "C" entry points of libgravac_b200.so (include/gravac_b200.h).
+// Argument validation mirrors the reference's ValueError checks; the kernels
+// live in gvc_select.cu / gvc_dense.cu.
+#include <atomic>
+#include <mutex>
+#include <stdarg.h>
+#include <vector>
+#include <stdio.h>
+#include <string.h>
+
+#include "gvc_internal.h"
+
+namespace gvc {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+// ---------------------------------------------------------------- profiler
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_pending;
+static std::vector<cudaEvent_t> g_prof_free;
+static double g_prof_ms[PROF_NCAT];
+static unsigned long long g_prof_cnt[PROF_NCAT];
+static std::atomic<unsigned long long> g_launches{0};
+
+static cudaEvent_t prof_event()
+{
+    if (!g_prof_free.empty()) {
+        cudaEvent_t e = g_prof_free.back();
+        g_prof_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(int cat, cudaStream_t st) : slot(-1), s(st)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_on)
+        return;
+    cudaEvent_t a = prof_event(), b = prof_event();
+    cudaEventRecord(a, s);
+    g_prof_pending.push_back({cat, {a, b}});
+    slot = (int)g_prof_pending.size() - 1;
+}
+
+ProfScope::~ProfScope()
+{
+    if (slot < 0)
+        return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(g_prof_pending[slot].second.second, s);
+}
+
+void count_launches(int n) { g_launches += (unsigned long long)n; }
+
+static int check_launch(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(GVC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return GVC_OK;
+}
+
+}  // namespace gvc
+
+using namespace gvc;
+
+#define STREAM(s) ((cudaStream_t)(s))
+
+extern "C" {
+
+const char *gvc_last_error(void) { return g_err; }
+
+int gvc_abi_version(void) { return GVC_ABI_VERSION; }
+
+void gvc_prof_enable(int on)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+}
+
+int gvc_prof_read(double *ms, unsigned long long *counts, int ncat)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &pe : g_prof_pending) {
+        float t = 0.f;
+        cudaEventSynchronize(pe.second.second);
+        if (cudaEventElapsedTime(&t, pe.second.first, pe.second.second) == cudaSuccess) {
+            g_prof_ms[pe.first] += t;
+            g_prof_cnt[pe.first] += 1;
+        }
+        g_prof_free.push_back(pe.second.first);
+        g_prof_free.push_back(pe.second.second);
+    }
+    g_prof_pending.clear();
+    for (int c = 0; c < ncat && c < PROF_NCAT; c++) {
+        ms[c] = g_prof_ms[c];
+        counts[c] = g_prof_cnt[c];
+        g_prof_ms[c] = 0.0;
+        g_prof_cnt[c] = 0;
+    }
+    return PROF_NCAT;
+}
+
+unsigned long long gvc_launch_count(void) { return g_launches.load(); }
+
+size_t gvc_select_workspace_bytes(int kind, uint64_t n) { return select_workspace_bytes(kind, n); }
+
+int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res, void *stream)
+{
+    if (!a || !ws || !res)
+        return set_error(GVC_ERR_ARG, "gvc_select: null argument");
+    if (a->kind < GVC_TOPK || a->kind > GVC_RANDOMK)
+        return set_error(GVC_ERR_ARG, "unknown compressor kind %d", a->kind);
+    if (a->kind == GVC_DGC)
+        return set_error(GVC_ERR_ARG, "dgc selection goes through gvc_dgc_select");
+    if (a->n < 1 || a->n >= (1ull << 32))
+        return set_error(GVC_ERR_ARG, "gradient length %llu outside [1, 2^32)", (unsigned long long)a->n);
+    if (a->n_ks < 1 || a->n_ks > GVC_MAX_LADDER)
+        return set_error(GVC_ERR_ARG, "ladder length %d outside [1, %d]", a->n_ks, GVC_MAX_LADDER);
+    for (int j = 0; j < a->n_ks; j++) {
+        if (a->ks[j] < 1 || a->ks[j] >= a->n)
+            return set_error(GVC_ERR_ARG, "keep count %llu outside [1, n)", (unsigned long long)a->ks[j]);
+        if (j && a->ks[j] > a->ks[j - 1])
+            return set_error(GVC_ERR_ARG, "keep counts must be non-increasing");
+    }
+    const bool ef = a->g_dev != nullptr;
+    if (ef ? (a->resid_dev == nullptr) : (a->values_dev == nullptr))
+        return set_error(GVC_ERR_ARG, "gvc_select: need values_dev, or g_dev and resid_dev");
+    const void *src = ef ? (const void *)a->g_dev : (const void *)a->values_dev;
+    if (((uintptr_t)src & 15) || (ef && ((uintptr_t)a->resid_dev & 15)))
+        return set_error(GVC_ERR_ARG, "gvc_select: inputs must be 16-byte aligned");
+    return select_run(a, ws, ws_bytes, res, STREAM(stream));
+}
+
+int gvc_emit(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
+             float *resid, double *stats, void *stream)
+{
+    if (!ws || !out_idx || !out_val)
+        return set_error(GVC_ERR_ARG, "gvc_emit: null argument");
+    return emit_run(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, stats, STREAM(stream));
+}
+
+int gvc_ef_add(const float *g, const float *r, float *out, uint64_t n, void *stream)
+{
+    if (!g || !r || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_ef_add: bad arguments");
+    int rc = ef_add_run(g, r, out, n, STREAM(stream));
+    return rc ? rc : check_launch("ef_add");
+}
+
+size_t gvc_sq_norm_workspace_bytes(uint64_t n) { return sq_norm_workspace_bytes(n); }
+
+int gvc_sq_norm(const float *x, uint64_t n, double *out, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!x || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "squared_l2_norm of empty vector");
+    int rc = sq_norm_run(x, n, out, ws, ws_bytes, STREAM(stream));
+    return rc ? rc : check_launch("sq_norm");
+}
+
+int gvc_update_residual(const float *ef, const uint32_t *idx, const float *vals, uint64_t k, uint64_t n,
+                        float *resid, void *stream)
+{
+    if (!ef || !resid || n < 1 || (k && (!idx || !vals)))
+        return set_error(GVC_ERR_ARG, "gvc_update_residual: bad arguments");
+    int rc = update_residual_run(ef, idx, vals, k, n, resid, STREAM(stream));
+    return rc ? rc : check_launch("update_residual");
+}
+
+int gvc_decompress(const uint32_t *idx, const float *vals, uint64_t k, uint64_t n, float *out, void *ws,
+                   size_t ws_bytes, void *stream)
+{
+    if (!idx || !vals || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_decompress: bad arguments");
+    int rc = decompress_run(idx, vals, k, n, out, ws, ws_bytes, STREAM(stream));
+    return rc ? rc : check_launch("decompress");
+}
+
+size_t gvc_aggregate_workspace_bytes(int nparts, uint64_t n) { return aggregate_workspace_bytes(nparts, n); }
+
+int gvc_aggregate(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
+                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, void *stream)
+{
+    if (nparts < 1)
+        return set_error(GVC_ERR_ARG, "aggregate of zero parts");
+    if (!idx || !vals || !offs || !counts || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_aggregate: bad arguments");
+    int rc = aggregate_run(idx, vals, offs, counts, nparts, n, out, ws, ws_bytes, STREAM(stream));
+    return rc ? rc : check_launch("aggregate");
+}
+
+int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, void *stream)
+{
+    if (nparts < 1)
+        return set_error(GVC_ERR_ARG, "aggregate of zero parts");
+    int rc = aggregate_dense_run(parts, nparts, n, out, STREAM(stream));
+    return rc ? rc : check_launch("aggregate_dense");
+}
+
+int gvc_iota(uint32_t *out, uint64_t n, void *stream)
+{
+    int rc = iota_run(out, n, STREAM(stream));
+    return rc ? rc : check_launch("iota");
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// gvc_common.cuh -- shared device helpers for the GraVAC sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gravac_b200.h"
+
+#define GVC_WARPS_PER_BLOCK 8
+#define GVC_THREADS (GVC_WARPS_PER_BLOCK * 32)
+// Segments: the input is cut into S contiguous ranges, one per warp of the
+// collect kernel.  S depends only on n (never on the device), so every
+// reduction order is a function of the input size alone.
+#define GVC_SEG_TARGET 9472  // 148 SMs x 8 blocks x 8 warps
+#define GVC_SEG_MAX 16384
+#define GVC_SEG_QUANTUM 512  // elements per warp iteration: 32 lanes x 4 float4
+#define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)
+#define GVC_HL_BINS 4096     // refinement histogram per ladder entry (global)
+#define GVC_SAMPLE_BINS 65536
+#define GVC_SAMPLE_SHIFT 15  // 31-bit magnitude key >> 15 -> 16-bit sample bin
+#define GVC_MAX_LEVELS 3
+
+namespace gvc {
+
+enum KeyMode { KEY_MAG = 0, KEY_HASH = 1 };
+
+// |x| as an order-preserving integer: clear the sign bit (-0 -> 0).  Monotone
+// for every non-NaN float; NaN keys are > 0x7f800000.
+__device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+
+// Philox4x32-10 (Salmon et al. SC'11), output word 0.  Counter-based position
+// hash replacing numpy Generator.choice (gradcore.py:144-149): counter =
+// (lo i, hi i, lo stream, hi stream), key = (lo seed, hi seed).
+__device__ __forceinline__ uint32_t philox_x0(uint64_t i, uint64_t stream, uint64_t seed)
+{
+    uint32_t c0 = (uint32_t)i, c1 = (uint32_t)(i >> 32), c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        if (r > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return c0;
+}
+
+// Random-k / DGC-sample selection key: the k SMALLEST hashes win, so the key
+// (larger wins) is the bitwise complement.
+__device__ __forceinline__ uint32_t hash_key(uint64_t pos, uint64_t stream, uint64_t seed)
+{
+    return ~philox_x0(pos, stream, seed);
+}
+
+__device__ __forceinline__ double warp_sum_f64(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
+
+// Streaming loads / stores: the gradient and residual are touched once per
+// step, so they should not displace the candidate buffer in L2.
+__device__ __forceinline__ float4 ld_stream(const float4 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
+
+}  // namespace gvc

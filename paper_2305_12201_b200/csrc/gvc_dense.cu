@@ -1,0 +1,307 @@
+// gvc_dense.cu -- dense-side kernels of the GraVAC step (sm_100a):
+// error-feedback add, fp64 norm, residual scatter, decompress and the
+// shared-memory-tiled fp64 decompress-average of N sparse parts.
+#include "gvc_common.cuh"
+#include "gvc_internal.h"
+
+namespace gvc {
+
+static inline int grid_for(uint64_t work, int per_block, int cap)
+{
+    uint64_t b = (work + per_block - 1) / per_block;
+    if (b < 1)
+        b = 1;
+    return (int)(b > (uint64_t)cap ? cap : b);
+}
+
+static inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+// ------------------------------------------------------------- EF add
+__global__ void k_ef_add(const float *__restrict__ g, const float *__restrict__ r, float *__restrict__ out,
+                         uint64_t n, int vec)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (vec) {
+        const uint64_t n4 = n / 4;
+        for (uint64_t i = t0; i < n4; i += stride) {
+            float4 a = ld_stream(reinterpret_cast<const float4 *>(g) + i);
+            float4 b = ld_stream(reinterpret_cast<const float4 *>(r) + i);
+            a.x = __fadd_rn(a.x, b.x);
+            a.y = __fadd_rn(a.y, b.y);
+            a.z = __fadd_rn(a.z, b.z);
+            a.w = __fadd_rn(a.w, b.w);
+            reinterpret_cast<float4 *>(out)[i] = a;
+        }
+        for (uint64_t i = n4 * 4 + t0; i < n; i += stride)
+            out[i] = __fadd_rn(g[i], r[i]);
+    } else {
+        for (uint64_t i = t0; i < n; i += stride)
+            out[i] = __fadd_rn(g[i], r[i]);
+    }
+}
+
+int ef_add_run(const float *g, const float *r, float *out, uint64_t n, cudaStream_t s)
+{
+    int vec = aligned16(g) && aligned16(r) && aligned16(out);
+    count_launches(1);
+    k_ef_add<<<grid_for(n / 4 + 1, 256, 148 * 16), 256, 0, s>>>(g, r, out, n, vec);
+    return GVC_OK;
+}
+
+// ------------------------------------------------------------- fp64 norm
+// Grid size depends on n only, so the reduction order is reproducible.
+#define NORM_BLOCKS_MAX 2048
+__global__ void k_sq_norm_part(const float *__restrict__ x, uint64_t n, double *part)
+{
+    __shared__ double red[256];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    double acc = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double v = (double)x[i];
+        acc = __fma_rn(v, v, acc);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        part[blockIdx.x] = red[0];
+}
+
+__global__ void k_sq_norm_final(const double *part, int nb, double *out)
+{
+    __shared__ double red[1024];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 1024)
+        acc += part[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        *out = red[0];
+}
+
+size_t sq_norm_workspace_bytes(uint64_t n)
+{
+    (void)n;
+    return NORM_BLOCKS_MAX * sizeof(double);
+}
+
+int sq_norm_run(const float *x, uint64_t n, double *out, void *ws, size_t ws_bytes, cudaStream_t s)
+{
+    if (ws_bytes < sq_norm_workspace_bytes(n))
+        return set_error(GVC_ERR_WORKSPACE, "sq_norm workspace too small");
+    int nb = grid_for(n, 256 * 16, NORM_BLOCKS_MAX);
+    count_launches(1);
+    k_sq_norm_part<<<nb, 256, 0, s>>>(x, n, (double *)ws);
+    count_launches(1);
+    k_sq_norm_final<<<1, 1024, 0, s>>>((const double *)ws, nb, out);
+    return GVC_OK;
+}
+
+// ---------------------------------------------------- residual scatter
+__global__ void k_sub_scatter(const uint32_t *__restrict__ idx, const float *__restrict__ vals, uint64_t k,
+                              float *resid)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        uint32_t p = idx[i];
+        resid[p] = __fsub_rn(resid[p], vals[i]);
+    }
+}
+
+int update_residual_run(const float *ef, const uint32_t *idx, const float *vals, uint64_t k, uint64_t n,
+                        float *resid, cudaStream_t s)
+{
+    if (ef != resid)
+        cudaMemcpyAsync(resid, ef, n * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    if (k)
+        count_launches(1);
+    k_sub_scatter<<<grid_for(k, 256, 148 * 16), 256, 0, s>>>(idx, vals, k, resid);
+    return GVC_OK;
+}
+
+// ------------------------------------------------- tiled decompress/average
+// One CTA owns a TILE-value slice of the dense output.  For every part (in
+// worker order) it binary-searches the slice's sub-range of that part's
+// ascending index list and accumulates into a shared-memory tile (fp64 for
+// the average, fp32 assignment for decompress); parts are separated by a
+// barrier so each position sees its adds in worker order, as
+// compressors.py:265-271 does.  The tile leaves in coalesced 128-bit stores.
+#define AGG_TILE 4096
+#define AGG_THREADS 256
+#define AGG_MAX_PARTS 64
+
+struct AggParts {
+    uint64_t off[AGG_MAX_PARTS];
+    uint64_t cnt[AGG_MAX_PARTS];
+};
+
+// Tile boundaries of every part in one streaming pass over the index lists:
+// bounds[p * (ntiles + 1) + b] = first entry of part p with index >= b * TILE.
+__global__ void k_tile_bounds(const uint32_t *__restrict__ idx, AggParts parts, int nparts, uint64_t ntiles,
+                              uint32_t *__restrict__ bounds)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const int p = blockIdx.y;
+    if (p >= nparts)
+        return;
+    const uint32_t *pi = idx + parts.off[p];
+    const uint64_t cnt = parts.cnt[p];
+    uint32_t *bp = bounds + (uint64_t)p * (ntiles + 1);
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= cnt; t += stride) {
+        int64_t prev = t == 0 ? -1 : (int64_t)(pi[t - 1] / AGG_TILE);
+        int64_t cur = t == cnt ? (int64_t)ntiles : (int64_t)(pi[t] / AGG_TILE);
+        for (int64_t b = prev + 1; b <= cur; b++)
+            bp[b] = (uint32_t)t;
+    }
+}
+
+template <bool AVG>
+__global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__restrict__ idx,
+                                                            const float *__restrict__ vals, AggParts parts,
+                                                            int nparts, uint64_t n, uint64_t ntiles,
+                                                            const uint32_t *__restrict__ bounds,
+                                                            float *__restrict__ out)
+{
+    __shared__ double acc[AVG ? AGG_TILE : 1];
+    __shared__ float accf[AVG ? 1 : AGG_TILE];
+    const uint64_t tile = blockIdx.x;
+    const uint64_t lo = tile * AGG_TILE;
+    const uint64_t hi = min(n, lo + AGG_TILE);
+    for (int i = threadIdx.x; i < AGG_TILE; i += AGG_THREADS) {
+        if (AVG)
+            acc[i] = 0.0;
+        else
+            accf[i] = 0.0f;
+    }
+    __syncthreads();
+    for (int p = 0; p < nparts; p++) {
+        const uint32_t *pi = idx + parts.off[p];
+        const float *pv = vals + parts.off[p];
+        const uint32_t *bp = bounds + (uint64_t)p * (ntiles + 1);
+        const uint32_t a = bp[tile], b = bp[tile + 1];
+        for (uint32_t t = a + threadIdx.x; t < b; t += AGG_THREADS) {
+            uint32_t r = pi[t] - (uint32_t)lo;
+            if (AVG)
+                acc[r] += (double)pv[t];
+            else
+                accf[r] = pv[t];
+        }
+        __syncthreads();  // worker order per position (compressors.py:266-269)
+    }
+    const double np = (double)nparts;
+    if (hi - lo == AGG_TILE && (((uintptr_t)(out + lo)) & 15) == 0) {
+        for (int i = threadIdx.x; i < AGG_TILE / 4; i += AGG_THREADS) {
+            float4 v;
+            if (AVG) {
+                v.x = (float)(acc[4 * i + 0] / np);
+                v.y = (float)(acc[4 * i + 1] / np);
+                v.z = (float)(acc[4 * i + 2] / np);
+                v.w = (float)(acc[4 * i + 3] / np);
+            } else {
+                v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+            }
+            st_stream(reinterpret_cast<float4 *>(out + lo) + i, v);
+        }
+    } else {
+        for (uint64_t i = lo + threadIdx.x; i < hi; i += AGG_THREADS)
+            out[i] = AVG ? (float)(acc[i - lo] / np) : accf[i - lo];
+    }
+}
+
+size_t aggregate_workspace_bytes(int nparts, uint64_t n)
+{
+    uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
+    return (size_t)(nparts < 1 ? 1 : nparts) * (ntiles + 1) * sizeof(uint32_t);
+}
+
+static int tile_merge_run(bool avg, const uint32_t *idx, const float *vals, const AggParts &P, int nparts,
+                          uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s)
+{
+    if (ws_bytes < aggregate_workspace_bytes(nparts, n))
+        return set_error(GVC_ERR_WORKSPACE, "aggregate workspace too small: %zu < %zu", ws_bytes,
+                         aggregate_workspace_bytes(nparts, n));
+    const uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
+    uint64_t maxcnt = 1;
+    for (int p = 0; p < nparts; p++)
+        maxcnt = P.cnt[p] + 1 > maxcnt ? P.cnt[p] + 1 : maxcnt;
+    dim3 bg((unsigned)grid_for(maxcnt, 256, 1024), (unsigned)nparts);
+    ProfScope pa(PROF_AGGREGATE, s);
+    count_launches(2);
+    k_tile_bounds<<<bg, 256, 0, s>>>(idx, P, nparts, ntiles, (uint32_t *)ws);
+    if (avg)
+        k_tile_merge<true><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles,
+                                                                    (const uint32_t *)ws, out);
+    else
+        k_tile_merge<false><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles,
+                                                                     (const uint32_t *)ws, out);
+    return GVC_OK;
+}
+
+int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
+                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s)
+{
+    if (nparts < 1 || nparts > AGG_MAX_PARTS)
+        return set_error(GVC_ERR_ARG, "aggregate: nparts %d outside [1, %d]", nparts, AGG_MAX_PARTS);
+    AggParts P;
+    for (int p = 0; p < nparts; p++) {
+        P.off[p] = offs[p];
+        P.cnt[p] = counts[p];
+    }
+    return tile_merge_run(true, idx, vals, P, nparts, n, out, ws, ws_bytes, s);
+}
+
+int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t n, float *out, void *ws,
+                   size_t ws_bytes, cudaStream_t s)
+{
+    AggParts P;
+    P.off[0] = 0;
+    P.cnt[0] = k;
+    return tile_merge_run(false, idx, vals, P, 1, n, out, ws, ws_bytes, s);
+}
+
+// --------------------------------------------------------- dense average
+__global__ void k_aggregate_dense(const float *__restrict__ parts, int nparts, uint64_t n, float *__restrict__ out)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double acc = 0.0;
+        for (int p = 0; p < nparts; p++)
+            acc += (double)parts[(uint64_t)p * n + i];
+        out[i] = (float)(acc / (double)nparts);
+    }
+}
+
+int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, cudaStream_t s)
+{
+    if (nparts < 1)
+        return set_error(GVC_ERR_ARG, "aggregate_dense of zero parts");
+    count_launches(1);
+    k_aggregate_dense<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(parts, nparts, n, out);
+    return GVC_OK;
+}
+
+__global__ void k_iota(uint32_t *out, uint64_t n)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = (uint32_t)i;
+}
+
+int iota_run(uint32_t *out, uint64_t n, cudaStream_t s)
+{
+    count_launches(1);
+    k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(out, n);
+    return GVC_OK;
+}
+
+}  // namespace gvc

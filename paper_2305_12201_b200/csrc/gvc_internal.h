@@ -1,0 +1,44 @@
+// gvc_internal.h -- declarations shared by the translation units of libgravac_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/gravac_b200.h"
+
+namespace gvc {
+
+// Records the message for gvc_last_error() and returns `code`.
+int set_error(int code, const char *fmt, ...);
+
+// Live kernel timing for bench.py (CUDA events on the launching stream).
+enum ProfCat { PROF_COLLECT = 0, PROF_SELECT = 1, PROF_EMIT = 2, PROF_AGGREGATE = 3, PROF_NCAT = 4 };
+struct ProfScope {
+    int slot;
+    cudaStream_t s;
+    ProfScope(int cat, cudaStream_t s);
+    ~ProfScope();
+};
+void count_launches(int n);
+
+size_t select_workspace_bytes(int kind, uint64_t n);
+int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
+               cudaStream_t s);
+int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx,
+             float *out_val, float *resid, double *stats, cudaStream_t s);
+
+size_t sq_norm_workspace_bytes(uint64_t n);
+int sq_norm_run(const float *x, uint64_t n, double *out, void *ws, size_t ws_bytes, cudaStream_t s);
+int ef_add_run(const float *g, const float *r, float *out, uint64_t n, cudaStream_t s);
+int update_residual_run(const float *ef, const uint32_t *idx, const float *vals, uint64_t k,
+                        uint64_t n, float *resid, cudaStream_t s);
+int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t n, float *out, void *ws,
+                   size_t ws_bytes, cudaStream_t s);
+size_t aggregate_workspace_bytes(int nparts, uint64_t n);
+int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
+                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s);
+int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, cudaStream_t s);
+int iota_run(uint32_t *out, uint64_t n, cudaStream_t s);
+
+}  // namespace gvc
