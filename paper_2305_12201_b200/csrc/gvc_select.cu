@@ -656,15 +656,21 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
             BA[b] = a;
         }
     }
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < nks; b++) {
-            unsigned long long c = 0;
-            for (uint32_t s = 0; s < S; s++)
-                c += p.band_cnt[(size_t)b * GVC_SEG_MAX + s];
-            BC[b] = c;
+    for (int b = 0; b < nks; b++) {
+        unsigned long long c = 0;
+        for (uint32_t s = threadIdx.x; s < S; s += 1024)
+            c += p.band_cnt[(size_t)b * GVC_SEG_MAX + s];
+        scratch[threadIdx.x] = c;
+        __syncthreads();
+        for (int o = 512; o > 0; o >>= 1) {
+            if (threadIdx.x < o)
+                scratch[threadIdx.x] += scratch[threadIdx.x + o];
+            __syncthreads();
         }
+        if (threadIdx.x == 0)
+            BC[b] = scratch[0];
+        __syncthreads();
     }
-    __syncthreads();
 
     for (int j = 0; j < nks; j++) {
         const uint32_t T = (uint32_t)st->js[j].lo;
@@ -837,8 +843,12 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
             uint32_t gi = idx_map ? idx_map[pos] : pos;
             out_idx[w] = gi;
             out_val[w] = sv;
-            if (resid)
-                resid[gi] = __fsub_rn(v, sv);
+            if (resid) {
+                // level-1 emits: the candidate value IS g_ef; a second-level emit
+                // (idx_map) carries level-1 SENT values, so read g_ef back
+                float ef = idx_map ? resid[gi] : v;
+                resid[gi] = __fsub_rn(ef, sv);
+            }
             e2 += (double)sv * (double)sv;
             ab += fabs((double)sv);
         }
