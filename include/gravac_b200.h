@@ -83,7 +83,8 @@ typedef struct {
     uint64_t rng_stream;          /* SeededRng.stream (after split)                         */
     uint64_t pos_base;            /* hash counter offset (layerwise segments)               */
     double dgc_sample_fraction;   /* CompressorKind.dgc_sample_fraction (compressors.py:36) */
-    int32_t force_exact;          /* 1: skip the threshold estimate (every value is a candidate) */
+    int32_t force_exact;          /* 1: skip the threshold estimate (every value is a candidate);
+                                     2: test hook, an estimate that misses (exercises the exact re-scan) */
     int32_t reserved;
 } gvc_select_args;
 

@@ -124,7 +124,7 @@ class Selection:
     def __init__(self, kind: CompressorKind, ks: Sequence[int], *, values: torch.Tensor | None = None,
                  g: torch.Tensor | None = None, resid: torch.Tensor | None = None,
                  rng: SeededRng | None = None, pos_base: int = 0, slot: str = "sel0",
-                 force_exact: bool = False):
+                 force_exact: int = 0):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -147,7 +147,7 @@ class Selection:
         a.rng_stream = rng.stream if rng is not None else 0
         a.pos_base = pos_base
         a.dgc_sample_fraction = kind.dgc_sample_fraction
-        a.force_exact = 1 if force_exact else 0
+        a.force_exact = int(force_exact)
         nat.check(lib.gvc_select(ctypes.byref(a), nat.ptr(self.ws), self.ws.numel(), nat.ptr(self.res_dev),
                                  nat.stream_ptr(self.device)), "gvc_select")
         self._result = None

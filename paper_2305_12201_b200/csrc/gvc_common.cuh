@@ -16,8 +16,9 @@
 #define GVC_SEG_QUANTUM 512  // elements per warp iteration: 32 lanes x 4 float4
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)
 #define GVC_HL_BINS 4096     // refinement histogram per ladder entry (global)
-#define GVC_SAMPLE_BINS 65536
-#define GVC_SAMPLE_SHIFT 15  // 31-bit magnitude key >> 15 -> 16-bit sample bin
+#define GVC_BLK_MAX (GVC_SEG_MAX / GVC_WARPS_PER_BLOCK)
+#define GVC_SAMPLE_BINS 16384  // shared-memory sample histogram (64 KB)
+#define GVC_SAMPLE_SHIFT 17    // 31-bit magnitude key >> 17 -> 14-bit bin (1/64 octave)
 #define GVC_MAX_LEVELS 3
 
 namespace gvc {
@@ -75,6 +76,63 @@ __device__ __forceinline__ uint32_t lanemask_lt()
 }
 
 __device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
+
+// Exclusive prefix sum across a 1024-thread block (warp shuffles, 2 barriers).
+// `sh` must hold 33 u64; *total (optional) receives the block total.
+__device__ __forceinline__ unsigned long long block_excl_prefix(unsigned long long v, unsigned long long *sh,
+                                                                unsigned long long *total = nullptr)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o)
+            x += y;
+    }
+    if (lane == 31)
+        sh[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = sh[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o)
+                wi += y;
+        }
+        sh[lane] = wi - w;
+        if (lane == 31)
+            sh[32] = wi;
+    }
+    __syncthreads();
+    unsigned long long r = sh[warp] + x - v;
+    if (total)
+        *total = sh[32];
+    __syncthreads();
+    return r;
+}
+
+// Deterministic fp64 sum across a 1024-thread block: fixed xor tree per warp,
+// then warps added in index order.  `sh` must hold 33 doubles.
+__device__ __forceinline__ double block_sum_f64(double v, double *sh)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum_f64(v);
+    if (lane == 0)
+        sh[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0;
+        for (int w = 0; w < 32; w++)
+            r += sh[w];
+        sh[32] = r;
+    }
+    __syncthreads();
+    double r = sh[32];
+    __syncthreads();
+    return r;
+}
 
 // Streaming loads / stores: the gradient and residual are touched once per
 // step, so they should not displace the candidate buffer in L2.

@@ -198,15 +198,23 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
         }
         __syncthreads();  // worker order per position (compressors.py:266-269)
     }
+    // x / N is exact-equivalent to x * (1/N) only for power-of-two N; zeros skip the divide
     const double np = (double)nparts;
+    const bool pow2 = (nparts & (nparts - 1)) == 0;
+    const double inv = 1.0 / np;
+    auto mean = [&](double a) -> float {
+        if (a == 0.0)
+            return 0.0f;
+        return (float)(pow2 ? a * inv : a / np);
+    };
     if (hi - lo == AGG_TILE && (((uintptr_t)(out + lo)) & 15) == 0) {
         for (int i = threadIdx.x; i < AGG_TILE / 4; i += AGG_THREADS) {
             float4 v;
             if (AVG) {
-                v.x = (float)(acc[4 * i + 0] / np);
-                v.y = (float)(acc[4 * i + 1] / np);
-                v.z = (float)(acc[4 * i + 2] / np);
-                v.w = (float)(acc[4 * i + 3] / np);
+                v.x = mean(acc[4 * i + 0]);
+                v.y = mean(acc[4 * i + 1]);
+                v.z = mean(acc[4 * i + 2]);
+                v.w = mean(acc[4 * i + 3]);
             } else {
                 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
             }
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
         }
     } else {
         for (uint64_t i = lo + threadIdx.x; i < hi; i += AGG_THREADS)
-            out[i] = AVG ? (float)(acc[i - lo] / np) : accf[i - lo];
+            out[i] = AVG ? mean(acc[i - lo]) : accf[i - lo];
     }
 }
 

@@ -7,19 +7,25 @@
 // energies the gain statistic needs (metrics.py:18-32).  Keys are the 31-bit
 // magnitude pattern (Top-k, Redsync, DGC) or a Philox position hash (Random-k).
 //
-// Pipeline (all stream-ordered, no host synchronisation):
-//   k_sample / k_sample_resolve   1-2% strided sample -> conservative key_est
+// Data layout: the input is cut into S contiguous segments, one per warp of
+// the collect kernel (8 warps = one "block" of 8 segments).  Candidates are
+// compacted IN INDEX ORDER into their segment's slice of the candidate buffer,
+// so every later pass reads only candidates and index order is free.
+//
+// Pipeline (stream-ordered, no host synchronisation):
+//   k_sample / k_sample_resolve   ~1.5% strided sample (smem histogram) ->
+//                                 conservative key_est + level-0 bin shift
 //   k_collect (EF fused)          ONE streaming pass over HBM: g_ef = g + r is
 //                                 written over r, fp64 ||g_ef||^2, and every
-//                                 key >= key_est is compacted, index-ordered,
-//                                 into the warp's segment of the candidate
-//                                 buffer with a level-0 histogram
+//                                 key >= key_est is compacted with a level-0
+//                                 shared-memory histogram
 //   k_resolve0 / k_collect(refill) exactness guard: if the estimate missed,
 //                                 every value becomes a candidate
 //   k_level_hist / k_level_resolve radix refinement over candidates only,
 //                                 until each k_j has its exact threshold key
-//   k_final / k_finish            per-segment band energies, tie counts, tie
-//                                 cut and output offsets for EVERY ladder entry
+//   k_final / k_finish            per-segment band counts and per-block band
+//                                 energies; tie cut, gains and per-block
+//                                 output offsets for EVERY ladder entry
 //   k_emit (gvc_emit)             ordered (idx, val) compaction of one entry,
 //                                 fused residual update
 #include <mutex>
@@ -53,7 +59,7 @@ struct SelState {
 
 struct Plan {
     uint64_t n;
-    uint32_t S, seg_len;
+    uint32_t S, B, seg_len;
     int n_ks, kind, keymode, ef, force_exact;
     const float *values;
     const float *g;
@@ -66,14 +72,14 @@ struct Plan {
     // workspace
     SelState *st;
     uint32_t *hist0, *histl, *shist;
-    uint32_t *seg_cnt;
-    double *norm_part;
-    uint32_t *band_cnt;  // [GVC_MAX_LADDER][SEG_MAX]
-    double *band_e2, *band_ab;
-    uint32_t *tie_cnt;
-    double *tie_e2, *tie_ab;
-    uint32_t *seg_take, *seg_off;
-    double *seg_emit;  // [2][SEG_MAX]
+    uint32_t *seg_cnt;                     // [SEG_MAX] candidates per segment
+    uint32_t *seg_band, *seg_tie;          // [L][SEG_MAX]
+    double *blk_norm;                      // [BLK_MAX]
+    uint32_t *blk_band_cnt, *blk_tie_cnt;  // [L][BLK_MAX]
+    double *blk_band_e2, *blk_band_ab;     // [L][BLK_MAX]
+    double *blk_tie_e2, *blk_tie_ab;       // [L][BLK_MAX]
+    uint32_t *blk_take, *blk_off;          // [L][BLK_MAX]
+    double *blk_emit;                      // [2][BLK_MAX]
     float *cand_val;
     uint32_t *cand_idx;
     gvc_select_result *res;
@@ -103,7 +109,7 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
         off += align256(bytes);
         return q;
     };
-    const size_t L = GVC_MAX_LADDER, SM = GVC_SEG_MAX;
+    const size_t L = GVC_MAX_LADDER, SM = GVC_SEG_MAX, BM = GVC_BLK_MAX;
     Plan tmp;
     Plan *q = p ? p : &tmp;
     q->st = (SelState *)take(sizeof(SelState));
@@ -111,19 +117,22 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
     q->histl = (uint32_t *)take(L * GVC_HL_BINS * 4);
     q->shist = (uint32_t *)take(GVC_SAMPLE_BINS * 4);
     q->seg_cnt = (uint32_t *)take(SM * 4);
-    q->norm_part = (double *)take(SM * 8);
-    q->band_cnt = (uint32_t *)take(L * SM * 4);
-    q->band_e2 = (double *)take(L * SM * 8);
-    q->band_ab = (double *)take(L * SM * 8);
-    q->tie_cnt = (uint32_t *)take(L * SM * 4);
-    q->tie_e2 = (double *)take(L * SM * 8);
-    q->tie_ab = (double *)take(L * SM * 8);
-    q->seg_take = (uint32_t *)take(L * SM * 4);
-    q->seg_off = (uint32_t *)take(L * SM * 4);
-    q->seg_emit = (double *)take(2 * SM * 8);
+    q->seg_band = (uint32_t *)take(L * SM * 4);
+    q->seg_tie = (uint32_t *)take(L * SM * 4);
+    q->blk_norm = (double *)take(BM * 8);
+    q->blk_band_cnt = (uint32_t *)take(L * BM * 4);
+    q->blk_tie_cnt = (uint32_t *)take(L * BM * 4);
+    q->blk_band_e2 = (double *)take(L * BM * 8);
+    q->blk_band_ab = (double *)take(L * BM * 8);
+    q->blk_tie_e2 = (double *)take(L * BM * 8);
+    q->blk_tie_ab = (double *)take(L * BM * 8);
+    q->blk_take = (uint32_t *)take(L * BM * 4);
+    q->blk_off = (uint32_t *)take(L * BM * 4);
+    q->blk_emit = (double *)take(2 * BM * 8);
     q->cand_val = (float *)take(n_pad * 4);
     q->cand_idx = (uint32_t *)take(n_pad * 4);
     q->S = S;
+    q->B = (S + GVC_WARPS_PER_BLOCK - 1) / GVC_WARPS_PER_BLOCK;
     q->seg_len = seg_len;
     return off;
 }
@@ -137,26 +146,59 @@ __device__ __forceinline__ uint32_t cand_key(const Plan &p, float v, uint32_t po
     return hash_key(p.pos_base + pos, p.stream, p.seed);
 }
 
-// ------------------------------------------------------------------ sample
-// Strided chunks of 128 contiguous values (one warp-load) -> 16-bit histogram
-// of magnitude keys in global memory.  Reads ~1.5% of the bytes.
-__global__ void __launch_bounds__(GVC_THREADS) k_sample(Plan p)
+// Four consecutive candidates of a segment (lane-major groups of 128):
+// values, positions and keys.  Entries at t >= cnt are invalid.
+template <int KM>
+__device__ __forceinline__ void load_cand4(const Plan &p, uint64_t beg, uint32_t t, uint32_t cnt, float (&v)[4],
+                                           uint32_t (&pos)[4], uint32_t (&key)[4], bool (&ok)[4], bool need_pos)
 {
+    float4 fv = *reinterpret_cast<const float4 *>(p.cand_val + beg + t);
+    v[0] = fv.x;
+    v[1] = fv.y;
+    v[2] = fv.z;
+    v[3] = fv.w;
+    if (need_pos || KM == KEY_HASH) {
+        uint4 iv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t);
+        pos[0] = iv.x;
+        pos[1] = iv.y;
+        pos[2] = iv.z;
+        pos[3] = iv.w;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        ok[c] = t + c < cnt;
+        key[c] = ok[c] ? cand_key<KM>(p, v[c], pos[c]) : 0u;
+    }
+}
+
+// ------------------------------------------------------------------ sample
+// Strided chunks of 128 contiguous values -> 14-bit shared-memory histogram of
+// magnitude keys, merged into global memory once per block.  Reads ~1.5%.
+__global__ void __launch_bounds__(1024) k_sample(Plan p)
+{
+    extern __shared__ uint32_t sh[];
+    for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
+        sh[i] = 0;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint64_t warps = (uint64_t)gridDim.x * GVC_WARPS_PER_BLOCK;
+    const uint64_t warps = (uint64_t)gridDim.x * 32;
     uint32_t kmax = 0;
-    for (uint64_t c = blockIdx.x * GVC_WARPS_PER_BLOCK + (threadIdx.x >> 5); c < p.s_chunks; c += warps) {
-        uint64_t base = c * p.s_stride;
+    for (uint64_t c = blockIdx.x * 32 + (threadIdx.x >> 5); c < p.s_chunks; c += warps) {
+        const uint64_t base = c * p.s_stride;
+        float v[4];
+        bool ok[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             uint64_t i = base + (uint64_t)q * 32 + lane;
-            if (i < p.n && i < base + 128) {
-                float v = p.ef ? p.g[i] + p.resid[i] : p.values[i];
-                uint32_t k = mag_key(v);
-                if (k <= 0x7f800000u) {
-                    atomicAdd(&p.shist[k >> GVC_SAMPLE_SHIFT], 1u);
-                    kmax = max(kmax, k);
-                }
+            ok[q] = i < p.n && i < base + 128;
+            v[q] = ok[q] ? (p.ef ? __fadd_rn(p.g[i], p.resid[i]) : p.values[i]) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint32_t k = mag_key(v[q]);
+            if (ok[q] && k <= 0x7f800000u) {
+                atomicAdd(&sh[k >> GVC_SAMPLE_SHIFT], 1u);
+                kmax = max(kmax, k);
             }
         }
     }
@@ -165,33 +207,10 @@ __global__ void __launch_bounds__(GVC_THREADS) k_sample(Plan p)
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
     if (lane == 0 && kmax)
         atomicMax(&p.st->max_key, kmax);
-}
-
-// Block-wide exclusive SUFFIX sums of a histogram: out[b] = sum_{b' > b} h[b'].
-// 1024 threads, nb a multiple of 1024; scratch holds 1024 u64.
-template <int NB>
-__device__ void suffix_counts(const uint32_t *h, unsigned long long *out, unsigned long long *scratch)
-{
-    constexpr int PER = NB / 1024;
-    const int t = threadIdx.x;
-    unsigned long long local = 0;
-    for (int i = 0; i < PER; i++)
-        local += h[t * PER + i];
-    scratch[t] = local;
     __syncthreads();
-    // inclusive suffix scan over scratch (Hillis-Steele, 10 steps)
-    for (int o = 1; o < 1024; o <<= 1) {
-        unsigned long long v = (t + o < 1024) ? scratch[t + o] : 0;
-        __syncthreads();
-        scratch[t] += v;
-        __syncthreads();
-    }
-    unsigned long long acc = (t + 1 < 1024) ? scratch[t + 1] : 0;  // bins beyond my range
-    for (int i = PER - 1; i >= 0; i--) {
-        out[t * PER + i] = acc;
-        acc += h[t * PER + i];
-    }
-    __syncthreads();
+    for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
+        if (sh[i])
+            atomicAdd(&p.shist[i], sh[i]);
 }
 
 // Chooses key_est (a lower bound for the k_0-th largest key, w.h.p.) and the
@@ -199,16 +218,22 @@ __device__ void suffix_counts(const uint32_t *h, unsigned long long *out, unsign
 // from the binomial tail (host-computed).
 __global__ void __launch_bounds__(1024) k_sample_resolve(Plan p)
 {
-    __shared__ unsigned long long scratch[1024];
-    __shared__ unsigned long long suf_chunk[1024];
+    __shared__ unsigned long long sh[33];
     SelState *st = p.st;
+    if (p.force_exact == 2) {  // test hook: an estimate that must miss -> exercises the refill path
+        if (threadIdx.x == 0) {
+            st->key_est = 0xffffffffu;
+            st->shift0 = 0;
+        }
+        return;
+    }
     if (p.keymode == KEY_HASH) {
         if (threadIdx.x == 0) {
             uint32_t est = p.force_exact ? 0u : p.hash_key_est;
             st->key_est = est;
             uint64_t span = (1ull << 32) - est;
-            int sh = bitlen64(span - 1) - 12;
-            st->shift0 = sh < 0 ? 0 : sh;
+            int shf = bitlen64(span - 1) - 12;
+            st->shift0 = shf < 0 ? 0 : shf;
         }
         return;
     }
@@ -219,42 +244,42 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(Plan p)
         }
         return;
     }
-    // per-thread chunk of 64 bins; suffix over chunks
+    constexpr int PER = GVC_SAMPLE_BINS / 1024;  // 16 bins per thread
     const int t = threadIdx.x;
+    uint32_t h[PER];
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.shist + t * PER);
     unsigned long long local = 0;
-    for (int i = 0; i < 64; i++)
-        local += p.shist[t * 64 + i];
-    scratch[t] = local;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        unsigned long long v = (t + o < 1024) ? scratch[t + o] : 0;
-        __syncthreads();
-        scratch[t] += v;
-        __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER / 4; q++) {
+        uint4 x = src[q];
+        h[4 * q] = x.x;
+        h[4 * q + 1] = x.y;
+        h[4 * q + 2] = x.z;
+        h[4 * q + 3] = x.w;
+        local += (unsigned long long)x.x + x.y + x.z + x.w;
     }
-    suf_chunk[t] = (t + 1 < 1024) ? scratch[t + 1] : 0;
-    __syncthreads();
+    unsigned long long total;
+    unsigned long long pre = block_excl_prefix(local, sh, &total);
+    unsigned long long acc = total - pre - local;  // keys in bins above my range
     const unsigned long long target = p.s_target;
-    const unsigned long long total = scratch[0];
-    if (t == 0 && total < target) {  // too few sampled values (e.g. NaN-only): exact path
-        st->key_est = 0;
-        st->shift0 = 19;
-    }
-    if (total >= target) {
-        unsigned long long acc = suf_chunk[t];
-        for (int i = 63; i >= 0; i--) {
-            uint32_t c = p.shist[t * 64 + i];
-            if (acc < target && acc + c >= target) {
-                uint32_t b = (uint32_t)(t * 64 + i);
-                uint32_t est = b << GVC_SAMPLE_SHIFT;
-                st->key_est = est;
-                uint32_t mk = st->max_key;
-                uint64_t span = mk > est ? (uint64_t)(mk - est) : 0;
-                int sh = bitlen64(span) - 12;
-                st->shift0 = sh < 0 ? 0 : sh;
-            }
-            acc += c;
+    if (total < target) {  // too few sampled values (e.g. NaN-only): exact path
+        if (t == 0) {
+            st->key_est = 0;
+            st->shift0 = 19;
         }
+        return;
+    }
+#pragma unroll
+    for (int i = PER - 1; i >= 0; i--) {
+        if (acc < target && acc + h[i] >= target) {
+            uint32_t est = (uint32_t)(t * PER + i) << GVC_SAMPLE_SHIFT;
+            st->key_est = est;
+            uint32_t mk = st->max_key;
+            uint64_t span = mk > est ? (uint64_t)(mk - est) : 0;
+            int shf = bitlen64(span) - 12;
+            st->shift0 = shf < 0 ? 0 : shf;
+        }
+        acc += h[i];
     }
 }
 
@@ -262,8 +287,8 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(Plan p)
 // Candidate compaction for 4 values of one lane in lane-major index order.
 template <int KM>
 __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32_t pos0, int valid,
-                                      uint32_t key_est, int shift0, uint32_t *h, float *cval,
-                                      uint32_t *cidx, uint32_t &ccount, uint32_t &nan_any)
+                                      uint32_t key_est, int shift0, uint32_t *h, float *cval, uint32_t *cidx,
+                                      uint32_t &ccount, uint32_t &nan_any)
 {
     uint32_t key[4];
     bool pr[4];
@@ -279,8 +304,7 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
     uint32_t m1 = __ballot_sync(0xffffffffu, pr[1]);
     uint32_t m2 = __ballot_sync(0xffffffffu, pr[2]);
     uint32_t m3 = __ballot_sync(0xffffffffu, pr[3]);
-    uint32_t any = m0 | m1 | m2 | m3;
-    if (any == 0)
+    if ((m0 | m1 | m2 | m3) == 0)
         return;
     uint32_t o = ccount + __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt) + __popc(m3 & lt);
 #pragma unroll
@@ -297,30 +321,31 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 }
 
 // One warp per segment.  EF: v = fl32(g + r) written back over r (the only
-// full-size write of the step); !EF: v read from `src`.  REFILL re-collects
+// full-size write of the step); !EF: v read from `values`.  REFILL re-collects
 // from the already-written g_ef with key_est = 0 (exactness fallback).
 template <int KM, bool EF>
 __global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
 {
     __shared__ uint32_t h[GVC_H0_BINS];
+    __shared__ double red[GVC_WARPS_PER_BLOCK];
     if (refill && !p.st->fallback)
         return;
     for (int i = threadIdx.x; i < GVC_H0_BINS; i += GVC_THREADS)
         h[i] = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
     const uint32_t key_est = refill ? 0u : p.st->key_est;
     const int shift0 = refill ? (KM == KEY_MAG ? 19 : 20) : p.st->shift0;
     const bool do_ef = EF && !refill;
     const float *src = (EF ? (refill ? p.resid : p.g) : p.values);
+    double nacc = 0.0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
         const uint64_t end = min(p.n, beg + p.seg_len);
         float *cval = p.cand_val + beg;
         uint32_t *cidx = p.cand_idx + beg;
         uint32_t ccount = 0, nan_any = 0;
-        double nacc = 0.0;
         uint64_t i = beg;
         for (; i + GVC_SEG_QUANTUM <= end; i += GVC_SEG_QUANTUM) {
             float4 a[4], b[4];
@@ -348,8 +373,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
                     for (int c = 0; c < 4; c++)
                         nacc = __fma_rn((double)v[c], (double)v[c], nacc);
                 }
-                push4<KM>(p, v, (uint32_t)(i + u * 128 + lane * 4), 4, key_est, shift0, h, cval, cidx,
-                          ccount, nan_any);
+                push4<KM>(p, v, (uint32_t)(i + u * 128 + lane * 4), 4, key_est, shift0, h, cval, cidx, ccount,
+                          nan_any);
             }
         }
         // tail: one value per lane, lane-major order preserved
@@ -369,76 +394,100 @@ __global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
             }
             push4<KM>(p, v, (uint32_t)t, valid, key_est, shift0, h, cval, cidx, ccount, nan_any);
         }
-        nacc = warp_sum_f64(nacc);
         nan_any = __any_sync(0xffffffffu, nan_any);
         if (lane == 0) {
             p.seg_cnt[seg] = ccount;
-            if (!refill)
-                p.norm_part[seg] = nacc;
             if (nan_any)
                 atomicOr(&p.st->nan_flag, 1u);
         }
     }
+    nacc = warp_sum_f64(nacc);
+    if (lane == 0)
+        red[warp] = nacc;
     __syncthreads();
+    if (threadIdx.x == 0 && !refill) {
+        double b = 0.0;
+        for (int w = 0; w < GVC_WARPS_PER_BLOCK; w++)
+            b += red[w];
+        p.blk_norm[blockIdx.x] = b;
+    }
     for (int i = threadIdx.x; i < GVC_H0_BINS; i += GVC_THREADS)
         if (h[i])
             atomicAdd(&p.hist0[i], h[i]);
 }
 
 // ----------------------------------------------------------------- resolve
-__device__ void set_jstate(JState &js, unsigned long long lo, unsigned long long hi,
-                           unsigned long long above, unsigned long long need)
+__device__ void set_jstate(JState &js, unsigned long long lo, unsigned long long hi, unsigned long long above,
+                           unsigned long long need)
 {
     js.lo = lo;
     js.hi = hi;
     js.above = above;
     js.need = need;
     unsigned long long w = hi - lo;
-    int sh = bitlen64(w - 1) - 12;
-    js.shift = sh < 0 ? 0 : sh;
+    int shf = bitlen64(w - 1) - 12;
+    js.shift = shf < 0 ? 0 : shf;
     js.resolved = (w == 1);
+}
+
+// For a 4096-bin histogram `h` (4 bins per thread of a 1024-thread block):
+// calls fn(j, bin, count_above_bin) for every need[j] whose crossing bin
+// (first bin from the top where the running count reaches need[j]) is local.
+template <typename F>
+__device__ __forceinline__ void find_crossings(const uint32_t *h, unsigned long long *sh, int nneed,
+                                               const unsigned long long *need, F fn)
+{
+    const int t = threadIdx.x;
+    uint4 x = reinterpret_cast<const uint4 *>(h)[t];
+    uint32_t c[4] = {x.x, x.y, x.z, x.w};
+    unsigned long long local = (unsigned long long)c[0] + c[1] + c[2] + c[3];
+    unsigned long long total;
+    unsigned long long pre = block_excl_prefix(local, sh, &total);
+    unsigned long long acc = total - pre - local;
+    for (int i = 3; i >= 0; i--) {
+        for (int j = 0; j < nneed; j++)
+            if (acc < need[j] && acc + c[i] >= need[j])
+                fn(j, 4 * t + i, acc);
+        acc += c[i];
+    }
 }
 
 // Level 0: candidate total, fallback decision, first interval per ladder entry.
 __global__ void __launch_bounds__(1024) k_resolve0(Plan p, int pass)
 {
-    __shared__ unsigned long long scratch[1024];
-    __shared__ unsigned long long suf[GVC_H0_BINS];
+    __shared__ unsigned long long sh[33];
+    __shared__ unsigned long long need[GVC_MAX_LADDER];
     SelState *st = p.st;
     if (pass == 1 && !st->fallback)
         return;
-    suffix_counts<GVC_H0_BINS>(p.hist0, suf, scratch);
-    const unsigned long long total = suf[0] + p.hist0[0];
+    if (threadIdx.x < p.n_ks)
+        need[threadIdx.x] = p.ks[threadIdx.x];
+    __syncthreads();
+    const uint32_t key_est = pass == 1 ? 0u : st->key_est;
+    const int shift0 = pass == 1 ? (p.keymode == KEY_MAG ? 19 : 20) : st->shift0;
+    uint4 x = reinterpret_cast<const uint4 *>(p.hist0)[threadIdx.x];
+    unsigned long long total;
+    block_excl_prefix((unsigned long long)x.x + x.y + x.z + x.w, sh, &total);
     if (pass == 0 && total < p.ks[0]) {
-        // estimate overshot: zero the histogram for the exact re-collect
-        for (int i = threadIdx.x; i < GVC_H0_BINS; i += 1024)
-            p.hist0[i] = 0;
+        // the estimate overshot: zero the histogram for the exact re-collect
+        reinterpret_cast<uint4 *>(p.hist0)[threadIdx.x] = make_uint4(0, 0, 0, 0);
         if (threadIdx.x == 0)
             st->fallback = 1;
         return;
     }
-    const uint32_t key_est = pass == 1 ? 0u : st->key_est;
-    const int shift0 = pass == 1 ? (p.keymode == KEY_MAG ? 19 : 20) : st->shift0;
-    if (pass == 1 && threadIdx.x == 0) {
-        st->key_est = key_est;
-        st->shift0 = shift0;
-    }
-    for (int b = threadIdx.x; b < GVC_H0_BINS; b += 1024) {
-        unsigned long long above = suf[b], c = p.hist0[b];
-        for (int j = 0; j < p.n_ks; j++) {
-            unsigned long long k = p.ks[j];
-            if (above < k && above + c >= k) {
-                unsigned long long lo = (unsigned long long)key_est + ((unsigned long long)b << shift0);
-                unsigned long long hi = (b == GVC_H0_BINS - 1) ? (1ull << 32)
-                                                                : lo + (1ull << shift0);
-                if (hi > (1ull << 32))
-                    hi = 1ull << 32;
-                set_jstate(st->js[j], lo, hi, above, k - above);
-            }
-        }
-    }
+    find_crossings(p.hist0, sh, p.n_ks, need, [&](int j, int b, unsigned long long above) {
+        unsigned long long lo = (unsigned long long)key_est + ((unsigned long long)b << shift0);
+        unsigned long long hi = (b == GVC_H0_BINS - 1) ? (1ull << 32) : lo + (1ull << shift0);
+        if (hi > (1ull << 32))
+            hi = 1ull << 32;
+        set_jstate(st->js[j], lo, hi, above, need[j] - above);
+    });
     __syncthreads();
     if (threadIdx.x == 0) {
+        if (pass == 1) {
+            st->key_est = key_est;
+            st->shift0 = shift0;
+        }
         st->cand_total = total;
         uint32_t pend = 0;
         for (int j = 0; j < p.n_ks; j++)
@@ -464,19 +513,26 @@ __global__ void __launch_bounds__(GVC_THREADS) k_level_hist(Plan p)
         return;
     const uint64_t beg = (uint64_t)seg * p.seg_len;
     const uint32_t cnt = p.seg_cnt[seg];
-    for (uint32_t t = lane; t < cnt; t += 32) {
-        uint32_t key = KM == KEY_MAG ? mag_key(p.cand_val[beg + t]) : cand_key<KM>(p, 0.f, p.cand_idx[beg + t]);
-        for (int j = 0; j < p.n_ks; j++) {
-            if (!js[j].resolved && key >= js[j].lo && key < js[j].hi)
-                atomicAdd(&p.histl[j * GVC_HL_BINS + (uint32_t)((key - js[j].lo) >> js[j].shift)], 1u);
+    for (uint32_t t = lane * 4; t < cnt; t += 128) {
+        float v[4];
+        uint32_t pos[4], key[4];
+        bool ok[4];
+        load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            if (!ok[c])
+                continue;
+            for (int j = 0; j < p.n_ks; j++) {
+                if (!js[j].resolved && key[c] >= js[j].lo && key[c] < js[j].hi)
+                    atomicAdd(&p.histl[j * GVC_HL_BINS + (uint32_t)((key[c] - js[j].lo) >> js[j].shift)], 1u);
+            }
         }
     }
 }
 
 __global__ void __launch_bounds__(1024) k_level_resolve(Plan p)
 {
-    __shared__ unsigned long long scratch[1024];
-    __shared__ unsigned long long suf[GVC_HL_BINS];
+    __shared__ unsigned long long sh[33];
     SelState *st = p.st;
     if (st->pending == 0)
         return;
@@ -484,22 +540,17 @@ __global__ void __launch_bounds__(1024) k_level_resolve(Plan p)
         if (st->js[j].resolved)
             continue;  // uniform across the block
         uint32_t *h = p.histl + j * GVC_HL_BINS;
-        suffix_counts<GVC_HL_BINS>(h, suf, scratch);
-        JState cur = st->js[j];
+        const JState cur = st->js[j];
+        const unsigned long long nd = cur.need;
         __syncthreads();
-        for (int b = threadIdx.x; b < GVC_HL_BINS; b += 1024) {
-            unsigned long long above = suf[b], c = h[b];
-            if (above < cur.need && above + c >= cur.need) {
-                unsigned long long lo = cur.lo + ((unsigned long long)b << cur.shift);
-                unsigned long long hi = lo + (1ull << cur.shift);
-                if (hi > cur.hi)
-                    hi = cur.hi;
-                set_jstate(st->js[j], lo, hi, cur.above + above, cur.need - above);
-            }
-        }
-        __syncthreads();
-        for (int b = threadIdx.x; b < GVC_HL_BINS; b += 1024)
-            h[b] = 0;
+        find_crossings(h, sh, 1, &nd, [&](int, int b, unsigned long long above) {
+            unsigned long long lo = cur.lo + ((unsigned long long)b << cur.shift);
+            unsigned long long hi = lo + (1ull << cur.shift);
+            if (hi > cur.hi)
+                hi = cur.hi;
+            set_jstate(st->js[j], lo, hi, cur.above + above, cur.need - above);
+        });
+        reinterpret_cast<uint4 *>(h)[threadIdx.x] = make_uint4(0, 0, 0, 0);
         __syncthreads();
     }
     if (threadIdx.x == 0) {
@@ -511,26 +562,27 @@ __global__ void __launch_bounds__(1024) k_level_resolve(Plan p)
 }
 
 // ------------------------------------------------------------------- final
-// Per segment: band counts / energies (band = #{j : T_j < key}) and, per
-// ladder entry, the count and energy of keys equal to T_j.  fp64 sums are
-// per-lane sequential then a fixed xor-tree: bit-reproducible.
+// Per segment: band counts (band = #{j : T_j < key}) and tie counts per
+// ladder entry (for the emit offsets); per block of 8 segments: band and tie
+// energies.  fp64 sums are per-lane sequential, a fixed xor tree per warp and
+// warps added in order: bit-reproducible.
 template <int KM, int NB>
 __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
 {
     __shared__ uint32_t Ts[GVC_MAX_LADDER];
+    __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
+    __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
     SelState *st = p.st;
     if (threadIdx.x < GVC_MAX_LADDER)
         Ts[threadIdx.x] = threadIdx.x < p.n_ks ? (uint32_t)st->js[threadIdx.x].lo : 0xffffffffu;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + (threadIdx.x >> 5);
-    if (seg >= p.S)
-        return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
+    const int nks = p.n_ks;
     uint32_t T[NB];
 #pragma unroll
     for (int j = 0; j < NB; j++)
         T[j] = Ts[j];
-    const int nks = p.n_ks;
     uint32_t bc[NB], tc[NB];
     double be[NB], ba[NB], te[NB], ta[NB];
 #pragma unroll
@@ -538,28 +590,37 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
         bc[j] = tc[j] = 0;
         be[j] = ba[j] = te[j] = ta[j] = 0.0;
     }
-    const uint64_t beg = (uint64_t)seg * p.seg_len;
-    const uint32_t cnt = p.seg_cnt[seg];
-    for (uint32_t t = lane; t < cnt; t += 32) {
-        float v = p.cand_val[beg + t];
-        uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + t]);
-        double v2 = (double)v * (double)v;
-        double av = fabs((double)v);
-        int band = 0;
+    if (seg < p.S) {
+        const uint64_t beg = (uint64_t)seg * p.seg_len;
+        const uint32_t cnt = p.seg_cnt[seg];
+        for (uint32_t t = lane * 4; t < cnt; t += 128) {
+            float v[4];
+            uint32_t pos[4], key[4];
+            bool ok[4];
+            load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
 #pragma unroll
-        for (int j = 0; j < NB; j++)
-            band += (j < nks && T[j] < key);
+            for (int c = 0; c < 4; c++) {
+                if (!ok[c])
+                    continue;
+                const double v2 = (double)v[c] * (double)v[c];
+                const double av = fabs((double)v[c]);
+                int band = 0;
 #pragma unroll
-        for (int j = 0; j < NB; j++) {
-            if (band == j + 1) {
-                bc[j]++;
-                be[j] += v2;
-                ba[j] += av;
-            }
-            if (j < nks && key == T[j]) {
-                tc[j]++;
-                te[j] += v2;
-                ta[j] += av;
+                for (int j = 0; j < NB; j++)
+                    band += (j < nks && T[j] < key[c]);
+#pragma unroll
+                for (int j = 0; j < NB; j++) {
+                    if (band == j + 1) {
+                        bc[j]++;
+                        be[j] += v2;
+                        ba[j] += av;
+                    }
+                    if (j < nks && key[c] == T[j]) {
+                        tc[j]++;
+                        te[j] += v2;
+                        ta[j] += av;
+                    }
+                }
             }
         }
     }
@@ -573,208 +634,180 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
         }
         double e1 = warp_sum_f64(be[j]), a1 = warp_sum_f64(ba[j]);
         double e2 = warp_sum_f64(te[j]), a2 = warp_sum_f64(ta[j]);
-        if (lane == 0 && j < nks) {
-            size_t o = (size_t)j * GVC_SEG_MAX + seg;
-            p.band_cnt[o] = c1;
-            p.band_e2[o] = e1;
-            p.band_ab[o] = a1;
-            p.tie_cnt[o] = c2;
-            p.tie_e2[o] = e2;
-            p.tie_ab[o] = a2;
+        if (lane == 0) {
+            wcnt[warp][0][j] = c1;
+            wcnt[warp][1][j] = c2;
+            wsum[warp][0][j] = e1;
+            wsum[warp][1][j] = a1;
+            wsum[warp][2][j] = e2;
+            wsum[warp][3][j] = a2;
+            if (seg < p.S && j < nks) {
+                p.seg_band[(size_t)j * GVC_SEG_MAX + seg] = c1;
+                p.seg_tie[(size_t)j * GVC_SEG_MAX + seg] = c2;
+            }
         }
     }
+    __syncthreads();
+    if (threadIdx.x < nks) {
+        const int j = threadIdx.x;
+        uint32_t c1 = 0, c2 = 0;
+        double e1 = 0.0, a1 = 0.0, e2 = 0.0, a2 = 0.0;
+        for (int w = 0; w < GVC_WARPS_PER_BLOCK; w++) {
+            c1 += wcnt[w][0][j];
+            c2 += wcnt[w][1][j];
+            e1 += wsum[w][0][j];
+            a1 += wsum[w][1][j];
+            e2 += wsum[w][2][j];
+            a2 += wsum[w][3][j];
+        }
+        const size_t o = (size_t)j * GVC_BLK_MAX + blockIdx.x;
+        p.blk_band_cnt[o] = c1;
+        p.blk_tie_cnt[o] = c2;
+        p.blk_band_e2[o] = e1;
+        p.blk_band_ab[o] = a1;
+        p.blk_tie_e2[o] = e2;
+        p.blk_tie_ab[o] = a2;
+    }
 }
 
-// Block (1024 threads) fixed-order sum of S doubles.
-__device__ double block_sum_f64(const double *x, uint32_t S, double *red)
-{
-    double acc = 0.0;
-    for (uint32_t s = threadIdx.x; s < S; s += 1024)
-        acc += x[s];
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = 512; o > 0; o >>= 1) {
-        if (threadIdx.x < o)
-            red[threadIdx.x] += red[threadIdx.x + o];
-        __syncthreads();
-    }
-    double r = red[0];
-    __syncthreads();
-    return r;
-}
-
-// Block exclusive scan of S u32 values (per-thread contiguous chunks).
-// Writes out[s] = sum_{s' < s} in[s'] and returns the total.
-__device__ unsigned long long block_excl_scan(const uint32_t *in, uint32_t *out, uint32_t S,
-                                              unsigned long long *scratch)
-{
-    const uint32_t per = (S + 1023) / 1024;
-    const uint32_t b0 = threadIdx.x * per, b1 = min(S, b0 + per);
-    unsigned long long local = 0;
-    for (uint32_t s = b0; s < b1; s++)
-        local += in[s];
-    scratch[threadIdx.x] = local;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        unsigned long long v = threadIdx.x >= o ? scratch[threadIdx.x - o] : 0;
-        __syncthreads();
-        scratch[threadIdx.x] += v;
-        __syncthreads();
-    }
-    unsigned long long acc = scratch[threadIdx.x] - local;
-    for (uint32_t s = b0; s < b1; s++) {
-        uint32_t v = in[s];
-        out[s] = (uint32_t)acc;
-        acc += v;
-    }
-    unsigned long long total = scratch[1023];
-    __syncthreads();
-    return total;
-}
-
-// Gains, tie cut and output offsets for every ladder entry (one block).
+// Gains, tie cut and per-block output offsets for every ladder entry (one block).
 template <int KM>
 __global__ void __launch_bounds__(1024) k_finish(Plan p)
 {
-    __shared__ double red[1024];
-    __shared__ unsigned long long scratch[1024];
+    __shared__ unsigned long long shu[33];
+    __shared__ double shd[33];
     __shared__ double BE[GVC_MAX_LADDER], BA[GVC_MAX_LADDER];
     __shared__ unsigned long long BC[GVC_MAX_LADDER];
-    __shared__ uint32_t part_seg;
+    __shared__ uint32_t part_blk;
     __shared__ unsigned long long part_take;
     SelState *st = p.st;
     gvc_select_result *res = p.res;
-    const uint32_t S = p.S;
+    const uint32_t B = p.B;
     const int nks = p.n_ks;
+    const int t = threadIdx.x;
+    constexpr int PER = GVC_BLK_MAX / 1024;  // 2 blocks per thread, contiguous
 
-    double norm = block_sum_f64(p.norm_part, S, red);
-    for (int b = 0; b < nks; b++) {
-        double e = block_sum_f64(p.band_e2 + (size_t)b * GVC_SEG_MAX, S, red);
-        double a = block_sum_f64(p.band_ab + (size_t)b * GVC_SEG_MAX, S, red);
-        if (threadIdx.x == 0) {
-            BE[b] = e;
-            BA[b] = a;
-        }
+    double acc = 0.0;
+    for (int i = 0; i < PER; i++) {
+        uint32_t b = t * PER + i;
+        if (b < B)
+            acc += p.blk_norm[b];
     }
-    for (int b = 0; b < nks; b++) {
+    const double norm = block_sum_f64(acc, shd);
+    for (int band = 0; band < nks; band++) {
+        double e = 0.0, a = 0.0;
         unsigned long long c = 0;
-        for (uint32_t s = threadIdx.x; s < S; s += 1024)
-            c += p.band_cnt[(size_t)b * GVC_SEG_MAX + s];
-        scratch[threadIdx.x] = c;
-        __syncthreads();
-        for (int o = 512; o > 0; o >>= 1) {
-            if (threadIdx.x < o)
-                scratch[threadIdx.x] += scratch[threadIdx.x + o];
-            __syncthreads();
+        for (int i = 0; i < PER; i++) {
+            uint32_t b = t * PER + i;
+            if (b < B) {
+                const size_t o = (size_t)band * GVC_BLK_MAX + b;
+                e += p.blk_band_e2[o];
+                a += p.blk_band_ab[o];
+                c += p.blk_band_cnt[o];
+            }
         }
-        if (threadIdx.x == 0)
-            BC[b] = scratch[0];
-        __syncthreads();
+        e = block_sum_f64(e, shd);
+        a = block_sum_f64(a, shd);
+        unsigned long long ct;
+        block_excl_prefix(c, shu, &ct);
+        if (t == 0) {
+            BE[band] = e;
+            BA[band] = a;
+            BC[band] = ct;
+        }
     }
+    __syncthreads();
 
     for (int j = 0; j < nks; j++) {
         const uint32_t T = (uint32_t)st->js[j].lo;
         const unsigned long long q = st->js[j].need;
-        // tie cut: exclusive prefix of per-segment tie counts
-        uint32_t *ties = p.tie_cnt + (size_t)j * GVC_SEG_MAX;
-        uint32_t *take = p.seg_take + (size_t)j * GVC_SEG_MAX;
-        block_excl_scan(ties, take, S, scratch);  // take[] temporarily = tie prefix
-        if (threadIdx.x == 0)
-            part_seg = 0xffffffffu;
-        __syncthreads();
-        for (uint32_t s = threadIdx.x; s < S; s += 1024) {
-            unsigned long long before = take[s], c = ties[s];
-            unsigned long long tk = before >= q ? 0 : (q - before < c ? q - before : c);
-            take[s] = (uint32_t)tk;
-            if (tk > 0 && tk < c) {
-                part_seg = s;
-                part_take = tk;
-            }
+        uint32_t tie[PER], sel[PER];
+        unsigned long long tl = 0;
+        for (int i = 0; i < PER; i++) {
+            uint32_t b = t * PER + i;
+            tie[i] = b < B ? p.blk_tie_cnt[(size_t)j * GVC_BLK_MAX + b] : 0u;
+            tl += tie[i];
         }
-        __syncthreads();
-        // energy of the fully-taken tie segments (fixed order)
+        if (t == 0)
+            part_blk = 0xffffffffu;
+        unsigned long long before = block_excl_prefix(tl, shu);
         double te = 0.0, ta = 0.0;
-        for (uint32_t s = threadIdx.x; s < S; s += 1024) {
-            size_t o = (size_t)j * GVC_SEG_MAX + s;
-            if (take[s] == p.tie_cnt[o] && take[s] > 0) {
-                te += p.tie_e2[o];
-                ta += p.tie_ab[o];
+        for (int i = 0; i < PER; i++) {
+            uint32_t b = t * PER + i;
+            unsigned long long tk = before >= q ? 0 : (q - before < tie[i] ? q - before : tie[i]);
+            before += tie[i];
+            if (b < B) {
+                const size_t o = (size_t)j * GVC_BLK_MAX + b;
+                p.blk_take[o] = (uint32_t)tk;
+                if (tk == tie[i] && tk > 0) {
+                    te += p.blk_tie_e2[o];
+                    ta += p.blk_tie_ab[o];
+                }
+                if (tk > 0 && tk < tie[i]) {
+                    part_blk = b;
+                    part_take = tk;
+                }
+                uint32_t s = (uint32_t)tk;
+                for (int band = j; band < nks; band++)
+                    s += p.blk_band_cnt[(size_t)band * GVC_BLK_MAX + b];
+                sel[i] = s;
+            } else {
+                sel[i] = 0;
             }
         }
-        // the one partially-taken segment: first `part_take` ties in index order
-        if (part_seg != 0xffffffffu) {
-            const uint32_t s = part_seg;
-            const uint64_t beg = (uint64_t)s * p.seg_len;
-            const uint32_t cnt = p.seg_cnt[s];
+        __syncthreads();
+        // the one partially-taken block: its first `part_take` ties in index order
+        if (part_blk != 0xffffffffu) {
             unsigned long long seen = 0;
-            for (uint32_t base = 0; base < cnt; base += 1024) {
-                uint32_t t = base + threadIdx.x;
-                bool tie = false;
-                float v = 0.f;
-                if (t < cnt) {
-                    v = p.cand_val[beg + t];
-                    uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + t]);
-                    tie = key == T;
+            const uint32_t s_end = min(p.S, (part_blk + 1) * GVC_WARPS_PER_BLOCK);
+            for (uint32_t sg = part_blk * GVC_WARPS_PER_BLOCK; sg < s_end; sg++) {
+                const uint64_t beg = (uint64_t)sg * p.seg_len;
+                const uint32_t cnt = p.seg_cnt[sg];
+                for (uint32_t base = 0; base < cnt; base += 1024) {
+                    const uint32_t tt = base + t;
+                    bool is_tie = false;
+                    float v = 0.f;
+                    if (tt < cnt) {
+                        v = p.cand_val[beg + tt];
+                        uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + tt]);
+                        is_tie = key == T;
+                    }
+                    unsigned long long tot;
+                    unsigned long long rank = seen + block_excl_prefix(is_tie ? 1ull : 0ull, shu, &tot);
+                    if (is_tie && rank < part_take) {
+                        te += (double)v * (double)v;
+                        ta += fabs((double)v);
+                    }
+                    seen += tot;
                 }
-                // block exclusive rank of ties
-                scratch[threadIdx.x] = tie;
-                __syncthreads();
-                for (int o = 1; o < 1024; o <<= 1) {
-                    unsigned long long x = threadIdx.x >= o ? scratch[threadIdx.x - o] : 0;
-                    __syncthreads();
-                    scratch[threadIdx.x] += x;
-                    __syncthreads();
-                }
-                unsigned long long rank = seen + scratch[threadIdx.x] - tie;
-                if (tie && rank < part_take) {
-                    te += (double)v * (double)v;
-                    ta += fabs((double)v);
-                }
-                seen += scratch[1023];
-                __syncthreads();
             }
         }
-        red[threadIdx.x] = te;
-        __syncthreads();
-        for (int o = 512; o > 0; o >>= 1) {
-            if (threadIdx.x < o)
-                red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
+        const double tie_e = block_sum_f64(te, shd);
+        const double tie_a = block_sum_f64(ta, shd);
+        unsigned long long sl = 0;
+        for (int i = 0; i < PER; i++)
+            sl += sel[i];
+        unsigned long long total_sel;
+        unsigned long long off = block_excl_prefix(sl, shu, &total_sel);
+        for (int i = 0; i < PER; i++) {
+            uint32_t b = t * PER + i;
+            if (b < B)
+                p.blk_off[(size_t)j * GVC_BLK_MAX + b] = (uint32_t)off;
+            off += sel[i];
         }
-        double tie_e = red[0];
-        __syncthreads();
-        red[threadIdx.x] = ta;
-        __syncthreads();
-        for (int o = 512; o > 0; o >>= 1) {
-            if (threadIdx.x < o)
-                red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
-        }
-        double tie_a = red[0];
-        __syncthreads();
-        // output offsets: selected per segment = sum_{b >= j} band_cnt + take
-        uint32_t *off = p.seg_off + (size_t)j * GVC_SEG_MAX;
-        for (uint32_t s = threadIdx.x; s < S; s += 1024) {
-            uint32_t sel = take[s];
-            for (int b = j; b < nks; b++)
-                sel += p.band_cnt[(size_t)b * GVC_SEG_MAX + s];
-            off[s] = sel;  // counts, scanned in place below
-        }
-        __syncthreads();
-        unsigned long long total_sel = block_excl_scan(off, off, S, scratch);
-        if (threadIdx.x == 0) {
+        if (t == 0) {
             double e_above = 0.0, a_above = 0.0;
             unsigned long long c_above = 0;
-            for (int b = j; b < nks; b++) {
-                e_above += BE[b];
-                a_above += BA[b];
-                c_above += BC[b];
+            for (int band = j; band < nks; band++) {
+                e_above += BE[band];
+                a_above += BA[band];
+                c_above += BC[band];
             }
             const unsigned long long k = p.ks[j];
-            double A = a_above + tie_a;
+            const double A = a_above + tie_a;
             double E = e_above + tie_e;
-            float m = (float)(A / (double)k);
-            unsigned long long nnz = k - ((KM == KEY_MAG && T == 0u) ? q : 0ull);
+            const float m = (float)(A / (double)k);
+            const unsigned long long nnz = k - ((KM == KEY_MAG && T == 0u) ? q : 0ull);
             if (p.kind == GVC_REDSYNC)
                 E = (double)nnz * ((double)m * (double)m);
             st->redsync_mean[j] = m;
@@ -790,7 +823,7 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
+    if (t == 0) {
         res->ef_norm_sq = norm;
         res->candidates = st->cand_total;
         res->status = (st->nan_flag & 1u) ? GVC_ERR_NAN : ((st->nan_flag & 2u) ? GVC_ERR_STATE : GVC_OK);
@@ -799,78 +832,141 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
 }
 
 // -------------------------------------------------------------------- emit
+// One warp per segment: in-block prefix of the 8 segments' tie / selected
+// counts (lanes 0..7), then an ordered 4-wide compaction.
 template <int KM>
-__global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map,
-                                                      uint32_t *out_idx, float *out_val, float *resid)
+__global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
+                                                      float *out_val, float *resid)
 {
-    const int lane = threadIdx.x & 31;
-    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + (threadIdx.x >> 5);
-    if (seg >= p.S)
-        return;
+    __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t blk = blockIdx.x;
+    const uint32_t seg = blk * GVC_WARPS_PER_BLOCK + warp;
     const SelState *st = p.st;
     const uint32_t T = (uint32_t)st->js[j].lo;
     const float m = st->redsync_mean[j];
     const bool redsync = p.kind == GVC_REDSYNC;
-    const size_t o = (size_t)j * GVC_SEG_MAX + seg;
-    const uint32_t take = p.seg_take[o];
-    uint32_t out = p.seg_off[o];
-    const uint64_t beg = (uint64_t)seg * p.seg_len;
-    const uint32_t cnt = p.seg_cnt[seg];
-    const uint32_t lt = lanemask_lt();
-    uint32_t ties_seen = 0;
+    const int nks = p.n_ks;
+    // per-segment counts of this block in lanes 0..7
+    uint32_t my_tie = 0, my_above = 0;
+    const uint32_t lseg = blk * GVC_WARPS_PER_BLOCK + lane;
+    if (lane < GVC_WARPS_PER_BLOCK && lseg < p.S) {
+        my_tie = p.seg_tie[(size_t)j * GVC_SEG_MAX + lseg];
+        for (int band = j; band < nks; band++)
+            my_above += p.seg_band[(size_t)band * GVC_SEG_MAX + lseg];
+    }
+    uint32_t tie_pre = my_tie;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, tie_pre, o);
+        if (lane >= o)
+            tie_pre += y;
+    }
+    tie_pre -= my_tie;
+    const uint32_t btake = p.blk_take[(size_t)j * GVC_BLK_MAX + blk];
+    const uint32_t my_take = tie_pre >= btake ? 0u : min(btake - tie_pre, my_tie);
+    const uint32_t my_sel = my_above + my_take;
+    uint32_t sel_pre = my_sel;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, sel_pre, o);
+        if (lane >= o)
+            sel_pre += y;
+    }
+    sel_pre -= my_sel;
+    const uint32_t take = __shfl_sync(0xffffffffu, my_take, warp);
+    uint32_t out = p.blk_off[(size_t)j * GVC_BLK_MAX + blk] + __shfl_sync(0xffffffffu, sel_pre, warp);
+
     double e2 = 0.0, ab = 0.0;
-    for (uint32_t base = 0; base < cnt; base += 32) {
-        uint32_t t = base + lane;
-        bool valid = t < cnt;
-        float v = 0.f;
-        uint32_t pos = 0, key = 0;
-        if (valid) {
-            v = p.cand_val[beg + t];
-            pos = p.cand_idx[beg + t];
-            key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, pos);
-        }
-        bool tie = valid && key == T;
-        uint32_t tb = __ballot_sync(0xffffffffu, tie);
-        bool sel = valid && (key > T || (tie && ties_seen + __popc(tb & lt) < take));
-        uint32_t sb = __ballot_sync(0xffffffffu, sel);
-        if (sel) {
-            uint32_t w = out + __popc(sb & lt);
-            float sv = v;
-            if (redsync) {
-                float sg = v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f);
-                sv = __fmul_rn(sg, m);
+    if (seg < p.S) {
+        const uint64_t beg = (uint64_t)seg * p.seg_len;
+        const uint32_t cnt = p.seg_cnt[seg];
+        const uint32_t lt = lanemask_lt();
+        uint32_t ties_seen = 0;
+        for (uint32_t t = lane * 4; t < cnt; t += 128) {
+            float v[4];
+            uint32_t pos[4], key[4];
+            bool ok[4];
+            load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, true);
+            bool tie[4];
+            uint32_t tb[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                tie[c] = ok[c] && key[c] == T;
+                tb[c] = __ballot_sync(0xffffffffu, tie[c]);
             }
-            uint32_t gi = idx_map ? idx_map[pos] : pos;
-            out_idx[w] = gi;
-            out_val[w] = sv;
-            if (resid) {
-                // level-1 emits: the candidate value IS g_ef; a second-level emit
-                // (idx_map) carries level-1 SENT values, so read g_ef back
-                float ef = idx_map ? resid[gi] : v;
-                resid[gi] = __fsub_rn(ef, sv);
+            uint32_t trank =
+                ties_seen + __popc(tb[0] & lt) + __popc(tb[1] & lt) + __popc(tb[2] & lt) + __popc(tb[3] & lt);
+            bool sel[4];
+            uint32_t sb[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                sel[c] = ok[c] && (key[c] > T || (tie[c] && trank < take));
+                trank += tie[c];
+                sb[c] = __ballot_sync(0xffffffffu, sel[c]);
             }
-            e2 += (double)sv * (double)sv;
-            ab += fabs((double)sv);
+            uint32_t w = out + __popc(sb[0] & lt) + __popc(sb[1] & lt) + __popc(sb[2] & lt) + __popc(sb[3] & lt);
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                if (sel[c]) {
+                    float sv = v[c];
+                    if (redsync) {
+                        float sg = v[c] > 0.f ? 1.f : (v[c] < 0.f ? -1.f : 0.f);
+                        sv = __fmul_rn(sg, m);
+                    }
+                    const uint32_t gi = idx_map ? idx_map[pos[c]] : pos[c];
+                    out_idx[w] = gi;
+                    out_val[w] = sv;
+                    if (resid) {
+                        // level-1 emits: the candidate value IS g_ef; a second-level
+                        // emit (idx_map) carries level-1 SENT values, so read g_ef back
+                        const float ef = idx_map ? resid[gi] : v[c];
+                        resid[gi] = __fsub_rn(ef, sv);
+                    }
+                    e2 += (double)sv * (double)sv;
+                    ab += fabs((double)sv);
+                    w++;
+                }
+            }
+            ties_seen += __popc(tb[0]) + __popc(tb[1]) + __popc(tb[2]) + __popc(tb[3]);
+            out += __popc(sb[0]) + __popc(sb[1]) + __popc(sb[2]) + __popc(sb[3]);
         }
-        ties_seen += __popc(tb);
-        out += __popc(sb);
     }
     e2 = warp_sum_f64(e2);
     ab = warp_sum_f64(ab);
     if (lane == 0) {
-        p.seg_emit[seg] = e2;
-        p.seg_emit[GVC_SEG_MAX + seg] = ab;
+        wst[warp][0] = e2;
+        wst[warp][1] = ab;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < GVC_WARPS_PER_BLOCK; w++) {
+            a += wst[w][0];
+            b += wst[w][1];
+        }
+        p.blk_emit[blk] = a;
+        p.blk_emit[GVC_BLK_MAX + blk] = b;
     }
 }
 
 __global__ void __launch_bounds__(1024) k_emit_finish(Plan p, double *stats)
 {
-    __shared__ double red[1024];
-    double e = block_sum_f64(p.seg_emit, p.S, red);
-    double a = block_sum_f64(p.seg_emit + GVC_SEG_MAX, p.S, red);
+    __shared__ double shd[33];
+    double a = 0.0, b = 0.0;
+    constexpr int PER = GVC_BLK_MAX / 1024;
+    for (int i = 0; i < PER; i++) {
+        uint32_t k = threadIdx.x * PER + i;
+        if (k < p.B) {
+            a += p.blk_emit[k];
+            b += p.blk_emit[GVC_BLK_MAX + k];
+        }
+    }
+    a = block_sum_f64(a, shd);
+    b = block_sum_f64(b, shd);
     if (threadIdx.x == 0) {
-        stats[0] = e;
-        stats[1] = a;
+        stats[0] = a;
+        stats[1] = b;
     }
 }
 
@@ -884,14 +980,12 @@ size_t select_workspace_bytes(int kind, uint64_t n)
     return carve(nullptr, nullptr, n);
 }
 
-static int nb_for(int n_ks)
-{
-    return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16;
-}
+static int nb_for(int n_ks) { return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16; }
 
 template <int KM>
-static void launch_final(const Plan &p, cudaStream_t s, int blocks)
+static void launch_final(const Plan &p, cudaStream_t s)
 {
+    const int blocks = (int)p.B;
     switch (nb_for(p.n_ks)) {
     case 1: k_final<KM, 1><<<blocks, GVC_THREADS, 0, s>>>(p); break;
     case 2: k_final<KM, 2><<<blocks, GVC_THREADS, 0, s>>>(p); break;
@@ -904,13 +998,18 @@ static void launch_final(const Plan &p, cudaStream_t s, int blocks)
 template <int KM>
 static void launch_pipeline(Plan &p, cudaStream_t s)
 {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
+        attr_done = true;
+    }
     ProfScope all(PROF_SELECT, s);
-    const int blocks = (int)((p.S + GVC_WARPS_PER_BLOCK - 1) / GVC_WARPS_PER_BLOCK);
+    const int blocks = (int)p.B;
     int launches = 0;
-    if (KM == KEY_MAG && !p.force_exact && p.s_target > 0) {
-        uint64_t wb = (p.s_chunks + GVC_WARPS_PER_BLOCK - 1) / GVC_WARPS_PER_BLOCK;
-        int sb = (int)(wb < 2048 ? (wb ? wb : 1) : 2048);
-        k_sample<<<sb, GVC_THREADS, 0, s>>>(p);
+    if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0) {
+        uint64_t wb = (p.s_chunks + 31) / 32;
+        int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
+        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p);
         launches++;
     }
     k_sample_resolve<<<1, 1024, 0, s>>>(p);
@@ -933,13 +1032,12 @@ static void launch_pipeline(Plan &p, cudaStream_t s)
         k_level_resolve<<<1, 1024, 0, s>>>(p);
         launches += 2;
     }
-    launch_final<KM>(p, s, blocks);
+    launch_final<KM>(p, s);
     k_finish<KM><<<1, 1024, 0, s>>>(p);
     count_launches(launches + 2);
 }
 
-int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
-               cudaStream_t s)
+int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res, cudaStream_t s)
 {
     Plan p;
     memset(&p, 0, sizeof(p));
@@ -971,11 +1069,8 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
         if (stride < 128)
             stride = 128;
         chunks = (n + stride - 1) / stride;
-        uint64_t sampled = 0;
-        {  // exact sample size: full chunks plus the clipped tail chunk
-            uint64_t last = (chunks - 1) * stride;
-            sampled = (chunks - 1) * 128 + (n - last < 128 ? n - last : 128);
-        }
+        const uint64_t last = (chunks - 1) * stride;
+        const uint64_t sampled = (chunks - 1) * 128 + (n - last < 128 ? n - last : 128);
         p.s_chunks = chunks;
         p.s_stride = stride;
         if (sampled >= n) {
@@ -1012,9 +1107,10 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     return GVC_OK;
 }
 
-int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx,
-             float *out_val, float *resid, double *stats, cudaStream_t s)
+int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
+             float *resid, double *stats, cudaStream_t s)
 {
+    (void)ws_bytes;
     Plan p;
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -1025,7 +1121,7 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
     }
     if (j < 0 || j >= p.n_ks)
         return set_error(GVC_ERR_ARG, "gvc_emit: ladder index %d out of range [0, %d)", j, p.n_ks);
-    const int blocks = (int)((p.S + GVC_WARPS_PER_BLOCK - 1) / GVC_WARPS_PER_BLOCK);
+    const int blocks = (int)p.B;
     ProfScope pe(PROF_EMIT, s);
     count_launches(stats ? 2 : 1);
     if (p.keymode == KEY_MAG)

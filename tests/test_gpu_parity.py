@@ -187,10 +187,12 @@ def test_topk_ladder_ef_vs_oracle(G, n, dist):
         res = sel.result()
         ef = O.ef_add(g_host, r_host)
         norm = O.sq_norm(ef)
-        assert res.ef_norm_sq == pytest.approx(norm, rel=1e-12)
+        # oracle sums sequentially (error ~n*eps); the GPU tree is closer to exact
+        assert res.ef_norm_sq == pytest.approx(norm, rel=1e-9)
+        assert res.fallback_used == 0
         for j, k in enumerate(ks):
             oi = O.topk_indices(ef, k)
-            assert res.kept_sq[j] == pytest.approx(O.sq_norm(ef[oi]), rel=1e-12)
+            assert res.kept_sq[j] == pytest.approx(O.sq_norm(ef[oi]), rel=1e-9)
         choose = it % 3
         idx, vals = sel.emit(choose, resid=r)
         oi = O.topk_indices(ef, ks[choose])
@@ -200,20 +202,28 @@ def test_topk_ladder_ef_vs_oracle(G, n, dist):
         assert np.array_equal(bits(host(r)), bits(r_host))
 
 
-def test_exact_path_equals_estimate_path(G):
+@pytest.mark.parametrize("kind", ["topk", "redsync", "randomk"])
+def test_exact_and_fallback_paths_equal_estimate_path(G, kind):
     from paper_2305_12201_b200.compressors import Selection
-    K = G.CompressorKind("topk")
-    x = torch.from_numpy(_vec("gauss", 3_000_000, 5)).cuda()
+    K = G.CompressorKind(kind)
+    x = torch.from_numpy(_vec("ties", 3_000_000, 5)).cuda()
     ks = [300_000, 30_000, 3_000]
-    a = Selection(K, ks, values=x, slot="x1")
-    b = Selection(K, ks, values=x, slot="x2", force_exact=True)
-    ra, rb = a.result(), b.result()
+    rng = G.SeededRng(4)
+    a = Selection(K, ks, values=x, slot="x1", rng=rng)
+    b = Selection(K, ks, values=x, slot="x2", rng=rng, force_exact=1)
+    c = Selection(K, ks, values=x, slot="x3", rng=rng, force_exact=2)
+    ra, rb, rc = a.result(), b.result(), c.result()
     assert rb.candidates == x.numel() and ra.candidates < x.numel() // 5
+    assert rc.fallback_used == 1 and rc.candidates == x.numel() and ra.fallback_used == 0
     for j in range(3):
-        assert ra.kept_sq[j] == rb.kept_sq[j]
+        assert ra.kept_sq[j] == rb.kept_sq[j] == rc.kept_sq[j]
         ia, va = a.emit(j)
         ib, vb = b.emit(j)
-        assert torch.equal(ia, ib) and torch.equal(va, vb)
+        ic, vc = c.emit(j)
+        assert torch.equal(ia, ib) and torch.equal(va, vb) and torch.equal(ia, ic) and torch.equal(va, vc)
+    oi, ov = O.select(kind, host(x), ks[0], seed=rng.seed, stream=rng.stream)
+    ia, va = a.emit(0)
+    assert np.array_equal(host(ia), oi)
 
 
 @pytest.mark.parametrize("n,cf", [(1000, 3.0), (65_536, 10.0), (1_000_000, 10.0), (4_000_037, 100.0)])
