@@ -513,7 +513,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_level_hist(Plan p)
         return;
     const uint64_t beg = (uint64_t)seg * p.seg_len;
     const uint32_t cnt = p.seg_cnt[seg];
-    for (uint32_t t = lane * 4; t < cnt; t += 128) {
+    for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
+            const uint32_t t = base + lane * 4;
         float v[4];
         uint32_t pos[4], key[4];
         bool ok[4];
@@ -593,7 +594,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
         const uint32_t cnt = p.seg_cnt[seg];
-        for (uint32_t t = lane * 4; t < cnt; t += 128) {
+        for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
+            const uint32_t t = base + lane * 4;
             float v[4];
             uint32_t pos[4], key[4];
             bool ok[4];
@@ -883,7 +885,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
         const uint32_t cnt = p.seg_cnt[seg];
         const uint32_t lt = lanemask_lt();
         uint32_t ties_seen = 0;
-        for (uint32_t t = lane * 4; t < cnt; t += 128) {
+        for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
+            const uint32_t t = base + lane * 4;
             float v[4];
             uint32_t pos[4], key[4];
             bool ok[4];
