@@ -85,7 +85,13 @@ typedef struct {
     double dgc_sample_fraction;   /* CompressorKind.dgc_sample_fraction (compressors.py:36) */
     int32_t force_exact;          /* 1: skip the threshold estimate (every value is a candidate);
                                      2: test hook, an estimate that misses (exercises the exact re-scan) */
-    int32_t reserved;
+    int32_t pending_mode;         /* deferred residual update of the previous step, see below   */
+    uint32_t *pending_mask_dev;   /* EF mode: bit i set = resid[i] still holds g_ef of a SENT   */
+    const float *pending_m_dev;   /*   position; the true residual is fl32(r - f(r)) with
+                                     f(r) = r (pending_mode 1: Top-k / Random-k / DGC) or
+                                     f(r) = sign(r) * m (mode 2, Redsync, m = *pending_m_dev).
+                                     The collect pass applies it while streaming r and clears
+                                     the consumed mask words (feedback.py:39-51, deferred). */
 } gvc_select_args;
 
 GVC_API const char *gvc_last_error(void);
@@ -112,11 +118,22 @@ GVC_API int gvc_select(const gvc_select_args *args, void *ws_dev, size_t ws_byte
  *   resid_dev:   optional; resid[index] = fl32(value - sent_value) at every sent
  *                position, i.e. update_residual (feedback.py:39-51) given that
  *                resid_dev holds g_ef;
+ *   sent_mask_dev: optional (instead of resid_dev); sets bit `index` for every sent
+ *                position -- the deferred form the next gvc_select applies;
+ *   sent_m_dev:  optional; receives the Redsync mean m of this entry (device float);
  *   sent_stats_dev: optional double[2] = {sum sent^2, sum |sent|} (fp64, fixed order).
  * Replaces compressors._select's sort+gather (compressors.py:185-190). */
 GVC_API int gvc_emit(void *ws_dev, size_t ws_bytes, int j, const uint32_t *idx_map_dev,
              uint32_t *out_idx_dev, float *out_val_dev, float *resid_dev,
-             double *sent_stats_dev, void *stream);
+             uint32_t *sent_mask_dev, float *sent_m_dev, double *sent_stats_dev, void *stream);
+
+/* Mark k sent positions in a deferred-residual mask (bit idx[i] of mask). */
+GVC_API int gvc_mark_sent(const uint32_t *idx_dev, uint64_t k, uint32_t *mask_dev, void *stream);
+
+/* Materialise a deferred residual update in place: resid[i] = fl32(r - f(r))
+ * wherever the mask bit is set (mode/m as in gvc_select_args), then clear the mask. */
+GVC_API int gvc_apply_pending(float *resid_dev, uint32_t *mask_dev, uint64_t n, int mode,
+                              const float *m_dev, void *stream);
 
 /* out = fl32(g + r) (feedback.py:32-36, non-mutating form). */
 GVC_API int gvc_ef_add(const float *g_dev, const float *r_dev, float *out_dev, uint64_t n, void *stream);

@@ -26,7 +26,7 @@ EXPORTS = (
     "gvc_last_error", "gvc_abi_version", "gvc_select_workspace_bytes", "gvc_select", "gvc_emit",
     "gvc_ef_add", "gvc_sq_norm_workspace_bytes", "gvc_sq_norm", "gvc_update_residual",
     "gvc_decompress", "gvc_aggregate", "gvc_aggregate_workspace_bytes", "gvc_aggregate_dense",
-    "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count",
+    "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
 )
 
 _u64, _i32, _f64, _vp, _sz = ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
@@ -39,7 +39,8 @@ class SelectArgs(ctypes.Structure):
         ("ks", _u64 * MAX_LADDER),
         ("seed", _u64), ("rng_stream", _u64), ("pos_base", _u64),
         ("dgc_sample_fraction", _f64),
-        ("force_exact", _i32), ("reserved", _i32),
+        ("force_exact", _i32), ("pending_mode", _i32),
+        ("pending_mask_dev", _vp), ("pending_m_dev", _vp),
     ]
 
 
@@ -88,7 +89,9 @@ def load(build_if_missing: bool = False):
         L.gvc_select_workspace_bytes.argtypes = [ctypes.c_int, _u64]
         L.gvc_select_workspace_bytes.restype = _sz
         L.gvc_select.argtypes = [ctypes.POINTER(SelectArgs), _vp, _sz, _vp, _vp]
-        L.gvc_emit.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.gvc_emit.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.gvc_mark_sent.argtypes = [_vp, _u64, _vp, _vp]
+        L.gvc_apply_pending.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp, _vp]
         L.gvc_ef_add.argtypes = [_vp, _vp, _vp, _u64, _vp]
         L.gvc_sq_norm_workspace_bytes.argtypes = [_u64]
         L.gvc_sq_norm_workspace_bytes.restype = _sz

@@ -124,7 +124,7 @@ class Selection:
     def __init__(self, kind: CompressorKind, ks: Sequence[int], *, values: torch.Tensor | None = None,
                  g: torch.Tensor | None = None, resid: torch.Tensor | None = None,
                  rng: SeededRng | None = None, pos_base: int = 0, slot: str = "sel0",
-                 force_exact: int = 0):
+                 force_exact: int = 0, pending=None):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -148,18 +148,25 @@ class Selection:
         a.pos_base = pos_base
         a.dgc_sample_fraction = kind.dgc_sample_fraction
         a.force_exact = int(force_exact)
+        if pending is not None:  # (mask, m, mode): deferred residual update of the previous step
+            a.pending_mask_dev = pending[0].data_ptr()
+            a.pending_m_dev = pending[1].data_ptr()
+            a.pending_mode = int(pending[2])
         nat.check(lib.gvc_select(ctypes.byref(a), nat.ptr(self.ws), self.ws.numel(), nat.ptr(self.res_dev),
                                  nat.stream_ptr(self.device)), "gvc_select")
         self._result = None
 
     def emit(self, j: int = 0, idx_map: torch.Tensor | None = None, resid: torch.Tensor | None = None,
-             stats: torch.Tensor | None = None):
+             stats: torch.Tensor | None = None, sent_mask: torch.Tensor | None = None,
+             sent_m: torch.Tensor | None = None):
+        """Index-ascending (indices, values) of ladder entry j; optionally the
+        residual update, either direct (``resid``) or deferred (``sent_mask``)."""
         k = self.ks[j]
         out_idx = torch.empty(k, dtype=torch.uint32, device=self.device)
         out_val = torch.empty(k, dtype=torch.float32, device=self.device)
         nat.check(nat.load().gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
-                                      nat.ptr(out_val), nat.ptr(resid), nat.ptr(stats),
-                                      nat.stream_ptr(self.device)), "gvc_emit")
+                                      nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
+                                      nat.ptr(stats), nat.stream_ptr(self.device)), "gvc_emit")
         return out_idx, out_val
 
     def result(self) -> nat.SelectResult:

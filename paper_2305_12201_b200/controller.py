@@ -174,9 +174,16 @@ class IterationResult:
 class _WorkerStep:
     """Device-side work of one worker for one iteration (level 1 + level 2)."""
 
-    def __init__(self, kind: CompressorKind, g: torch.Tensor, resid: torch.Tensor, k1: int, k2: int,
+    def __init__(self, kind: CompressorKind, g: torch.Tensor, store: ResidualStore, k1: int, k2: int,
                  extra_ks: Sequence[int], rng: SeededRng, i: int, w: int):
         self.kind, self.k1, self.k2 = kind, k1, k2
+        self.store = store
+        if k1 >= g.numel():
+            resid = store.residual  # materialise any deferred update first
+            pending = None
+        else:
+            pending = store._take_pending()
+            resid = store._resid
         self.resid = resid
         self.n = g.numel()
         self.g_min: SparseGradient | None = None
@@ -203,10 +210,11 @@ class _WorkerStep:
         if kind.name == TOPK:
             # F2: nested Top-k == exact top-k2 of the whole vector -> one sweep
             self.ladder = [k1, k2] + list(extra_ks)
-            self.sel1 = Selection(kind, self.ladder, g=g, resid=resid, rng=rng0, slot=slot + "a")
+            self.sel1 = Selection(kind, self.ladder, g=g, resid=resid, rng=rng0, slot=slot + "a",
+                                  pending=pending)
         else:
             self.ladder = [k1]
-            self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a")
+            self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a", pending=pending)
             idx, vals = self.sel1.emit(0)
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
             if k2 < k1:
@@ -250,20 +258,38 @@ class _WorkerStep:
         return norm, e_min, e_c, []
 
     def emit(self, candidate: bool) -> SparseGradient:
-        """Materialise the chosen view and leave g_ef - sent in the residual."""
+        """Materialise the chosen view; the residual update g_ef - sent is
+        deferred into the store's sent-mask (applied by the next fused pass)."""
         lib = nat.load()
-        if self.kind.name == TOPK and not self.identity1:
+        store = self.store
+        mode = 2 if self.kind.name == "redsync" else 1
+        if self.identity1:
+            # theta_min == 1 (level 1 keeps everything): direct update, no mask
+            if candidate and self.sel2 is not None:
+                idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, resid=self.resid)
+                return SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
+            part = self.g_min
+            nat.check(lib.gvc_update_residual(nat.ptr(self.resid), nat.ptr(part.indices), nat.ptr(part.vals),
+                                              part.kept, self.n, nat.ptr(self.resid),
+                                              nat.stream_ptr(self.resid.device)), "update_residual")
+            return part
+        mask = store._mask_buf()
+        if self.kind.name == TOPK:
             j = 1 if candidate else 0
             k = self.ladder[j]
-            idx, vals = self.sel1.emit(j, resid=self.resid)
-            return SparseGradient._wrap(idx, vals, self.n, self.n / k)
-        if candidate and self.sel2 is not None:
-            idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, resid=self.resid)
-            return SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
-        part = self.g_min
-        nat.check(lib.gvc_update_residual(nat.ptr(self.resid), nat.ptr(part.indices), nat.ptr(part.vals),
-                                          part.kept, self.n, nat.ptr(self.resid),
-                                          nat.stream_ptr(self.resid.device)), "update_residual")
+            idx, vals = self.sel1.emit(j, sent_mask=mask, sent_m=store._pm)
+            part = SparseGradient._wrap(idx, vals, self.n, self.n / k)
+        elif candidate and self.sel2 is not None:
+            idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, sent_mask=mask, sent_m=store._pm)
+            part = SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
+        else:
+            part = self.g_min
+            nat.check(lib.gvc_mark_sent(nat.ptr(part.indices), part.kept, nat.ptr(mask),
+                                        nat.stream_ptr(self.resid.device)), "mark_sent")
+            if mode == 2:  # the level-1 Redsync mean, straight from the device result
+                off = nat.SelectResult.redsync_mean.offset
+                store._pm.copy_(self.sel1.res_dev[off:off + 4].view(torch.float32))
+        store._pmode = mode
         return part
 
 
@@ -320,7 +346,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         if g.length != store.length:
             raise ValueError(f"length mismatch: gradient {g.length}, residual {store.length}")
         nat.require_cuda(g.values)
-        steps.append(_WorkerStep(kind, g.values, store.residual, k1, k2, extra_ks, rng, i, rank + w))
+        steps.append(_WorkerStep(kind, g.values, store, k1, k2, extra_ks, rng, i, rank + w))
 
     # ---- one device->host read per iteration: every worker's norms and energies
     norm_host = None
@@ -344,8 +370,8 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         # vanished gradient: dense no-op (controller.py:217-230)
         sent = []
         for store in stores:
-            sent.append(GradientVector._wrap(store.residual, grads[0].layer_offsets))
-            store.residual = torch.zeros_like(store.residual)
+            sent.append(GradientVector._wrap(store._resid, grads[0].layer_offsets))
+            store._resid = torch.zeros_like(store._resid)
         t_sync = allreduce_time(dense_message_words(length), cost)
         decision = CfDecision(DENSE, 1.0, 1.0, 1.0, 1.0)
         t_iter = iteration_time(decision, cost.t_compute, 0.0, t_sync)
@@ -371,9 +397,10 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     if decision.choice == DENSE:
         sent = []
         for store in stores:
-            # the residual buffer holds g_ef: hand it over as the dense message
-            sent.append(GradientVector._wrap(store.residual, grads[0].layer_offsets))
-            store.residual = torch.zeros_like(store.residual)
+            # the residual buffer holds g_ef (the pending mask was consumed by the
+            # fused pass): hand it over as the dense message, restart from zero
+            sent.append(GradientVector._wrap(store._resid, grads[0].layer_offsets))
+            store._resid = torch.zeros_like(store._resid)
         floats = length
         words = dense_message_words(length)
     else:

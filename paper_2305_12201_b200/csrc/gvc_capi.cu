@@ -137,6 +137,9 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             return set_error(GVC_ERR_ARG, "keep counts must be non-increasing");
     }
     const bool ef = a->g_dev != nullptr;
+    if (a->pending_mask_dev && (!ef || a->pending_mode < 1 || a->pending_mode > 2 ||
+                                (a->pending_mode == 2 && !a->pending_m_dev)))
+        return set_error(GVC_ERR_ARG, "gvc_select: pending mask needs EF mode and mode 1 or 2 (+m)");
     if (ef ? (a->resid_dev == nullptr) : (a->values_dev == nullptr))
         return set_error(GVC_ERR_ARG, "gvc_select: need values_dev, or g_dev and resid_dev");
     const void *src = ef ? (const void *)a->g_dev : (const void *)a->values_dev;
@@ -146,11 +149,29 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
 }
 
 int gvc_emit(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
-             float *resid, double *stats, void *stream)
+             float *resid, uint32_t *sent_mask, float *sent_m, double *stats, void *stream)
 {
     if (!ws || !out_idx || !out_val)
         return set_error(GVC_ERR_ARG, "gvc_emit: null argument");
-    return emit_run(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, stats, STREAM(stream));
+    if (resid && sent_mask)
+        return set_error(GVC_ERR_ARG, "gvc_emit: pass resid_dev or sent_mask_dev, not both");
+    return emit_run(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, sent_mask, sent_m, stats, STREAM(stream));
+}
+
+int gvc_mark_sent(const uint32_t *idx, uint64_t k, uint32_t *mask, void *stream)
+{
+    if ((k && !idx) || !mask)
+        return set_error(GVC_ERR_ARG, "gvc_mark_sent: bad arguments");
+    int rc = mark_sent_run(idx, k, mask, STREAM(stream));
+    return rc ? rc : check_launch("mark_sent");
+}
+
+int gvc_apply_pending(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m, void *stream)
+{
+    if (!resid || !mask || n < 1 || mode < 1 || mode > 2 || (mode == 2 && !m))
+        return set_error(GVC_ERR_ARG, "gvc_apply_pending: bad arguments");
+    int rc = apply_pending_run(resid, mask, n, mode, m, STREAM(stream));
+    return rc ? rc : check_launch("apply_pending");
 }
 
 int gvc_ef_add(const float *g, const float *r, float *out, uint64_t n, void *stream)

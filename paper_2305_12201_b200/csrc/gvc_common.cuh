@@ -11,7 +11,8 @@
 // Segments: the input is cut into S contiguous ranges, one per warp of the
 // collect kernel.  S depends only on n (never on the device), so every
 // reduction order is a function of the input size alone.
-#define GVC_SEG_TARGET 9472  // 148 SMs x 8 blocks x 8 warps
+#define GVC_COLLECT_BLOCKS_PER_SM 6
+#define GVC_SEG_TARGET 7104  // 148 SMs x 6 resident blocks x 8 warps: the collect grid is one full wave
 #define GVC_SEG_MAX 16384
 #define GVC_SEG_QUANTUM 512  // elements per warp iteration: 32 lanes x 4 float4
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)
@@ -132,6 +133,17 @@ __device__ __forceinline__ double block_sum_f64(double v, double *sh)
     double r = sh[32];
     __syncthreads();
     return r;
+}
+
+// Deferred residual (gvc_select_args.pending_*): the true residual of a sent
+// position whose buffer still holds g_ef.
+__device__ __forceinline__ float pending_resid(float r, int mode, float m)
+{
+    if (mode == 2) {
+        const float sg = r > 0.f ? 1.f : (r < 0.f ? -1.f : 0.f);
+        return __fsub_rn(r, __fmul_rn(sg, m));
+    }
+    return __fsub_rn(r, r);
 }
 
 // Streaming loads / stores: the gradient and residual are touched once per

@@ -129,6 +129,60 @@ int update_residual_run(const float *ef, const uint32_t *idx, const float *vals,
     return GVC_OK;
 }
 
+// ---------------------------------------------- deferred residual masks
+__global__ void k_mark_sent(const uint32_t *__restrict__ idx, uint64_t k, uint32_t *mask)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    // grid-stride in whole warps so the per-word OR can use warp collectives
+    for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; base < k; base += stride) {
+        const uint64_t i = base + lane;
+        const bool ok = i < k;
+        const uint32_t gi = ok ? idx[i] : 0xffffffffu;
+        const uint32_t word = gi >> 5;
+        const uint32_t grp = __match_any_sync(0xffffffffu, word);
+        const uint32_t bits = __reduce_or_sync(grp, ok ? (1u << (gi & 31)) : 0u);
+        if (ok && (__ffs(grp) - 1) == lane)
+            atomicOr(&mask[word], bits);
+    }
+}
+
+int mark_sent_run(const uint32_t *idx, uint64_t k, uint32_t *mask, cudaStream_t s)
+{
+    if (k) {
+        count_launches(1);
+        k_mark_sent<<<grid_for(k, 256, 148 * 16), 256, 0, s>>>(idx, k, mask);
+    }
+    return GVC_OK;
+}
+
+__global__ void k_apply_pending(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m_ptr)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const float m = (mode == 2 && m_ptr) ? *m_ptr : 0.f;
+    const uint64_t nw = (n + 31) / 32;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
+        uint32_t bits = mask[w];
+        if (!bits)
+            continue;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const uint64_t i = w * 32 + b;
+            if (i < n)
+                resid[i] = pending_resid(resid[i], mode, m);
+        }
+        mask[w] = 0u;
+    }
+}
+
+int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m, cudaStream_t s)
+{
+    count_launches(1);
+    k_apply_pending<<<grid_for((n + 31) / 32, 256, 148 * 16), 256, 0, s>>>(resid, mask, n, mode, m);
+    return GVC_OK;
+}
+
 // ------------------------------------------------- tiled decompress/average
 // One CTA owns a TILE-value slice of the dense output.  For every part (in
 // worker order) it binary-searches the slice's sub-range of that part's
@@ -165,23 +219,26 @@ __global__ void k_tile_bounds(const uint32_t *__restrict__ idx, AggParts parts, 
     }
 }
 
-template <bool AVG>
+// MODE 0: decompress (fp32 assignment, -0.0 kept); 1: mean of ONE part
+// (0.0 + v in fp64 then /1: v, except -0.0 -> +0.0); 2: fp64 mean of N parts.
+template <int MODE>
 __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__restrict__ idx,
                                                             const float *__restrict__ vals, AggParts parts,
                                                             int nparts, uint64_t n, uint64_t ntiles,
                                                             const uint32_t *__restrict__ bounds,
                                                             float *__restrict__ out)
 {
-    __shared__ double acc[AVG ? AGG_TILE : 1];
-    __shared__ float accf[AVG ? 1 : AGG_TILE];
-    const uint64_t tile = blockIdx.x;
-    const uint64_t lo = tile * AGG_TILE;
-    const uint64_t hi = min(n, lo + AGG_TILE);
-    for (int i = threadIdx.x; i < AGG_TILE; i += AGG_THREADS) {
-        if (AVG)
-            acc[i] = 0.0;
-        else
-            accf[i] = 0.0f;
+    __shared__ __align__(16) double acc[MODE == 2 ? AGG_TILE : 2];
+    __shared__ __align__(16) float accf[MODE == 2 ? 4 : AGG_TILE];
+    const uint32_t tile = blockIdx.x;
+    const uint64_t lo = (uint64_t)tile * AGG_TILE;
+    const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
+    if (MODE == 2) {
+        for (int i = threadIdx.x; i < AGG_TILE / 2; i += AGG_THREADS)
+            reinterpret_cast<double2 *>(acc)[i] = make_double2(0.0, 0.0);
+    } else {
+        for (int i = threadIdx.x; i < AGG_TILE / 4; i += AGG_THREADS)
+            reinterpret_cast<float4 *>(accf)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
     for (int p = 0; p < nparts; p++) {
@@ -190,15 +247,21 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
         const uint32_t *bp = bounds + (uint64_t)p * (ntiles + 1);
         const uint32_t a = bp[tile], b = bp[tile + 1];
         for (uint32_t t = a + threadIdx.x; t < b; t += AGG_THREADS) {
-            uint32_t r = pi[t] - (uint32_t)lo;
-            if (AVG)
-                acc[r] += (double)pv[t];
+            const uint32_t r = pi[t] - (uint32_t)lo;
+            const float v = pv[t];
+            if (MODE == 2)
+                acc[r] += (double)v;
+            else if (MODE == 1)
+                accf[r] = v == 0.0f ? 0.0f : v;
             else
-                accf[r] = pv[t];
+                accf[r] = v;
         }
-        __syncthreads();  // worker order per position (compressors.py:266-269)
+        if (MODE == 2)
+            __syncthreads();  // worker order per position (compressors.py:266-269)
     }
-    // x / N is exact-equivalent to x * (1/N) only for power-of-two N; zeros skip the divide
+    if (MODE != 2)
+        __syncthreads();
+    // x / N == x * (1/N) exactly only for power-of-two N; zeros skip the divide
     const double np = (double)nparts;
     const bool pow2 = (nparts & (nparts - 1)) == 0;
     const double inv = 1.0 / np;
@@ -207,22 +270,21 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
             return 0.0f;
         return (float)(pow2 ? a * inv : a / np);
     };
-    if (hi - lo == AGG_TILE && (((uintptr_t)(out + lo)) & 15) == 0) {
+    if (width == AGG_TILE && (((uintptr_t)(out + lo)) & 15) == 0) {
         for (int i = threadIdx.x; i < AGG_TILE / 4; i += AGG_THREADS) {
             float4 v;
-            if (AVG) {
-                v.x = mean(acc[4 * i + 0]);
-                v.y = mean(acc[4 * i + 1]);
-                v.z = mean(acc[4 * i + 2]);
-                v.w = mean(acc[4 * i + 3]);
+            if (MODE == 2) {
+                const double2 d0 = reinterpret_cast<const double2 *>(acc)[2 * i];
+                const double2 d1 = reinterpret_cast<const double2 *>(acc)[2 * i + 1];
+                v = make_float4(mean(d0.x), mean(d0.y), mean(d1.x), mean(d1.y));
             } else {
-                v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+                v = reinterpret_cast<const float4 *>(accf)[i];
             }
             st_stream(reinterpret_cast<float4 *>(out + lo) + i, v);
         }
     } else {
-        for (uint64_t i = lo + threadIdx.x; i < hi; i += AGG_THREADS)
-            out[i] = AVG ? mean(acc[i - lo]) : accf[i - lo];
+        for (uint32_t i = threadIdx.x; i < width; i += AGG_THREADS)
+            out[lo + i] = MODE == 2 ? mean(acc[i]) : accf[i];
     }
 }
 
@@ -246,12 +308,13 @@ static int tile_merge_run(bool avg, const uint32_t *idx, const float *vals, cons
     ProfScope pa(PROF_AGGREGATE, s);
     count_launches(2);
     k_tile_bounds<<<bg, 256, 0, s>>>(idx, P, nparts, ntiles, (uint32_t *)ws);
-    if (avg)
-        k_tile_merge<true><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles,
-                                                                    (const uint32_t *)ws, out);
+    const uint32_t *bd = (const uint32_t *)ws;
+    if (!avg)
+        k_tile_merge<0><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, out);
+    else if (nparts == 1)
+        k_tile_merge<1><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, out);
     else
-        k_tile_merge<false><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles,
-                                                                     (const uint32_t *)ws, out);
+        k_tile_merge<2><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, out);
     return GVC_OK;
 }
 

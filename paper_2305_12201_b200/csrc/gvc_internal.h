@@ -26,7 +26,9 @@ size_t select_workspace_bytes(int kind, uint64_t n);
 int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
                cudaStream_t s);
 int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx,
-             float *out_val, float *resid, double *stats, cudaStream_t s);
+             float *out_val, float *resid, uint32_t *sent_mask, float *sent_m, double *stats, cudaStream_t s);
+int mark_sent_run(const uint32_t *idx, uint64_t k, uint32_t *mask, cudaStream_t s);
+int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m, cudaStream_t s);
 
 size_t sq_norm_workspace_bytes(uint64_t n);
 int sq_norm_run(const float *x, uint64_t n, double *out, void *ws, size_t ws_bytes, cudaStream_t s);

@@ -66,6 +66,10 @@ struct Plan {
     float *resid;
     uint64_t seed, stream, pos_base;
     uint64_t ks[GVC_MAX_LADDER];
+    // deferred residual update of the previous step (EF mode)
+    uint32_t *pmask;
+    const float *pm;
+    int pmode;
     // sample
     uint64_t s_chunks, s_stride, s_target;
     uint32_t hash_key_est;
@@ -182,6 +186,7 @@ __global__ void __launch_bounds__(1024) k_sample(Plan p)
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * 32;
+    const float pm = (p.pmask && p.pmode == 2) ? *p.pm : 0.f;
     uint32_t kmax = 0;
     for (uint64_t c = blockIdx.x * 32 + (threadIdx.x >> 5); c < p.s_chunks; c += warps) {
         const uint64_t base = c * p.s_stride;
@@ -191,7 +196,18 @@ __global__ void __launch_bounds__(1024) k_sample(Plan p)
         for (int q = 0; q < 4; q++) {
             uint64_t i = base + (uint64_t)q * 32 + lane;
             ok[q] = i < p.n && i < base + 128;
-            v[q] = ok[q] ? (p.ef ? __fadd_rn(p.g[i], p.resid[i]) : p.values[i]) : 0.f;
+            if (ok[q]) {
+                if (p.ef) {
+                    float r = p.resid[i];
+                    if (p.pmask && ((p.pmask[i >> 5] >> (i & 31)) & 1u))
+                        r = pending_resid(r, p.pmode, pm);
+                    v[q] = __fadd_rn(p.g[i], r);
+                } else {
+                    v[q] = p.values[i];
+                }
+            } else {
+                v[q] = 0.f;
+            }
         }
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -324,7 +340,7 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // full-size write of the step); !EF: v read from `values`.  REFILL re-collects
 // from the already-written g_ef with key_est = 0 (exactness fallback).
 template <int KM, bool EF>
-__global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
+__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS_PER_SM) k_collect(Plan p, int refill)
 {
     __shared__ uint32_t h[GVC_H0_BINS];
     __shared__ double red[GVC_WARPS_PER_BLOCK];
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
     const int shift0 = refill ? (KM == KEY_MAG ? 19 : 20) : p.st->shift0;
     const bool do_ef = EF && !refill;
     const float *src = (EF ? (refill ? p.resid : p.g) : p.values);
+    const float pm = (do_ef && p.pmask && p.pmode == 2) ? *p.pm : 0.f;
     double nacc = 0.0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
@@ -356,6 +373,24 @@ __global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
 #pragma unroll
                 for (int u = 0; u < 4; u++)
                     b[u] = ld_stream(reinterpret_cast<const float4 *>(p.resid + i + u * 128) + lane);
+                if (p.pmask) {
+                    // deferred update of the previous step: 4 bits of one mask word per lane;
+                    // the first lane of each word clears it after use
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint64_t pos = i + u * 128 + lane * 4;
+                        const uint32_t w = p.pmask[pos >> 5];
+                        const uint32_t bits = (w >> (pos & 31)) & 0xfu;
+                        if (bits) {
+                            if (bits & 1u) b[u].x = pending_resid(b[u].x, p.pmode, pm);
+                            if (bits & 2u) b[u].y = pending_resid(b[u].y, p.pmode, pm);
+                            if (bits & 4u) b[u].z = pending_resid(b[u].z, p.pmode, pm);
+                            if (bits & 8u) b[u].w = pending_resid(b[u].w, p.pmode, pm);
+                        }
+                        if ((lane & 7) == 0 && w)
+                            p.pmask[pos >> 5] = 0u;
+                    }
+                }
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     a[u].x = __fadd_rn(a[u].x, b[u].x);
@@ -385,7 +420,15 @@ __global__ void __launch_bounds__(GVC_THREADS) k_collect(Plan p, int refill)
             if (valid) {
                 float x = src[t];
                 if (do_ef) {
-                    x = __fadd_rn(x, p.resid[t]);
+                    float r = p.resid[t];
+                    if (p.pmask) {
+                        const uint32_t bit = 1u << (t & 31);
+                        if (p.pmask[t >> 5] & bit) {
+                            r = pending_resid(r, p.pmode, pm);
+                            atomicAnd(&p.pmask[t >> 5], ~bit);
+                        }
+                    }
+                    x = __fadd_rn(x, r);
                     p.resid[t] = x;
                 }
                 v[0] = x;
@@ -567,8 +610,8 @@ __global__ void __launch_bounds__(1024) k_level_resolve(Plan p)
 // ladder entry (for the emit offsets); per block of 8 segments: band and tie
 // energies.  fp64 sums are per-lane sequential, a fixed xor tree per warp and
 // warps added in order: bit-reproducible.
-template <int KM, int NB>
-__global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
+template <int KM, int NB, bool ABS>
+__global__ void __launch_bounds__(GVC_THREADS, 4) k_final(Plan p)
 {
     __shared__ uint32_t Ts[GVC_MAX_LADDER];
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
@@ -583,7 +626,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
     uint32_t T[NB];
 #pragma unroll
     for (int j = 0; j < NB; j++)
-        T[j] = Ts[j];
+        T[j] = Ts[j];  // 0xffffffff beyond n_ks: never below a key, never equal to a valid one
     uint32_t bc[NB], tc[NB];
     double be[NB], ba[NB], te[NB], ta[NB];
 #pragma unroll
@@ -602,25 +645,25 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
             load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                if (!ok[c])
-                    continue;
-                const double v2 = (double)v[c] * (double)v[c];
-                const double av = fabs((double)v[c]);
+                // branch-free: selects feed the adds (x + 0.0 == x for these
+                // non-negative sums, and no 0 * inf NaN can arise)
+                const double v2 = ok[c] ? (double)v[c] * (double)v[c] : 0.0;
+                const double av = ok[c] ? fabs((double)v[c]) : 0.0;
                 int band = 0;
 #pragma unroll
                 for (int j = 0; j < NB; j++)
-                    band += (j < nks && T[j] < key[c]);
+                    band += (ok[c] && j < nks && T[j] < key[c]);
 #pragma unroll
                 for (int j = 0; j < NB; j++) {
-                    if (band == j + 1) {
-                        bc[j]++;
-                        be[j] += v2;
-                        ba[j] += av;
-                    }
-                    if (j < nks && key[c] == T[j]) {
-                        tc[j]++;
-                        te[j] += v2;
-                        ta[j] += av;
+                    const bool inb = band == j + 1;
+                    const bool tie = ok[c] && j < nks && key[c] == T[j];
+                    bc[j] += inb;
+                    tc[j] += tie;
+                    be[j] += inb ? v2 : 0.0;
+                    te[j] += tie ? v2 : 0.0;
+                    if (ABS) {
+                        ba[j] += inb ? av : 0.0;
+                        ta[j] += tie ? av : 0.0;
                     }
                 }
             }
@@ -951,7 +994,7 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
 // counts (lanes 0..7), then an ordered 4-wide compaction.
 template <int KM>
 __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
-                                                      float *out_val, float *resid)
+                                                      float *out_val, float *resid, uint32_t *smask, float *sm_out)
 {
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -992,6 +1035,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
     const uint32_t take = __shfl_sync(0xffffffffu, my_take, warp);
     uint32_t out = p.blk_off[(size_t)j * GVC_BLK_MAX + blk] + __shfl_sync(0xffffffffu, sel_pre, warp);
 
+    if (sm_out && blk == 0 && threadIdx.x == 0)
+        *sm_out = m;
     double e2 = 0.0, ab = 0.0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
@@ -1020,6 +1065,16 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                 const uint32_t tb = __ballot_sync(0xffffffffu, tie);
                 const bool sel = ok[c] && (key[c] > T || (tie && ties_seen + __popc(tb & lt) < take));
                 const uint32_t sb = __ballot_sync(0xffffffffu, sel);
+                if (smask) {
+                    // deferred residual: OR this sub-group's sent bits into the mask, one
+                    // atomic per distinct word (sent indices ascend across the lanes)
+                    const uint32_t gi = sel ? (idx_map ? idx_map[pos[c]] : pos[c]) : 0xffffffffu;
+                    const uint32_t word = gi >> 5;
+                    const uint32_t grp = __match_any_sync(0xffffffffu, word);
+                    const uint32_t bits = __reduce_or_sync(grp, sel ? (1u << (gi & 31)) : 0u);
+                    if (sel && (__ffs(grp) - 1) == lane)
+                        atomicOr(&smask[word], bits);
+                }
                 if (sel) {
                     float sv = v[c];
                     if (redsync) {
@@ -1094,17 +1149,27 @@ size_t select_workspace_bytes(int kind, uint64_t n)
 
 static int nb_for(int n_ks) { return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16; }
 
-template <int KM>
-static void launch_final(const Plan &p, cudaStream_t s)
+template <int KM, bool ABS>
+static void launch_final_abs(const Plan &p, cudaStream_t s)
 {
     const int blocks = (int)p.B;
     switch (nb_for(p.n_ks)) {
-    case 1: k_final<KM, 1><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    case 2: k_final<KM, 2><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    case 4: k_final<KM, 4><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    case 8: k_final<KM, 8><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    default: k_final<KM, 16><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+    case 1: k_final<KM, 1, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+    case 2: k_final<KM, 2, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+    case 4: k_final<KM, 4, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+    case 8: k_final<KM, 8, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+    default: k_final<KM, 16, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
     }
+}
+
+// |v| sums are only consumed by Redsync's mean (compressors.py:188)
+template <int KM>
+static void launch_final(const Plan &p, cudaStream_t s)
+{
+    if (p.kind == GVC_REDSYNC)
+        launch_final_abs<KM, true>(p, s);
+    else
+        launch_final_abs<KM, false>(p, s);
 }
 
 template <int KM>
@@ -1174,6 +1239,9 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.seed = a->seed;
     p.stream = a->rng_stream;
     p.pos_base = a->pos_base;
+    p.pmask = p.ef ? a->pending_mask_dev : nullptr;
+    p.pm = a->pending_m_dev;
+    p.pmode = a->pending_mode;
     for (int j = 0; j < a->n_ks; j++)
         p.ks[j] = a->ks[j];
     p.res = res;
@@ -1226,7 +1294,7 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
 }
 
 int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
-             float *resid, double *stats, cudaStream_t s)
+             float *resid, uint32_t *smask, float *sm_out, double *stats, cudaStream_t s)
 {
     (void)ws_bytes;
     Plan p;
@@ -1243,9 +1311,9 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
     ProfScope pe(PROF_EMIT, s);
     count_launches(stats ? 2 : 1);
     if (p.keymode == KEY_MAG)
-        k_emit<KEY_MAG><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid);
+        k_emit<KEY_MAG><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask, sm_out);
     else
-        k_emit<KEY_HASH><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid);
+        k_emit<KEY_HASH><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask, sm_out);
     if (stats)
         k_emit_finish<<<1, 1024, 0, s>>>(p, stats);
     cudaError_t e = cudaGetLastError();

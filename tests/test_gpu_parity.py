@@ -306,3 +306,52 @@ def test_determinism(G):
         r = sel.result()
         outs.append((r.ef_norm_sq, r.kept_sq[0], r.kept_sq[1], host(sel.emit(0)[0]).tobytes()))
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("kind", ["topk", "redsync", "randomk"])
+@pytest.mark.parametrize("workers", [1, 2])
+def test_run_iteration_vs_oracle(G, kind, workers):
+    """Fused step (deferred residual mask included) vs an oracle replay of
+    controller.py:192-281's data plane, every kind, 8 chained iterations."""
+    n = 300_007
+    cfg = G.ControllerConfig(theta_min=10.0, theta_max=1000.0, epsilon=0.3 if kind != "randomk" else 0.05,
+                             omega=0.05, window=3, compressor=G.CompressorKind(kind))
+    state = G.ControllerState.fresh(cfg, workers)
+    cost = G.CostModelParams(workers=workers)
+    rng = G.SeededRng(11)
+    stores = [G.ResidualStore(n) for _ in range(workers)]
+    r_host = [np.zeros(n, dtype=np.float32) for _ in range(workers)]
+    seen = set()
+    for it in range(1, 9):
+        gs = [_vec("gauss" if w == 0 else "layered", n, 31 * it + w) for w in range(workers)]
+        tmin, ts = state.theta_min, state.theta_s
+        res = G.run_iteration(state, [gv(G, g) for g in gs], stores, cost, rng)
+        seen.add(res.decision.choice)
+        k1 = O.keep_count(n, tmin)
+        gmin_raw, gc_raw = [], []
+        for w in range(workers):
+            ef = O.ef_add(gs[w], r_host[w])
+            norm = O.sq_norm(ef)
+            s0 = rng.split(it, w, 0)
+            s1 = rng.split(it, w, 1)
+            i1, v1 = O.select(kind, ef, k1, seed=s0.seed, stream=s0.stream)
+            i2, v2, _ = O.compress_further(kind, i1, v1, n, ts, seed=s1.seed, stream=s1.stream)
+            gmin_raw.append(min(1.0, O.sq_norm(v1) / norm))
+            gc_raw.append(min(1.0, O.sq_norm(v2) / norm))
+            if res.decision.choice == "dense":
+                r_host[w] = np.zeros(n, dtype=np.float32)
+                continue
+            ci, cv = (i2, v2) if res.decision.choice == "candidate" else (i1, v1)
+            part = res.sent[w]
+            assert np.array_equal(host(part.indices), ci), (it, w)
+            np.testing.assert_allclose(host(part.vals), cv, rtol=GAIN_RTOL)
+            r_host[w] = O.update_residual(ef, ci, cv)
+        assert res.gain_min_raw == pytest.approx(sum(gmin_raw) / workers, rel=GAIN_RTOL)
+        assert res.gain_c_raw == pytest.approx(sum(gc_raw) / workers, rel=GAIN_RTOL)
+        if kind != "redsync":  # Redsync values carry the 1e-6 mean tolerance into r
+            for w in range(workers):
+                assert np.array_equal(bits(host(stores[w].residual)), bits(r_host[w])), (it, w)
+        else:
+            for w in range(workers):
+                np.testing.assert_allclose(host(stores[w].residual), r_host[w], rtol=1e-5, atol=1e-6)
+    assert seen - {"dense"}, seen
