@@ -340,7 +340,7 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // full-size write of the step); !EF: v read from `values`.  REFILL re-collects
 // from the already-written g_ef with key_est = 0 (exactness fallback).
 template <int KM, bool EF>
-__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS_PER_SM) k_collect(Plan p, int refill)
+__global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
 {
     __shared__ uint32_t h[GVC_H0_BINS];
     __shared__ double red[GVC_WARPS_PER_BLOCK];
@@ -374,22 +374,24 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS_PER_SM) k_coll
                 for (int u = 0; u < 4; u++)
                     b[u] = ld_stream(reinterpret_cast<const float4 *>(p.resid + i + u * 128) + lane);
                 if (p.pmask) {
-                    // deferred update of the previous step: 4 bits of one mask word per lane;
-                    // the first lane of each word clears it after use
+                    // deferred update of the previous step: the 16 mask words of this
+                    // 512-value chunk in one coalesced load (lanes 0..15), shuffled to
+                    // the lanes that own their 4-bit slices, cleared after use
+                    const uint64_t w0 = i >> 5;
+                    const uint32_t wreg = lane < 16 ? p.pmask[w0 + lane] : 0u;
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
-                        const uint64_t pos = i + u * 128 + lane * 4;
-                        const uint32_t w = p.pmask[pos >> 5];
-                        const uint32_t bits = (w >> (pos & 31)) & 0xfu;
+                        const uint32_t w = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3));
+                        const uint32_t bits = (w >> ((lane & 7) * 4)) & 0xfu;
                         if (bits) {
                             if (bits & 1u) b[u].x = pending_resid(b[u].x, p.pmode, pm);
                             if (bits & 2u) b[u].y = pending_resid(b[u].y, p.pmode, pm);
                             if (bits & 4u) b[u].z = pending_resid(b[u].z, p.pmode, pm);
                             if (bits & 8u) b[u].w = pending_resid(b[u].w, p.pmode, pm);
                         }
-                        if ((lane & 7) == 0 && w)
-                            p.pmask[pos >> 5] = 0u;
                     }
+                    if (wreg)
+                        p.pmask[w0 + lane] = 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
@@ -992,11 +994,23 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
 // -------------------------------------------------------------------- emit
 // One warp per segment: in-block prefix of the 8 segments' tie / selected
 // counts (lanes 0..7), then an ordered 4-wide compaction.
-template <int KM>
+// Sent-mask words of a level-1 emit are private to the segment (segments are
+// 512-aligned), so each warp builds them in shared memory and writes every
+// word of its segment once, coalesced.  Second-level emits (idx_map) map to
+// arbitrary words and OR into global memory.
+template <int KM, bool SMEM_MASK>
 __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
                                                       float *out_val, float *resid, uint32_t *smask, float *sm_out)
 {
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
+    extern __shared__ uint32_t mwords[];  // [8][seg_len / 32] when SMEM_MASK
+    const uint32_t nwords = p.seg_len >> 5;
+    uint32_t *mw = mwords + (threadIdx.x >> 5) * nwords;
+    if (SMEM_MASK) {
+        for (uint32_t w = threadIdx.x & 31; w < nwords; w += 32)
+            mw[w] = 0u;
+        __syncwarp();
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t blk = blockIdx.x;
     const uint32_t seg = blk * GVC_WARPS_PER_BLOCK + warp;
@@ -1065,16 +1079,6 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                 const uint32_t tb = __ballot_sync(0xffffffffu, tie);
                 const bool sel = ok[c] && (key[c] > T || (tie && ties_seen + __popc(tb & lt) < take));
                 const uint32_t sb = __ballot_sync(0xffffffffu, sel);
-                if (smask) {
-                    // deferred residual: OR this sub-group's sent bits into the mask, one
-                    // atomic per distinct word (sent indices ascend across the lanes)
-                    const uint32_t gi = sel ? (idx_map ? idx_map[pos[c]] : pos[c]) : 0xffffffffu;
-                    const uint32_t word = gi >> 5;
-                    const uint32_t grp = __match_any_sync(0xffffffffu, word);
-                    const uint32_t bits = __reduce_or_sync(grp, sel ? (1u << (gi & 31)) : 0u);
-                    if (sel && (__ffs(grp) - 1) == lane)
-                        atomicOr(&smask[word], bits);
-                }
                 if (sel) {
                     float sv = v[c];
                     if (redsync) {
@@ -1085,6 +1089,10 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                     const uint32_t gi = idx_map ? idx_map[pos[c]] : pos[c];
                     out_idx[w] = gi;
                     out_val[w] = sv;
+                    if (SMEM_MASK)
+                        atomicOr(&mw[(pos[c] - (uint32_t)beg) >> 5], 1u << (pos[c] & 31));
+                    else if (smask)
+                        atomicOr(&smask[gi >> 5], 1u << (gi & 31));
                     if (resid) {
                         // level-1 emits: the candidate value IS g_ef; a second-level
                         // emit (idx_map) carries level-1 SENT values, so read g_ef back
@@ -1098,6 +1106,13 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                 out += __popc(sb);
             }
         }
+    }
+    if (SMEM_MASK && seg < p.S) {
+        __syncwarp();
+        const uint64_t beg = (uint64_t)seg * p.seg_len;
+        const uint32_t live = (uint32_t)((min(p.n, beg + p.seg_len) - beg + 31) >> 5);
+        for (uint32_t w = lane; w < live; w += 32)
+            smask[(beg >> 5) + w] = mw[w];
     }
     e2 = warp_sum_f64(e2);
     ab = warp_sum_f64(ab);
@@ -1310,10 +1325,29 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
     const int blocks = (int)p.B;
     ProfScope pe(PROF_EMIT, s);
     count_launches(stats ? 2 : 1);
-    if (p.keymode == KEY_MAG)
-        k_emit<KEY_MAG><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask, sm_out);
-    else
-        k_emit<KEY_HASH><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask, sm_out);
+    const size_t mbytes = (size_t)GVC_WARPS_PER_BLOCK * (p.seg_len >> 5) * 4;
+    const bool smem_mask = smask && !idx_map && mbytes <= 96 * 1024;
+    if (smem_mask) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_emit<KEY_MAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(k_emit<KEY_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            attr = true;
+        }
+        if (p.keymode == KEY_MAG)
+            k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                       sm_out);
+        else
+            k_emit<KEY_HASH, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
+                                                                        smask, sm_out);
+    } else {
+        if (p.keymode == KEY_MAG)
+            k_emit<KEY_MAG, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                   sm_out);
+        else
+            k_emit<KEY_HASH, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                    sm_out);
+    }
     if (stats)
         k_emit_finish<<<1, 1024, 0, s>>>(p, stats);
     cudaError_t e = cudaGetLastError();
