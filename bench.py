@@ -56,48 +56,52 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled through NVML every ~2 ms while the
+    timed region runs (nvidia-smi's own polling is too coarse for a region of
+    a few milliseconds)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.rows, self.stop, self.thread = gpu, [], threading.Event(), None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report it instead of guessing
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(1.0)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled: " + getattr(self, "err", "")]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": getattr(self, "max_sm", None),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
 # ------------------------------------------------------------- CPU legs
@@ -208,7 +212,8 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     chosen.clear()
     nat.prof_read()
-    nat.prof_enable(True)
+    prof_on = os.environ.get("GVC_BENCH_NOPROF") != "1"
+    nat.prof_enable(prof_on)
     launches0 = nat.launch_count()
     with ClockSampler(local) as clocks:
         for s in range(args.steps):
@@ -257,13 +262,13 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     col_ms, col_n = prof["collect"]
     col_launch = col_ms / max(col_n, 1)
     col_bytes = 12 * M  # read g, read r, write g_ef: the algorithmic bytes of the fused EF pass
-    achieved = col_bytes / (col_launch * 1e-3) / 1e9
+    achieved = col_bytes / (col_launch * 1e-3) / 1e9 if col_launch > 0 else None
     k1 = G.keep_count(M, theta_min)
     sel_ms = prof["select"][0] / max(prof["select"][1], 1)
     emit_ms = prof["emit"][0] / max(prof["emit"][1], 1)
     agg_ms = prof["aggregate"][0] / max(prof["aggregate"][1], 1)
     comp_bytes = 12 * M + 8 * k1
-    comp_achieved = comp_bytes / ((sel_ms + emit_ms) * 1e-3) / 1e9
+    comp_achieved = comp_bytes / ((sel_ms + emit_ms) * 1e-3) / 1e9 if sel_ms > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -275,10 +280,11 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
                    "parallelism": f"dp{world}"},
         "roofline": {"bound": "hbm", "kernel": "k_collect (fused EF add + fp64 norm + candidate compaction)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "algorithmic_bytes_per_launch": col_bytes,
+                     "frac": achieved / peak if achieved else None, "traffic": None, "algorithmic_bytes_per_launch": col_bytes,
                      "launch_ms": col_launch},
         "compress_stage": {"what": "gvc_select (all kernels) + gvc_emit, algorithmic 12M + 8k bytes",
-                           "ms": sel_ms + emit_ms, "achieved": comp_achieved, "frac": comp_achieved / peak},
+                           "ms": sel_ms + emit_ms, "achieved": comp_achieved,
+                           "frac": comp_achieved / peak if comp_achieved else None},
         "breakdown_ms": {"collect": col_launch, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),

@@ -89,6 +89,13 @@ void gvc_prof_enable(int on)
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof_on = on != 0;
+    // pre-create events so the timed region never pays cudaEventCreate
+    while (g_prof_on && g_prof_free.size() < 4096) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess)
+            break;
+        g_prof_free.push_back(e);
+    }
 }
 
 int gvc_prof_read(double *ms, unsigned long long *counts, int ncat)

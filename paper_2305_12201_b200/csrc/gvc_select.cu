@@ -542,35 +542,42 @@ __global__ void __launch_bounds__(1024) k_resolve0(Plan p, int pass)
 }
 
 // Refinement histogram: candidates whose key lies in an unresolved interval.
-template <int KM>
+// Intervals are hoisted into registers as 32-bit (lo, width-1, shift) so the
+// membership test is one wrapping subtract and compare per ladder entry.
+template <int KM, int NB>
 __global__ void __launch_bounds__(GVC_THREADS) k_level_hist(Plan p)
 {
-    __shared__ JState js[GVC_MAX_LADDER];
     SelState *st = p.st;
     if (st->pending == 0)
         return;
-    if (threadIdx.x < p.n_ks)
-        js[threadIdx.x] = st->js[threadIdx.x];
-    __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + (threadIdx.x >> 5);
     if (seg >= p.S)
         return;
+    uint32_t lo[NB], wm1[NB], sh[NB];
+    bool act[NB];
+#pragma unroll
+    for (int j = 0; j < NB; j++) {
+        act[j] = j < p.n_ks && !st->js[j].resolved;
+        lo[j] = act[j] ? (uint32_t)st->js[j].lo : 0u;
+        wm1[j] = act[j] ? (uint32_t)(st->js[j].hi - st->js[j].lo - 1) : 0u;
+        sh[j] = act[j] ? (uint32_t)st->js[j].shift : 0u;
+    }
     const uint64_t beg = (uint64_t)seg * p.seg_len;
     const uint32_t cnt = p.seg_cnt[seg];
     for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
-            const uint32_t t = base + lane * 4;
+        const uint32_t t = base + lane * 4;
         float v[4];
         uint32_t pos[4], key[4];
         bool ok[4];
         load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-            if (!ok[c])
-                continue;
-            for (int j = 0; j < p.n_ks; j++) {
-                if (!js[j].resolved && key[c] >= js[j].lo && key[c] < js[j].hi)
-                    atomicAdd(&p.histl[j * GVC_HL_BINS + (uint32_t)((key[c] - js[j].lo) >> js[j].shift)], 1u);
+#pragma unroll
+            for (int j = 0; j < NB; j++) {
+                const uint32_t d = key[c] - lo[j];
+                if (act[j] && ok[c] && d <= wm1[j])
+                    atomicAdd(&p.histl[j * GVC_HL_BINS + (d >> sh[j])], 1u);
             }
         }
     }
@@ -613,29 +620,45 @@ __global__ void __launch_bounds__(1024) k_level_resolve(Plan p)
 // energies.  fp64 sums are per-lane sequential, a fixed xor tree per warp and
 // warps added in order: bit-reproducible.
 template <int KM, int NB, bool ABS>
-__global__ void __launch_bounds__(GVC_THREADS, 4) k_final(Plan p)
+__global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
 {
-    __shared__ uint32_t Ts[GVC_MAX_LADDER];
+    // thread-private band accumulators live in shared memory ([slot][thread],
+    // conflict-free), so each candidate costs one indexed update instead of
+    // NB predicated ones; ties (key == T_j, rare) take a branch
+    extern __shared__ __align__(16) unsigned char fsm[];
+    double(*acc_e)[GVC_THREADS] = reinterpret_cast<double(*)[GVC_THREADS]>(fsm);
+    double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
+    uint32_t(*acc_c)[GVC_THREADS] = reinterpret_cast<uint32_t(*)[GVC_THREADS]>(acc_a + (ABS ? NB + 1 : 0));
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
     __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
     SelState *st = p.st;
-    if (threadIdx.x < GVC_MAX_LADDER)
-        Ts[threadIdx.x] = threadIdx.x < p.n_ks ? (uint32_t)st->js[threadIdx.x].lo : 0xffffffffu;
-    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
     const int nks = p.n_ks;
     uint32_t T[NB];
 #pragma unroll
     for (int j = 0; j < NB; j++)
-        T[j] = Ts[j];  // 0xffffffff beyond n_ks: never below a key, never equal to a valid one
-    uint32_t bc[NB], tc[NB];
-    double be[NB], ba[NB], te[NB], ta[NB];
+        T[j] = j < nks ? (uint32_t)st->js[j].lo : 0xffffffffu;
+    // 0xffffffff beyond n_ks: never below a key (band stays < n_ks + 1)
+#pragma unroll
+    for (int b = 0; b <= NB; b++) {
+        acc_e[b][threadIdx.x] = 0.0;
+        if (ABS)
+            acc_a[b][threadIdx.x] = 0.0;
+        acc_c[b][threadIdx.x] = 0u;
+    }
+    uint32_t tc[NB];
+    double te[NB], ta[NB];
 #pragma unroll
     for (int j = 0; j < NB; j++) {
-        bc[j] = tc[j] = 0;
-        be[j] = ba[j] = te[j] = ta[j] = 0.0;
+        tc[j] = 0;
+        te[j] = ta[j] = 0.0;
     }
+    uint32_t tmax = 0;  // largest valid threshold
+#pragma unroll
+    for (int j = 0; j < NB; j++)
+        if (j < nks)
+            tmax = max(tmax, T[j]);
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
         const uint32_t cnt = p.seg_cnt[seg];
@@ -647,40 +670,43 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_final(Plan p)
             load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                // branch-free: selects feed the adds (x + 0.0 == x for these
-                // non-negative sums, and no 0 * inf NaN can arise)
-                const double v2 = ok[c] ? (double)v[c] * (double)v[c] : 0.0;
-                const double av = ok[c] ? fabs((double)v[c]) : 0.0;
+                if (!ok[c])
+                    continue;
+                const double v2 = (double)v[c] * (double)v[c];
                 int band = 0;
 #pragma unroll
                 for (int j = 0; j < NB; j++)
-                    band += (ok[c] && j < nks && T[j] < key[c]);
+                    band += T[j] < key[c];
+                acc_e[band][threadIdx.x] += v2;
+                if (ABS)
+                    acc_a[band][threadIdx.x] += fabs((double)v[c]);
+                acc_c[band][threadIdx.x] += 1u;
+                if (key[c] <= tmax) {
 #pragma unroll
-                for (int j = 0; j < NB; j++) {
-                    const bool inb = band == j + 1;
-                    const bool tie = ok[c] && j < nks && key[c] == T[j];
-                    bc[j] += inb;
-                    tc[j] += tie;
-                    be[j] += inb ? v2 : 0.0;
-                    te[j] += tie ? v2 : 0.0;
-                    if (ABS) {
-                        ba[j] += inb ? av : 0.0;
-                        ta[j] += tie ? av : 0.0;
+                    for (int j = 0; j < NB; j++) {
+                        if (key[c] == T[j]) {
+                            tc[j]++;
+                            te[j] += v2;
+                            ta[j] += fabs((double)v[c]);
+                        }
                     }
                 }
             }
         }
     }
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < NB; j++) {
-        uint32_t c1 = bc[j], c2 = tc[j];
+        // band j+1 holds keys in (T_j, T_{j+1}]; band 0 (key <= T_0) is never kept
+        uint32_t c1 = acc_c[j + 1][threadIdx.x], c2 = tc[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             c1 += __shfl_xor_sync(0xffffffffu, c1, o);
             c2 += __shfl_xor_sync(0xffffffffu, c2, o);
         }
-        double e1 = warp_sum_f64(be[j]), a1 = warp_sum_f64(ba[j]);
-        double e2 = warp_sum_f64(te[j]), a2 = warp_sum_f64(ta[j]);
+        double e1 = warp_sum_f64(acc_e[j + 1][threadIdx.x]);
+        double a1 = ABS ? warp_sum_f64(acc_a[j + 1][threadIdx.x]) : 0.0;
+        double e2 = warp_sum_f64(te[j]), a2 = ABS ? warp_sum_f64(ta[j]) : 0.0;
         if (lane == 0) {
             wcnt[warp][0][j] = c1;
             wcnt[warp][1][j] = c2;
@@ -1164,16 +1190,27 @@ size_t select_workspace_bytes(int kind, uint64_t n)
 
 static int nb_for(int n_ks) { return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16; }
 
+template <int KM, int NB, bool ABS>
+static void launch_final_nb(const Plan &p, cudaStream_t s)
+{
+    const size_t smem = (size_t)(NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_final<KM, NB, ABS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_final<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(p);
+}
+
 template <int KM, bool ABS>
 static void launch_final_abs(const Plan &p, cudaStream_t s)
 {
-    const int blocks = (int)p.B;
     switch (nb_for(p.n_ks)) {
-    case 1: k_final<KM, 1, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    case 2: k_final<KM, 2, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    case 4: k_final<KM, 4, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    case 8: k_final<KM, 8, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-    default: k_final<KM, 16, ABS><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+    case 1: launch_final_nb<KM, 1, ABS>(p, s); break;
+    case 2: launch_final_nb<KM, 2, ABS>(p, s); break;
+    case 4: launch_final_nb<KM, 4, ABS>(p, s); break;
+    case 8: launch_final_nb<KM, 8, ABS>(p, s); break;
+    default: launch_final_nb<KM, 16, ABS>(p, s); break;
     }
 }
 
@@ -1220,7 +1257,13 @@ static void launch_pipeline(Plan &p, cudaStream_t s)
     k_resolve0<<<1, 1024, 0, s>>>(p, 1);
     launches += 5;
     for (int l = 0; l < GVC_MAX_LEVELS; l++) {
-        k_level_hist<KM><<<blocks, GVC_THREADS, 0, s>>>(p);
+        switch (nb_for(p.n_ks)) {
+        case 1: k_level_hist<KM, 1><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+        case 2: k_level_hist<KM, 2><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+        case 4: k_level_hist<KM, 4><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+        case 8: k_level_hist<KM, 8><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+        default: k_level_hist<KM, 16><<<blocks, GVC_THREADS, 0, s>>>(p); break;
+        }
         k_level_resolve<<<1, 1024, 0, s>>>(p);
         launches += 2;
     }
