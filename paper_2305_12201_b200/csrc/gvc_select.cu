@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(Plan p)
 
 // ----------------------------------------------------------------- collect
 // Candidate compaction for 4 values of one lane in lane-major index order.
+// Straight-line (no early exit) so the four ballots stay warp-convergent; the
+// per-candidate stores and histogram atomics are predicated.
 template <int KM>
 __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32_t pos0, int valid,
                                       uint32_t key_est, int shift0, uint32_t *h, float *cval, uint32_t *cidx,
@@ -308,32 +310,31 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 {
     uint32_t key[4];
     bool pr[4];
+    uint32_t m[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
         key[c] = cand_key<KM>(p, v[c], pos0 + c);
         pr[c] = (c < valid) && key[c] >= key_est;
-        if (KM == KEY_MAG && c < valid && key[c] > 0x7f800000u)
-            nan_any = 1;
+        if (KM == KEY_MAG)
+            nan_any |= (uint32_t)((c < valid) & (key[c] > 0x7f800000u));
+        m[c] = __ballot_sync(0xffffffffu, pr[c]);
     }
     const uint32_t lt = lanemask_lt();
-    uint32_t m0 = __ballot_sync(0xffffffffu, pr[0]);
-    uint32_t m1 = __ballot_sync(0xffffffffu, pr[1]);
-    uint32_t m2 = __ballot_sync(0xffffffffu, pr[2]);
-    uint32_t m3 = __ballot_sync(0xffffffffu, pr[3]);
-    if ((m0 | m1 | m2 | m3) == 0)
-        return;
-    uint32_t o = ccount + __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt) + __popc(m3 & lt);
+    uint32_t o = ccount + __popc(m[0] & lt) + __popc(m[1] & lt) + __popc(m[2] & lt) + __popc(m[3] & lt);
 #pragma unroll
     for (int c = 0; c < 4; c++) {
+        // the histogram update is unconditional (non-candidates hit a per-lane
+        // dummy bin past the end) so only the two stores are predicated
+        const uint32_t bin = pr[c] ? min((key[c] - key_est) >> shift0, (uint32_t)GVC_H0_BINS - 1)
+                                   : (uint32_t)GVC_H0_BINS + (threadIdx.x & 31);
+        atomicAdd(&h[bin], 1u);
         if (pr[c]) {
             cval[o] = v[c];
             cidx[o] = pos0 + c;
-            uint32_t bin = (key[c] - key_est) >> shift0;
-            atomicAdd(&h[bin < GVC_H0_BINS ? bin : GVC_H0_BINS - 1], 1u);
-            o++;
         }
+        o += pr[c];
     }
-    ccount += __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
+    ccount += __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
 }
 
 // One warp per segment.  EF: v = fl32(g + r) written back over r (the only
@@ -342,11 +343,11 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 template <int KM, bool EF>
 __global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
 {
-    __shared__ uint32_t h[GVC_H0_BINS];
+    __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
     if (refill && !p.st->fallback)
         return;
-    for (int i = threadIdx.x; i < GVC_H0_BINS; i += GVC_THREADS)
+    for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += GVC_THREADS)
         h[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -383,12 +384,10 @@ __global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
                     for (int u = 0; u < 4; u++) {
                         const uint32_t w = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3));
                         const uint32_t bits = (w >> ((lane & 7) * 4)) & 0xfu;
-                        if (bits) {
-                            if (bits & 1u) b[u].x = pending_resid(b[u].x, p.pmode, pm);
-                            if (bits & 2u) b[u].y = pending_resid(b[u].y, p.pmode, pm);
-                            if (bits & 4u) b[u].z = pending_resid(b[u].z, p.pmode, pm);
-                            if (bits & 8u) b[u].w = pending_resid(b[u].w, p.pmode, pm);
-                        }
+                        b[u].x = (bits & 1u) ? pending_resid(b[u].x, p.pmode, pm) : b[u].x;
+                        b[u].y = (bits & 2u) ? pending_resid(b[u].y, p.pmode, pm) : b[u].y;
+                        b[u].z = (bits & 4u) ? pending_resid(b[u].z, p.pmode, pm) : b[u].z;
+                        b[u].w = (bits & 8u) ? pending_resid(b[u].w, p.pmode, pm) : b[u].w;
                     }
                     if (wreg)
                         p.pmask[w0 + lane] = 0u;
