@@ -64,6 +64,7 @@ typedef struct {
     int32_t fallback_used;                  /* 1 when the threshold estimate missed (exact re-scan ran) */
     uint64_t kept_count[GVC_MAX_LADDER];    /* == ks[j] (sanity)                               */
     uint64_t kept_nonzero[GVC_MAX_LADDER];  /* kept entries with |v| > 0                       */
+    uint64_t shortfall;                     /* allow_short: ks[0] - candidates (else 0)        */
 } gvc_select_result;
 
 /* Arguments of one selection over n values.  Two input modes:
@@ -92,6 +93,13 @@ typedef struct {
                                      f(r) = sign(r) * m (mode 2, Redsync, m = *pending_m_dev).
                                      The collect pass applies it while streaming r and clears
                                      the consumed mask words (feedback.py:39-51, deferred). */
+    const uint32_t *key_est_dev;  /* optional: force the candidate threshold to this device key
+                                     (DGC's sampled threshold, compressors.py:121-123): the
+                                     candidates are then exactly {key >= *key_est_dev}        */
+    int32_t allow_short;          /* with key_est_dev: if fewer than ks[0] candidates exist, keep
+                                     them ALL (DGC overshoot, compressors.py:126-128) and report
+                                     the shortfall in gvc_select_result.shortfall              */
+    int32_t reserved2;
 } gvc_select_args;
 
 GVC_API const char *gvc_last_error(void);
@@ -178,6 +186,25 @@ GVC_API int gvc_aggregate_dense(const float *parts_dev, int nparts, uint64_t n, 
 GVC_API void gvc_prof_enable(int on);
 GVC_API int gvc_prof_read(double *ms, unsigned long long *counts, int ncat);
 GVC_API unsigned long long gvc_launch_count(void);
+
+/* DGC helpers (compressors.py:110-137).
+ * gvc_gather_ef: out[i] = values at pos[i]: fl32(g + r_true) in EF mode (g_dev and
+ *   resid_dev, with the deferred mask of gvc_select_args applied), else values_dev[pos[i]].
+ * gvc_below_keys: out[i] = a non-negative float whose magnitude key is key(v[i]) + 1
+ *   when key(v[i]) < *thr_dev and (excl_mask_dev == NULL or bit pos[i] clear), else +0.0;
+ *   a Top-k over `out` ranks exactly "the largest below the threshold, ties to the
+ *   lower index" (:129-131, :102-107); *count_dev += number of eligible entries.
+ * gvc_compact_mask: the set bits of mask[0..ceil(n/32)) as ascending positions;
+ *   *count_dev = their number.  Workspace: gvc_compact_workspace_bytes(n). */
+GVC_API int gvc_gather_ef(const uint32_t *pos_dev, uint64_t k, const float *values_dev, const float *g_dev,
+                          const float *resid_dev, const uint32_t *pending_mask_dev, const float *pending_m_dev,
+                          int pending_mode, float *out_dev, void *stream);
+GVC_API int gvc_below_keys(const float *v_dev, const uint32_t *pos_dev, uint64_t n, const uint32_t *thr_dev,
+                           const uint32_t *excl_mask_dev, float *out_dev, unsigned long long *count_dev,
+                           void *stream);
+GVC_API size_t gvc_compact_workspace_bytes(uint64_t n);
+GVC_API int gvc_compact_mask(const uint32_t *mask_dev, uint64_t n, uint32_t *out_dev,
+                             unsigned long long *count_dev, void *ws_dev, size_t ws_bytes, void *stream);
 
 /* Fill out[i] = i (identity support for k >= n, compressors.py:172-173). */
 GVC_API int gvc_iota(uint32_t *out_dev, uint64_t n, void *stream);

@@ -27,6 +27,7 @@ EXPORTS = (
     "gvc_ef_add", "gvc_sq_norm_workspace_bytes", "gvc_sq_norm", "gvc_update_residual",
     "gvc_decompress", "gvc_aggregate", "gvc_aggregate_workspace_bytes", "gvc_aggregate_dense",
     "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
+    "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
 )
 
 _u64, _i32, _f64, _vp, _sz = ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
@@ -41,6 +42,7 @@ class SelectArgs(ctypes.Structure):
         ("dgc_sample_fraction", _f64),
         ("force_exact", _i32), ("pending_mode", _i32),
         ("pending_mask_dev", _vp), ("pending_m_dev", _vp),
+        ("key_est_dev", _vp), ("allow_short", _i32), ("reserved2", _i32),
     ]
 
 
@@ -58,6 +60,7 @@ class SelectResult(ctypes.Structure):
         ("fallback_used", _i32),
         ("kept_count", _u64 * MAX_LADDER),
         ("kept_nonzero", _u64 * MAX_LADDER),
+        ("shortfall", _u64),
     ]
 
 
@@ -103,6 +106,11 @@ def load(build_if_missing: bool = False):
         L.gvc_aggregate_workspace_bytes.restype = _sz
         L.gvc_aggregate_dense.argtypes = [_vp, ctypes.c_int, _u64, _vp, _vp]
         L.gvc_iota.argtypes = [_vp, _u64, _vp]
+        L.gvc_gather_ef.argtypes = [_vp, _u64, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _vp]
+        L.gvc_below_keys.argtypes = [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]
+        L.gvc_compact_workspace_bytes.argtypes = [_u64]
+        L.gvc_compact_workspace_bytes.restype = _sz
+        L.gvc_compact_mask.argtypes = [_vp, _u64, _vp, _vp, _vp, _sz, _vp]
         L.gvc_prof_enable.argtypes = [ctypes.c_int]
         L.gvc_prof_enable.restype = None
         L.gvc_prof_read.argtypes = [_vp, _vp, ctypes.c_int]

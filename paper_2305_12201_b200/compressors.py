@@ -124,7 +124,8 @@ class Selection:
     def __init__(self, kind: CompressorKind, ks: Sequence[int], *, values: torch.Tensor | None = None,
                  g: torch.Tensor | None = None, resid: torch.Tensor | None = None,
                  rng: SeededRng | None = None, pos_base: int = 0, slot: str = "sel0",
-                 force_exact: int = 0, pending=None):
+                 force_exact: int = 0, pending=None, key_est: torch.Tensor | None = None,
+                 allow_short: bool = False):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -148,6 +149,10 @@ class Selection:
         a.pos_base = pos_base
         a.dgc_sample_fraction = kind.dgc_sample_fraction
         a.force_exact = int(force_exact)
+        if key_est is not None:  # forced candidate threshold (DGC), a device u32/i32 scalar
+            a.key_est_dev = key_est.data_ptr()
+            a.allow_short = 1 if allow_short else 0
+        self._keep = (key_est,)  # keep device scalars alive until the stream consumed them
         if pending is not None:  # (mask, m, mode): deferred residual update of the previous step
             a.pending_mask_dev = pending[0].data_ptr()
             a.pending_m_dev = pending[1].data_ptr()
@@ -158,10 +163,11 @@ class Selection:
 
     def emit(self, j: int = 0, idx_map: torch.Tensor | None = None, resid: torch.Tensor | None = None,
              stats: torch.Tensor | None = None, sent_mask: torch.Tensor | None = None,
-             sent_m: torch.Tensor | None = None):
+             sent_m: torch.Tensor | None = None, count: int | None = None):
         """Index-ascending (indices, values) of ladder entry j; optionally the
-        residual update, either direct (``resid``) or deferred (``sent_mask``)."""
-        k = self.ks[j]
+        residual update, either direct (``resid``) or deferred (``sent_mask``).
+        ``count`` overrides the entry count (a DGC overshoot keeps fewer)."""
+        k = self.ks[j] if count is None else int(count)
         out_idx = torch.empty(k, dtype=torch.uint32, device=self.device)
         out_val = torch.empty(k, dtype=torch.float32, device=self.device)
         nat.check(nat.load().gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),

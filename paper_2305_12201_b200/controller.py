@@ -229,8 +229,9 @@ class _WorkerStep:
             out.append(self.sel2.res_dev)
         return out
 
-    def gains_from(self, results: list[nat.SelectResult], norm_host: float | None):
+    def gains_from(self, raw: list[bytes], norm_host: float | None):
         """(ef_norm, E_min, E_c, extra energies) from the read-back results."""
+        results = [nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES]) for b in raw]
         r1 = results[0] if self.sel1 is not None else None
         r2 = results[-1] if self.sel2 is not None else None
         for r in results:
@@ -293,11 +294,76 @@ class _WorkerStep:
         return part
 
 
-def _read_results(tensors: list[torch.Tensor]) -> list[nat.SelectResult]:
+def _read_results(tensors: list[torch.Tensor]) -> list[bytes]:
+    """One device->host copy for every worker's device-side statistics."""
     if not tensors:
         return []
-    raw = torch.stack(tensors).cpu().numpy()
-    return [nat.SelectResult.from_buffer_copy(row.tobytes()[:nat.RESULT_BYTES]) for row in raw]
+    flat = torch.cat([t.reshape(-1).view(torch.uint8) for t in tensors]).cpu().numpy().tobytes()
+    out, pos = [], 0
+    for t in tensors:
+        nb = t.numel() * t.element_size()
+        out.append(flat[pos:pos + nb])
+        pos += nb
+    return out
+
+
+class _DgcStep:
+    """DGC worker step: level 1 over g_ef (fused EF pass with the sampled
+    threshold), level 2 over the level-1 values (compressors.py:226-246)."""
+
+    def __init__(self, kind: CompressorKind, g: torch.Tensor, store: ResidualStore, k1: int, k2: int,
+                 rng: SeededRng, i: int, w: int):
+        from .dgc import dgc_select
+        from .gradcore import squared_l2_norm_dev
+        self.kind, self.k1, self.k2, self.store = kind, k1, k2, store
+        self.n = g.numel()
+        self.identity1 = False
+        rng0 = rng.split(i, w, _STAGE_MIN)
+        rng1 = rng.split(i, w, _STAGE_STEP)
+        slot = f"dgc{w}"
+        if k1 >= self.n:
+            resid = store.residual
+            nat.check(nat.load().gvc_ef_add(nat.ptr(g), nat.ptr(resid), nat.ptr(resid), self.n,
+                                            nat.stream_ptr(g.device)), "apply_feedback")
+            self.g_min = SparseGradient._wrap(_iota(self.n, g.device), resid.clone(), self.n, 1.0)
+            self.norm = None
+        else:
+            pending = store._take_pending()
+            idx, vals, res = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
+                                        slot=slot + "a", want_result=True)
+            self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
+            self.norm = res.ef_norm_sq
+        if k2 < self.g_min.kept:
+            idx2, vals2 = dgc_select(kind, self.g_min.vals, k2, rng1, idx_map=self.g_min.indices, slot=slot + "b")
+            self.g_c = SparseGradient._wrap(idx2, vals2, self.n, self.n / k2)
+        else:
+            self.g_c = self.g_min
+        self.stats = torch.stack([squared_l2_norm_dev(self.g_min.vals), squared_l2_norm_dev(self.g_c.vals),
+                                  squared_l2_norm_dev(store._resid) if self.norm is None
+                                  else torch.zeros((), dtype=torch.float64, device=g.device)])
+
+    def stats_dev(self) -> list[torch.Tensor]:
+        return [self.stats]
+
+    def gains_from(self, raw: list[bytes], norm_host=None):
+        import numpy as np
+        e_min, e_c, n_id = np.frombuffer(raw[0], dtype=np.float64)
+        norm = self.norm if self.norm is not None else float(n_id)
+        return norm, float(e_min) if self.norm is not None else norm, float(e_c), []
+
+    def emit(self, candidate: bool) -> SparseGradient:
+        part = self.g_c if candidate else self.g_min
+        store = self.store
+        if self.norm is None:  # identity level 1: direct residual update
+            nat.check(nat.load().gvc_update_residual(nat.ptr(store._resid), nat.ptr(part.indices),
+                                                     nat.ptr(part.vals), part.kept, self.n, nat.ptr(store._resid),
+                                                     nat.stream_ptr(store._resid.device)), "update_residual")
+            return part
+        mask = store._mask_buf()
+        nat.check(nat.load().gvc_mark_sent(nat.ptr(part.indices), part.kept, nat.ptr(mask),
+                                           nat.stream_ptr(mask.device)), "mark_sent")
+        store._pmode = 1
+        return part
 
 
 def _mean_raw_gain(energies: Sequence[float], ef_norms: Sequence[float]) -> float:
@@ -346,11 +412,14 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         if g.length != store.length:
             raise ValueError(f"length mismatch: gradient {g.length}, residual {store.length}")
         nat.require_cuda(g.values)
-        steps.append(_WorkerStep(kind, g.values, store, k1, k2, extra_ks, rng, i, rank + w))
+        if kind.name == "dgc":
+            steps.append(_DgcStep(kind, g.values, store, k1, k2, rng, i, rank + w))
+        else:
+            steps.append(_WorkerStep(kind, g.values, store, k1, k2, extra_ks, rng, i, rank + w))
 
     # ---- one device->host read per iteration: every worker's norms and energies
     norm_host = None
-    if steps[0].identity1:
+    if getattr(steps[0], "identity1", False):
         from .gradcore import squared_l2_norm_dev
         norm_dev = [squared_l2_norm_dev(s.resid) for s in steps]
         norm_host = [float(x) for x in torch.stack(norm_dev).cpu()]

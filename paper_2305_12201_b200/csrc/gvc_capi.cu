@@ -132,7 +132,9 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     if (a->kind < GVC_TOPK || a->kind > GVC_RANDOMK)
         return set_error(GVC_ERR_ARG, "unknown compressor kind %d", a->kind);
     if (a->kind == GVC_DGC)
-        return set_error(GVC_ERR_ARG, "dgc selection goes through gvc_dgc_select");
+        return set_error(GVC_ERR_ARG, "dgc is composed from gvc_select (kind topk, key_est_dev) and the DGC helpers");
+    if (a->allow_short && (!a->key_est_dev || a->n_ks != 1 || a->kind != GVC_TOPK))
+        return set_error(GVC_ERR_ARG, "allow_short needs key_est_dev, one ladder entry and magnitude keys");
     if (a->n < 1 || a->n >= (1ull << 32))
         return set_error(GVC_ERR_ARG, "gradient length %llu outside [1, 2^32)", (unsigned long long)a->n);
     if (a->n_ks < 1 || a->n_ks > GVC_MAX_LADDER)
@@ -236,6 +238,35 @@ int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, 
         return set_error(GVC_ERR_ARG, "aggregate of zero parts");
     int rc = aggregate_dense_run(parts, nparts, n, out, STREAM(stream));
     return rc ? rc : check_launch("aggregate_dense");
+}
+
+int gvc_gather_ef(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,
+                  const uint32_t *pmask, const float *pm, int pmode, float *out, void *stream)
+{
+    if ((k && !pos) || !out || (g ? !resid : !values) || (pmask && (!g || pmode < 1 || pmode > 2)))
+        return set_error(GVC_ERR_ARG, "gvc_gather_ef: bad arguments");
+    int rc = gather_ef_run(pos, k, values, g, resid, pmask, pm, pmode, out, STREAM(stream));
+    return rc ? rc : check_launch("gather_ef");
+}
+
+int gvc_below_keys(const float *v, const uint32_t *pos, uint64_t n, const uint32_t *thr, const uint32_t *excl,
+                   float *out, unsigned long long *count, void *stream)
+{
+    if (!v || !thr || !out || !count || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_below_keys: bad arguments");
+    int rc = below_keys_run(v, pos, n, thr, excl, out, count, STREAM(stream));
+    return rc ? rc : check_launch("below_keys");
+}
+
+size_t gvc_compact_workspace_bytes(uint64_t n) { return compact_workspace_bytes(n); }
+
+int gvc_compact_mask(const uint32_t *mask, uint64_t n, uint32_t *out, unsigned long long *count, void *ws,
+                     size_t ws_bytes, void *stream)
+{
+    if (!mask || !out || !count || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_compact_mask: bad arguments");
+    int rc = compact_mask_run(mask, n, out, count, ws, ws_bytes, STREAM(stream));
+    return rc ? rc : check_launch("compact_mask");
 }
 
 int gvc_iota(uint32_t *out, uint64_t n, void *stream)

@@ -183,6 +183,148 @@ int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const 
     return GVC_OK;
 }
 
+// ------------------------------------------------------------ DGC helpers
+__global__ void k_gather_ef(const uint32_t *__restrict__ pos, uint64_t k, const float *__restrict__ values,
+                            const float *__restrict__ g, const float *__restrict__ resid, const uint32_t *pmask,
+                            const float *pm_ptr, int pmode, float *__restrict__ out)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const float pm = (pmask && pmode == 2) ? *pm_ptr : 0.f;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const uint32_t q = pos[i];
+        if (g) {
+            float r = resid[q];
+            if (pmask && ((pmask[q >> 5] >> (q & 31)) & 1u))
+                r = pending_resid(r, pmode, pm);
+            out[i] = __fadd_rn(g[q], r);
+        } else {
+            out[i] = values[q];
+        }
+    }
+}
+
+int gather_ef_run(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,
+                  const uint32_t *pmask, const float *pm, int pmode, float *out, cudaStream_t s)
+{
+    if (k) {
+        count_launches(1);
+        k_gather_ef<<<grid_for(k, 256, 148 * 16), 256, 0, s>>>(pos, k, values, g, resid, pmask, pm, pmode, out);
+    }
+    return GVC_OK;
+}
+
+__global__ void k_below_keys(const float *__restrict__ v, const uint32_t *__restrict__ pos, uint64_t n,
+                             const uint32_t *thr_ptr, const uint32_t *excl, float *__restrict__ out,
+                             unsigned long long *count)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t thr = *thr_ptr;
+    unsigned long long c = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t key = mag_key(v[i]);
+        bool ok = key < thr;
+        if (ok && excl) {
+            const uint32_t q = pos ? pos[i] : (uint32_t)i;
+            ok = !((excl[q >> 5] >> (q & 31)) & 1u);
+        }
+        // key + 1 keeps the order of eligible magnitudes and lifts |v| = 0 above
+        // the excluded entries (+0.0); keys < thr < 2^31 so key + 1 is a finite float
+        out[i] = __uint_as_float(ok ? key + 1u : 0u);
+        c += ok;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c)
+        atomicAdd(count, c);
+}
+
+int below_keys_run(const float *v, const uint32_t *pos, uint64_t n, const uint32_t *thr, const uint32_t *excl,
+                   float *out, unsigned long long *count, cudaStream_t s)
+{
+    count_launches(1);
+    k_below_keys<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(v, pos, n, thr, excl, out, count);
+    return GVC_OK;
+}
+
+// Ordered compaction of a bit mask: block b owns 1024 words (4 per thread).
+#define CMP_WORDS 1024
+__global__ void k_compact_count(const uint32_t *__restrict__ mask, uint64_t nw, unsigned long long *blk)
+{
+    __shared__ unsigned long long sh[33];
+    const uint64_t w0 = (uint64_t)blockIdx.x * CMP_WORDS + threadIdx.x * 4;
+    unsigned long long c = 0;
+    for (int q = 0; q < 4; q++)
+        if (w0 + q < nw)
+            c += __popc(mask[w0 + q]);
+    unsigned long long tot;
+    block_excl_prefix(c, sh, &tot);
+    if (threadIdx.x == 0)
+        blk[blockIdx.x] = tot;
+}
+
+__global__ void k_compact_scan(unsigned long long *blk, uint64_t nb, unsigned long long *count)
+{
+    __shared__ unsigned long long sh[33];
+    const uint64_t per = (nb + 1023) / 1024;
+    const uint64_t b0 = threadIdx.x * per;
+    unsigned long long local = 0;
+    for (uint64_t b = b0; b < min(nb, b0 + per); b++)
+        local += blk[b];
+    unsigned long long tot;
+    unsigned long long acc = block_excl_prefix(local, sh, &tot);
+    for (uint64_t b = b0; b < min(nb, b0 + per); b++) {
+        const unsigned long long v = blk[b];
+        blk[b] = acc;
+        acc += v;
+    }
+    if (threadIdx.x == 0)
+        *count = tot;
+}
+
+__global__ void k_compact_write(const uint32_t *__restrict__ mask, uint64_t nw, const unsigned long long *blk,
+                                uint32_t *__restrict__ out)
+{
+    __shared__ unsigned long long sh[33];
+    const uint64_t w0 = (uint64_t)blockIdx.x * CMP_WORDS + threadIdx.x * 4;
+    uint32_t w[4];
+    unsigned long long c = 0;
+    for (int q = 0; q < 4; q++) {
+        w[q] = w0 + q < nw ? mask[w0 + q] : 0u;
+        c += __popc(w[q]);
+    }
+    unsigned long long o = blk[blockIdx.x] + block_excl_prefix(c, sh);
+    for (int q = 0; q < 4; q++) {
+        uint32_t bits = w[q];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            out[o++] = (uint32_t)((w0 + q) * 32 + b);
+        }
+    }
+}
+
+size_t compact_workspace_bytes(uint64_t n)
+{
+    const uint64_t nw = (n + 31) / 32;
+    return (size_t)((nw + CMP_WORDS - 1) / CMP_WORDS + 1) * sizeof(unsigned long long);
+}
+
+int compact_mask_run(const uint32_t *mask, uint64_t n, uint32_t *out, unsigned long long *count, void *ws,
+                     size_t ws_bytes, cudaStream_t s)
+{
+    if (ws_bytes < compact_workspace_bytes(n))
+        return set_error(GVC_ERR_WORKSPACE, "compact workspace too small");
+    const uint64_t nw = (n + 31) / 32;
+    const uint64_t nb = (nw + CMP_WORDS - 1) / CMP_WORDS;
+    unsigned long long *blk = (unsigned long long *)ws;
+    count_launches(3);
+    k_compact_count<<<(unsigned)nb, 256, 0, s>>>(mask, nw, blk);
+    k_compact_scan<<<1, 1024, 0, s>>>(blk, nb, count);
+    k_compact_write<<<(unsigned)nb, 256, 0, s>>>(mask, nw, blk, out);
+    return GVC_OK;
+}
+
 // ------------------------------------------------- tiled decompress/average
 // One CTA owns a TILE-value slice of the dense output.  For every part (in
 // worker order) it binary-searches the slice's sub-range of that part's

@@ -42,5 +42,12 @@ int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, 
                   int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s);
 int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, cudaStream_t s);
 int iota_run(uint32_t *out, uint64_t n, cudaStream_t s);
+int gather_ef_run(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,
+                  const uint32_t *pmask, const float *pm, int pmode, float *out, cudaStream_t s);
+int below_keys_run(const float *v, const uint32_t *pos, uint64_t n, const uint32_t *thr, const uint32_t *excl,
+                   float *out, unsigned long long *count, cudaStream_t s);
+size_t compact_workspace_bytes(uint64_t n);
+int compact_mask_run(const uint32_t *mask, uint64_t n, uint32_t *out, unsigned long long *count, void *ws,
+                     size_t ws_bytes, cudaStream_t s);
 
 }  // namespace gvc

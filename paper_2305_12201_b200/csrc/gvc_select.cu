@@ -53,6 +53,7 @@ struct SelState {
     uint32_t fallback;
     uint32_t pending;
     unsigned long long cand_total;
+    unsigned long long shortfall;
     JState js[GVC_MAX_LADDER];
     float redsync_mean[GVC_MAX_LADDER];
 };
@@ -66,6 +67,9 @@ struct Plan {
     float *resid;
     uint64_t seed, stream, pos_base;
     uint64_t ks[GVC_MAX_LADDER];
+    // forced candidate threshold (DGC)
+    const uint32_t *key_est_dev;
+    int allow_short;
     // deferred residual update of the previous step (EF mode)
     uint32_t *pmask;
     const float *pm;
@@ -236,6 +240,16 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(Plan p)
 {
     __shared__ unsigned long long sh[33];
     SelState *st = p.st;
+    if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
+        if (threadIdx.x == 0) {
+            const uint32_t est = *p.key_est_dev;
+            st->key_est = est;
+            const uint64_t span = (1ull << 31) - (est < (1u << 31) ? est : (1u << 31) - 1);
+            int shf = bitlen64(span - 1) - 12;
+            st->shift0 = shf < 0 ? 0 : shf;
+        }
+        return;
+    }
     if (p.force_exact == 2) {  // test hook: an estimate that must miss -> exercises the refill path
         if (threadIdx.x == 0) {
             st->key_est = 0xffffffffu;
@@ -513,11 +527,28 @@ __global__ void __launch_bounds__(1024) k_resolve0(Plan p, int pass)
     unsigned long long total;
     block_excl_prefix((unsigned long long)x.x + x.y + x.z + x.w, sh, &total);
     if (pass == 0 && total < p.ks[0]) {
-        // the estimate overshot: zero the histogram for the exact re-collect
-        reinterpret_cast<uint4 *>(p.hist0)[threadIdx.x] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x == 0)
-            st->fallback = 1;
-        return;
+        if (p.allow_short) {
+            // DGC overshoot (compressors.py:126-128): keep every candidate
+            if (threadIdx.x == 0)
+                st->shortfall = p.ks[0] - total;
+            __syncthreads();
+            need[0] = total;
+            if (total == 0) {
+                if (threadIdx.x == 0) {
+                    set_jstate(st->js[0], 0xffffffffull, 1ull << 32, 0, 0);
+                    st->js[0].resolved = 1;
+                    st->cand_total = 0;
+                    st->pending = 0;
+                }
+                return;
+            }
+        } else {
+            // the estimate overshot: zero the histogram for the exact re-collect
+            reinterpret_cast<uint4 *>(p.hist0)[threadIdx.x] = make_uint4(0, 0, 0, 0);
+            if (threadIdx.x == 0)
+                st->fallback = 1;
+            return;
+        }
     }
     find_crossings(p.hist0, sh, p.n_ks, need, [&](int j, int b, unsigned long long above) {
         unsigned long long lo = (unsigned long long)key_est + ((unsigned long long)b << shift0);
@@ -989,7 +1020,7 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
                     c_above += cnt_tot[band];
                 }
             }
-            const unsigned long long k = p.ks[j];
+            const unsigned long long k = p.ks[j] - (j == 0 ? st->shortfall : 0ull);
             const double A = a_above + tsum[NB + j];
             double E = e_above + tsum[j];
             const float m = (float)(A / (double)k);
@@ -1013,6 +1044,7 @@ __global__ void __launch_bounds__(1024) k_finish(Plan p)
         res->candidates = st->cand_total;
         res->status = (st->nan_flag & 1u) ? GVC_ERR_NAN : ((st->nan_flag & 2u) ? GVC_ERR_STATE : GVC_OK);
         res->fallback_used = (int)st->fallback;
+        res->shortfall = st->shortfall;
     }
 }
 
@@ -1234,7 +1266,7 @@ static void launch_pipeline(Plan &p, cudaStream_t s)
     ProfScope all(PROF_SELECT, s);
     const int blocks = (int)p.B;
     int launches = 0;
-    if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0) {
+    if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
         uint64_t wb = (p.s_chunks + 31) / 32;
         int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
         k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p);
@@ -1296,6 +1328,8 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.seed = a->seed;
     p.stream = a->rng_stream;
     p.pos_base = a->pos_base;
+    p.key_est_dev = a->key_est_dev;
+    p.allow_short = a->key_est_dev ? a->allow_short : 0;
     p.pmask = p.ef ? a->pending_mask_dev : nullptr;
     p.pm = a->pending_m_dev;
     p.pmode = a->pending_mode;

@@ -308,13 +308,13 @@ def test_determinism(G):
     assert outs[0] == outs[1]
 
 
-@pytest.mark.parametrize("kind", ["topk", "redsync", "randomk"])
+@pytest.mark.parametrize("kind", ["topk", "redsync", "randomk", "dgc"])
 @pytest.mark.parametrize("workers", [1, 2])
 def test_run_iteration_vs_oracle(G, kind, workers):
     """Fused step (deferred residual mask included) vs an oracle replay of
     controller.py:192-281's data plane, every kind, 8 chained iterations."""
     n = 300_007
-    cfg = G.ControllerConfig(theta_min=10.0, theta_max=1000.0, epsilon=0.3 if kind != "randomk" else 0.05,
+    cfg = G.ControllerConfig(theta_min=10.0, theta_max=1000.0, epsilon=0.05 if kind == "randomk" else 0.3,
                              omega=0.05, window=3, compressor=G.CompressorKind(kind))
     state = G.ControllerState.fresh(cfg, workers)
     cost = G.CostModelParams(workers=workers)
@@ -355,3 +355,59 @@ def test_run_iteration_vs_oracle(G, kind, workers):
             for w in range(workers):
                 np.testing.assert_allclose(host(stores[w].residual), r_host[w], rtol=1e-5, atol=1e-6)
     assert seen - {"dense"}, seen
+
+
+# ------------------------------------------------------------------- DGC
+def test_dgc_degenerate_golden(G, golden):
+    """n <= 256: the sample is the whole vector, DGC == exact top-k (compressors.py:112-115)."""
+    d = golden("dgc_small")
+    K = G.CompressorKind("dgc")
+    for i in range(int(d["n_cases"])):
+        s, _ = G.compress(K, gv(G, d[f"{i}/x"]), float(d[f"{i}/cf"]), G.SeededRng(i))
+        assert np.array_equal(host(s.indices), d[f"{i}/idx"]), i
+        assert np.array_equal(bits(host(s.vals)), bits(d[f"{i}/vals"])), i
+
+
+@pytest.mark.parametrize("n", [300, 5_000, 20_000, 300_001, 4_000_000])
+def test_dgc_vs_oracle(G, n):
+    """Both DGC branches (exact top-k of `chosen`, and the overshoot pad/top-up)
+    bit-exact against the oracle's restatement over many seeds and CFs."""
+    K = G.CompressorKind("dgc")
+    for t, dist in enumerate(["gauss", "ties", "layered", "zeros"]):
+        x = _vec(dist, n, 70 + t)
+        g = gv(G, x)
+        for cf in (2.0, 10.0, 100.0, 1000.0):
+            if G.keep_count(n, cf) >= n:
+                continue
+            for seed in range(3 if n > 1_000_000 else 6):
+                rng = G.SeededRng(seed).split(t, int(cf))
+                s, _ = G.compress(K, g, cf, rng)
+                oi, ov = O.select("dgc", x, G.keep_count(n, cf), seed=rng.seed, stream=rng.stream)
+                assert np.array_equal(host(s.indices), oi), (dist, cf, seed)
+                assert np.array_equal(bits(host(s.vals)), bits(ov)), (dist, cf, seed)
+
+
+def test_dgc_overlap_distribution(G, golden):
+    """Reference's test_compressors.py:88-96 as a distribution over 300 seeds."""
+    d = golden("dgc_stats")
+    x = d["x"]
+    top = set(np.lexsort((np.arange(x.size), -np.abs(x)))[:100].tolist())
+    g = gv(G, x)
+    ours = []
+    for s in range(300):
+        sp, _ = G.compress(G.CompressorKind("dgc"), g, 100, G.SeededRng(s))
+        ours.append(len(set(host(sp.indices).tolist()) & top) / 100)
+    ours, ref = np.array(ours), d["overlaps"]
+    assert abs(ours.mean() - ref.mean()) < 0.03
+
+
+def test_dgc_compress_further_vs_oracle(G):
+    K = G.CompressorKind("dgc")
+    x = _vec("gauss", 200_003, 5)
+    for step in (2.0, 10.0, 100.0):
+        r1, r2 = G.SeededRng(1), G.SeededRng(2)
+        s1, _ = G.compress(K, gv(G, x), 10.0, r1)
+        s2, _ = G.compress_further(K, s1, step, r2)
+        i1, v1, _ = O.compress("dgc", x, 10.0, seed=1, stream=r1.stream)
+        i2, v2, _ = O.compress_further("dgc", i1, v1, x.size, step, seed=2, stream=r2.stream)
+        assert np.array_equal(host(s2.indices), i2) and np.array_equal(bits(host(s2.vals)), bits(v2))
