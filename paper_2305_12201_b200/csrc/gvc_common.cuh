@@ -77,7 +77,7 @@ __device__ __forceinline__ uint32_t lanemask_lt()
 
 __device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
 
-// Exclusive prefix sum across a 1024-thread block (warp shuffles, 2 barriers).
+// Exclusive prefix sum across a block of up to 1024 threads (warp shuffles, 2 barriers).
 // `sh` must hold 33 u64; *total (optional) receives the block total.
 __device__ __forceinline__ unsigned long long block_excl_prefix(unsigned long long v, unsigned long long *sh,
                                                                 unsigned long long *total = nullptr)
@@ -94,7 +94,8 @@ __device__ __forceinline__ unsigned long long block_excl_prefix(unsigned long lo
         sh[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        unsigned long long w = sh[lane], wi = w;
+        const int nwarps = (int)(blockDim.x >> 5);
+        unsigned long long w = lane < nwarps ? sh[lane] : 0ull, wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
@@ -113,7 +114,7 @@ __device__ __forceinline__ unsigned long long block_excl_prefix(unsigned long lo
     return r;
 }
 
-// Deterministic fp64 sum across a 1024-thread block: fixed xor tree per warp,
+// Deterministic fp64 sum across a block (<= 1024 threads): fixed xor tree per warp,
 // then warps added in index order.  `sh` must hold 33 doubles.
 __device__ __forceinline__ double block_sum_f64(double v, double *sh)
 {
@@ -124,7 +125,8 @@ __device__ __forceinline__ double block_sum_f64(double v, double *sh)
     __syncthreads();
     if (threadIdx.x == 0) {
         double r = 0.0;
-        for (int w = 0; w < 32; w++)
+        const int nwarps = (int)(blockDim.x >> 5);
+        for (int w = 0; w < nwarps; w++)
             r += sh[w];
         sh[32] = r;
     }
