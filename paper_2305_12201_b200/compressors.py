@@ -66,7 +66,7 @@ class SparseGradient:
     tensors produced by the kernels are trusted (the parity suite checks them).
     """
 
-    __slots__ = ("indices", "vals", "original_length", "achieved_cf")
+    __slots__ = ("indices", "vals", "original_length", "achieved_cf", "_payload")
 
     def __init__(self, indices, vals, original_length: int, achieved_cf: float, device=None):
         if isinstance(indices, torch.Tensor) and indices.is_cuda:
@@ -86,6 +86,7 @@ class SparseGradient:
         self.vals = vals_t
         self.original_length = int(original_length)
         self.achieved_cf = float(achieved_cf)
+        self._payload = None
 
     @classmethod
     def _wrap(cls, indices: torch.Tensor, vals: torch.Tensor, original_length: int,
@@ -95,6 +96,7 @@ class SparseGradient:
         s.vals = vals
         s.original_length = int(original_length)
         s.achieved_cf = float(achieved_cf)
+        s._payload = None
         return s
 
     @property
@@ -163,13 +165,18 @@ class Selection:
 
     def emit(self, j: int = 0, idx_map: torch.Tensor | None = None, resid: torch.Tensor | None = None,
              stats: torch.Tensor | None = None, sent_mask: torch.Tensor | None = None,
-             sent_m: torch.Tensor | None = None, count: int | None = None):
+             sent_m: torch.Tensor | None = None, count: int | None = None,
+             payload: torch.Tensor | None = None):
         """Index-ascending (indices, values) of ladder entry j; optionally the
         residual update, either direct (``resid``) or deferred (``sent_mask``).
         ``count`` overrides the entry count (a DGC overshoot keeps fewer)."""
         k = self.ks[j] if count is None else int(count)
-        out_idx = torch.empty(k, dtype=torch.uint32, device=self.device)
-        out_val = torch.empty(k, dtype=torch.float32, device=self.device)
+        if payload is not None:  # write straight into the packed wire buffer (exchange.new_payload)
+            out_idx = payload[0, :k].view(torch.uint32)
+            out_val = payload[1, :k].view(torch.float32)
+        else:
+            out_idx = torch.empty(k, dtype=torch.uint32, device=self.device)
+            out_val = torch.empty(k, dtype=torch.float32, device=self.device)
         nat.check(nat.load().gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
                                       nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
                                       nat.ptr(stats), nat.stream_ptr(self.device)), "gvc_emit")
@@ -273,13 +280,17 @@ def decompress(s: SparseGradient, layer_offsets: Sequence[int] | None = None) ->
 
 
 def aggregate_packed(idx: torch.Tensor, vals: torch.Tensor, counts: Sequence[int], n: int,
-                     out: torch.Tensor | None = None) -> torch.Tensor:
-    """fp64 worker-ordered mean of parts stored back to back in (idx, vals)."""
+                     out: torch.Tensor | None = None, offs: Sequence[int] | None = None) -> torch.Tensor:
+    """fp64 worker-ordered mean of parts in (idx, vals); part p starts at offs[p]
+    (default: back to back)."""
     dev = vals.device
     lib = nat.load()
     nparts = len(counts)
-    offs = np.zeros(nparts, dtype=np.uint64)
-    offs[1:] = np.cumsum(np.asarray(counts, dtype=np.uint64))[:-1]
+    if offs is None:
+        offs = np.zeros(nparts, dtype=np.uint64)
+        offs[1:] = np.cumsum(np.asarray(counts, dtype=np.uint64))[:-1]
+    else:
+        offs = np.asarray(offs, dtype=np.uint64)
     cnts = np.asarray(counts, dtype=np.uint64)
     if out is None:
         out = torch.empty(n, dtype=torch.float32, device=dev)

@@ -198,7 +198,8 @@ class _WorkerStep:
                                             nat.stream_ptr(g.device)), "apply_feedback")
             self.g_min = SparseGradient._wrap(_iota(self.n, g.device), resid.clone(), self.n, 1.0)
             self.sel1 = None
-            self._norm_dev = None
+            from .gradcore import squared_l2_norm_dev
+            self._norm_dev = squared_l2_norm_dev(resid)
             self.ladder = [k2] + list(extra_ks)
             if kind.name == TOPK:
                 ks = [k for k in self.ladder if k < self.n]
@@ -222,7 +223,7 @@ class _WorkerStep:
 
     def stats_dev(self) -> list[torch.Tensor]:
         """Device tensors whose bytes the host reads once per iteration."""
-        out = []
+        out = [self._norm_dev.reshape(1)] if self.identity1 else []
         if self.sel1 is not None:
             out.append(self.sel1.res_dev)
         if self.sel2 is not None:
@@ -231,6 +232,10 @@ class _WorkerStep:
 
     def gains_from(self, raw: list[bytes], norm_host: float | None):
         """(ef_norm, E_min, E_c, extra energies) from the read-back results."""
+        if self.identity1:
+            import numpy as np
+            norm_host = float(np.frombuffer(raw[0], dtype=np.float64)[0])
+            raw = raw[1:]
         results = [nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES]) for b in raw]
         r1 = results[0] if self.sel1 is not None else None
         r2 = results[-1] if self.sel2 is not None else None
@@ -258,9 +263,21 @@ class _WorkerStep:
         e_c = r2.kept_sq[0] if r2 is not None else e_min
         return norm, e_min, e_c, []
 
-    def emit(self, candidate: bool) -> SparseGradient:
-        """Materialise the chosen view; the residual update g_ef - sent is
-        deferred into the store's sent-mask (applied by the next fused pass)."""
+    def chosen_count(self, candidate: bool) -> int:
+        if self.kind.name == TOPK and not self.identity1:
+            return self.ladder[1 if candidate else 0]
+        return self.k2 if (candidate and self.sel2 is not None) else self.g_min.kept
+
+    def emit(self, candidate: bool, payload: torch.Tensor | None = None) -> SparseGradient:
+        """Materialise the chosen view (into ``payload`` when given); the residual
+        update g_ef - sent is deferred into the store's sent-mask (applied by the
+        next fused pass)."""
+        part = self._emit(candidate, payload)
+        if payload is not None and part.vals.data_ptr() == payload[1].data_ptr():
+            part._payload = payload
+        return part
+
+    def _emit(self, candidate: bool, payload: torch.Tensor | None) -> SparseGradient:
         lib = nat.load()
         store = self.store
         mode = 2 if self.kind.name == "redsync" else 1
@@ -278,10 +295,11 @@ class _WorkerStep:
         if self.kind.name == TOPK:
             j = 1 if candidate else 0
             k = self.ladder[j]
-            idx, vals = self.sel1.emit(j, sent_mask=mask, sent_m=store._pm)
+            idx, vals = self.sel1.emit(j, sent_mask=mask, sent_m=store._pm, payload=payload)
             part = SparseGradient._wrap(idx, vals, self.n, self.n / k)
         elif candidate and self.sel2 is not None:
-            idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, sent_mask=mask, sent_m=store._pm)
+            idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, sent_mask=mask, sent_m=store._pm,
+                                       payload=payload)
             part = SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
         else:
             part = self.g_min
@@ -327,7 +345,9 @@ class _DgcStep:
                                             nat.stream_ptr(g.device)), "apply_feedback")
             self.g_min = SparseGradient._wrap(_iota(self.n, g.device), resid.clone(), self.n, 1.0)
             self.norm = None
+            self.identity_level1 = True
         else:
+            self.identity_level1 = False
             pending = store._take_pending()
             idx, vals, res = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
                                         slot=slot + "a", want_result=True)
@@ -338,20 +358,26 @@ class _DgcStep:
             self.g_c = SparseGradient._wrap(idx2, vals2, self.n, self.n / k2)
         else:
             self.g_c = self.g_min
+        # (E_min, E_c, ||g_ef||^2) as device scalars: every rank's row travels the same way in C2
+        norm_dev = (squared_l2_norm_dev(store._resid) if self.norm is None
+                    else torch.full((), self.norm, dtype=torch.float64, device=g.device))
         self.stats = torch.stack([squared_l2_norm_dev(self.g_min.vals), squared_l2_norm_dev(self.g_c.vals),
-                                  squared_l2_norm_dev(store._resid) if self.norm is None
-                                  else torch.zeros((), dtype=torch.float64, device=g.device)])
+                                  norm_dev])
 
     def stats_dev(self) -> list[torch.Tensor]:
         return [self.stats]
 
     def gains_from(self, raw: list[bytes], norm_host=None):
         import numpy as np
-        e_min, e_c, n_id = np.frombuffer(raw[0], dtype=np.float64)
-        norm = self.norm if self.norm is not None else float(n_id)
-        return norm, float(e_min) if self.norm is not None else norm, float(e_c), []
+        e_min, e_c, norm = (float(x) for x in np.frombuffer(raw[0], dtype=np.float64))
+        if self.identity_level1:  # theta_min == 1: the level-1 gain is exactly 1 (same sum)
+            e_min = norm
+        return norm, e_min, e_c, []
 
-    def emit(self, candidate: bool) -> SparseGradient:
+    def chosen_count(self, candidate: bool) -> int:
+        return (self.g_c if candidate else self.g_min).kept
+
+    def emit(self, candidate: bool, payload: torch.Tensor | None = None) -> SparseGradient:
         part = self.g_c if candidate else self.g_min
         store = self.store
         if self.norm is None:  # identity level 1: direct residual update
@@ -418,21 +444,31 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
             steps.append(_WorkerStep(kind, g.values, store, k1, k2, extra_ks, rng, i, rank + w))
 
     # ---- one device->host read per iteration: every worker's norms and energies
-    norm_host = None
-    if getattr(steps[0], "identity1", False):
-        from .gradcore import squared_l2_norm_dev
-        norm_dev = [squared_l2_norm_dev(s.resid) for s in steps]
-        norm_host = [float(x) for x in torch.stack(norm_dev).cpu()]
-    results = _read_results([t for s in steps for t in s.stats_dev()])
-    local = []
-    pos = 0
-    for w, s in enumerate(steps):
-        cnt = len(s.stats_dev())
-        local.append(s.gains_from(results[pos:pos + cnt], norm_host[w] if norm_host else None))
-        pos += cnt
+    stats = [t for s in steps for t in s.stats_dev()]
     if group is not None:
-        from .exchange import allgather_gain_rows
-        local = allgather_gain_rows(local[0], group, grads[0].values.device)
+        # C2: the raw result bytes of every rank, gathered on the device, read once
+        from .exchange import allgather_stats
+        flat = torch.cat([t.reshape(-1).view(torch.uint8) for t in stats])
+        import torch.distributed as dist
+        if dist.get_backend(group) != "nccl":
+            flat = flat.cpu()
+        rows = allgather_stats(flat, group)
+        sizes = [t.numel() * t.element_size() for t in stats]
+        local = []
+        for row in rows:
+            raw, pos = [], 0
+            for nb in sizes:
+                raw.append(row[pos:pos + nb].tobytes())
+                pos += nb
+            local.append(steps[0].gains_from(raw, None))
+    else:
+        results = _read_results(stats)
+        local = []
+        pos = 0
+        for w, s in enumerate(steps):
+            cnt = len(s.stats_dev())
+            local.append(s.gains_from(results[pos:pos + cnt], None))
+            pos += cnt
     ef_norms = [x[0] for x in local]
 
     if all(nv == 0.0 for nv in ef_norms):
@@ -473,7 +509,12 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         floats = length
         words = dense_message_words(length)
     else:
-        sent = [s.emit(decision.choice == CANDIDATE) for s in steps]
+        cand = decision.choice == CANDIDATE
+        if group is not None:  # emit straight into the packed wire buffer of the all-gather
+            from .exchange import new_payload
+            sent = [s.emit(cand, new_payload(s.chosen_count(cand), grads[0].values.device)) for s in steps]
+        else:
+            sent = [s.emit(cand) for s in steps]
         floats = sent[0].kept
         words = sparse_message_words(sent[0])
 

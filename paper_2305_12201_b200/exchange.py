@@ -17,6 +17,7 @@ host-side packing logic.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -24,28 +25,38 @@ from .compressors import SparseGradient, aggregate_packed
 from .gradcore import GradientVector
 
 
-def allgather_gain_rows(row, group, device) -> list:
-    """C2: (ef_norm, E_min, E_c, [extra...]) of every rank, in rank order.
+def allgather_stats(flat: torch.Tensor, group=None) -> "np.ndarray":
+    """C2: every rank's raw statistics bytes (selection result structs), rank order.
 
-    An all-gather (not an all-reduce) so every rank sums the ratios in the
-    reference's worker order (controller.py:284-288) and takes the identical
-    epsilon decision.
+    The rows are gathered straight from device memory and read back once, so
+    every rank forms the reference's worker-ordered mean (controller.py:284-288)
+    from identical inputs and takes the identical epsilon decision.  An
+    all-gather, not an all-reduce: the summation order must be the reference's.
     """
-    norm, e_min, e_c, extra = row
-    t = torch.tensor([[norm, e_min, e_c, *extra]], dtype=torch.float64)
-    if dist.get_backend(group) == "nccl":
-        t = t.to(device)
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(out, t, group=group)
-    return [(r[0], r[1], r[2], list(r[3:])) for r in torch.cat(out).cpu().tolist()]
+    world = dist.get_world_size(group)
+    out = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(out, flat, group=group)
+    return torch.stack(out).cpu().numpy()
+
+
+def payload_width(k: int) -> int:
+    """Row length of the packed payload: k rounded up to 4 so both rows stay 16-byte aligned."""
+    return (k + 3) & ~3
+
+
+def new_payload(k: int, device) -> torch.Tensor:
+    """(2, kpad) int32 wire buffer: row 0 index bits, row 1 value bits."""
+    return torch.empty((2, payload_width(k)), dtype=torch.int32, device=device)
 
 
 def pack_payload(part: SparseGradient) -> torch.Tensor:
-    """(2, k) int32 view-compatible buffer: row 0 indices bits, row 1 value bits."""
+    buf = getattr(part, "_payload", None)
+    if buf is not None:
+        return buf
     k = part.kept
-    buf = torch.empty((2, k), dtype=torch.int32, device=part.vals.device)
-    buf[0].copy_(part.indices.view(torch.int32))
-    buf[1].copy_(part.vals.view(torch.int32))
+    buf = new_payload(k, part.vals.device)
+    buf[0, :k].copy_(part.indices.view(torch.int32))
+    buf[1, :k].copy_(part.vals.view(torch.int32))
     return buf
 
 
@@ -53,19 +64,28 @@ def allgather_payload(part: SparseGradient, group=None) -> tuple[torch.Tensor, t
     """C1: every rank's (indices, vals), concatenated in rank order."""
     world = dist.get_world_size(group)
     payload = pack_payload(part)
-    k = part.kept
-    out = torch.empty((world, 2, k), dtype=torch.int32, device=payload.device)
+    k, kp = part.kept, payload.shape[1]
+    out = torch.empty((world, 2, kp), dtype=torch.int32, device=payload.device)
     dist.all_gather_into_tensor(out, payload, group=group)
-    idx = out[:, 0, :].contiguous().view(torch.uint32).reshape(-1)
-    vals = out[:, 1, :].contiguous().view(torch.float32).reshape(-1)
+    idx = out[:, 0, :k].contiguous().view(torch.uint32).reshape(-1)
+    vals = out[:, 1, :k].contiguous().view(torch.float32).reshape(-1)
     return idx, vals
 
 
 def allgather_aggregate(part: SparseGradient, group=None, out: torch.Tensor | None = None) -> GradientVector:
-    """C1 + K7: the rank-ordered fp64 mean of every rank's sparse part."""
+    """C1 + K7: the rank-ordered fp64 mean of every rank's sparse part.
+
+    The all-gathered (world, 2, kpad) buffer is averaged in place: part r's
+    indices start at r*2*kpad, its values kpad words later -- no repacking.
+    """
     world = dist.get_world_size(group)
-    idx, vals = allgather_payload(part, group)
-    res = aggregate_packed(idx, vals, [part.kept] * world, part.original_length, out=out)
+    payload = pack_payload(part)
+    k, kp = part.kept, payload.shape[1]
+    buf = torch.empty((world, 2, kp), dtype=torch.int32, device=payload.device)
+    dist.all_gather_into_tensor(buf, payload, group=group)
+    flat = buf.view(-1)
+    res = aggregate_packed(flat.view(torch.uint32), flat[kp:].view(torch.float32), [k] * world,
+                           part.original_length, out=out, offs=[r * 2 * kp for r in range(world)])
     return GradientVector._wrap(res)
 
 

@@ -188,10 +188,12 @@ def test_product_never_imports_oracle():
 
 def _gain_worker(rank, world, port, q):
     import torch.distributed as dist
-    from paper_2305_12201_b200.exchange import allgather_gain_rows
+    from paper_2305_12201_b200.exchange import allgather_stats
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    rows = allgather_gain_rows((10.0 + rank, 4.0 + rank, 1.0 + rank, [0.5 * rank]), None, torch.device("cpu"))
-    q.put((rank, rows, C._mean_raw_gain([r[1] for r in rows], [r[0] for r in rows])))
+    row = torch.tensor([10.0 + rank, 4.0 + rank, 1.0 + rank, 0.5 * rank], dtype=torch.float64)
+    rows = allgather_stats(row.view(torch.uint8), None)
+    vals = [np.frombuffer(r.tobytes(), dtype=np.float64).tolist() for r in rows]
+    q.put((rank, vals, C._mean_raw_gain([v[1] for v in vals], [v[0] for v in vals])))
     dist.destroy_process_group()
 
 
@@ -209,5 +211,5 @@ def test_gain_exchange_gloo_world2():
     out = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(60)
-    assert out[0][1] == out[1][1] == [(10.0, 4.0, 1.0, [0.0]), (11.0, 5.0, 2.0, [0.5])]
+    assert out[0][1] == out[1][1] == [[10.0, 4.0, 1.0, 0.0], [11.0, 5.0, 2.0, 0.5]]
     assert out[0][2] == out[1][2] == (0.4 + 5.0 / 11.0) / 2
