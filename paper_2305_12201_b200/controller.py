@@ -316,7 +316,8 @@ def _read_results(tensors: list[torch.Tensor]) -> list[bytes]:
     """One device->host copy for every worker's device-side statistics."""
     if not tensors:
         return []
-    flat = torch.cat([t.reshape(-1).view(torch.uint8) for t in tensors]).cpu().numpy().tobytes()
+    flat = nat.d2h_bytes(tensors[0] if len(tensors) == 1 else
+                         torch.cat([t.reshape(-1).view(torch.uint8) for t in tensors]))
     out, pos = [], 0
     for t in tensors:
         nb = t.numel() * t.element_size()

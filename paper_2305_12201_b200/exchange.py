@@ -34,9 +34,14 @@ def allgather_stats(flat: torch.Tensor, group=None) -> "np.ndarray":
     all-gather, not an all-reduce: the summation order must be the reference's.
     """
     world = dist.get_world_size(group)
+    if flat.is_cuda:
+        out = torch.empty((world, flat.numel()), dtype=flat.dtype, device=flat.device)
+        dist.all_gather_into_tensor(out, flat, group=group)
+        from . import _native as nat
+        return np.frombuffer(nat.d2h_bytes(out), dtype=np.uint8).reshape(world, -1)
     out = [torch.empty_like(flat) for _ in range(world)]
     dist.all_gather(out, flat, group=group)
-    return torch.stack(out).cpu().numpy()
+    return torch.stack(out).numpy()
 
 
 def payload_width(k: int) -> int:
