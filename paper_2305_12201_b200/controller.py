@@ -444,6 +444,20 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         else:
             steps.append(_WorkerStep(kind, g.values, store, k1, k2, extra_ks, rng, i, rank + w))
 
+    # ---- speculative emit: enqueue the previous step's choice right behind the
+    # select so the GPU keeps working while the host reads the gains back; a
+    # misprediction is re-emitted below (the sent mask is rebuilt from zero)
+    dev = grads[0].values.device
+    spec = getattr(state, "_spec_choice", CANDIDATE)
+    spec_parts = None
+    if kind.name == TOPK and not steps[0].identity1 and spec in (CANDIDATE, MINIMUM):
+        c = spec == CANDIDATE
+        if group is not None:
+            from .exchange import new_payload
+            spec_parts = [s.emit(c, new_payload(s.chosen_count(c), dev)) for s in steps]
+        else:
+            spec_parts = [s.emit(c) for s in steps]
+
     # ---- one device->host read per iteration: every worker's norms and energies
     stats = [t for s in steps for t in s.stats_dev()]
     if group is not None:
@@ -472,8 +486,16 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
             pos += cnt
     ef_norms = [x[0] for x in local]
 
+    def drop_speculation():
+        for store in stores:
+            if store._mask is not None:
+                store._mask.zero_()
+            store._pmode = 0
+
     if all(nv == 0.0 for nv in ef_norms):
         # vanished gradient: dense no-op (controller.py:217-230)
+        if spec_parts is not None:
+            drop_speculation()
         sent = []
         for store in stores:
             sent.append(GradientVector._wrap(store._resid, grads[0].layer_offsets))
@@ -500,6 +522,11 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     t_compress = t_min + t_step
 
     decision = select_cf(delta_c, delta_min, cfg.epsilon, candidate_cf=candidate_cf, minimum_cf=theta_min)
+    if decision.choice != DENSE:
+        state._spec_choice = decision.choice
+    if spec_parts is not None and decision.choice != spec:
+        drop_speculation()
+        spec_parts = None
     if decision.choice == DENSE:
         sent = []
         for store in stores:
@@ -511,9 +538,11 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         words = dense_message_words(length)
     else:
         cand = decision.choice == CANDIDATE
-        if group is not None:  # emit straight into the packed wire buffer of the all-gather
+        if spec_parts is not None:
+            sent = spec_parts
+        elif group is not None:  # emit straight into the packed wire buffer of the all-gather
             from .exchange import new_payload
-            sent = [s.emit(cand, new_payload(s.chosen_count(cand), grads[0].values.device)) for s in steps]
+            sent = [s.emit(cand, new_payload(s.chosen_count(cand), dev)) for s in steps]
         else:
             sent = [s.emit(cand) for s in steps]
         floats = sent[0].kept
