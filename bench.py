@@ -55,53 +55,71 @@ def peaks():
         return 6650.0, "fallback"
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        print(sm, rs, flush=True)
+    except Exception:
+        pass
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
     """SM clock and throttle reasons sampled through NVML every ~2 ms while the
-    timed region runs (nvidia-smi's own polling is too coarse for a region of
-    a few milliseconds)."""
+    timed region runs, from a separate process (no GIL contention with the
+    step's host code; nvidia-smi's own polling is too coarse here)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.stop, self.thread = gpu, [], threading.Event(), None
+        self.gpu, self.lines, self.proc = gpu, [], None
 
     def __enter__(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.thread = threading.Thread(target=self._run, daemon=True)
+            env = dict(os.environ)
+            env.pop("CUDA_VISIBLE_DEVICES", None)
+            phys = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+            idx = phys[self.gpu] if phys and phys[0] and self.gpu < len(phys) else str(self.gpu)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, idx], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True, env=env)
+            self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
-        except Exception as e:  # no NVML: report it instead of guessing
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10:  # wait for the first sample
+                time.sleep(0.01)
+        except Exception as e:
             self.err = repr(e)
         return self
 
-    def _run(self):
-        nv = self.nv
-        while not self.stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append((sm, rs))
-            except Exception:
-                pass
-            time.sleep(0.002)
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.split())
 
     def __exit__(self, *exc):
-        self.stop.set()
-        if self.thread is not None:
-            self.thread.join(1.0)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = [(int(a), int(b)) for a, b in (ln for ln in self.lines if len(ln) == 2 and ln[0] != "max")]
+        mx = [int(ln[1]) for ln in self.lines if len(ln) == 2 and ln[0] == "max"]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled: " + getattr(self, "err", "")]}
-        sm = [r[0] for r in self.rows]
-        reasons = sorted({name for _, rs in self.rows for name, bit in self.REASONS.items() if rs & bit})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": getattr(self, "max_sm", None),
-                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
+        sm = [r[0] for r in rows]
+        reasons = sorted({name for _, rs in rows for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx[0] if mx else None, "reasons": reasons,
+                "samples": len(rows), "source": "nvml"}
 
 
 # ------------------------------------------------------------- CPU legs
