@@ -236,6 +236,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         dist.barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region (re-enabled right after)
     chosen.clear()
     nat.prof_read()
     prof_on = os.environ.get("GVC_BENCH_NOPROF") != "1"
@@ -252,7 +255,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     launches = nat.launch_count() - launches0
     prof = nat.prof_read()
     nat.prof_enable(False)
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    gc.enable()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if pg is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -315,6 +320,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
                            "frac": comp_achieved / peak if comp_achieved else None},
         "breakdown_ms": {"collect": col_launch, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms},
         "gpu_launches": int(launches),
+        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * M,
                 "d2h_bytes_per_step": nat.RESULT_BYTES, "ms_per_step": e2e_step},
