@@ -314,48 +314,47 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(Plan p)
 }
 
 // ----------------------------------------------------------------- collect
-// Candidate compaction for 4 values of one lane in lane-major index order.
-// Straight-line (no early exit) so the four ballots stay warp-convergent; the
-// per-candidate stores and histogram atomics are predicated.
+// Candidate compaction for 4 consecutive values of one lane (lane-major index
+// order within the warp).  Straight-line so the ballots stay convergent; the
+// histogram atomic is unconditional (non-candidates hit a per-lane dummy bin)
+// and only the two candidate stores are predicated.  `o` is the segment-local
+// candidate count; `pos` the global position of v[0].
 template <int KM>
-__device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32_t pos0, int valid,
-                                      uint32_t key_est, int shift0, uint32_t *h, float *cval, uint32_t *cidx,
-                                      uint32_t &ccount, uint32_t &nan_any)
+__device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32_t pos, uint32_t valid,
+                                      uint32_t key_est, int shift0, uint32_t *h, uint32_t dummy, float *cval,
+                                      uint32_t *cidx, uint32_t &ccount)
 {
-    uint32_t key[4];
+    uint32_t key[4], m[4];
     bool pr[4];
-    uint32_t m[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        key[c] = cand_key<KM>(p, v[c], pos0 + c);
-        pr[c] = (c < valid) && key[c] >= key_est;
-        if (KM == KEY_MAG)
-            nan_any |= (uint32_t)((c < valid) & (key[c] > 0x7f800000u));
+        key[c] = cand_key<KM>(p, v[c], pos + c);
+        pr[c] = ((uint32_t)c < valid) & (key[c] >= key_est);
         m[c] = __ballot_sync(0xffffffffu, pr[c]);
     }
     const uint32_t lt = lanemask_lt();
     uint32_t o = ccount + __popc(m[0] & lt) + __popc(m[1] & lt) + __popc(m[2] & lt) + __popc(m[3] & lt);
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        // the histogram update is unconditional (non-candidates hit a per-lane
-        // dummy bin past the end) so only the two stores are predicated
-        const uint32_t bin = pr[c] ? min((key[c] - key_est) >> shift0, (uint32_t)GVC_H0_BINS - 1)
-                                   : (uint32_t)GVC_H0_BINS + (threadIdx.x & 31);
+        const uint32_t bin = pr[c] ? min((key[c] - key_est) >> shift0, (uint32_t)GVC_H0_BINS - 1) : dummy;
         atomicAdd(&h[bin], 1u);
         if (pr[c]) {
             cval[o] = v[c];
-            cidx[o] = pos0 + c;
+            cidx[o] = pos + c;
         }
         o += pr[c];
     }
     ccount += __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
 }
 
-// One warp per segment.  EF: v = fl32(g + r) written back over r (the only
-// full-size write of the step); !EF: v read from `values`.  REFILL re-collects
-// from the already-written g_ef with key_est = 0 (exactness fallback).
-template <int KM, bool EF>
-__global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
+// One warp per segment.  EF: v = fl32(g + r_true) written back over r (the only
+// full-size write of the step), where r_true applies the previous step's
+// deferred residual update (PM = pending mode, 0 none); !EF: v read from
+// `values`.  REFILL re-collects from the already-written g_ef with key_est = 0
+// (exactness fallback).  NaN keys are always candidates and are flagged by the
+// candidate passes, not here.
+template <int KM, bool EF, int PM>
+__global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(Plan p, int refill)
 {
     __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
@@ -369,17 +368,20 @@ __global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
     const uint32_t key_est = refill ? 0u : p.st->key_est;
     const int shift0 = refill ? (KM == KEY_MAG ? 19 : 20) : p.st->shift0;
     const bool do_ef = EF && !refill;
-    const float *src = (EF ? (refill ? p.resid : p.g) : p.values);
-    const float pm = (do_ef && p.pmask && p.pmode == 2) ? *p.pm : 0.f;
+    const float pm = (EF && PM == 2 && !refill) ? *p.pm : 0.f;
+    const uint32_t dummy = GVC_H0_BINS + lane;
     double nacc = 0.0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
-        const uint64_t end = min(p.n, beg + p.seg_len);
+        const uint32_t len = (uint32_t)(min(p.n, beg + p.seg_len) - beg);
+        const float *src = (EF ? (refill ? p.resid : p.g) : p.values) + beg;
+        float *rp = p.resid + beg;
+        const uint32_t *mp = p.pmask + (beg >> 5);
         float *cval = p.cand_val + beg;
         uint32_t *cidx = p.cand_idx + beg;
-        uint32_t ccount = 0, nan_any = 0;
-        uint64_t i = beg;
-        for (; i + GVC_SEG_QUANTUM <= end; i += GVC_SEG_QUANTUM) {
+        uint32_t ccount = 0;
+        uint32_t i = 0;
+        for (; i + GVC_SEG_QUANTUM <= len; i += GVC_SEG_QUANTUM) {
             float4 a[4], b[4];
 #pragma unroll
             for (int u = 0; u < 4; u++)
@@ -387,24 +389,21 @@ __global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
             if (do_ef) {
 #pragma unroll
                 for (int u = 0; u < 4; u++)
-                    b[u] = ld_stream(reinterpret_cast<const float4 *>(p.resid + i + u * 128) + lane);
-                if (p.pmask) {
-                    // deferred update of the previous step: the 16 mask words of this
-                    // 512-value chunk in one coalesced load (lanes 0..15), shuffled to
-                    // the lanes that own their 4-bit slices, cleared after use
-                    const uint64_t w0 = i >> 5;
-                    const uint32_t wreg = lane < 16 ? p.pmask[w0 + lane] : 0u;
+                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
+                if (PM) {
+                    // the 16 mask words of this chunk in one load (lanes 0..15), shuffled
+                    // to the lanes owning their 4-bit slices, cleared after use
+                    const uint32_t wreg = lane < 16 ? mp[(i >> 5) + lane] : 0u;
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
-                        const uint32_t w = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3));
-                        const uint32_t bits = (w >> ((lane & 7) * 4)) & 0xfu;
-                        b[u].x = (bits & 1u) ? pending_resid(b[u].x, p.pmode, pm) : b[u].x;
-                        b[u].y = (bits & 2u) ? pending_resid(b[u].y, p.pmode, pm) : b[u].y;
-                        b[u].z = (bits & 4u) ? pending_resid(b[u].z, p.pmode, pm) : b[u].z;
-                        b[u].w = (bits & 8u) ? pending_resid(b[u].w, p.pmode, pm) : b[u].w;
+                        const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
+                        b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
+                        b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
+                        b[u].z = (bits & 4u) ? pending_resid(b[u].z, PM, pm) : b[u].z;
+                        b[u].w = (bits & 8u) ? pending_resid(b[u].w, PM, pm) : b[u].w;
                     }
                     if (wreg)
-                        p.pmask[w0 + lane] = 0u;
+                        p.pmask[(beg >> 5) + (i >> 5) + lane] = 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
@@ -412,52 +411,49 @@ __global__ void __launch_bounds__(GVC_THREADS, 5) k_collect(Plan p, int refill)
                     a[u].y = __fadd_rn(a[u].y, b[u].y);
                     a[u].z = __fadd_rn(a[u].z, b[u].z);
                     a[u].w = __fadd_rn(a[u].w, b[u].w);
-                    st_stream(reinterpret_cast<float4 *>(p.resid + i + u * 128) + lane, a[u]);
+                    st_stream(reinterpret_cast<float4 *>(rp + i + u * 128) + lane, a[u]);
                 }
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
-                float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+                const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
                 if (!refill) {
 #pragma unroll
                     for (int c = 0; c < 4; c++)
                         nacc = __fma_rn((double)v[c], (double)v[c], nacc);
                 }
-                push4<KM>(p, v, (uint32_t)(i + u * 128 + lane * 4), 4, key_est, shift0, h, cval, cidx, ccount,
-                          nan_any);
+                push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
+                          cidx, ccount);
             }
         }
         // tail: one value per lane, lane-major order preserved
-        for (; i < end; i += 32) {
-            uint64_t t = i + lane;
+        for (; i < len; i += 32) {
+            const uint32_t t = i + lane;
             float v[4] = {0.f, 0.f, 0.f, 0.f};
-            int valid = t < end ? 1 : 0;
+            const uint32_t valid = t < len ? 1u : 0u;
             if (valid) {
                 float x = src[t];
                 if (do_ef) {
-                    float r = p.resid[t];
-                    if (p.pmask) {
-                        const uint32_t bit = 1u << (t & 31);
-                        if (p.pmask[t >> 5] & bit) {
-                            r = pending_resid(r, p.pmode, pm);
-                            atomicAnd(&p.pmask[t >> 5], ~bit);
+                    float r = rp[t];
+                    if (PM) {
+                        const uint64_t gpos = beg + t;
+                        const uint32_t bit = 1u << (gpos & 31);
+                        if (p.pmask[gpos >> 5] & bit) {
+                            r = pending_resid(r, PM, pm);
+                            atomicAnd(&p.pmask[gpos >> 5], ~bit);
                         }
                     }
                     x = __fadd_rn(x, r);
-                    p.resid[t] = x;
+                    rp[t] = x;
                 }
                 v[0] = x;
                 if (!refill)
                     nacc = __fma_rn((double)x, (double)x, nacc);
             }
-            push4<KM>(p, v, (uint32_t)t, valid, key_est, shift0, h, cval, cidx, ccount, nan_any);
+            push4<KM>(p, v, (uint32_t)beg + t, valid, key_est, shift0, h, dummy, cval, cidx, ccount);
         }
-        nan_any = __any_sync(0xffffffffu, nan_any);
-        if (lane == 0) {
+        if (lane == 0)
             p.seg_cnt[seg] = ccount;
-            if (nan_any)
-                atomicOr(&p.st->nan_flag, 1u);
-        }
     }
     nacc = warp_sum_f64(nacc);
     if (lane == 0)
@@ -702,6 +698,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
             for (int c = 0; c < 4; c++) {
                 if (!ok[c])
                     continue;
+                if (KM == KEY_MAG && key[c] > 0x7f800000u)
+                    atomicOr(&st->nan_flag, 1u);  // NaN keys are always candidates
                 const double v2 = (double)v[c] * (double)v[c];
                 int band = 0;
 #pragma unroll
@@ -1275,16 +1273,20 @@ static void launch_pipeline(Plan &p, cudaStream_t s)
     k_sample_resolve<<<1, 1024, 0, s>>>(p);
     {
         ProfScope pc(PROF_COLLECT, s);
-        if (p.ef)
-            k_collect<KM, true><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+        if (!p.ef)
+            k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+        else if (!p.pmask)
+            k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+        else if (p.pmode == 1)
+            k_collect<KM, true, 1><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
         else
-            k_collect<KM, false><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+            k_collect<KM, true, 2><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
     }
     k_resolve0<<<1, 1024, 0, s>>>(p, 0);
     if (p.ef)
-        k_collect<KM, true><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
+        k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     else
-        k_collect<KM, false><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
+        k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     k_resolve0<<<1, 1024, 0, s>>>(p, 1);
     launches += 5;
     for (int l = 0; l < GVC_MAX_LEVELS; l++) {
