@@ -381,21 +381,37 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(Plan p, int refill)
         uint32_t *cidx = p.cand_idx + beg;
         uint32_t ccount = 0;
         uint32_t i = 0;
-        for (; i + GVC_SEG_QUANTUM <= len; i += GVC_SEG_QUANTUM) {
-            float4 a[4], b[4];
+        // software pipeline over 256-value steps: the next step's g / r loads are
+        // in flight while this step is added, reduced and compacted
+        constexpr uint32_t STEP = 256;
+        const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
+        float4 a[2], b[2];
+        if (nfull) {
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
+            for (int u = 0; u < 2; u++) {
+                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + u * 128) + lane);
+                if (do_ef)
+                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + u * 128) + lane);
+            }
+        }
+        for (; i < nfull; i += STEP) {
+            float4 na[2], nb[2];
+            const bool more = i + STEP < nfull;
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    na[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + STEP + u * 128) + lane);
+                    if (do_ef)
+                        nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
+                }
+            }
             if (do_ef) {
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
                 if (PM) {
-                    // the 16 mask words of this chunk in one load (lanes 0..15), shuffled
-                    // to the lanes owning their 4-bit slices, cleared after use
-                    const uint32_t wreg = lane < 16 ? mp[(i >> 5) + lane] : 0u;
+                    // the 8 mask words of this step in one load (lanes 0..7), shuffled to
+                    // the lanes owning their 4-bit slices, cleared after use
+                    const uint32_t wreg = lane < 8 ? mp[(i >> 5) + lane] : 0u;
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < 2; u++) {
                         const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
                         b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
                         b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(Plan p, int refill)
                         p.pmask[(beg >> 5) + (i >> 5) + lane] = 0u;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < 2; u++) {
                     a[u].x = __fadd_rn(a[u].x, b[u].x);
                     a[u].y = __fadd_rn(a[u].y, b[u].y);
                     a[u].z = __fadd_rn(a[u].z, b[u].z);
@@ -415,7 +431,7 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(Plan p, int refill)
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < 2; u++) {
                 const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
                 if (!refill) {
 #pragma unroll
@@ -424,6 +440,13 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(Plan p, int refill)
                 }
                 push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
                           cidx, ccount);
+            }
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    a[u] = na[u];
+                    b[u] = nb[u];
+                }
             }
         }
         // tail: one value per lane, lane-major order preserved
