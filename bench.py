@@ -240,6 +240,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region (re-enabled right after)
     chosen.clear()
+    from paper_2305_12201_b200.controller import STATS
+    for key in STATS:
+        STATS[key] = 0
     nat.prof_read()
     prof_on = os.environ.get("GVC_BENCH_NOPROF") != "1"
     nat.prof_enable(prof_on)
@@ -320,7 +323,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
                            "frac": comp_achieved / peak if comp_achieved else None},
         "breakdown_ms": {"collect": col_launch, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms},
         "gpu_launches": int(launches),
-        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms),
+                    "argmax": step_ms.index(max(step_ms))},
+        "controller": dict(STATS),
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * M,
                 "d2h_bytes_per_step": nat.RESULT_BYTES, "ms_per_step": e2e_step},

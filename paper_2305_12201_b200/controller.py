@@ -34,6 +34,10 @@ CANDIDATE = "candidate"
 MINIMUM = "minimum"
 DENSE = "dense"
 
+# observability counters (bench.py reports them): exact-path re-scans after a
+# missed threshold estimate, and speculative emits that had to be redone
+STATS = {"fallbacks": 0, "spec_misses": 0, "steps": 0}
+
 _STAGE_MIN = 0   # rng substream tags (controller.py:33-35)
 _STAGE_STEP = 1
 
@@ -237,6 +241,7 @@ class _WorkerStep:
             norm_host = float(np.frombuffer(raw[0], dtype=np.float64)[0])
             raw = raw[1:]
         results = [nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES]) for b in raw]
+        STATS["fallbacks"] += sum(int(r.fallback_used) for r in results)
         r1 = results[0] if self.sel1 is not None else None
         r2 = results[-1] if self.sel2 is not None else None
         for r in results:
@@ -524,7 +529,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     decision = select_cf(delta_c, delta_min, cfg.epsilon, candidate_cf=candidate_cf, minimum_cf=theta_min)
     if decision.choice != DENSE:
         state._spec_choice = decision.choice
+    STATS["steps"] += 1
     if spec_parts is not None and decision.choice != spec:
+        STATS["spec_misses"] += 1
         drop_speculation()
         spec_parts = None
     if decision.choice == DENSE:
