@@ -81,6 +81,8 @@ struct Plan {
     SelState *st;
     uint32_t *hist0, *histl, *shist;
     uint32_t *seg_cnt;                     // [SEG_MAX] candidates per segment
+    uint32_t *seg_mcnt;                    // [SEG_MAX] level-0 bin members per segment
+    uint32_t *mem_idx;                     // [n_pad] members: segment-local candidate offsets
     uint32_t *seg_band, *seg_tie;          // [L][SEG_MAX]
     double *blk_norm;                      // [BLK_MAX]
     uint32_t *blk_band_cnt, *blk_tie_cnt;  // [L][BLK_MAX]
@@ -125,6 +127,7 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
     q->histl = (uint32_t *)take(L * GVC_HL_BINS * 4);
     q->shist = (uint32_t *)take(GVC_SAMPLE_BINS * 4);
     q->seg_cnt = (uint32_t *)take(SM * 4);
+    q->seg_mcnt = (uint32_t *)take(SM * 4);
     q->seg_band = (uint32_t *)take(L * SM * 4);
     q->seg_tie = (uint32_t *)take(L * SM * 4);
     q->blk_norm = (double *)take(BM * 8);
@@ -139,6 +142,7 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
     q->blk_emit = (double *)take(2 * BM * 8);
     q->cand_val = (float *)take(n_pad * 4);
     q->cand_idx = (uint32_t *)take(n_pad * 4);
+    q->mem_idx = (uint32_t *)take(n_pad * 4);
     q->S = S;
     q->B = (S + GVC_WARPS_PER_BLOCK - 1) / GVC_WARPS_PER_BLOCK;
     q->seg_len = seg_len;
@@ -590,105 +594,40 @@ __global__ void __launch_bounds__(1024) k_resolve0(Plan p, int pass)
     }
 }
 
-// Refinement histogram: candidates whose key lies in an unresolved interval.
-// Intervals are hoisted into registers as 32-bit (lo, width-1, shift) so the
-// membership test is one wrapping subtract and compare per ladder entry.
-template <int KM, int NB>
-__global__ void __launch_bounds__(GVC_THREADS) k_level_hist(Plan p)
-{
-    SelState *st = p.st;
-    if (st->pending == 0)
-        return;
-    const int lane = threadIdx.x & 31;
-    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + (threadIdx.x >> 5);
-    if (seg >= p.S)
-        return;
-    uint32_t lo[NB], wm1[NB], sh[NB];
-    bool act[NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        act[j] = j < p.n_ks && !st->js[j].resolved;
-        lo[j] = act[j] ? (uint32_t)st->js[j].lo : 0u;
-        wm1[j] = act[j] ? (uint32_t)(st->js[j].hi - st->js[j].lo - 1) : 0u;
-        sh[j] = act[j] ? (uint32_t)st->js[j].shift : 0u;
-    }
-    const uint64_t beg = (uint64_t)seg * p.seg_len;
-    const uint32_t cnt = p.seg_cnt[seg];
-    for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
-        const uint32_t t = base + lane * 4;
-        float v[4];
-        uint32_t pos[4], key[4];
-        bool ok[4];
-        load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-#pragma unroll
-            for (int j = 0; j < NB; j++) {
-                const uint32_t d = key[c] - lo[j];
-                if (act[j] && ok[c] && d <= wm1[j])
-                    atomicAdd(&p.histl[j * GVC_HL_BINS + (d >> sh[j])], 1u);
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_level_resolve(Plan p)
-{
-    __shared__ unsigned long long sh[33];
-    SelState *st = p.st;
-    if (st->pending == 0)
-        return;
-    for (int j = 0; j < p.n_ks; j++) {
-        if (st->js[j].resolved)
-            continue;  // uniform across the block
-        uint32_t *h = p.histl + j * GVC_HL_BINS;
-        const JState cur = st->js[j];
-        const unsigned long long nd = cur.need;
-        __syncthreads();
-        find_crossings(h, sh, 1, &nd, [&](int, int b, unsigned long long above) {
-            unsigned long long lo = cur.lo + ((unsigned long long)b << cur.shift);
-            unsigned long long hi = lo + (1ull << cur.shift);
-            if (hi > cur.hi)
-                hi = cur.hi;
-            set_jstate(st->js[j], lo, hi, cur.above + above, cur.need - above);
-        });
-        reinterpret_cast<uint4 *>(h)[threadIdx.x] = make_uint4(0, 0, 0, 0);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        uint32_t pend = 0;
-        for (int j = 0; j < p.n_ks; j++)
-            pend += !st->js[j].resolved;
-        st->pending = pend;
-    }
-}
-
-// ------------------------------------------------------------------- final
-// Per segment: band counts (band = #{j : T_j < key}) and tie counts per
-// ladder entry (for the emit offsets); per block of 8 segments: band and tie
-// energies.  fp64 sums are per-lane sequential, a fixed xor tree per warp and
-// warps added in order: bit-reproducible.
+// ------------------------------------------------------- candidate pass
+// After level 0 every ladder entry j has an interval [lo_j, hi_j) (its
+// threshold bin).  ONE pass over the candidates:
+//   * a candidate outside every interval is classified exactly: its band
+//     (#{j : key >= hi_j}) goes into per-segment counts and per-block fp64
+//     energies -- these are final;
+//   * a candidate inside some interval (a "member") is compacted, in index
+//     order, into the segment's member list and counted into the level-1
+//     histogram of every interval it falls in.
+// Members are few (the threshold bins are ~1/1000 octave wide), so the exact
+// thresholds and the members' own contributions are finished on them alone.
 template <int KM, int NB, bool ABS>
-__global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
+__global__ void __launch_bounds__(GVC_THREADS) k_pass1(Plan p)
 {
-    // thread-private band accumulators live in shared memory ([slot][thread],
-    // conflict-free), so each candidate costs one indexed update instead of
-    // NB predicated ones; ties (key == T_j, rare) take a branch
     extern __shared__ __align__(16) unsigned char fsm[];
     double(*acc_e)[GVC_THREADS] = reinterpret_cast<double(*)[GVC_THREADS]>(fsm);
     double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
     uint32_t(*acc_c)[GVC_THREADS] = reinterpret_cast<uint32_t(*)[GVC_THREADS]>(acc_a + (ABS ? NB + 1 : 0));
-    __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
-    __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
-    SelState *st = p.st;
+    __shared__ double wsum[GVC_WARPS_PER_BLOCK][2][NB];
+    const SelState *st = p.st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
     const int nks = p.n_ks;
-    uint32_t T[NB];
+    uint32_t lo[NB], wm1[NB], him1[NB], sh[NB];
+    bool act[NB];  // level-1 histogram needed (interval wider than one key)
 #pragma unroll
-    for (int j = 0; j < NB; j++)
-        T[j] = j < nks ? (uint32_t)st->js[j].lo : 0xffffffffu;
-    // 0xffffffff beyond n_ks: never below a key (band stays < n_ks + 1)
+    for (int j = 0; j < NB; j++) {
+        const bool valid = j < nks;
+        lo[j] = valid ? (uint32_t)st->js[j].lo : 0xffffffffu;
+        wm1[j] = valid ? (uint32_t)(st->js[j].hi - st->js[j].lo - 1) : 0u;
+        him1[j] = valid ? (uint32_t)(st->js[j].hi - 1) : 0xffffffffu;
+        sh[j] = valid ? (uint32_t)st->js[j].shift : 0u;
+        act[j] = valid && !st->js[j].resolved;
+    }
 #pragma unroll
     for (int b = 0; b <= NB; b++) {
         acc_e[b][threadIdx.x] = 0.0;
@@ -696,79 +635,220 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
             acc_a[b][threadIdx.x] = 0.0;
         acc_c[b][threadIdx.x] = 0u;
     }
-    uint32_t tc[NB];
-    double te[NB], ta[NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        tc[j] = 0;
-        te[j] = ta[j] = 0.0;
-    }
-    uint32_t tmax = 0;  // largest valid threshold
-#pragma unroll
-    for (int j = 0; j < NB; j++)
-        if (j < nks)
-            tmax = max(tmax, T[j]);
+    uint32_t nan_any = 0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
         const uint32_t cnt = p.seg_cnt[seg];
+        uint32_t *mem = p.mem_idx + beg;
+        const uint32_t lt = lanemask_lt();
+        uint32_t mcount = 0;
         for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
             const uint32_t t = base + lane * 4;
             float v[4];
             uint32_t pos[4], key[4];
             bool ok[4];
             load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
+            bool memb[4];
+            uint32_t mb[4];
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                if (!ok[c])
-                    continue;
-                if (KM == KEY_MAG && key[c] > 0x7f800000u)
-                    atomicOr(&st->nan_flag, 1u);  // NaN keys are always candidates
-                const double v2 = (double)v[c] * (double)v[c];
+                int band = 0;
+                bool in = false;
+#pragma unroll
+                for (int j = 0; j < NB; j++) {
+                    const uint32_t d = key[c] - lo[j];
+                    const bool inj = j < nks && d <= wm1[j];
+                    in |= inj;
+                    band += key[c] > him1[j];
+                    if (ok[c] && inj && act[j])
+                        atomicAdd(&p.histl[j * GVC_HL_BINS + (d >> sh[j])], 1u);
+                }
+                memb[c] = ok[c] && in;
+                if (KM == KEY_MAG)
+                    nan_any |= (uint32_t)(ok[c] && key[c] > 0x7f800000u);
+                if (ok[c] && !in) {
+                    acc_e[band][threadIdx.x] += (double)v[c] * (double)v[c];
+                    if (ABS)
+                        acc_a[band][threadIdx.x] += fabs((double)v[c]);
+                    acc_c[band][threadIdx.x] += 1u;
+                }
+                mb[c] = __ballot_sync(0xffffffffu, memb[c]);
+            }
+            uint32_t o = mcount + __popc(mb[0] & lt) + __popc(mb[1] & lt) + __popc(mb[2] & lt) + __popc(mb[3] & lt);
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                if (memb[c])
+                    mem[o] = t + c;
+                o += memb[c];
+            }
+            mcount += __popc(mb[0]) + __popc(mb[1]) + __popc(mb[2]) + __popc(mb[3]);
+        }
+        if (lane == 0)
+            p.seg_mcnt[seg] = mcount;
+    }
+    __syncwarp();
+    nan_any = __any_sync(0xffffffffu, nan_any);
+    if (lane == 0 && nan_any)
+        atomicOr(&p.st->nan_flag, 1u);
+#pragma unroll
+    for (int j = 0; j < NB; j++) {
+        // band j+1: exactly j+1 thresholds lie below the key; band 0 is never kept
+        uint32_t c1 = acc_c[j + 1][threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        const double e1 = warp_sum_f64(acc_e[j + 1][threadIdx.x]);
+        const double a1 = ABS ? warp_sum_f64(acc_a[j + 1][threadIdx.x]) : 0.0;
+        if (lane == 0) {
+            wsum[warp][0][j] = e1;
+            wsum[warp][1][j] = a1;
+            if (seg < p.S && j < nks)
+                p.seg_band[(size_t)j * GVC_SEG_MAX + seg] = c1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nks) {
+        const int j = threadIdx.x;
+        double e1 = 0.0, a1 = 0.0;
+        for (int w = 0; w < GVC_WARPS_PER_BLOCK; w++) {
+            e1 += wsum[w][0][j];
+            a1 += wsum[w][1][j];
+        }
+        const size_t o = (size_t)j * GVC_BLK_MAX + blockIdx.x;
+        p.blk_band_e2[o] = e1;
+        p.blk_band_ab[o] = a1;
+    }
+}
+
+// Exact thresholds (one block): the level-1 histogram, then -- only if an
+// interval is still wider than one key -- radix refinement over the members
+// in shared memory.
+template <int KM>
+__global__ void __launch_bounds__(1024) k_resolve1(Plan p)
+{
+    __shared__ unsigned long long sh[33];
+    __shared__ __align__(16) uint32_t hs[GVC_HL_BINS];
+    SelState *st = p.st;
+    for (int j = 0; j < p.n_ks; j++) {
+        if (st->js[j].resolved)
+            continue;  // uniform across the block
+        uint32_t *h = p.histl + j * GVC_HL_BINS;
+        bool from_global = true;
+        while (true) {
+            const JState cur = st->js[j];
+            if (cur.resolved)
+                break;
+            const unsigned long long nd = cur.need;
+            __syncthreads();
+            find_crossings(from_global ? h : hs, sh, 1, &nd, [&](int, int b, unsigned long long above) {
+                unsigned long long lo = cur.lo + ((unsigned long long)b << cur.shift);
+                unsigned long long hi = lo + (1ull << cur.shift);
+                if (hi > cur.hi)
+                    hi = cur.hi;
+                set_jstate(st->js[j], lo, hi, cur.above + above, cur.need - above);
+            });
+            if (from_global)
+                reinterpret_cast<uint4 *>(h)[threadIdx.x] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+            const JState nx = st->js[j];
+            if (nx.resolved)
+                break;
+            // refine on the members that fall in the narrowed interval
+            reinterpret_cast<uint4 *>(hs)[threadIdx.x] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+            const uint32_t lo = (uint32_t)nx.lo, wm1 = (uint32_t)(nx.hi - nx.lo - 1);
+            for (uint32_t sg = threadIdx.x; sg < p.S; sg += 1024) {
+                const uint64_t beg = (uint64_t)sg * p.seg_len;
+                const uint32_t mc = p.seg_mcnt[sg];
+                for (uint32_t i = 0; i < mc; i++) {
+                    const uint32_t t = p.mem_idx[beg + i];
+                    const float v = p.cand_val[beg + t];
+                    const uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + t]);
+                    if (key - lo <= wm1)
+                        atomicAdd(&hs[(key - lo) >> nx.shift], 1u);
+                }
+            }
+            from_global = false;
+        }
+    }
+}
+
+// Members' own contributions: exact band (#{j : T_j < key}), ties per entry;
+// adds to the per-segment counts and per-block energies of k_pass1 in a fixed
+// order (pass-1 part first, then the members in index order).
+template <int KM, int NB, bool ABS>
+__global__ void __launch_bounds__(GVC_THREADS) k_members(Plan p)
+{
+    __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
+    __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
+    const SelState *st = p.st;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
+    const int nks = p.n_ks;
+    uint32_t T[NB];
+#pragma unroll
+    for (int j = 0; j < NB; j++)
+        T[j] = j < nks ? (uint32_t)st->js[j].lo : 0xffffffffu;
+    uint32_t bc[NB], tc[NB];
+    double be[NB], ba[NB], te[NB], ta[NB];
+#pragma unroll
+    for (int j = 0; j < NB; j++) {
+        bc[j] = tc[j] = 0;
+        be[j] = ba[j] = te[j] = ta[j] = 0.0;
+    }
+    if (seg < p.S) {
+        const uint64_t beg = (uint64_t)seg * p.seg_len;
+        const uint32_t mc = p.seg_mcnt[seg];
+        for (uint32_t base = 0; base < mc; base += 32) {
+            const uint32_t i = base + lane;
+            if (i < mc) {
+                const uint32_t t = p.mem_idx[beg + i];
+                const float v = p.cand_val[beg + t];
+                const uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + t]);
+                const double v2 = (double)v * (double)v, av = fabs((double)v);
                 int band = 0;
 #pragma unroll
                 for (int j = 0; j < NB; j++)
-                    band += T[j] < key[c];
-                acc_e[band][threadIdx.x] += v2;
-                if (ABS)
-                    acc_a[band][threadIdx.x] += fabs((double)v[c]);
-                acc_c[band][threadIdx.x] += 1u;
-                if (key[c] <= tmax) {
+                    band += j < nks && T[j] < key;
 #pragma unroll
-                    for (int j = 0; j < NB; j++) {
-                        if (key[c] == T[j]) {
-                            tc[j]++;
-                            te[j] += v2;
-                            ta[j] += fabs((double)v[c]);
-                        }
+                for (int j = 0; j < NB; j++) {
+                    const bool inb = band == j + 1;
+                    const bool tie = j < nks && key == T[j];
+                    bc[j] += inb;
+                    tc[j] += tie;
+                    be[j] += inb ? v2 : 0.0;
+                    te[j] += tie ? v2 : 0.0;
+                    if (ABS) {
+                        ba[j] += inb ? av : 0.0;
+                        ta[j] += tie ? av : 0.0;
                     }
                 }
             }
         }
     }
-    __syncwarp();
 #pragma unroll
     for (int j = 0; j < NB; j++) {
-        // band j+1 holds keys in (T_j, T_{j+1}]; band 0 (key <= T_0) is never kept
-        uint32_t c1 = acc_c[j + 1][threadIdx.x], c2 = tc[j];
+        uint32_t c1 = bc[j], c2 = tc[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             c1 += __shfl_xor_sync(0xffffffffu, c1, o);
             c2 += __shfl_xor_sync(0xffffffffu, c2, o);
         }
-        double e1 = warp_sum_f64(acc_e[j + 1][threadIdx.x]);
-        double a1 = ABS ? warp_sum_f64(acc_a[j + 1][threadIdx.x]) : 0.0;
-        double e2 = warp_sum_f64(te[j]), a2 = ABS ? warp_sum_f64(ta[j]) : 0.0;
+        const double e1 = warp_sum_f64(be[j]), a1 = ABS ? warp_sum_f64(ba[j]) : 0.0;
+        const double e2 = warp_sum_f64(te[j]), a2 = ABS ? warp_sum_f64(ta[j]) : 0.0;
         if (lane == 0) {
-            wcnt[warp][0][j] = c1;
+            uint32_t band_total = 0;
+            if (seg < p.S && j < nks) {
+                band_total = p.seg_band[(size_t)j * GVC_SEG_MAX + seg] + c1;
+                p.seg_band[(size_t)j * GVC_SEG_MAX + seg] = band_total;
+                p.seg_tie[(size_t)j * GVC_SEG_MAX + seg] = c2;
+            }
+            wcnt[warp][0][j] = band_total;
             wcnt[warp][1][j] = c2;
             wsum[warp][0][j] = e1;
             wsum[warp][1][j] = a1;
             wsum[warp][2][j] = e2;
             wsum[warp][3][j] = a2;
-            if (seg < p.S && j < nks) {
-                p.seg_band[(size_t)j * GVC_SEG_MAX + seg] = c1;
-                p.seg_tie[(size_t)j * GVC_SEG_MAX + seg] = c2;
-            }
         }
     }
     __syncthreads();
@@ -785,10 +865,10 @@ __global__ void __launch_bounds__(GVC_THREADS) k_final(Plan p)
             a2 += wsum[w][3][j];
         }
         const size_t o = (size_t)j * GVC_BLK_MAX + blockIdx.x;
+        p.blk_band_e2[o] += e1;
+        p.blk_band_ab[o] += a1;
         p.blk_band_cnt[o] = c1;
         p.blk_tie_cnt[o] = c2;
-        p.blk_band_e2[o] = e1;
-        p.blk_band_ab[o] = a1;
         p.blk_tie_e2[o] = e2;
         p.blk_tie_ab[o] = a2;
     }
@@ -1243,37 +1323,31 @@ size_t select_workspace_bytes(int kind, uint64_t n)
 static int nb_for(int n_ks) { return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16; }
 
 template <int KM, int NB, bool ABS>
-static void launch_final_nb(const Plan &p, cudaStream_t s)
+static void launch_tail_nb(const Plan &p, cudaStream_t s)
 {
     const size_t smem = (size_t)(NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_final<KM, NB, ABS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_pass1<KM, NB, ABS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_final<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(p);
-}
-
-template <int KM, bool ABS>
-static void launch_final_abs(const Plan &p, cudaStream_t s)
-{
-    switch (nb_for(p.n_ks)) {
-    case 1: launch_final_nb<KM, 1, ABS>(p, s); break;
-    case 2: launch_final_nb<KM, 2, ABS>(p, s); break;
-    case 4: launch_final_nb<KM, 4, ABS>(p, s); break;
-    case 8: launch_final_nb<KM, 8, ABS>(p, s); break;
-    default: launch_final_nb<KM, 16, ABS>(p, s); break;
-    }
+    k_pass1<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(p);
+    k_resolve1<KM><<<1, 1024, 0, s>>>(p);
+    k_members<KM, NB, ABS><<<(int)p.B, GVC_THREADS, 0, s>>>(p);
 }
 
 // |v| sums are only consumed by Redsync's mean (compressors.py:188)
 template <int KM>
-static void launch_final(const Plan &p, cudaStream_t s)
+static void launch_tail(const Plan &p, cudaStream_t s)
 {
-    if (p.kind == GVC_REDSYNC)
-        launch_final_abs<KM, true>(p, s);
-    else
-        launch_final_abs<KM, false>(p, s);
+    const bool abs_sums = p.kind == GVC_REDSYNC;
+    switch (nb_for(p.n_ks)) {
+    case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, s) : launch_tail_nb<KM, 1, false>(p, s); break;
+    case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, s) : launch_tail_nb<KM, 2, false>(p, s); break;
+    case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, s) : launch_tail_nb<KM, 4, false>(p, s); break;
+    case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, s) : launch_tail_nb<KM, 8, false>(p, s); break;
+    default: abs_sums ? launch_tail_nb<KM, 16, true>(p, s) : launch_tail_nb<KM, 16, false>(p, s); break;
+    }
 }
 
 template <int KM>
@@ -1312,18 +1386,8 @@ static void launch_pipeline(Plan &p, cudaStream_t s)
         k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     k_resolve0<<<1, 1024, 0, s>>>(p, 1);
     launches += 5;
-    for (int l = 0; l < GVC_MAX_LEVELS; l++) {
-        switch (nb_for(p.n_ks)) {
-        case 1: k_level_hist<KM, 1><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-        case 2: k_level_hist<KM, 2><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-        case 4: k_level_hist<KM, 4><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-        case 8: k_level_hist<KM, 8><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-        default: k_level_hist<KM, 16><<<blocks, GVC_THREADS, 0, s>>>(p); break;
-        }
-        k_level_resolve<<<1, 1024, 0, s>>>(p);
-        launches += 2;
-    }
-    launch_final<KM>(p, s);
+    launch_tail<KM>(p, s);
+    launches += 3;
     switch (nb_for(p.n_ks)) {
     case 1: k_finish<KM, 1><<<1, 1024, 0, s>>>(p); break;
     case 2: k_finish<KM, 2><<<1, 1024, 0, s>>>(p); break;
