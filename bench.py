@@ -217,20 +217,14 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     trace = os.environ.get("GVC_BENCH_TRACE") == "1"
 
     def step(g):
-        res = G.run_iteration(state, G.GradientVector._wrap(g), store, cost, rng, extra_cfs=extra, group=pg)
+        res = G.run_iteration(state, G.GradientVector._wrap(g), store, cost, rng, extra_cfs=extra, group=pg,
+                              average=True, average_out=avg)
         chosen[res.decision.cf] = chosen.get(res.decision.cf, 0) + 1
         if trace:
             print(f"[rank {rank}] it={state.iteration} {res.decision.choice} cf={res.decision.cf} "
                   f"gmin={res.gain_min_raw:.6f} gc={res.gain_c_raw:.6f} dmin={res.decision.delta_min:.6f}",
                   file=sys.stderr, flush=True)
-        part = res.sent[0]
-        if res.decision.choice == "dense":
-            out = allgather_dense_mean(part, pg) if pg is not None else part
-        elif pg is not None:
-            out = allgather_aggregate(part, pg, out=avg)
-        else:
-            out = aggregate_packed(part.indices, part.vals, [part.kept], M, out=avg)
-        return res, out
+        return res, res.averaged
 
     # warm-up mirrors the timed loop exactly (the previous step's outputs stay
     # alive while the next one runs), so the caching allocator is warm

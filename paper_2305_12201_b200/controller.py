@@ -172,6 +172,8 @@ class IterationResult:
     theta_min: float
     # beyond the reference: raw mean gain of every CF evaluated in the fused sweep
     ladder_gains: dict = field(default_factory=dict)
+    # run_iteration(average=True): the exchanged, averaged gradient of this step
+    averaged: GradientVector | None = None
 
 
 # ------------------------------------------------------------ fused step
@@ -404,8 +406,29 @@ def _mean_raw_gain(energies: Sequence[float], ef_norms: Sequence[float]) -> floa
     return sum(gains) / len(gains)
 
 
+def _average(sent, group, out: torch.Tensor | None):
+    """The step's exchange + mean of the sent views: worker parts on this GPU
+    (compressors.aggregate / aggregate_dense) or, with a process group, C1 + K7
+    (sparse) / C3 (dense) across the ranks."""
+    from .compressors import aggregate_packed, aggregate_dense
+    if isinstance(sent[0], SparseGradient):
+        if group is not None:
+            from .exchange import allgather_aggregate
+            return allgather_aggregate(sent[0], group, out=out)
+        if len(sent) == 1:
+            p0 = sent[0]
+            return GradientVector._wrap(aggregate_packed(p0.indices, p0.vals, [p0.kept], p0.original_length, out=out))
+        from .compressors import aggregate
+        return aggregate(sent)
+    if group is not None:
+        from .exchange import allgather_dense_mean
+        return allgather_dense_mean(sent[0], group)
+    return aggregate_dense(sent)
+
+
 def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelParams, rng: SeededRng,
-                  batch_size: int = 1, *, extra_cfs: Sequence[float] = (), group=None) -> IterationResult:
+                  batch_size: int = 1, *, extra_cfs: Sequence[float] = (), group=None,
+                  average: bool = False, average_out: torch.Tensor | None = None) -> IterationResult:
     """One adaptive GraVAC step (controller.py:192-281) on the GPU.
 
     ``gradients``/``residuals``: one object (one worker) or worker-ascending
@@ -415,7 +438,11 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     all-gathered so every rank takes the same decision in the reference's
     worker order.  ``extra_cfs``: more CFs (>= theta_min) whose gains the Top-k
     sweep evaluates in the same pass; reported in ``ladder_gains`` but never
-    fed to the EWMA trackers.
+    fed to the EWMA trackers.  ``average=True`` also performs the
+    step's exchange and mean (what the reference's simworkers does after
+    run_iteration, simworkers.py:242-245) into ``IterationResult.averaged``;
+    it is enqueued behind the speculative emit, so the device never waits for
+    the host's decision.
     """
     cfg = state.config
     grads = [gradients] if isinstance(gradients, GradientVector) else list(gradients)
@@ -462,6 +489,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
             spec_parts = [s.emit(c, new_payload(s.chosen_count(c), dev)) for s in steps]
         else:
             spec_parts = [s.emit(c) for s in steps]
+    spec_avg = _average(spec_parts, group, average_out) if (average and spec_parts is not None) else None
 
     # ---- one device->host read per iteration: every worker's norms and energies
     stats = [t for s in steps for t in s.stats_dev()]
@@ -512,8 +540,11 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         d_min = state.gains.value(theta_min) if state.gains.has(theta_min) else None
         d_c = state.gains.value(candidate_cf) if state.gains.has(candidate_cf) else None
         check_gravac(state, i, d_min, d_c)
-        return IterationResult(sent, decision, cost.t_compute, 0.0, t_sync, t_iter, length,
-                               dense_message_words(length), 1.0, 1.0, candidate_cf, theta_min)
+        out = IterationResult(sent, decision, cost.t_compute, 0.0, t_sync, t_iter, length,
+                              dense_message_words(length), 1.0, 1.0, candidate_cf, theta_min)
+        if average:
+            out.averaged = _average(sent, group, None)
+        return out
 
     raw_min = _mean_raw_gain([x[1] for x in local], ef_norms)
     delta_min = state.gains.observe(theta_min, raw_min)
@@ -559,5 +590,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     t_iter = iteration_time(decision, cost.t_compute, t_compress, t_sync)
     update_step(state.table, decision.cf, decision.gain, t_iter, cost.workers, batch_size)
     check_gravac(state, i, delta_min, delta_c)
-    return IterationResult(sent, decision, cost.t_compute, 0.0 if decision.choice == DENSE else t_compress,
-                           t_sync, t_iter, floats, words, raw_min, raw_c, candidate_cf, theta_min, ladder)
+    out = IterationResult(sent, decision, cost.t_compute, 0.0 if decision.choice == DENSE else t_compress,
+                          t_sync, t_iter, floats, words, raw_min, raw_c, candidate_cf, theta_min, ladder)
+    if average:
+        out.averaged = spec_avg if (spec_parts is not None and sent is spec_parts) else \
+            _average(sent, group, average_out if decision.choice != DENSE else None)
+    return out

@@ -29,9 +29,11 @@ def _worker(rank, world, port, kind, q):
     out = []
     for it in range(1, 6):
         g = np.random.default_rng(100 * it + rank).standard_normal(n).astype(np.float32) * (1 + rank)
-        res = G.run_iteration(state, G.GradientVector(g), store, cost, rng, group=dist.group.WORLD)
+        res = G.run_iteration(state, G.GradientVector(g), store, cost, rng, group=dist.group.WORLD,
+                              average=True)
         part = res.sent[0]
-        avg = allgather_aggregate(part, dist.group.WORLD)
+        avg = res.averaged
+        assert torch.equal(avg.values, allgather_aggregate(part, dist.group.WORLD).values)
         idx, vals = allgather_payload(part, dist.group.WORLD)
         parts = [G.SparseGradient._wrap(idx[r * part.kept:(r + 1) * part.kept],
                                         vals[r * part.kept:(r + 1) * part.kept], n, part.achieved_cf)

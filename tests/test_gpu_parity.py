@@ -325,7 +325,7 @@ def test_run_iteration_vs_oracle(G, kind, workers):
     for it in range(1, 9):
         gs = [_vec("gauss" if w == 0 else "layered", n, 31 * it + w) for w in range(workers)]
         tmin, ts = state.theta_min, state.theta_s
-        res = G.run_iteration(state, [gv(G, g) for g in gs], stores, cost, rng)
+        res = G.run_iteration(state, [gv(G, g) for g in gs], stores, cost, rng, average=True)
         seen.add(res.decision.choice)
         k1 = O.keep_count(n, tmin)
         gmin_raw, gc_raw = [], []
@@ -346,6 +346,9 @@ def test_run_iteration_vs_oracle(G, kind, workers):
             assert np.array_equal(host(part.indices), ci), (it, w)
             np.testing.assert_allclose(host(part.vals), cv, rtol=GAIN_RTOL)
             r_host[w] = O.update_residual(ef, ci, cv)
+        if res.decision.choice != "dense":  # the step's average (simworkers.py:242-245)
+            want = O.aggregate([(host(p.indices), host(p.vals)) for p in res.sent], n)
+            assert np.array_equal(bits(host(res.averaged.values)), bits(want)), it
         assert res.gain_min_raw == pytest.approx(sum(gmin_raw) / workers, rel=GAIN_RTOL)
         assert res.gain_c_raw == pytest.approx(sum(gc_raw) / workers, rel=GAIN_RTOL)
         if kind != "redsync":  # Redsync values carry the 1e-6 mean tolerance into r
