@@ -47,7 +47,7 @@ static cudaEvent_t prof_event()
 ProfScope::ProfScope(int cat, cudaStream_t st) : slot(-1), s(st)
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    if (!g_prof_on)
+    if (!g_prof_on || cat < 0)
         return;
     cudaEvent_t a = prof_event(), b = prof_event();
     cudaEventRecord(a, s);
@@ -64,6 +64,12 @@ ProfScope::~ProfScope()
 }
 
 void count_launches(int n) { g_launches += (unsigned long long)n; }
+
+bool prof_enabled()
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    return g_prof_on;
+}
 
 static int check_launch(const char *what)
 {

@@ -21,6 +21,7 @@ struct ProfScope {
     ~ProfScope();
 };
 void count_launches(int n);
+bool prof_enabled();
 
 size_t select_workspace_bytes(int kind, uint64_t n);
 int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
