@@ -192,7 +192,7 @@ __device__ __forceinline__ void load_cand4(const Plan &p, uint64_t beg, uint32_t
 // magnitude keys, merged into global memory once per block.  Reads ~1.5%.
 __global__ void __launch_bounds__(1024) k_sample(const Plan *__restrict__ pp)
 {
-    const Plan &p = *pp;
+    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     extern __shared__ uint32_t sh[];
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
         sh[i] = 0;
@@ -366,7 +366,7 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 template <int KM, bool EF, int PM>
 __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan *__restrict__ pp, int refill)
 {
-    const Plan &p = *pp;
+    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
     if (refill && !p.st->fallback)
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(1024) k_resolve0(const Plan *__restrict__ pp, 
 template <int KM, int NB, bool ABS>
 __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan *__restrict__ pp)
 {
-    const Plan &p = *pp;
+    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     extern __shared__ __align__(16) unsigned char fsm[];
     double(*acc_e)[GVC_THREADS] = reinterpret_cast<double(*)[GVC_THREADS]>(fsm);
     double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan *__restrict__ pp)
 template <int KM, int NB, bool ABS>
 __global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan *__restrict__ pp)
 {
-    const Plan &p = *pp;
+    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
     __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
     const SelState *st = p.st;
