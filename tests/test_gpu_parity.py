@@ -414,3 +414,24 @@ def test_dgc_compress_further_vs_oracle(G):
         i1, v1, _ = O.compress("dgc", x, 10.0, seed=1, stream=r1.stream)
         i2, v2, _ = O.compress_further("dgc", i1, v1, x.size, step, seed=2, stream=r2.stream)
         assert np.array_equal(host(s2.indices), i2) and np.array_equal(bits(host(s2.vals)), bits(v2))
+
+
+def test_graph_and_direct_launch_paths_agree(G):
+    """The captured CUDA-graph select and the probed direct-launch select
+    (bench.py's measurement pass) must produce identical results."""
+    from paper_2305_12201_b200 import _native as nat
+    from paper_2305_12201_b200.compressors import Selection
+    K = G.CompressorKind("topk")
+    x = torch.from_numpy(_vec("layered", 2_000_003, 12)).cuda()
+    outs = []
+    for probed in (False, True, False):
+        nat.prof_enable(probed)
+        try:
+            sel = Selection(K, [200_000, 20_000, 2_000], values=x, slot="gp")
+            r = sel.result()
+            i, v = sel.emit(1)
+            outs.append((r.ef_norm_sq, tuple(r.kept_sq[:3]), host(i).tobytes(), host(v).tobytes()))
+        finally:
+            nat.prof_enable(False)
+            nat.prof_read()
+    assert outs[0] == outs[1] == outs[2]
