@@ -37,6 +37,7 @@ extern "C" {
 
 #define GVC_ABI_VERSION 1
 #define GVC_MAX_LADDER 16
+#define GVC_AGG_TILE 4096 /* outputs per CTA of the decompress-average */
 
 typedef enum {
     GVC_OK = 0,
@@ -129,11 +130,15 @@ GVC_API int gvc_select(const gvc_select_args *args, void *ws_dev, size_t ws_byte
  *   sent_mask_dev: optional (instead of resid_dev); sets bit `index` for every sent
  *                position -- the deferred form the next gvc_select applies;
  *   sent_m_dev:  optional; receives the Redsync mean m of this entry (device float);
+ *   tile_bounds_dev: optional (level-1 emits only), u32[ceil(n / GVC_AGG_TILE) + 1]: entry t =
+ *                first output position whose index is >= t * GVC_AGG_TILE -- the tile
+ *                boundaries gvc_aggregate needs, produced while the list is written;
  *   sent_stats_dev: optional double[2] = {sum sent^2, sum |sent|} (fp64, fixed order).
  * Replaces compressors._select's sort+gather (compressors.py:185-190). */
 GVC_API int gvc_emit(void *ws_dev, size_t ws_bytes, int j, const uint32_t *idx_map_dev,
              uint32_t *out_idx_dev, float *out_val_dev, float *resid_dev,
-             uint32_t *sent_mask_dev, float *sent_m_dev, double *sent_stats_dev, void *stream);
+             uint32_t *sent_mask_dev, float *sent_m_dev, uint32_t *tile_bounds_dev,
+             double *sent_stats_dev, void *stream);
 
 /* Mark k sent positions in a deferred-residual mask (bit idx[i] of mask). */
 GVC_API int gvc_mark_sent(const uint32_t *idx_dev, uint64_t k, uint32_t *mask_dev, void *stream);
@@ -166,11 +171,14 @@ GVC_API int gvc_decompress(const uint32_t *idx_dev, const float *vals_dev, uint6
  * order, /nparts, -> fp32 (compressors.py:256-271).  Part p is
  * (idx_dev + offs[p], vals_dev + offs[p]) with counts[p] entries; offs/counts are
  * HOST arrays.  Shared-memory tiles of the dense output, one coalesced
- * 128-bit store per 4 outputs.  This is the decompress-average half of the
+ * 128-bit store per 4 outputs.  bounds_dev (optional): part p's tile boundaries
+ * (gvc_emit tile_bounds_dev) at bounds_dev + p * bounds_stride; otherwise they are
+ * computed in a first pass.  This is the decompress-average half of the
  * sparse allgather. */
 GVC_API int gvc_aggregate(const uint32_t *idx_dev, const float *vals_dev, const uint64_t *offs,
                   const uint64_t *counts, int nparts, uint64_t n, float *out_dev,
-                  void *ws_dev, size_t ws_bytes, void *stream);
+                  void *ws_dev, size_t ws_bytes, const uint32_t *bounds_dev, uint64_t bounds_stride,
+                  void *stream);
 GVC_API size_t gvc_aggregate_workspace_bytes(int nparts, uint64_t n);
 
 /* fp64 mean of nparts dense vectors laid out [nparts][n] (compressors.py:274-285). */

@@ -20,6 +20,7 @@ GVC_OK, GVC_ERR_ARG, GVC_ERR_NAN, GVC_ERR_WORKSPACE, GVC_ERR_CUDA, GVC_ERR_STATE
 GVC_TOPK, GVC_DGC, GVC_REDSYNC, GVC_RANDOMK = 0, 1, 2, 3
 KIND_IDS = {"topk": GVC_TOPK, "dgc": GVC_DGC, "redsync": GVC_REDSYNC, "randomk": GVC_RANDOMK}
 MAX_LADDER = 16
+AGG_TILE = 4096  # GVC_AGG_TILE: outputs per CTA of the decompress-average
 
 # every symbol include/gravac_b200.h declares (tests assert the .so exports them)
 EXPORTS = (
@@ -92,7 +93,7 @@ def load(build_if_missing: bool = False):
         L.gvc_select_workspace_bytes.argtypes = [ctypes.c_int, _u64]
         L.gvc_select_workspace_bytes.restype = _sz
         L.gvc_select.argtypes = [ctypes.POINTER(SelectArgs), _vp, _sz, _vp, _vp]
-        L.gvc_emit.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.gvc_emit.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.gvc_mark_sent.argtypes = [_vp, _u64, _vp, _vp]
         L.gvc_apply_pending.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp, _vp]
         L.gvc_ef_add.argtypes = [_vp, _vp, _vp, _u64, _vp]
@@ -101,7 +102,7 @@ def load(build_if_missing: bool = False):
         L.gvc_sq_norm.argtypes = [_vp, _u64, _vp, _vp, _sz, _vp]
         L.gvc_update_residual.argtypes = [_vp, _vp, _vp, _u64, _u64, _vp, _vp]
         L.gvc_decompress.argtypes = [_vp, _vp, _u64, _u64, _vp, _vp, _sz, _vp]
-        L.gvc_aggregate.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, _vp, _sz, _vp]
+        L.gvc_aggregate.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, _vp, _sz, _vp, _u64, _vp]
         L.gvc_aggregate_workspace_bytes.argtypes = [ctypes.c_int, _u64]
         L.gvc_aggregate_workspace_bytes.restype = _sz
         L.gvc_aggregate_dense.argtypes = [_vp, ctypes.c_int, _u64, _vp, _vp]

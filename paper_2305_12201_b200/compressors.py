@@ -66,7 +66,7 @@ class SparseGradient:
     tensors produced by the kernels are trusted (the parity suite checks them).
     """
 
-    __slots__ = ("indices", "vals", "original_length", "achieved_cf", "_payload")
+    __slots__ = ("indices", "vals", "original_length", "achieved_cf", "_payload", "_bounds")
 
     def __init__(self, indices, vals, original_length: int, achieved_cf: float, device=None):
         if isinstance(indices, torch.Tensor) and indices.is_cuda:
@@ -87,6 +87,7 @@ class SparseGradient:
         self.original_length = int(original_length)
         self.achieved_cf = float(achieved_cf)
         self._payload = None
+        self._bounds = None
 
     @classmethod
     def _wrap(cls, indices: torch.Tensor, vals: torch.Tensor, original_length: int,
@@ -97,6 +98,7 @@ class SparseGradient:
         s.original_length = int(original_length)
         s.achieved_cf = float(achieved_cf)
         s._payload = None
+        s._bounds = None
         return s
 
     @property
@@ -166,20 +168,20 @@ class Selection:
     def emit(self, j: int = 0, idx_map: torch.Tensor | None = None, resid: torch.Tensor | None = None,
              stats: torch.Tensor | None = None, sent_mask: torch.Tensor | None = None,
              sent_m: torch.Tensor | None = None, count: int | None = None,
-             payload: torch.Tensor | None = None):
+             payload=None, tile_bounds: torch.Tensor | None = None):
         """Index-ascending (indices, values) of ladder entry j; optionally the
         residual update, either direct (``resid``) or deferred (``sent_mask``).
         ``count`` overrides the entry count (a DGC overshoot keeps fewer)."""
         k = self.ks[j] if count is None else int(count)
-        if payload is not None:  # write straight into the packed wire buffer (exchange.new_payload)
-            out_idx = payload[0, :k].view(torch.uint32)
-            out_val = payload[1, :k].view(torch.float32)
+        if payload is not None:  # write straight into the packed wire buffer (exchange.Payload)
+            out_idx, out_val = payload.idx[:k], payload.vals[:k]
+            tile_bounds = payload.bounds if payload.bounds is not None else tile_bounds
         else:
             out_idx = torch.empty(k, dtype=torch.uint32, device=self.device)
             out_val = torch.empty(k, dtype=torch.float32, device=self.device)
         nat.check(nat.load().gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
                                       nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
-                                      nat.ptr(stats), nat.stream_ptr(self.device)), "gvc_emit")
+                                      nat.ptr(tile_bounds), nat.ptr(stats), nat.stream_ptr(self.device)), "gvc_emit")
         return out_idx, out_val
 
     def result(self) -> nat.SelectResult:
@@ -280,9 +282,11 @@ def decompress(s: SparseGradient, layer_offsets: Sequence[int] | None = None) ->
 
 
 def aggregate_packed(idx: torch.Tensor, vals: torch.Tensor, counts: Sequence[int], n: int,
-                     out: torch.Tensor | None = None, offs: Sequence[int] | None = None) -> torch.Tensor:
+                     out: torch.Tensor | None = None, offs: Sequence[int] | None = None,
+                     bounds: torch.Tensor | None = None, bounds_stride: int = 0) -> torch.Tensor:
     """fp64 worker-ordered mean of parts in (idx, vals); part p starts at offs[p]
-    (default: back to back)."""
+    (default: back to back).  ``bounds``: precomputed tile boundaries of every
+    part (gvc_emit tile_bounds_dev), part p's at bounds + p * bounds_stride."""
     dev = vals.device
     lib = nat.load()
     nparts = len(counts)
@@ -297,7 +301,7 @@ def aggregate_packed(idx: torch.Tensor, vals: torch.Tensor, counts: Sequence[int
     ws = nat.Workspace.get(dev, "agg", int(lib.gvc_aggregate_workspace_bytes(nparts, n)))
     nat.check(lib.gvc_aggregate(nat.ptr(idx), nat.ptr(vals), offs.ctypes.data_as(ctypes.c_void_p),
                                 cnts.ctypes.data_as(ctypes.c_void_p), nparts, n, nat.ptr(out), nat.ptr(ws),
-                                ws.numel(), nat.stream_ptr(dev)), "aggregate")
+                                ws.numel(), nat.ptr(bounds), bounds_stride, nat.stream_ptr(dev)), "aggregate")
     return out
 
 

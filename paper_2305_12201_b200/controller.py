@@ -275,13 +275,18 @@ class _WorkerStep:
             return self.ladder[1 if candidate else 0]
         return self.k2 if (candidate and self.sel2 is not None) else self.g_min.kept
 
-    def emit(self, candidate: bool, payload: torch.Tensor | None = None) -> SparseGradient:
-        """Materialise the chosen view (into ``payload`` when given); the residual
-        update g_ef - sent is deferred into the store's sent-mask (applied by the
-        next fused pass)."""
+    def emit(self, candidate: bool, payload=None, bounds: bool = False) -> SparseGradient:
+        """Materialise the chosen view (into ``payload`` when given, with the
+        K7 tile bounds when ``bounds``); the residual update g_ef - sent is
+        deferred into the store's sent-mask (applied by the next fused pass)."""
+        self._tile_bounds = None
+        if bounds and payload is None and self.kind.name == TOPK and not self.identity1:
+            self._tile_bounds = torch.empty((self.n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1, dtype=torch.int32,
+                                            device=self.resid.device).view(torch.uint32)
         part = self._emit(candidate, payload)
-        if payload is not None and part.vals.data_ptr() == payload[1].data_ptr():
+        if payload is not None and part.vals.data_ptr() == payload.vals.data_ptr():
             part._payload = payload
+        part._bounds = self._tile_bounds
         return part
 
     def _emit(self, candidate: bool, payload: torch.Tensor | None) -> SparseGradient:
@@ -302,7 +307,8 @@ class _WorkerStep:
         if self.kind.name == TOPK:
             j = 1 if candidate else 0
             k = self.ladder[j]
-            idx, vals = self.sel1.emit(j, sent_mask=mask, sent_m=store._pm, payload=payload)
+            idx, vals = self.sel1.emit(j, sent_mask=mask, sent_m=store._pm, payload=payload,
+                                       tile_bounds=self._tile_bounds)
             part = SparseGradient._wrap(idx, vals, self.n, self.n / k)
         elif candidate and self.sel2 is not None:
             idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, sent_mask=mask, sent_m=store._pm,
@@ -385,7 +391,7 @@ class _DgcStep:
     def chosen_count(self, candidate: bool) -> int:
         return (self.g_c if candidate else self.g_min).kept
 
-    def emit(self, candidate: bool, payload: torch.Tensor | None = None) -> SparseGradient:
+    def emit(self, candidate: bool, payload=None, bounds: bool = False) -> SparseGradient:
         part = self.g_c if candidate else self.g_min
         store = self.store
         if self.norm is None:  # identity level 1: direct residual update
@@ -417,7 +423,8 @@ def _average(sent, group, out: torch.Tensor | None):
             return allgather_aggregate(sent[0], group, out=out)
         if len(sent) == 1:
             p0 = sent[0]
-            return GradientVector._wrap(aggregate_packed(p0.indices, p0.vals, [p0.kept], p0.original_length, out=out))
+            return GradientVector._wrap(aggregate_packed(p0.indices, p0.vals, [p0.kept], p0.original_length, out=out,
+                                                         bounds=p0._bounds))
         from .compressors import aggregate
         return aggregate(sent)
     if group is not None:
@@ -486,9 +493,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         c = spec == CANDIDATE
         if group is not None:
             from .exchange import new_payload
-            spec_parts = [s.emit(c, new_payload(s.chosen_count(c), dev)) for s in steps]
+            spec_parts = [s.emit(c, new_payload(s.chosen_count(c), dev, n=length)) for s in steps]
         else:
-            spec_parts = [s.emit(c) for s in steps]
+            spec_parts = [s.emit(c, bounds=average) for s in steps]
     spec_avg = _average(spec_parts, group, average_out) if (average and spec_parts is not None) else None
 
     # ---- one device->host read per iteration: every worker's norms and energies
@@ -580,9 +587,10 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
             sent = spec_parts
         elif group is not None:  # emit straight into the packed wire buffer of the all-gather
             from .exchange import new_payload
-            sent = [s.emit(cand, new_payload(s.chosen_count(cand), dev)) for s in steps]
+            bnd = kind.name == TOPK and not steps[0].identity1
+            sent = [s.emit(cand, new_payload(s.chosen_count(cand), dev, n=length if bnd else None)) for s in steps]
         else:
-            sent = [s.emit(cand) for s in steps]
+            sent = [s.emit(cand, bounds=average) for s in steps]
         floats = sent[0].kept
         words = sparse_message_words(sent[0])
 

@@ -164,13 +164,16 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
 }
 
 int gvc_emit(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
-             float *resid, uint32_t *sent_mask, float *sent_m, double *stats, void *stream)
+             float *resid, uint32_t *sent_mask, float *sent_m, uint32_t *tile_bounds, double *stats, void *stream)
 {
     if (!ws || !out_idx || !out_val)
         return set_error(GVC_ERR_ARG, "gvc_emit: null argument");
     if (resid && sent_mask)
         return set_error(GVC_ERR_ARG, "gvc_emit: pass resid_dev or sent_mask_dev, not both");
-    return emit_run(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, sent_mask, sent_m, stats, STREAM(stream));
+    if (tile_bounds && idx_map)
+        return set_error(GVC_ERR_ARG, "gvc_emit: tile bounds need output indices in selection order (no idx_map)");
+    return emit_run(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, sent_mask, sent_m, tile_bounds, stats,
+                    STREAM(stream));
 }
 
 int gvc_mark_sent(const uint32_t *idx, uint64_t k, uint32_t *mask, void *stream)
@@ -228,13 +231,15 @@ int gvc_decompress(const uint32_t *idx, const float *vals, uint64_t k, uint64_t 
 size_t gvc_aggregate_workspace_bytes(int nparts, uint64_t n) { return aggregate_workspace_bytes(nparts, n); }
 
 int gvc_aggregate(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
-                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, void *stream)
+                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *bounds,
+                  uint64_t bounds_stride, void *stream)
 {
     if (nparts < 1)
         return set_error(GVC_ERR_ARG, "aggregate of zero parts");
     if (!idx || !vals || !offs || !counts || !out || n < 1)
         return set_error(GVC_ERR_ARG, "gvc_aggregate: bad arguments");
-    int rc = aggregate_run(idx, vals, offs, counts, nparts, n, out, ws, ws_bytes, STREAM(stream));
+    int rc = aggregate_run(idx, vals, offs, counts, nparts, n, out, ws, ws_bytes, bounds, bounds_stride,
+                           STREAM(stream));
     return rc ? rc : check_launch("aggregate");
 }
 

@@ -332,7 +332,7 @@ int compact_mask_run(const uint32_t *mask, uint64_t n, uint32_t *out, unsigned l
 // the average, fp32 assignment for decompress); parts are separated by a
 // barrier so each position sees its adds in worker order, as
 // compressors.py:265-271 does.  The tile leaves in coalesced 128-bit stores.
-#define AGG_TILE 4096
+#define AGG_TILE GVC_AGG_TILE
 #define AGG_THREADS 256
 #define AGG_MAX_PARTS 64
 
@@ -367,7 +367,7 @@ template <int MODE>
 __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__restrict__ idx,
                                                             const float *__restrict__ vals, AggParts parts,
                                                             int nparts, uint64_t n, uint64_t ntiles,
-                                                            const uint32_t *__restrict__ bounds,
+                                                            const uint32_t *__restrict__ bounds, uint64_t bstride,
                                                             float *__restrict__ out)
 {
     __shared__ __align__(16) double acc[MODE == 2 ? AGG_TILE : 2];
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
     for (int p = 0; p < nparts; p++) {
         const uint32_t *pi = idx + parts.off[p];
         const float *pv = vals + parts.off[p];
-        const uint32_t *bp = bounds + (uint64_t)p * (ntiles + 1);
+        const uint32_t *bp = bounds + (uint64_t)p * bstride;
         const uint32_t a = bp[tile], b = bp[tile + 1];
         for (uint32_t t = a + threadIdx.x; t < b; t += AGG_THREADS) {
             const uint32_t r = pi[t] - (uint32_t)lo;
@@ -437,31 +437,39 @@ size_t aggregate_workspace_bytes(int nparts, uint64_t n)
 }
 
 static int tile_merge_run(bool avg, const uint32_t *idx, const float *vals, const AggParts &P, int nparts,
-                          uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s)
+                          uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *ext_bounds,
+                          uint64_t ext_stride, cudaStream_t s)
 {
-    if (ws_bytes < aggregate_workspace_bytes(nparts, n))
-        return set_error(GVC_ERR_WORKSPACE, "aggregate workspace too small: %zu < %zu", ws_bytes,
-                         aggregate_workspace_bytes(nparts, n));
     const uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
-    uint64_t maxcnt = 1;
-    for (int p = 0; p < nparts; p++)
-        maxcnt = P.cnt[p] + 1 > maxcnt ? P.cnt[p] + 1 : maxcnt;
-    dim3 bg((unsigned)grid_for(maxcnt, 256, 1024), (unsigned)nparts);
     ProfScope pa(PROF_AGGREGATE, s);
-    count_launches(2);
-    k_tile_bounds<<<bg, 256, 0, s>>>(idx, P, nparts, ntiles, (uint32_t *)ws);
-    const uint32_t *bd = (const uint32_t *)ws;
+    const uint32_t *bd = ext_bounds;
+    uint64_t bstride = ext_stride;
+    if (!bd) {
+        if (ws_bytes < aggregate_workspace_bytes(nparts, n))
+            return set_error(GVC_ERR_WORKSPACE, "aggregate workspace too small: %zu < %zu", ws_bytes,
+                             aggregate_workspace_bytes(nparts, n));
+        uint64_t maxcnt = 1;
+        for (int p = 0; p < nparts; p++)
+            maxcnt = P.cnt[p] + 1 > maxcnt ? P.cnt[p] + 1 : maxcnt;
+        dim3 bg((unsigned)grid_for(maxcnt, 256, 1024), (unsigned)nparts);
+        count_launches(1);
+        k_tile_bounds<<<bg, 256, 0, s>>>(idx, P, nparts, ntiles, (uint32_t *)ws);
+        bd = (const uint32_t *)ws;
+        bstride = ntiles + 1;
+    }
+    count_launches(1);
     if (!avg)
-        k_tile_merge<0><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, out);
+        k_tile_merge<0><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, bstride, out);
     else if (nparts == 1)
-        k_tile_merge<1><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, out);
+        k_tile_merge<1><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, bstride, out);
     else
-        k_tile_merge<2><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, out);
+        k_tile_merge<2><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, bstride, out);
     return GVC_OK;
 }
 
 int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
-                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s)
+                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *bounds,
+                  uint64_t bounds_stride, cudaStream_t s)
 {
     if (nparts < 1 || nparts > AGG_MAX_PARTS)
         return set_error(GVC_ERR_ARG, "aggregate: nparts %d outside [1, %d]", nparts, AGG_MAX_PARTS);
@@ -470,7 +478,7 @@ int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, 
         P.off[p] = offs[p];
         P.cnt[p] = counts[p];
     }
-    return tile_merge_run(true, idx, vals, P, nparts, n, out, ws, ws_bytes, s);
+    return tile_merge_run(true, idx, vals, P, nparts, n, out, ws, ws_bytes, bounds, bounds_stride, s);
 }
 
 int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t n, float *out, void *ws,
@@ -479,7 +487,7 @@ int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t 
     AggParts P;
     P.off[0] = 0;
     P.cnt[0] = k;
-    return tile_merge_run(false, idx, vals, P, 1, n, out, ws, ws_bytes, s);
+    return tile_merge_run(false, idx, vals, P, 1, n, out, ws, ws_bytes, nullptr, 0, s);
 }
 
 // --------------------------------------------------------- dense average

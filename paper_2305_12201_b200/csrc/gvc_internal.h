@@ -27,7 +27,8 @@ size_t select_workspace_bytes(int kind, uint64_t n);
 int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
                cudaStream_t s);
 int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx,
-             float *out_val, float *resid, uint32_t *sent_mask, float *sent_m, double *stats, cudaStream_t s);
+             float *out_val, float *resid, uint32_t *sent_mask, float *sent_m, uint32_t *tile_bounds,
+             double *stats, cudaStream_t s);
 int mark_sent_run(const uint32_t *idx, uint64_t k, uint32_t *mask, cudaStream_t s);
 int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m, cudaStream_t s);
 
@@ -40,7 +41,8 @@ int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t 
                    size_t ws_bytes, cudaStream_t s);
 size_t aggregate_workspace_bytes(int nparts, uint64_t n);
 int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
-                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, cudaStream_t s);
+                  int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *bounds,
+                  uint64_t bounds_stride, cudaStream_t s);
 int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, cudaStream_t s);
 int iota_run(uint32_t *out, uint64_t n, cudaStream_t s);
 int gather_ef_run(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,

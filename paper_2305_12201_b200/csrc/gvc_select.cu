@@ -1170,7 +1170,8 @@ __global__ void __launch_bounds__(1024) k_finish(const Plan *__restrict__ pp)
 // arbitrary words and OR into global memory.
 template <int KM, bool SMEM_MASK>
 __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
-                                                      float *out_val, float *resid, uint32_t *smask, float *sm_out)
+                                                      float *out_val, float *resid, uint32_t *smask, float *sm_out,
+                                                      uint32_t *tile_b)
 {
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
     extern __shared__ uint32_t mwords[];  // [8][seg_len / 32] when SMEM_MASK
@@ -1227,6 +1228,9 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
         const uint32_t cnt = p.seg_cnt[seg];
         const uint32_t lt = lanemask_lt();
         uint32_t ties_seen = 0;
+        // tile boundaries (tb): the next output tile whose first position is
+        // still unassigned; this segment owns the tiles starting inside it
+        uint32_t t_next = (uint32_t)((beg + GVC_AGG_TILE - 1) / GVC_AGG_TILE);
         // 4 coalesced 32-wide sub-groups per trip: loads in flight together,
         // stores stay contiguous across the warp
         for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
@@ -1249,6 +1253,20 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                 const uint32_t tb = __ballot_sync(0xffffffffu, tie);
                 const bool sel = ok[c] && (key[c] > T || (tie && ties_seen + __popc(tb & lt) < take));
                 const uint32_t sb = __ballot_sync(0xffffffffu, sel);
+                if (tile_b) {
+                    // tiles starting in (previous selected index, this index] begin here
+                    const uint32_t prior = sb & lt;
+                    const int pl = prior ? 31 - __clz(prior) : 0;
+                    const uint32_t gprev = __shfl_sync(0xffffffffu, pos[c], pl);
+                    if (sel) {
+                        const uint32_t t_lo = prior ? gprev / GVC_AGG_TILE + 1 : t_next;
+                        const uint32_t t_hi = pos[c] / GVC_AGG_TILE;
+                        for (uint32_t t = t_lo; t <= t_hi; t++)
+                            tile_b[t] = out + __popc(sb & lt);
+                    }
+                    if (sb)
+                        t_next = __shfl_sync(0xffffffffu, pos[c], 31 - __clz(sb)) / GVC_AGG_TILE + 1;
+                }
                 if (sel) {
                     float sv = v[c];
                     if (redsync) {
@@ -1275,6 +1293,15 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                 ties_seen += __popc(tb);
                 out += __popc(sb);
             }
+        }
+        if (tile_b) {
+            // tiles starting after this segment's last output and before its end;
+            // the last segment also writes entry ntiles (= the total count)
+            const uint64_t end = min(p.n, beg + p.seg_len);
+            const uint64_t ntiles = (p.n + GVC_AGG_TILE - 1) / GVC_AGG_TILE;
+            const uint64_t t_end = end == p.n ? ntiles : (end - 1) / GVC_AGG_TILE;
+            for (uint64_t t = t_next + lane; t <= t_end; t += 32)
+                tile_b[t] = out;
         }
     }
     if (SMEM_MASK && seg < p.S) {
@@ -1569,7 +1596,7 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
 }
 
 int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
-             float *resid, uint32_t *smask, float *sm_out, double *stats, cudaStream_t s)
+             float *resid, uint32_t *smask, float *sm_out, uint32_t *tile_b, double *stats, cudaStream_t s)
 {
     (void)ws_bytes;
     Plan p;
@@ -1596,17 +1623,17 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         }
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                       sm_out);
+                                                                       sm_out, tile_b);
         else
             k_emit<KEY_HASH, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
-                                                                        smask, sm_out);
+                                                                        smask, sm_out, tile_b);
     } else {
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                   sm_out);
+                                                                   sm_out, tile_b);
         else
             k_emit<KEY_HASH, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                    sm_out);
+                                                                    sm_out, tile_b);
     }
     if (stats)
         k_emit_finish<<<1, 1024, 0, s>>>(p, stats);

@@ -21,6 +21,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _native as nat
 from .compressors import SparseGradient, aggregate_packed
 from .gradcore import GradientVector
 
@@ -44,53 +45,74 @@ def allgather_stats(flat: torch.Tensor, group=None) -> "np.ndarray":
     return torch.stack(out).numpy()
 
 
-def payload_width(k: int) -> int:
-    """Row length of the packed payload: k rounded up to 4 so both rows stay 16-byte aligned."""
-    return (k + 3) & ~3
+class Payload:
+    """Flat int32 wire buffer of one rank: [idx (kpad) | vals (kpad) | tile bounds (bpad)].
+
+    kpad/bpad round to 4 words so every section stays 16-byte aligned.  The
+    tile bounds (gvc_emit tile_bounds_dev) let K7 skip its boundary pass on the
+    gathered parts; every rank uses the same layout (same kind, same k, n).
+    """
+
+    __slots__ = ("buf", "k", "kpad", "nb", "bpad", "idx", "vals", "bounds")
+
+    def __init__(self, k: int, n: int, device, with_bounds: bool = True):
+        self.k = k
+        self.kpad = (k + 3) & ~3
+        self.nb = (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1 if with_bounds else 0
+        self.bpad = (self.nb + 3) & ~3
+        self.buf = torch.empty(2 * self.kpad + self.bpad, dtype=torch.int32, device=device)
+        self.idx = self.buf[:self.kpad].view(torch.uint32)
+        self.vals = self.buf[self.kpad:2 * self.kpad].view(torch.float32)
+        self.bounds = self.buf[2 * self.kpad:2 * self.kpad + self.nb].view(torch.uint32) if with_bounds else None
+
+    @property
+    def words(self) -> int:
+        return self.buf.numel()
 
 
-def new_payload(k: int, device) -> torch.Tensor:
-    """(2, kpad) int32 wire buffer: row 0 index bits, row 1 value bits."""
-    return torch.empty((2, payload_width(k)), dtype=torch.int32, device=device)
+def new_payload(k: int, device, n: int | None = None) -> Payload:
+    return Payload(k, n if n is not None else 0, device, with_bounds=n is not None)
 
 
-def pack_payload(part: SparseGradient) -> torch.Tensor:
-    buf = getattr(part, "_payload", None)
-    if buf is not None:
-        return buf
-    k = part.kept
-    buf = new_payload(k, part.vals.device)
-    buf[0, :k].copy_(part.indices.view(torch.int32))
-    buf[1, :k].copy_(part.vals.view(torch.int32))
-    return buf
+def pack_payload(part: SparseGradient) -> Payload:
+    pl = getattr(part, "_payload", None)
+    if pl is not None:
+        return pl
+    pl = Payload(part.kept, part.original_length, part.vals.device, with_bounds=False)
+    pl.idx[:part.kept].copy_(part.indices)
+    pl.vals[:part.kept].copy_(part.vals)
+    return pl
 
 
 def allgather_payload(part: SparseGradient, group=None) -> tuple[torch.Tensor, torch.Tensor]:
     """C1: every rank's (indices, vals), concatenated in rank order."""
     world = dist.get_world_size(group)
-    payload = pack_payload(part)
-    k, kp = part.kept, payload.shape[1]
-    out = torch.empty((world, 2, kp), dtype=torch.int32, device=payload.device)
-    dist.all_gather_into_tensor(out, payload, group=group)
-    idx = out[:, 0, :k].contiguous().view(torch.uint32).reshape(-1)
-    vals = out[:, 1, :k].contiguous().view(torch.float32).reshape(-1)
+    pl = pack_payload(part)
+    out = torch.empty((world, pl.words), dtype=torch.int32, device=pl.buf.device)
+    dist.all_gather_into_tensor(out, pl.buf, group=group)
+    k = part.kept
+    idx = out[:, :k].contiguous().view(torch.uint32).reshape(-1)
+    vals = out[:, pl.kpad:pl.kpad + k].contiguous().view(torch.float32).reshape(-1)
     return idx, vals
 
 
 def allgather_aggregate(part: SparseGradient, group=None, out: torch.Tensor | None = None) -> GradientVector:
     """C1 + K7: the rank-ordered fp64 mean of every rank's sparse part.
 
-    The all-gathered (world, 2, kpad) buffer is averaged in place: part r's
-    indices start at r*2*kpad, its values kpad words later -- no repacking.
+    The all-gathered (world, words) buffer is averaged in place: part r's
+    indices start at r*words, its values kpad words later, its tile bounds
+    (when the emit produced them) 2*kpad words later -- no repacking.
     """
     world = dist.get_world_size(group)
-    payload = pack_payload(part)
-    k, kp = part.kept, payload.shape[1]
-    buf = torch.empty((world, 2, kp), dtype=torch.int32, device=payload.device)
-    dist.all_gather_into_tensor(buf, payload, group=group)
+    pl = pack_payload(part)
+    L = pl.words
+    buf = torch.empty((world, L), dtype=torch.int32, device=pl.buf.device)
+    dist.all_gather_into_tensor(buf, pl.buf, group=group)
     flat = buf.view(-1)
-    res = aggregate_packed(flat.view(torch.uint32), flat[kp:].view(torch.float32), [k] * world,
-                           part.original_length, out=out, offs=[r * 2 * kp for r in range(world)])
+    bounds = flat[2 * pl.kpad:].view(torch.uint32) if pl.bounds is not None else None
+    res = aggregate_packed(flat.view(torch.uint32), flat[pl.kpad:].view(torch.float32), [pl.k] * world,
+                           part.original_length, out=out, offs=[r * L for r in range(world)],
+                           bounds=bounds, bounds_stride=L)
     return GradientVector._wrap(res)
 
 

@@ -435,3 +435,25 @@ def test_graph_and_direct_launch_paths_agree(G):
             nat.prof_enable(False)
             nat.prof_read()
     assert outs[0] == outs[1] == outs[2]
+
+
+@pytest.mark.parametrize("n,k", [(10, 3), (4096, 1), (4097, 4096), (100_000, 7), (1_000_003, 100_000),
+                                 (3_000_000, 30)])
+def test_emit_tile_bounds(G, n, k):
+    """gvc_emit's tile bounds == searchsorted of the output indices at every
+    4096-boundary, and the K7 average that consumes them is unchanged."""
+    from paper_2305_12201_b200 import _native as nat
+    from paper_2305_12201_b200.compressors import Selection, aggregate_packed
+    x = torch.from_numpy(_vec("layered", n, n % 97)).cuda()
+    if k >= n:
+        pytest.skip("identity")
+    sel = Selection(G.CompressorKind("topk"), [k], values=x, slot="tb")
+    ntiles = (n + nat.AGG_TILE - 1) // nat.AGG_TILE
+    tb = torch.full((ntiles + 1,), -1, dtype=torch.int32, device="cuda").view(torch.uint32)
+    idx, vals = sel.emit(0, tile_bounds=tb)
+    hidx = host(idx).astype(np.int64)
+    want = np.searchsorted(hidx, np.arange(ntiles + 1, dtype=np.int64) * nat.AGG_TILE, side="left")
+    assert np.array_equal(host(tb).astype(np.int64), want)
+    a = aggregate_packed(idx, vals, [k], n)
+    b = aggregate_packed(idx, vals, [k], n, bounds=tb)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
