@@ -274,10 +274,14 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     gc.enable()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    mine = torch.tensor([total_ms, statistics.median(step_ms), max(step_ms), float(step_ms.index(max(step_ms)))],
+                        dtype=torch.float64, device=dev)
+    per_rank = [mine.tolist()]
     if pg is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item()) / args.steps
+        allr = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [r.tolist() for r in allr]
+    ms_step = max(r[0] for r in per_rank) / args.steps
     value = world * 4 * M / (ms_step * 1e-3) / 1e9
 
     # ---- end to end through the public API: pinned host gradient -> H2D -> step -> D2H of the decision
@@ -340,6 +344,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms),
                     "argmax": step_ms.index(max(step_ms))},
         "controller": dict(STATS),
+        "per_rank_ms": [{"total": r[0], "median": r[1], "max": r[2], "argmax": int(r[3])} for r in per_rank],
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * M,
                 "d2h_bytes_per_step": nat.RESULT_BYTES, "ms_per_step": e2e_step},
