@@ -64,7 +64,7 @@ while True:
     try:
         sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
         rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-        print(sm, rs, flush=True)
+        print(sm, rs, time.time(), flush=True)
     except Exception:
         pass
     time.sleep(0.002)
@@ -96,7 +96,7 @@ class ClockSampler:
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
             t0 = time.time()
-            while not self.lines and time.time() - t0 < 10:  # wait for the first sample
+            while len(self.lines) < 2 and time.time() - t0 < 60:  # wait for the first clock sample
                 time.sleep(0.01)
         except Exception as e:
             self.err = repr(e)
@@ -114,13 +114,22 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def mark(self, which):
+        """Bracket the timed region (host wall clock; samples are kept from
+        just before its start to just after its end)."""
+        setattr(self, which, time.time())
+
     def summary(self):
-        rows = [(int(a), int(b)) for a, b in (ln for ln in self.lines if len(ln) == 2 and ln[0] != "max")]
+        all_rows = [(int(a), int(b), float(t)) for a, b, t in (ln for ln in self.lines if len(ln) == 3)]
+        t0, t1 = getattr(self, "t0", 0.0) - 0.005, getattr(self, "t1", 1e30) + 0.005
+        rows = [r for r in all_rows if t0 <= r[2] <= t1]
+        if not rows and all_rows:  # a very short region: the samples closest to it
+            rows = sorted(all_rows, key=lambda r: abs(r[2] - t0))[:2]
         mx = [int(ln[1]) for ln in self.lines if len(ln) == 2 and ln[0] == "max"]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled: " + getattr(self, "err", "")]}
         sm = [r[0] for r in rows]
-        reasons = sorted({name for _, rs in rows for name, bit in self.REASONS.items() if rs & bit})
+        reasons = sorted({name for _, rs, _t in rows for name, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx[0] if mx else None, "reasons": reasons,
                 "samples": len(rows), "source": "nvml"}
 
@@ -228,6 +237,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
 
     # warm-up mirrors the timed loop exactly (the previous step's outputs stay
     # alive while the next one runs), so the caching allocator is warm
+    clocks = ClockSampler(local).__enter__()  # started early: its start-up stays out of the timed region
     res = None
     for w in range(args.warmup):
         g = fresh()
@@ -248,14 +258,16 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     for key in STATS:
         STATS[key] = 0
     launches0 = nat.launch_count()
-    with ClockSampler(local) as clocks:
-        for s in range(args.steps):
-            g = fresh()
-            flush.fill_(float(s))  # evict g / r / candidates from L2 (outside the timed events)
-            ev[s][0].record()
-            res, _ = step(g)
-            ev[s][1].record()
-        torch.cuda.synchronize()
+    clocks.mark("t0")
+    for s in range(args.steps):
+        g = fresh()
+        flush.fill_(float(s))  # evict g / r / candidates from L2 (outside the timed events)
+        ev[s][0].record()
+        res, _ = step(g)
+        ev[s][1].record()
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    clocks.__exit__(None, None, None)
     launches = nat.launch_count() - launches0
     # kernel-level probes: a separate pass of the same step with CUDA events
     # around the collect kernel / select / emit / average (the timed loop above
@@ -372,7 +384,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="resnet101")

@@ -32,6 +32,7 @@
 #include <stdio.h>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "gvc_common.cuh"
 #include "gvc_internal.h"
@@ -95,7 +96,6 @@ struct Plan {
     float *cand_val;
     uint32_t *cand_idx;
     gvc_select_result *res;
-    Plan *plan_dev;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -126,7 +126,6 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
     Plan tmp;
     Plan *q = p ? p : &tmp;
     q->st = (SelState *)take(sizeof(SelState));
-    q->plan_dev = (Plan *)take(sizeof(Plan));
     q->hist0 = (uint32_t *)take(GVC_H0_BINS * 4);
     q->histl = (uint32_t *)take(L * GVC_HL_BINS * 4);
     q->shist = (uint32_t *)take(GVC_SAMPLE_BINS * 4);
@@ -190,9 +189,8 @@ __device__ __forceinline__ void load_cand4(const Plan &p, uint64_t beg, uint32_t
 // ------------------------------------------------------------------ sample
 // Strided chunks of 128 contiguous values -> 14-bit shared-memory histogram of
 // magnitude keys, merged into global memory once per block.  Reads ~1.5%.
-__global__ void __launch_bounds__(1024) k_sample(const Plan *__restrict__ pp)
+__global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
 {
-    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     extern __shared__ uint32_t sh[];
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
         sh[i] = 0;
@@ -245,9 +243,8 @@ __global__ void __launch_bounds__(1024) k_sample(const Plan *__restrict__ pp)
 // Chooses key_est (a lower bound for the k_0-th largest key, w.h.p.) and the
 // level-0 bin shift.  Magnitude keys: from the sample histogram.  Hash keys:
 // from the binomial tail (host-computed).
-__global__ void __launch_bounds__(1024) k_sample_resolve(const Plan *__restrict__ pp)
+__global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
 {
-    const Plan &p = *pp;
     __shared__ unsigned long long sh[33];
     SelState *st = p.st;
     if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
@@ -364,9 +361,8 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // (exactness fallback).  NaN keys are always candidates and are flagged by the
 // candidate passes, not here.
 template <int KM, bool EF, int PM>
-__global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan *__restrict__ pp, int refill)
+__global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan p, int refill)
 {
-    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
     if (refill && !p.st->fallback)
@@ -541,9 +537,8 @@ __device__ __forceinline__ void find_crossings(const uint32_t *h, unsigned long 
 }
 
 // Level 0: candidate total, fallback decision, first interval per ladder entry.
-__global__ void __launch_bounds__(1024) k_resolve0(const Plan *__restrict__ pp, int pass)
+__global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int pass)
 {
-    const Plan &p = *pp;
     __shared__ unsigned long long sh[33];
     __shared__ unsigned long long need[GVC_MAX_LADDER];
     SelState *st = p.st;
@@ -614,9 +609,8 @@ __global__ void __launch_bounds__(1024) k_resolve0(const Plan *__restrict__ pp, 
 // Members are few (the threshold bins are ~1/1000 octave wide), so the exact
 // thresholds and the members' own contributions are finished on them alone.
 template <int KM, int NB, bool ABS>
-__global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan *__restrict__ pp)
+__global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
 {
-    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     extern __shared__ __align__(16) unsigned char fsm[];
     double(*acc_e)[GVC_THREADS] = reinterpret_cast<double(*)[GVC_THREADS]>(fsm);
     double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
@@ -733,9 +727,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan *__restrict__ 
 // interval is still wider than one key -- radix refinement over the members
 // in shared memory.
 template <int KM>
-__global__ void __launch_bounds__(1024) k_resolve1(const Plan *__restrict__ pp)
+__global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
 {
-    const Plan &p = *pp;
     __shared__ unsigned long long sh[33];
     __shared__ __align__(16) uint32_t hs[GVC_HL_BINS];
     SelState *st = p.st;
@@ -787,9 +780,8 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan *__restrict__ pp)
 // adds to the per-segment counts and per-block energies of k_pass1 in a fixed
 // order (pass-1 part first, then the members in index order).
 template <int KM, int NB, bool ABS>
-__global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan *__restrict__ pp)
+__global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan p, int)
 {
-    const Plan p = *pp;  // by value: the hot loop keeps the fields in registers
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
     __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
     const SelState *st = p.st;
@@ -962,9 +954,8 @@ __device__ __forceinline__ void block_excl_prefix_vec(unsigned long long (&v)[K]
 // Gains, tie cut and per-block output offsets for every ladder entry (one
 // block; all entries reduced together, ~10 barrier phases in total).
 template <int KM, int NB>
-__global__ void __launch_bounds__(1024) k_finish(const Plan *__restrict__ pp)
+__global__ void __launch_bounds__(1024) k_finish(const Plan p, int)
 {
-    const Plan &p = *pp;
     constexpr int PER = GVC_BLK_MAX / 1024;  // 2 blocks per thread, contiguous
     __shared__ unsigned long long shu[33 * NB];
     __shared__ double shd[33 * (2 * NB + 1)];
@@ -1362,25 +1353,25 @@ size_t select_workspace_bytes(int kind, uint64_t n)
 static int nb_for(int n_ks) { return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16; }
 
 template <int KM, int NB, bool ABS>
-static void launch_tail_nb(const Plan &p, const Plan *pd, cudaStream_t s)
+static void launch_tail_nb(const Plan &p, cudaStream_t s)
 {
     const size_t smem = (size_t)(NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4);
-    k_pass1<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(pd);
-    k_resolve1<KM><<<1, 1024, 0, s>>>(pd);
-    k_members<KM, NB, ABS><<<(int)p.B, GVC_THREADS, 0, s>>>(pd);
+    k_pass1<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(p, 0);
+    k_resolve1<KM><<<1, 1024, 0, s>>>(p, 0);
+    k_members<KM, NB, ABS><<<(int)p.B, GVC_THREADS, 0, s>>>(p, 0);
 }
 
 // |v| sums are only consumed by Redsync's mean (compressors.py:188)
 template <int KM>
-static void launch_tail(const Plan &p, const Plan *pd, cudaStream_t s)
+static void launch_tail(const Plan &p, cudaStream_t s)
 {
     const bool abs_sums = p.kind == GVC_REDSYNC;
     switch (nb_for(p.n_ks)) {
-    case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, pd, s) : launch_tail_nb<KM, 1, false>(p, pd, s); break;
-    case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, pd, s) : launch_tail_nb<KM, 2, false>(p, pd, s); break;
-    case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, pd, s) : launch_tail_nb<KM, 4, false>(p, pd, s); break;
-    case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, pd, s) : launch_tail_nb<KM, 8, false>(p, pd, s); break;
-    default: abs_sums ? launch_tail_nb<KM, 16, true>(p, pd, s) : launch_tail_nb<KM, 16, false>(p, pd, s); break;
+    case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, s) : launch_tail_nb<KM, 1, false>(p, s); break;
+    case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, s) : launch_tail_nb<KM, 2, false>(p, s); break;
+    case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, s) : launch_tail_nb<KM, 4, false>(p, s); break;
+    case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, s) : launch_tail_nb<KM, 8, false>(p, s); break;
+    default: abs_sums ? launch_tail_nb<KM, 16, true>(p, s) : launch_tail_nb<KM, 16, false>(p, s); break;
     }
 }
 
@@ -1404,10 +1395,10 @@ static void set_attributes()
     GVC_PASS1_ATTR_KM(KEY_HASH)
 }
 
-// The select pipeline on stream s, reading the plan from device memory (pd);
-// the host copy p only sizes the grids.  Returns the number of kernels.
+// The select pipeline on stream s; every kernel takes the plan by value (its
+// fields live in the constant bank).  Returns the number of kernels.
 template <int KM>
-static int launch_pipeline(const Plan &p, const Plan *pd, cudaStream_t s, bool probes)
+static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes)
 {
     ProfScope all(probes ? PROF_SELECT : -1, s);
     const int blocks = (int)p.B;
@@ -1415,66 +1406,64 @@ static int launch_pipeline(const Plan &p, const Plan *pd, cudaStream_t s, bool p
     if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
         uint64_t wb = (p.s_chunks + 31) / 32;
         int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
-        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(pd);
+        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);
         launches++;
     }
-    k_sample_resolve<<<1, 1024, 0, s>>>(pd);
+    k_sample_resolve<<<1, 1024, 0, s>>>(p, 0);
     {
         ProfScope pc(probes ? PROF_COLLECT : -1, s);
         if (!p.ef)
-            k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(pd, 0);
+            k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
         else if (!p.pmask)
-            k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(pd, 0);
+            k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
         else if (p.pmode == 1)
-            k_collect<KM, true, 1><<<blocks, GVC_THREADS, 0, s>>>(pd, 0);
+            k_collect<KM, true, 1><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
         else
-            k_collect<KM, true, 2><<<blocks, GVC_THREADS, 0, s>>>(pd, 0);
+            k_collect<KM, true, 2><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
     }
-    k_resolve0<<<1, 1024, 0, s>>>(pd, 0);
+    k_resolve0<<<1, 1024, 0, s>>>(p, 0);
     if (p.ef)
-        k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(pd, 1);
+        k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     else
-        k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(pd, 1);
-    k_resolve0<<<1, 1024, 0, s>>>(pd, 1);
+        k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
+    k_resolve0<<<1, 1024, 0, s>>>(p, 1);
     launches += 5;
-    launch_tail<KM>(p, pd, s);
+    launch_tail<KM>(p, s);
     launches += 3;
     switch (nb_for(p.n_ks)) {
-    case 1: k_finish<KM, 1><<<1, 1024, 0, s>>>(pd); break;
-    case 2: k_finish<KM, 2><<<1, 1024, 0, s>>>(pd); break;
-    case 4: k_finish<KM, 4><<<1, 1024, 0, s>>>(pd); break;
-    case 8: k_finish<KM, 8><<<1, 1024, 0, s>>>(pd); break;
-    default: k_finish<KM, 16><<<1, 1024, 0, s>>>(pd); break;
+    case 1: k_finish<KM, 1><<<1, 1024, 0, s>>>(p, 0); break;
+    case 2: k_finish<KM, 2><<<1, 1024, 0, s>>>(p, 0); break;
+    case 4: k_finish<KM, 4><<<1, 1024, 0, s>>>(p, 0); break;
+    case 8: k_finish<KM, 8><<<1, 1024, 0, s>>>(p, 0); break;
+    default: k_finish<KM, 16><<<1, 1024, 0, s>>>(p, 0); break;
     }
     return launches + 2;
 }
 
-__global__ void k_set_plan(Plan p, Plan *dst)
-{
-    // the only per-call parameter of the captured pipeline: the plan itself
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(&p);
-    uint32_t *d = reinterpret_cast<uint32_t *>(dst);
-    for (uint32_t i = threadIdx.x; i < sizeof(Plan) / 4; i += blockDim.x)
-        d[i] = src[i];
-}
+static_assert(sizeof(Plan) <= 4000, "the plan is passed as a kernel parameter");
 
-static void enqueue_select(const Plan &p, Plan *pd, cudaStream_t s, bool probes, int *launches)
+static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *launches)
 {
-    k_set_plan<<<1, 128, 0, s>>>(p, pd);
     cudaMemsetAsync(p.st, 0, sizeof(SelState), s);
     cudaMemsetAsync(p.hist0, 0, GVC_H0_BINS * 4, s);
     cudaMemsetAsync(p.histl, 0, GVC_MAX_LADDER * GVC_HL_BINS * 4, s);
     if (p.keymode == KEY_MAG)
         cudaMemsetAsync(p.shist, 0, GVC_SAMPLE_BINS * 4, s);
-    *launches = 1 + (p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, pd, s, probes)
-                                          : launch_pipeline<KEY_HASH>(p, pd, s, probes));
+    *launches = p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, s, probes) : launch_pipeline<KEY_HASH>(p, s, probes);
 }
 
-// CUDA graphs of the select pipeline, one per launch shape; per call only the
-// root k_set_plan node's argument (the plan) is updated before the launch.
+// CUDA graphs of the select pipeline, one per launch shape.  Every kernel has
+// the signature (Plan, int); per call the plan argument of each kernel node is
+// replaced (host-side only, no extra device work) before the launch.
+struct GraphNode {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams kp;
+    int aux;
+};
 struct GraphEntry {
+    cudaGraph_t graph;
     cudaGraphExec_t exec;
-    cudaGraphNode_t plan_node;
+    std::vector<GraphNode> nodes;
     int launches;
 };
 static std::unordered_map<std::string, GraphEntry> g_graphs;
@@ -1551,7 +1540,7 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     int launches = 0;
     if (prof_enabled()) {
         // measurement mode: direct launches bracketed by CUDA events (bench.py roofline)
-        enqueue_select(p, p.plan_dev, s, true, &launches);
+        enqueue_select(p, s, true, &launches);
     } else {
         const std::string key = graph_key(p, ws);
         std::lock_guard<std::mutex> glk(g_mu);
@@ -1563,29 +1552,42 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             cudaGraph_t graph;
             GraphEntry ge;
             cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
-            enqueue_select(p, p.plan_dev, cs, false, &ge.launches);
+            enqueue_select(p, cs, false, &ge.launches);
             cudaError_t ce = cudaStreamEndCapture(cs, &graph);
             if (ce != cudaSuccess)
                 return set_error(GVC_ERR_CUDA, "select graph capture: %s", cudaGetErrorString(ce));
-            size_t nroots = 1;
-            cudaGraphNode_t root;
-            cudaGraphGetRootNodes(graph, &root, &nroots);
-            ge.plan_node = root;
+            size_t nn = 0;
+            cudaGraphGetNodes(graph, nullptr, &nn);
+            std::vector<cudaGraphNode_t> all(nn);
+            cudaGraphGetNodes(graph, all.data(), &nn);
+            for (cudaGraphNode_t nd : all) {
+                cudaGraphNodeType ty;
+                cudaGraphNodeGetType(nd, &ty);
+                if (ty != cudaGraphNodeTypeKernel)
+                    continue;
+                GraphNode gn;
+                gn.node = nd;
+                cudaGraphKernelNodeGetParams(nd, &gn.kp);
+                gn.aux = *(const int *)gn.kp.kernelParams[1];
+                gn.kp.kernelParams = nullptr;
+                gn.kp.extra = nullptr;
+                ge.nodes.push_back(gn);
+            }
             ce = cudaGraphInstantiate(&ge.exec, graph, 0);
+            ge.graph = graph;  // kept alive: the exec-node updates name its nodes
             if (ce != cudaSuccess)
                 return set_error(GVC_ERR_CUDA, "select graph instantiate: %s", cudaGetErrorString(ce));
-            it = g_graphs.emplace(key, ge).first;
+            it = g_graphs.emplace(key, std::move(ge)).first;
         }
-        Plan *pd = p.plan_dev;
-        void *args[2] = {(void *)&p, (void *)&pd};
-        cudaKernelNodeParams kp = {};
-        kp.func = (void *)k_set_plan;
-        kp.gridDim = dim3(1);
-        kp.blockDim = dim3(128);
-        kp.sharedMemBytes = 0;
-        kp.kernelParams = args;
-        kp.extra = nullptr;
-        cudaGraphExecKernelNodeSetParams(it->second.exec, it->second.plan_node, &kp);
+        for (GraphNode &gn : it->second.nodes) {
+            int aux = gn.aux;
+            void *args[2] = {(void *)&p, (void *)&aux};
+            cudaKernelNodeParams kp = gn.kp;
+            kp.kernelParams = args;
+            cudaError_t ue = cudaGraphExecKernelNodeSetParams(it->second.exec, gn.node, &kp);
+            if (ue != cudaSuccess)
+                return set_error(GVC_ERR_CUDA, "select graph update: %s", cudaGetErrorString(ue));
+        }
         cudaGraphLaunch(it->second.exec, s);
         launches = it->second.launches;
     }
