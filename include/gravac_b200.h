@@ -181,6 +181,54 @@ GVC_API int gvc_aggregate(const uint32_t *idx_dev, const float *vals_dev, const 
                   void *stream);
 GVC_API size_t gvc_aggregate_workspace_bytes(int nparts, uint64_t n);
 
+/* ---- fused sparse allgather + decompress-average over peer memory (C1 + K7) ----
+ * The reference simulates the workers in one process and calls
+ * aggregate(parts) (compressors.py:256-271; simworkers.py:242-245).  On one
+ * NVLink/NVSwitch node every rank's payload lives in a peer-mapped
+ * (symmetric) buffer, and K7 reads the peers' (idx, vals, tile bounds)
+ * directly -- the all-gather never materialises a gathered copy.
+ *
+ * gvc_peer_signal: once this rank's payload is complete (stream order), post
+ *   `epoch` into peer_flags[q][rank] for every rank q (own included).
+ *   peer_flags: HOST array of nranks device pointers (each rank's u32 flag
+ *   array of >= nranks words, peer-mapped).
+ * gvc_aggregate_peers: every CTA first waits until flags_dev[p] >= epoch
+ *   (wrap-around compare) for p < nparts, then averages the parts exactly as
+ *   gvc_aggregate (fp64, part order, /nparts).  idx/vals/bounds: HOST arrays
+ *   of nparts device pointers (peer-mapped), bounds as gvc_emit's
+ *   tile_bounds_dev; counts: HOST array.
+ * Reuse rule (the caller's): with a payload double buffer and one epoch per
+ *   exchange, slot e % 2 is rewritten only after every rank has posted epoch
+ *   e + 1, i.e. after every rank's merge of epoch e has completed. */
+#define GVC_MAX_PEERS 8
+
+/* Push form of the exchange: the emit also writes its (idx, vals, tile
+ * bounds) into up to GVC_MAX_PEERS - 1 further destinations -- the peers'
+ * receive slots in their symmetric buffers -- with ordinary stores over
+ * NVLink while it runs, then every thread issues a system-scope fence.  The
+ * NVLink transfer overlaps the emit itself, and the merge reads only local
+ * memory.  Fields: count (0..GVC_MAX_PEERS-1) and per destination the device
+ * pointers (bounds_dev only used when the emit writes tile bounds). */
+typedef struct gvc_emit_mirrors {
+    int32_t count;
+    int32_t reserved;
+    uint32_t *idx_dev[GVC_MAX_PEERS];
+    float *vals_dev[GVC_MAX_PEERS];
+    uint32_t *bounds_dev[GVC_MAX_PEERS];
+} gvc_emit_mirrors;
+/* gvc_emit plus mirrors (NULL mirrors == gvc_emit). */
+GVC_API int gvc_emit_mirrored(void *ws_dev, size_t ws_bytes, int j, const uint32_t *idx_map_dev,
+             uint32_t *out_idx_dev, float *out_val_dev, float *resid_dev,
+             uint32_t *sent_mask_dev, float *sent_m_dev, uint32_t *tile_bounds_dev,
+             double *sent_stats_dev, const gvc_emit_mirrors *mirrors, void *stream);
+GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, uint32_t epoch, void *stream);
+GVC_API int gvc_aggregate_peers(const uint32_t *const *idx_dev, const float *const *vals_dev,
+                        const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,
+                        const uint32_t *flags_dev, uint32_t epoch, float *out_dev, void *stream);
+/* Tile boundaries (gvc_emit's tile_bounds_dev layout) of one index-ascending
+ * list of k entries over [0, n): u32[ceil(n / GVC_AGG_TILE) + 1]. */
+GVC_API int gvc_tile_bounds(const uint32_t *idx_dev, uint64_t k, uint64_t n, uint32_t *bounds_dev, void *stream);
+
 /* fp64 mean of nparts dense vectors laid out [nparts][n] (compressors.py:274-285). */
 GVC_API int gvc_aggregate_dense(const float *parts_dev, int nparts, uint64_t n, float *out_dev,
                         void *stream);

@@ -29,7 +29,9 @@ EXPORTS = (
     "gvc_decompress", "gvc_aggregate", "gvc_aggregate_workspace_bytes", "gvc_aggregate_dense",
     "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
+    "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
 )
+MAX_PEERS = 8  # GVC_MAX_PEERS
 
 _u64, _i32, _f64, _vp, _sz = ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
 
@@ -66,6 +68,12 @@ class SelectResult(ctypes.Structure):
 
 
 RESULT_BYTES = ctypes.sizeof(SelectResult)
+
+
+class EmitMirrors(ctypes.Structure):
+    """gvc_emit_mirrors: peer destinations the emit also writes (push exchange)."""
+    _fields_ = [("count", _i32), ("reserved", _i32), ("idx_dev", _vp * 8), ("vals_dev", _vp * 8),
+                ("bounds_dev", _vp * 8)]
 
 _lib = None
 _lock = threading.Lock()
@@ -112,6 +120,11 @@ def load(build_if_missing: bool = False):
         L.gvc_compact_workspace_bytes.argtypes = [_u64]
         L.gvc_compact_workspace_bytes.restype = _sz
         L.gvc_compact_mask.argtypes = [_vp, _u64, _vp, _vp, _vp, _sz, _vp]
+        L.gvc_peer_signal.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, _vp]
+        L.gvc_aggregate_peers.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32, _vp, _vp]
+        L.gvc_tile_bounds.argtypes = [_vp, _u64, _u64, _vp, _vp]
+        L.gvc_emit_mirrored.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        ctypes.POINTER(EmitMirrors), _vp]
         L.gvc_prof_enable.argtypes = [ctypes.c_int]
         L.gvc_prof_enable.restype = None
         L.gvc_prof_read.argtypes = [_vp, _vp, ctypes.c_int]
@@ -203,6 +216,58 @@ def d2h_bytes(t: torch.Tensor) -> bytes:
     while not ev.query():
         pass
     return host.numpy().tobytes()
+
+
+_side: dict = {}
+
+
+def side_stream(device) -> torch.cuda.Stream:
+    """A per-device side stream for read-backs and small collectives that
+    must not queue behind the main stream's later work."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    s = _side.get(idx)
+    if s is None:
+        s = torch.cuda.Stream(device=device)
+        _side[idx] = s
+    return s
+
+
+class PendingRead:
+    """A device->host copy started on the side stream; ``wait()`` spins on its event."""
+
+    __slots__ = ("host", "ev", "src")
+
+    def __init__(self, host, ev, src):
+        self.host, self.ev, self.src = host, ev, src
+
+    def wait(self) -> bytes:
+        while not self.ev.query():
+            pass
+        self.src = None
+        return self.host.numpy().tobytes()
+
+
+def d2h_start(t: torch.Tensor, ready: "torch.cuda.Event | None" = None) -> PendingRead:
+    """Start the read-back of a small tensor once the current stream reaches
+    this point (or ``ready``), on the side stream: work enqueued afterwards on
+    the current stream is not delayed by the copy, and the host can wait for
+    this result while that work runs."""
+    nb = t.numel() * t.element_size()
+    key = ("async", t.device.index, nb)
+    buf = _pinned.get(key)
+    if buf is None:
+        buf = (torch.empty(nb, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+        _pinned[key] = buf
+    host, ev = buf
+    side = side_stream(t.device)
+    if ready is None:
+        ready = torch.cuda.Event()
+        ready.record()
+    side.wait_event(ready)
+    with torch.cuda.stream(side):
+        host.copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+        ev.record()
+    return PendingRead(host, ev, t)
 
 
 def read_result(res_dev: torch.Tensor) -> SelectResult:

@@ -173,15 +173,25 @@ class Selection:
         residual update, either direct (``resid``) or deferred (``sent_mask``).
         ``count`` overrides the entry count (a DGC overshoot keeps fewer)."""
         k = self.ks[j] if count is None else int(count)
+        mirrors = None
         if payload is not None:  # write straight into the packed wire buffer (exchange.Payload)
             out_idx, out_val = payload.idx[:k], payload.vals[:k]
             tile_bounds = payload.bounds if payload.bounds is not None else tile_bounds
+            mirrors = payload.mirrors
         else:
             out_idx = torch.empty(k, dtype=torch.uint32, device=self.device)
             out_val = torch.empty(k, dtype=torch.float32, device=self.device)
-        nat.check(nat.load().gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
-                                      nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
-                                      nat.ptr(tile_bounds), nat.ptr(stats), nat.stream_ptr(self.device)), "gvc_emit")
+        lib = nat.load()
+        if mirrors is not None:  # push exchange: the peers' receive slots get the same stores
+            nat.check(lib.gvc_emit_mirrored(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
+                                            nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
+                                            nat.ptr(tile_bounds), nat.ptr(stats), ctypes.byref(mirrors),
+                                            nat.stream_ptr(self.device)), "gvc_emit")
+            payload.pushed = tile_bounds is not None and count is None
+        else:
+            nat.check(lib.gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
+                                   nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
+                                   nat.ptr(tile_bounds), nat.ptr(stats), nat.stream_ptr(self.device)), "gvc_emit")
         return out_idx, out_val
 
     def result(self) -> nat.SelectResult:

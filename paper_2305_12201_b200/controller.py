@@ -15,6 +15,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Sequence
 
+import numpy as np
 import torch
 
 from . import _native as nat
@@ -325,20 +326,6 @@ class _WorkerStep:
         return part
 
 
-def _read_results(tensors: list[torch.Tensor]) -> list[bytes]:
-    """One device->host copy for every worker's device-side statistics."""
-    if not tensors:
-        return []
-    flat = nat.d2h_bytes(tensors[0] if len(tensors) == 1 else
-                         torch.cat([t.reshape(-1).view(torch.uint8) for t in tensors]))
-    out, pos = [], 0
-    for t in tensors:
-        nb = t.numel() * t.element_size()
-        out.append(flat[pos:pos + nb])
-        pos += nb
-    return out
-
-
 class _DgcStep:
     """DGC worker step: level 1 over g_ef (fused EF pass with the sampled
     threshold), level 2 over the level-1 values (compressors.py:226-246)."""
@@ -406,18 +393,31 @@ class _DgcStep:
         return part
 
 
+TIMELINE = None  # development aid (scripts/timeline.py): a list receiving (name, event, host time)
+
+
+def _mark(name: str, stream=None) -> None:
+    if TIMELINE is not None:
+        import time
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        TIMELINE.append((name, ev, time.perf_counter()))
+
+
 def _mean_raw_gain(energies: Sequence[float], ef_norms: Sequence[float]) -> float:
     """Mean over non-zero-norm workers of min(1, E/||g_ef||^2), worker order (controller.py:284-288)."""
     gains = [min(1.0, e / n) for e, n in zip(energies, ef_norms) if n > 0.0]
     return sum(gains) / len(gains)
 
 
-def _average(sent, group, out: torch.Tensor | None):
+def _average(sent, group, out: torch.Tensor | None, peer=None):
     """The step's exchange + mean of the sent views: worker parts on this GPU
     (compressors.aggregate / aggregate_dense) or, with a process group, C1 + K7
-    (sparse) / C3 (dense) across the ranks."""
+    (sparse; fused over peer memory when ``peer``) / C3 (dense) across the ranks."""
     from .compressors import aggregate_packed, aggregate_dense
     if isinstance(sent[0], SparseGradient):
+        if peer is not None:
+            return GradientVector._wrap(peer.aggregate(sent[0], out=out))
         if group is not None:
             from .exchange import allgather_aggregate
             return allgather_aggregate(sent[0], group, out=out)
@@ -451,6 +451,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     it is enqueued behind the speculative emit, so the device never waits for
     the host's decision.
     """
+    _mark("start")
     cfg = state.config
     grads = [gradients] if isinstance(gradients, GradientVector) else list(gradients)
     stores = [residuals] if isinstance(residuals, ResidualStore) else list(residuals)
@@ -483,32 +484,69 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         else:
             steps.append(_WorkerStep(kind, g.values, store, k1, k2, extra_ks, rng, i, rank + w))
 
+    _mark("selected")
+    dev = grads[0].values.device
+    peer = None
+    if group is not None:
+        from .exchange import PeerExchange, use_peer_exchange
+        if use_peer_exchange(group):
+            peer = PeerExchange.get(group, dev)
+
+    # ---- one device->host read per iteration: every worker's norms and
+    # energies (with a process group: C2, all-gathered first).  Started on the
+    # side stream BEFORE the speculative emit is enqueued, so the host decides
+    # while the GPU emits and exchanges.
+    stats = [t for s in steps for t in s.stats_dev()]
+    sizes = [t.numel() * t.element_size() for t in stats]
+    flat = stats[0].reshape(-1).view(torch.uint8) if len(stats) == 1 else \
+        torch.cat([t.reshape(-1).view(torch.uint8) for t in stats])
+    pending = rows = None
+    if group is not None:
+        import torch.distributed as dist
+        if dist.get_backend(group) == "nccl":
+            ready = torch.cuda.Event()
+            ready.record()
+            side = nat.side_stream(dev)
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                gathered = torch.empty((dist.get_world_size(group), flat.numel()), dtype=torch.uint8, device=dev)
+                dist.all_gather_into_tensor(gathered, flat, group=group)
+                pending = nat.d2h_start(gathered)
+                _mark("c2_read", side)
+        else:
+            from .exchange import allgather_stats
+            rows = allgather_stats(flat.cpu(), group)
+    else:
+        pending = nat.d2h_start(flat)
+
     # ---- speculative emit: enqueue the previous step's choice right behind the
     # select so the GPU keeps working while the host reads the gains back; a
     # misprediction is re-emitted below (the sent mask is rebuilt from zero)
-    dev = grads[0].values.device
     spec = getattr(state, "_spec_choice", CANDIDATE)
     spec_parts = None
+
+    def wire(s, c, bnd):
+        if peer is not None:
+            return peer.slot(s.chosen_count(c), length, push=bnd)
+        from .exchange import new_payload
+        return new_payload(s.chosen_count(c), dev, n=length if bnd else None)
+
     if kind.name == TOPK and not steps[0].identity1 and spec in (CANDIDATE, MINIMUM):
         c = spec == CANDIDATE
         if group is not None:
-            from .exchange import new_payload
-            spec_parts = [s.emit(c, new_payload(s.chosen_count(c), dev, n=length)) for s in steps]
+            spec_parts = [s.emit(c, wire(s, c, True)) for s in steps]
         else:
             spec_parts = [s.emit(c, bounds=average) for s in steps]
-    spec_avg = _average(spec_parts, group, average_out) if (average and spec_parts is not None) else None
+    _mark("spec_emitted")
+    spec_avg = _average(spec_parts, group, average_out, peer) if (average and spec_parts is not None) else None
+    _mark("spec_averaged")
 
-    # ---- one device->host read per iteration: every worker's norms and energies
-    stats = [t for s in steps for t in s.stats_dev()]
+    if pending is not None:
+        raw_all = pending.wait()
+        _mark("host_has_stats")
+        if group is not None:
+            rows = np.frombuffer(raw_all, dtype=np.uint8).reshape(-1, flat.numel())
     if group is not None:
-        # C2: the raw result bytes of every rank, gathered on the device, read once
-        from .exchange import allgather_stats
-        flat = torch.cat([t.reshape(-1).view(torch.uint8) for t in stats])
-        import torch.distributed as dist
-        if dist.get_backend(group) != "nccl":
-            flat = flat.cpu()
-        rows = allgather_stats(flat, group)
-        sizes = [t.numel() * t.element_size() for t in stats]
         local = []
         for row in rows:
             raw, pos = [], 0
@@ -517,13 +555,14 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
                 pos += nb
             local.append(steps[0].gains_from(raw, None))
     else:
-        results = _read_results(stats)
-        local = []
-        pos = 0
-        for w, s in enumerate(steps):
-            cnt = len(s.stats_dev())
-            local.append(s.gains_from(results[pos:pos + cnt], None))
-            pos += cnt
+        local, pos, t = [], 0, 0
+        for s in steps:
+            raw = []
+            for _ in range(len(s.stats_dev())):
+                raw.append(raw_all[pos:pos + sizes[t]])
+                pos += sizes[t]
+                t += 1
+            local.append(s.gains_from(raw, None))
     ef_norms = [x[0] for x in local]
 
     def drop_speculation():
@@ -550,7 +589,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         out = IterationResult(sent, decision, cost.t_compute, 0.0, t_sync, t_iter, length,
                               dense_message_words(length), 1.0, 1.0, candidate_cf, theta_min)
         if average:
-            out.averaged = _average(sent, group, None)
+            out.averaged = _average(sent, group, None, peer)
         return out
 
     raw_min = _mean_raw_gain([x[1] for x in local], ef_norms)
@@ -585,10 +624,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         cand = decision.choice == CANDIDATE
         if spec_parts is not None:
             sent = spec_parts
-        elif group is not None:  # emit straight into the packed wire buffer of the all-gather
-            from .exchange import new_payload
+        elif group is not None:  # emit straight into the wire buffer (peer slot / all-gather payload)
             bnd = kind.name == TOPK and not steps[0].identity1
-            sent = [s.emit(cand, new_payload(s.chosen_count(cand), dev, n=length if bnd else None)) for s in steps]
+            sent = [s.emit(cand, wire(s, cand, bnd)) for s in steps]
         else:
             sent = [s.emit(cand, bounds=average) for s in steps]
         floats = sent[0].kept
@@ -602,5 +640,6 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
                           t_sync, t_iter, floats, words, raw_min, raw_c, candidate_cf, theta_min, ladder)
     if average:
         out.averaged = spec_avg if (spec_parts is not None and sent is spec_parts) else \
-            _average(sent, group, average_out if decision.choice != DENSE else None)
+            _average(sent, group, average_out if decision.choice != DENSE else None, peer)
+    _mark("end")
     return out

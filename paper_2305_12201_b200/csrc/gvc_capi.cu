@@ -163,8 +163,9 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     return select_run(a, ws, ws_bytes, res, STREAM(stream));
 }
 
-int gvc_emit(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
-             float *resid, uint32_t *sent_mask, float *sent_m, uint32_t *tile_bounds, double *stats, void *stream)
+int gvc_emit_mirrored(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
+                      float *resid, uint32_t *sent_mask, float *sent_m, uint32_t *tile_bounds, double *stats,
+                      const gvc_emit_mirrors *mirrors, void *stream)
 {
     if (!ws || !out_idx || !out_val)
         return set_error(GVC_ERR_ARG, "gvc_emit: null argument");
@@ -172,8 +173,22 @@ int gvc_emit(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         return set_error(GVC_ERR_ARG, "gvc_emit: pass resid_dev or sent_mask_dev, not both");
     if (tile_bounds && idx_map)
         return set_error(GVC_ERR_ARG, "gvc_emit: tile bounds need output indices in selection order (no idx_map)");
+    if (mirrors) {
+        if (mirrors->count < 0 || mirrors->count >= GVC_MAX_PEERS)
+            return set_error(GVC_ERR_ARG, "gvc_emit: %d mirrors (at most %d)", mirrors->count, GVC_MAX_PEERS - 1);
+        for (int m = 0; m < mirrors->count; m++)
+            if (!mirrors->idx_dev[m] || !mirrors->vals_dev[m] || (tile_bounds && !mirrors->bounds_dev[m]))
+                return set_error(GVC_ERR_ARG, "gvc_emit: mirror %d has a null pointer", m);
+    }
     return emit_run(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, sent_mask, sent_m, tile_bounds, stats,
-                    STREAM(stream));
+                    mirrors, STREAM(stream));
+}
+
+int gvc_emit(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
+             float *resid, uint32_t *sent_mask, float *sent_m, uint32_t *tile_bounds, double *stats, void *stream)
+{
+    return gvc_emit_mirrored(ws, ws_bytes, j, idx_map, out_idx, out_val, resid, sent_mask, sent_m, tile_bounds,
+                             stats, nullptr, stream);
 }
 
 int gvc_mark_sent(const uint32_t *idx, uint64_t k, uint32_t *mask, void *stream)
@@ -241,6 +256,32 @@ int gvc_aggregate(const uint32_t *idx, const float *vals, const uint64_t *offs, 
     int rc = aggregate_run(idx, vals, offs, counts, nparts, n, out, ws, ws_bytes, bounds, bounds_stride,
                            STREAM(stream));
     return rc ? rc : check_launch("aggregate");
+}
+
+int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, uint32_t epoch, void *stream)
+{
+    if (!peer_flags)
+        return set_error(GVC_ERR_ARG, "gvc_peer_signal: null flag array");
+    int rc = peer_signal_run(peer_flags, nranks, rank, epoch, STREAM(stream));
+    return rc ? rc : check_launch("peer_signal");
+}
+
+int gvc_aggregate_peers(const uint32_t *const *idx, const float *const *vals, const uint32_t *const *bounds,
+                        const uint64_t *counts, int nparts, uint64_t n, const uint32_t *flags, uint32_t epoch,
+                        float *out, void *stream)
+{
+    if (!idx || !vals || !bounds || !counts || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_aggregate_peers: bad arguments");
+    int rc = aggregate_peers_run(idx, vals, bounds, counts, nparts, n, flags, epoch, out, STREAM(stream));
+    return rc ? rc : check_launch("aggregate_peers");
+}
+
+int gvc_tile_bounds(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, void *stream)
+{
+    if (!idx || !bounds || n < 1 || k > n)
+        return set_error(GVC_ERR_ARG, "gvc_tile_bounds: bad arguments");
+    int rc = tile_bounds_run(idx, k, n, bounds, STREAM(stream));
+    return rc ? rc : check_launch("tile_bounds");
 }
 
 int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, void *stream)

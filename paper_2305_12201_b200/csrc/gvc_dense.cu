@@ -336,21 +336,28 @@ int compact_mask_run(const uint32_t *mask, uint64_t n, uint32_t *out, unsigned l
 #define AGG_THREADS 256
 #define AGG_MAX_PARTS 64
 
+// Every part by its own pointers: the parts of one gathered buffer, or the
+// payload slots of the peers' symmetric buffers (read over NVLink).
+struct PeerFlags {
+    uint32_t *flags[GVC_MAX_PEERS];
+};
+
 struct AggParts {
-    uint64_t off[AGG_MAX_PARTS];
+    const uint32_t *idx[AGG_MAX_PARTS];
+    const float *vals[AGG_MAX_PARTS];
+    const uint32_t *bounds[AGG_MAX_PARTS];
     uint64_t cnt[AGG_MAX_PARTS];
 };
 
 // Tile boundaries of every part in one streaming pass over the index lists:
 // bounds[p * (ntiles + 1) + b] = first entry of part p with index >= b * TILE.
-__global__ void k_tile_bounds(const uint32_t *__restrict__ idx, AggParts parts, int nparts, uint64_t ntiles,
-                              uint32_t *__restrict__ bounds)
+__global__ void k_tile_bounds(AggParts parts, int nparts, uint64_t ntiles, uint32_t *__restrict__ bounds)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const int p = blockIdx.y;
     if (p >= nparts)
         return;
-    const uint32_t *pi = idx + parts.off[p];
+    const uint32_t *pi = parts.idx[p];
     const uint64_t cnt = parts.cnt[p];
     uint32_t *bp = bounds + (uint64_t)p * (ntiles + 1);
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= cnt; t += stride) {
@@ -361,17 +368,34 @@ __global__ void k_tile_bounds(const uint32_t *__restrict__ idx, AggParts parts, 
     }
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // MODE 0: decompress (fp32 assignment, -0.0 kept); 1: mean of ONE part
 // (0.0 + v in fp64 then /1: v, except -0.0 -> +0.0); 2: fp64 mean of N parts.
-template <int MODE>
-__global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__restrict__ idx,
-                                                            const float *__restrict__ vals, AggParts parts,
-                                                            int nparts, uint64_t n, uint64_t ntiles,
-                                                            const uint32_t *__restrict__ bounds, uint64_t bstride,
-                                                            float *__restrict__ out)
+// Parts are taken in groups of NP: the group's tile bounds are fetched by NP
+// threads at once, then (when every part of the group has at most
+// U * AGG_THREADS entries in this tile, the common case) ALL their entries
+// are loaded into registers before the part-ordered accumulation starts, so
+// a tile costs two dependent memory latencies instead of two per part --
+// what matters when the parts sit behind NVLink.
+// WAIT: the parts live in the peers' memory; before reading part p a thread
+// waits until peer p has posted `epoch` into flags[p] (its payload is
+// complete), and all part reads bypass L1 (ld.global.cg), so no stale line of
+// an earlier exchange through the same slot can be hit.
+template <int MODE, bool WAIT, int NP>
+__global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int nparts, uint64_t n,
+                                                            float *__restrict__ out, const uint32_t *flags,
+                                                            uint32_t epoch)
 {
+    constexpr int U = NP >= 8 ? 2 : 4;
     __shared__ __align__(16) double acc[MODE == 2 ? AGG_TILE : 2];
     __shared__ __align__(16) float accf[MODE == 2 ? 4 : AGG_TILE];
+    __shared__ uint32_t s_a[NP], s_b[NP];
     const uint32_t tile = blockIdx.x;
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
@@ -382,27 +406,85 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
         for (int i = threadIdx.x; i < AGG_TILE / 4; i += AGG_THREADS)
             reinterpret_cast<float4 *>(accf)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    __syncthreads();
-    for (int p = 0; p < nparts; p++) {
-        const uint32_t *pi = idx + parts.off[p];
-        const float *pv = vals + parts.off[p];
-        const uint32_t *bp = bounds + (uint64_t)p * bstride;
-        const uint32_t a = bp[tile], b = bp[tile + 1];
-        for (uint32_t t = a + threadIdx.x; t < b; t += AGG_THREADS) {
-            const uint32_t r = pi[t] - (uint32_t)lo;
-            const float v = pv[t];
-            if (MODE == 2)
-                acc[r] += (double)v;
-            else if (MODE == 1)
-                accf[r] = v == 0.0f ? 0.0f : v;
-            else
-                accf[r] = v;
-        }
+    auto put = [&](uint32_t r, float v) {
         if (MODE == 2)
-            __syncthreads();  // worker order per position (compressors.py:266-269)
-    }
-    if (MODE != 2)
+            acc[r] += (double)v;
+        else if (MODE == 1)
+            accf[r] = v == 0.0f ? 0.0f : v;
+        else
+            accf[r] = v;
+    };
+    for (int p0 = 0; p0 < nparts; p0 += NP) {
+        const int np = min(NP, nparts - p0);
+        if (threadIdx.x < np) {
+            const int p = p0 + threadIdx.x;
+            if (WAIT) {
+                while ((int32_t)(ld_acquire_sys(flags + p) - epoch) < 0)
+                    __nanosleep(64);
+            }
+            s_a[threadIdx.x] = __ldcg(parts.bounds[p] + tile);
+            s_b[threadIdx.x] = __ldcg(parts.bounds[p] + tile + 1);
+        }
         __syncthreads();
+        uint32_t maxlen = 0;
+        for (int q = 0; q < np; q++)
+            maxlen = max(maxlen, s_b[q] - s_a[q]);
+        if (maxlen <= U * AGG_THREADS) {
+            uint32_t r[NP][U];
+            float v[NP][U];
+#pragma unroll
+            for (int q = 0; q < NP; q++) {
+                if (q < np) {
+                    const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
+                    const uint32_t *pi = parts.idx[p0 + q];
+                    const float *pv = parts.vals[p0 + q];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        if (a + u * AGG_THREADS < b) {
+                            r[q][u] = __ldcg(pi + a + u * AGG_THREADS) - (uint32_t)lo;
+                            v[q][u] = __ldcg(pv + a + u * AGG_THREADS);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NP; q++) {
+                if (q < np) {
+                    const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
+#pragma unroll
+                    for (int u = 0; u < U; u++)
+                        if (a + u * AGG_THREADS < b)
+                            put(r[q][u], v[q][u]);
+                    if (MODE == 2)
+                        __syncthreads();  // worker order per position (compressors.py:266-269)
+                }
+            }
+        } else {
+            for (int q = 0; q < np; q++) {
+                const uint32_t *pi = parts.idx[p0 + q];
+                const float *pv = parts.vals[p0 + q];
+                const uint32_t b = s_b[q];
+                for (uint32_t t0 = s_a[q] + threadIdx.x; t0 < b; t0 += U * AGG_THREADS) {
+                    uint32_t r[U];
+                    float v[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        if (t0 + u * AGG_THREADS < b) {
+                            r[u] = __ldcg(pi + t0 + u * AGG_THREADS) - (uint32_t)lo;
+                            v[u] = __ldcg(pv + t0 + u * AGG_THREADS);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++)
+                        if (t0 + u * AGG_THREADS < b)
+                            put(r[u], v[u]);
+                }
+                if (MODE == 2)
+                    __syncthreads();
+            }
+        }
+        __syncthreads();  // s_a / s_b are rewritten by the next group
+    }
     // x / N == x * (1/N) exactly only for power-of-two N; zeros skip the divide
     const double np = (double)nparts;
     const bool pow2 = (nparts & (nparts - 1)) == 0;
@@ -430,21 +512,214 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(const uint32_t *__re
     }
 }
 
+// The same tile merge for nparts <= NP <= 4 without the fp64 read-modify-
+// write: every part scatters its values into its OWN fp32 shared tile (no
+// ordering between parts needed, one barrier), and each output is then
+// formed in registers as ((0.0 + v_0) + v_1 + ...) in fp64, part order --
+// exactly aggregate()'s sum, because a part without an entry at a position
+// contributes +0.0, which leaves any fp64 sum starting from +0.0 unchanged
+// (it can never be -0.0).  MODE 0: decompress (one part, fp32 copy, -0.0
+// kept); MODE 1: average.  Dynamic shared memory: NP * AGG_TILE floats.
+template <int MODE, bool WAIT, int NP>
+__global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int nparts, uint64_t n,
+                                                           float *__restrict__ out, const uint32_t *flags,
+                                                           uint32_t epoch)
+{
+    constexpr int U = NP >= 4 ? 2 : 4;
+    extern __shared__ __align__(16) float tiles[];
+    __shared__ uint32_t s_a[NP], s_b[NP];
+    const uint32_t tile = blockIdx.x;
+    const uint64_t lo = (uint64_t)tile * AGG_TILE;
+    const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
+    if (threadIdx.x < nparts) {
+        const int p = threadIdx.x;
+        if (WAIT) {
+            while ((int32_t)(ld_acquire_sys(flags + p) - epoch) < 0)
+                __nanosleep(64);
+        }
+        s_a[p] = __ldcg(parts.bounds[p] + tile);
+        s_b[p] = __ldcg(parts.bounds[p] + tile + 1);
+    }
+    for (int i = threadIdx.x; i < nparts * (AGG_TILE / 4); i += AGG_THREADS)
+        reinterpret_cast<float4 *>(tiles)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    uint32_t maxlen = 0;
+    for (int q = 0; q < nparts; q++)
+        maxlen = max(maxlen, s_b[q] - s_a[q]);
+    if (maxlen <= U * AGG_THREADS) {
+        // every entry of every part in flight before the first store
+        uint32_t r[NP][U];
+        float v[NP][U];
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+            if (q < nparts) {
+                const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (a + u * AGG_THREADS < b) {
+                        r[q][u] = __ldcg(parts.idx[q] + a + u * AGG_THREADS) - (uint32_t)lo;
+                        v[q][u] = __ldcg(parts.vals[q] + a + u * AGG_THREADS);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+            if (q < nparts) {
+                const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (a + u * AGG_THREADS < b)
+                        tiles[q * AGG_TILE + r[q][u]] = v[q][u];
+            }
+        }
+    } else {
+        for (int q = 0; q < nparts; q++) {
+            const uint32_t *pi = parts.idx[q];
+            const float *pv = parts.vals[q];
+            const uint32_t b = s_b[q];
+            for (uint32_t t0 = s_a[q] + threadIdx.x; t0 < b; t0 += U * AGG_THREADS) {
+                uint32_t r[U];
+                float v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (t0 + u * AGG_THREADS < b) {
+                        r[u] = __ldcg(pi + t0 + u * AGG_THREADS) - (uint32_t)lo;
+                        v[u] = __ldcg(pv + t0 + u * AGG_THREADS);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (t0 + u * AGG_THREADS < b)
+                        tiles[q * AGG_TILE + r[u]] = v[u];
+            }
+        }
+    }
+    __syncthreads();
+    // Output = fl32(((0.0 + v_0) + v_1 + ...) / N) in fp64, part order.  For a
+    // power-of-two N with at most two non-zero terms the fp32 evaluation
+    // ((0.0f + v_0) + v_1 + ...) * (1/N) is bit-identical: adding zeros is
+    // exact, one fp32 add of two fp32 values rounds exactly like the fp64 add
+    // followed by the fp32 rounding (the fp64 sum of two fp32 values is exact
+    // unless their exponents differ by > 29, and then both round to the larger
+    // term), and the 1/N scaling is exact above the subnormal range.  Every
+    // other output (>= 3 non-zero terms, a tiny sum, non-power-of-two N) takes
+    // the fp64 path, as does an fp32 sum that overflowed.  This keeps the fp64 convert/add units -- a fraction of
+    // the fp32 rate -- off the common path.
+    const double np = (double)nparts;
+    const bool pow2 = (nparts & (nparts - 1)) == 0;
+    const double inv = 1.0 / np;
+    const float invf = (float)inv;
+    auto combine = [&](const float (&t)[NP]) -> float {
+        if (MODE == 0)
+            return t[0];
+        float s = 0.0f;
+        int nz = 0;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+            if (q < nparts) {
+                s += t[q];
+                nz += t[q] != 0.0f;
+            }
+        }
+        if (NP == 1)
+            return s;  // 0.0f + v: -0.0 -> +0.0, exact otherwise
+        // fp32 fast path unless the sum is tiny (scaling could round) or
+        // overflowed in fp32 (the fp64 sum may still be finite)
+        if (pow2 && nz <= 2 && (s == 0.0f || (fabsf(s) >= 0x1p-100f && fabsf(s) <= 3.4028234663852886e38f)))
+            return s * invf;
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < NP; q++)
+            if (q < nparts)
+                acc += (double)t[q];
+        if (acc == 0.0)
+            return 0.0f;
+        return (float)(pow2 ? acc * inv : acc / np);
+    };
+    // |s| == 0 or 2^-100 <= |s| <= FLT_MAX, on the bits
+    auto range_ok = [](float x) -> bool {
+        const uint32_t u = __float_as_uint(x) & 0x7fffffffu;
+        return u == 0u || (u - 0x0d800000u) < (0x7f800000u - 0x0d800000u);
+    };
+    if (width == AGG_TILE && (((uintptr_t)(out + lo)) & 15) == 0) {
+        for (int i = threadIdx.x; i < AGG_TILE / 4; i += AGG_THREADS) {
+            float4 t4[NP];
+#pragma unroll
+            for (int q = 0; q < NP; q++)
+                t4[q] = q < nparts ? reinterpret_cast<const float4 *>(tiles + q * AGG_TILE)[i]
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 o;
+            if (MODE == 0) {
+                o = t4[0];
+            } else {
+                // fp32 sums from +0.0 in part order (parts past nparts add +0.0)
+                float4 s4 = make_float4(0.0f + t4[0].x, 0.0f + t4[0].y, 0.0f + t4[0].z, 0.0f + t4[0].w);
+#pragma unroll
+                for (int q = 1; q < NP; q++) {
+                    s4.x += t4[q].x;
+                    s4.y += t4[q].y;
+                    s4.z += t4[q].z;
+                    s4.w += t4[q].w;
+                }
+                bool ok = true;
+                if (NP > 1) {
+                    ok = pow2 && range_ok(s4.x) && range_ok(s4.y) && range_ok(s4.z) && range_ok(s4.w);
+                    if (NP > 2) {  // at most two non-zero terms per output
+                        int mx = 0;
+                        auto nzc = [&](int c) {
+                            int z = 0;
+#pragma unroll
+                            for (int q = 0; q < NP; q++) {
+                                const float v = c == 0 ? t4[q].x : c == 1 ? t4[q].y : c == 2 ? t4[q].z : t4[q].w;
+                                z += (__float_as_uint(v) << 1) != 0u;
+                            }
+                            return z;
+                        };
+                        mx = max(max(nzc(0), nzc(1)), max(nzc(2), nzc(3)));
+                        ok = ok && mx <= 2;
+                    }
+                }
+                if (ok) {
+                    o = NP == 1 ? s4 : make_float4(s4.x * invf, s4.y * invf, s4.z * invf, s4.w * invf);
+                } else {
+                    float tx[NP], ty[NP], tz[NP], tw[NP];
+#pragma unroll
+                    for (int q = 0; q < NP; q++) {
+                        tx[q] = t4[q].x;
+                        ty[q] = t4[q].y;
+                        tz[q] = t4[q].z;
+                        tw[q] = t4[q].w;
+                    }
+                    o = make_float4(combine(tx), combine(ty), combine(tz), combine(tw));
+                }
+            }
+            st_stream(reinterpret_cast<float4 *>(out + lo) + i, o);
+        }
+    } else {
+        for (uint32_t i = threadIdx.x; i < width; i += AGG_THREADS) {
+            float t[NP];
+#pragma unroll
+            for (int q = 0; q < NP; q++)
+                t[q] = q < nparts ? tiles[q * AGG_TILE + i] : 0.0f;
+            out[lo + i] = combine(t);
+        }
+    }
+}
+
 size_t aggregate_workspace_bytes(int nparts, uint64_t n)
 {
     uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
     return (size_t)(nparts < 1 ? 1 : nparts) * (ntiles + 1) * sizeof(uint32_t);
 }
 
-static int tile_merge_run(bool avg, const uint32_t *idx, const float *vals, const AggParts &P, int nparts,
-                          uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *ext_bounds,
-                          uint64_t ext_stride, cudaStream_t s)
+// Parts without tile bounds get them from k_tile_bounds into ws first.
+static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes,
+                          const uint32_t *flags, uint32_t epoch, cudaStream_t s)
 {
     const uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
     ProfScope pa(PROF_AGGREGATE, s);
-    const uint32_t *bd = ext_bounds;
-    uint64_t bstride = ext_stride;
-    if (!bd) {
+    if (!P.bounds[0]) {
         if (ws_bytes < aggregate_workspace_bytes(nparts, n))
             return set_error(GVC_ERR_WORKSPACE, "aggregate workspace too small: %zu < %zu", ws_bytes,
                              aggregate_workspace_bytes(nparts, n));
@@ -453,17 +728,37 @@ static int tile_merge_run(bool avg, const uint32_t *idx, const float *vals, cons
             maxcnt = P.cnt[p] + 1 > maxcnt ? P.cnt[p] + 1 : maxcnt;
         dim3 bg((unsigned)grid_for(maxcnt, 256, 1024), (unsigned)nparts);
         count_launches(1);
-        k_tile_bounds<<<bg, 256, 0, s>>>(idx, P, nparts, ntiles, (uint32_t *)ws);
-        bd = (const uint32_t *)ws;
-        bstride = ntiles + 1;
+        k_tile_bounds<<<bg, 256, 0, s>>>(P, nparts, ntiles, (uint32_t *)ws);
+        for (int p = 0; p < nparts; p++)
+            P.bounds[p] = (const uint32_t *)ws + (uint64_t)p * (ntiles + 1);
     }
     count_launches(1);
-    if (!avg)
-        k_tile_merge<0><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, bstride, out);
-    else if (nparts == 1)
-        k_tile_merge<1><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, bstride, out);
-    else
-        k_tile_merge<2><<<(unsigned)ntiles, AGG_THREADS, 0, s>>>(idx, vals, P, nparts, n, ntiles, bd, bstride, out);
+    const unsigned g = (unsigned)ntiles;
+    const size_t sm1 = AGG_TILE * 4, sm2 = 2 * sm1, sm4 = 4 * sm1;
+    static bool attr = false;
+    if (!attr) {
+        attr = true;
+        cudaFuncSetAttribute(k_tile_part<1, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+        cudaFuncSetAttribute(k_tile_part<1, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+    }
+    if (flags) {
+        if (nparts <= 2)
+            k_tile_part<1, true, 2><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch);
+        else if (nparts <= 4)
+            k_tile_part<1, true, 4><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch);
+        else
+            k_tile_merge<2, true, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch);
+    } else if (!avg) {
+        k_tile_part<0, false, 1><<<g, AGG_THREADS, sm1, s>>>(P, nparts, n, out, nullptr, 0);
+    } else if (nparts == 1) {
+        k_tile_part<1, false, 1><<<g, AGG_THREADS, sm1, s>>>(P, nparts, n, out, nullptr, 0);
+    } else if (nparts == 2) {
+        k_tile_part<1, false, 2><<<g, AGG_THREADS, sm2, s>>>(P, nparts, n, out, nullptr, 0);
+    } else if (nparts <= 4) {
+        k_tile_part<1, false, 4><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, nullptr, 0);
+    } else {
+        k_tile_merge<2, false, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0);
+    }
     return GVC_OK;
 }
 
@@ -475,19 +770,84 @@ int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, 
         return set_error(GVC_ERR_ARG, "aggregate: nparts %d outside [1, %d]", nparts, AGG_MAX_PARTS);
     AggParts P;
     for (int p = 0; p < nparts; p++) {
-        P.off[p] = offs[p];
+        P.idx[p] = idx + offs[p];
+        P.vals[p] = vals + offs[p];
+        P.bounds[p] = bounds ? bounds + (uint64_t)p * bounds_stride : nullptr;
         P.cnt[p] = counts[p];
     }
-    return tile_merge_run(true, idx, vals, P, nparts, n, out, ws, ws_bytes, bounds, bounds_stride, s);
+    return tile_merge_run(true, P, nparts, n, out, ws, ws_bytes, nullptr, 0, s);
 }
 
 int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t n, float *out, void *ws,
                    size_t ws_bytes, cudaStream_t s)
 {
     AggParts P;
-    P.off[0] = 0;
+    P.idx[0] = idx;
+    P.vals[0] = vals;
+    P.bounds[0] = nullptr;
     P.cnt[0] = k;
-    return tile_merge_run(false, idx, vals, P, 1, n, out, ws, ws_bytes, nullptr, 0, s);
+    return tile_merge_run(false, P, 1, n, out, ws, ws_bytes, nullptr, 0, s);
+}
+
+// ------------------------------------------------ peer-memory exchange (C1+K7)
+// Rank `rank` posts `epoch` into slot [rank] of every rank's flag array (its
+// own included) once its payload is complete.  The payload was written by
+// earlier kernels of this stream, so it sits in this GPU's L2 -- the point
+// of coherence for the peers' NVLink reads -- and the system-scope fence +
+// release store order the flag after it.
+__global__ void k_peer_signal(PeerFlags f, int nranks, int rank, uint32_t epoch)
+{
+    const int q = threadIdx.x;
+    if (q < nranks) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.flags[q] + rank), "r"(epoch) : "memory");
+    }
+}
+
+int peer_signal_run(uint32_t *const *peer_flags, int nranks, int rank, uint32_t epoch, cudaStream_t s)
+{
+    if (nranks < 1 || nranks > GVC_MAX_PEERS || rank < 0 || rank >= nranks)
+        return set_error(GVC_ERR_ARG, "peer_signal: rank %d of %d (at most %d ranks)", rank, nranks, GVC_MAX_PEERS);
+    PeerFlags f;
+    for (int q = 0; q < nranks; q++) {
+        if (!peer_flags[q])
+            return set_error(GVC_ERR_ARG, "peer_signal: null flag pointer of rank %d", q);
+        f.flags[q] = peer_flags[q];
+    }
+    count_launches(1);
+    k_peer_signal<<<1, 32, 0, s>>>(f, nranks, rank, epoch);
+    return GVC_OK;
+}
+
+int aggregate_peers_run(const uint32_t *const *idx, const float *const *vals, const uint32_t *const *bounds,
+                        const uint64_t *counts, int nparts, uint64_t n, const uint32_t *flags, uint32_t epoch,
+                        float *out, cudaStream_t s)
+{
+    if (nparts < 1 || nparts > GVC_MAX_PEERS)
+        return set_error(GVC_ERR_ARG, "aggregate_peers: nparts %d outside [1, %d]", nparts, GVC_MAX_PEERS);
+    if (!flags)
+        return set_error(GVC_ERR_ARG, "aggregate_peers: null flags");
+    AggParts P;
+    for (int p = 0; p < nparts; p++) {
+        if (!idx[p] || !vals[p] || !bounds[p])
+            return set_error(GVC_ERR_ARG, "aggregate_peers: part %d has a null pointer", p);
+        P.idx[p] = idx[p];
+        P.vals[p] = vals[p];
+        P.bounds[p] = bounds[p];
+        P.cnt[p] = counts[p];
+    }
+    return tile_merge_run(true, P, nparts, n, out, nullptr, 0, flags, epoch, s);
+}
+
+int tile_bounds_run(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, cudaStream_t s)
+{
+    AggParts P;
+    P.idx[0] = idx;
+    P.cnt[0] = k;
+    const uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
+    count_launches(1);
+    k_tile_bounds<<<dim3((unsigned)grid_for(k + 1, 256, 1024), 1), 256, 0, s>>>(P, 1, ntiles, bounds);
+    return GVC_OK;
 }
 
 // --------------------------------------------------------- dense average

@@ -26,9 +26,9 @@ bool prof_enabled();
 size_t select_workspace_bytes(int kind, uint64_t n);
 int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
                cudaStream_t s);
-int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx,
-             float *out_val, float *resid, uint32_t *sent_mask, float *sent_m, uint32_t *tile_bounds,
-             double *stats, cudaStream_t s);
+int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
+             float *resid, uint32_t *smask, float *sm_out, uint32_t *tile_b, double *stats,
+             const gvc_emit_mirrors *mirrors, cudaStream_t s);
 int mark_sent_run(const uint32_t *idx, uint64_t k, uint32_t *mask, cudaStream_t s);
 int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m, cudaStream_t s);
 
@@ -40,6 +40,11 @@ int update_residual_run(const float *ef, const uint32_t *idx, const float *vals,
 int decompress_run(const uint32_t *idx, const float *vals, uint64_t k, uint64_t n, float *out, void *ws,
                    size_t ws_bytes, cudaStream_t s);
 size_t aggregate_workspace_bytes(int nparts, uint64_t n);
+int peer_signal_run(uint32_t *const *peer_flags, int nranks, int rank, uint32_t epoch, cudaStream_t s);
+int aggregate_peers_run(const uint32_t *const *idx, const float *const *vals, const uint32_t *const *bounds,
+                        const uint64_t *counts, int nparts, uint64_t n, const uint32_t *flags, uint32_t epoch,
+                        float *out, cudaStream_t s);
+int tile_bounds_run(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, cudaStream_t s);
 int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
                   int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *bounds,
                   uint64_t bounds_stride, cudaStream_t s);

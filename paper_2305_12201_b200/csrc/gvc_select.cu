@@ -1159,10 +1159,21 @@ __global__ void __launch_bounds__(1024) k_finish(const Plan p, int)
 // 512-aligned), so each warp builds them in shared memory and writes every
 // word of its segment once, coalesced.  Second-level emits (idx_map) map to
 // arbitrary words and OR into global memory.
+// Mirrors (push exchange): every output store is repeated into the peers'
+// receive slots (ordinary stores to peer-mapped memory over NVLink), and each
+// thread ends with a system-scope fence so the payload is complete at every
+// peer before the signal that follows this kernel.
+struct Mirrors {
+    int n;
+    uint32_t *idx[GVC_MAX_PEERS];
+    float *val[GVC_MAX_PEERS];
+    uint32_t *tb[GVC_MAX_PEERS];
+};
+
 template <int KM, bool SMEM_MASK>
 __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
                                                       float *out_val, float *resid, uint32_t *smask, float *sm_out,
-                                                      uint32_t *tile_b)
+                                                      uint32_t *tile_b, Mirrors mir)
 {
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
     extern __shared__ uint32_t mwords[];  // [8][seg_len / 32] when SMEM_MASK
@@ -1252,8 +1263,11 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                     if (sel) {
                         const uint32_t t_lo = prior ? gprev / GVC_AGG_TILE + 1 : t_next;
                         const uint32_t t_hi = pos[c] / GVC_AGG_TILE;
-                        for (uint32_t t = t_lo; t <= t_hi; t++)
+                        for (uint32_t t = t_lo; t <= t_hi; t++) {
                             tile_b[t] = out + __popc(sb & lt);
+                            for (int q = 0; q < mir.n; q++)
+                                mir.tb[q][t] = out + __popc(sb & lt);
+                        }
                     }
                     if (sb)
                         t_next = __shfl_sync(0xffffffffu, pos[c], 31 - __clz(sb)) / GVC_AGG_TILE + 1;
@@ -1268,6 +1282,10 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                     const uint32_t gi = idx_map ? idx_map[pos[c]] : pos[c];
                     out_idx[w] = gi;
                     out_val[w] = sv;
+                    for (int q = 0; q < mir.n; q++) {
+                        mir.idx[q][w] = gi;
+                        mir.val[q][w] = sv;
+                    }
                     if (SMEM_MASK)
                         atomicOr(&mw[(pos[c] - (uint32_t)beg) >> 5], 1u << (pos[c] & 31));
                     else if (smask)
@@ -1291,10 +1309,15 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
             const uint64_t end = min(p.n, beg + p.seg_len);
             const uint64_t ntiles = (p.n + GVC_AGG_TILE - 1) / GVC_AGG_TILE;
             const uint64_t t_end = end == p.n ? ntiles : (end - 1) / GVC_AGG_TILE;
-            for (uint64_t t = t_next + lane; t <= t_end; t += 32)
+            for (uint64_t t = t_next + lane; t <= t_end; t += 32) {
                 tile_b[t] = out;
+                for (int q = 0; q < mir.n; q++)
+                    mir.tb[q][t] = out;
+            }
         }
     }
+    if (mir.n)
+        __threadfence_system();
     if (SMEM_MASK && seg < p.S) {
         __syncwarp();
         const uint64_t beg = (uint64_t)seg * p.seg_len;
@@ -1598,8 +1621,19 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
 }
 
 int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
-             float *resid, uint32_t *smask, float *sm_out, uint32_t *tile_b, double *stats, cudaStream_t s)
+             float *resid, uint32_t *smask, float *sm_out, uint32_t *tile_b, double *stats,
+             const gvc_emit_mirrors *mirrors, cudaStream_t s)
 {
+    Mirrors mir;
+    memset(&mir, 0, sizeof(mir));
+    if (mirrors) {
+        mir.n = mirrors->count;
+        for (int q = 0; q < mir.n; q++) {
+            mir.idx[q] = mirrors->idx_dev[q];
+            mir.val[q] = mirrors->vals_dev[q];
+            mir.tb[q] = mirrors->bounds_dev[q];
+        }
+    }
     (void)ws_bytes;
     Plan p;
     {
@@ -1625,17 +1659,17 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         }
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                       sm_out, tile_b);
+                                                                       sm_out, tile_b, mir);
         else
             k_emit<KEY_HASH, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
-                                                                        smask, sm_out, tile_b);
+                                                                        smask, sm_out, tile_b, mir);
     } else {
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                   sm_out, tile_b);
+                                                                   sm_out, tile_b, mir);
         else
             k_emit<KEY_HASH, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                    sm_out, tile_b);
+                                                                    sm_out, tile_b, mir);
     }
     if (stats)
         k_emit_finish<<<1, 1024, 0, s>>>(p, stats);

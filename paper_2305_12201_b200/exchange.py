@@ -17,6 +17,8 @@ host-side packing logic.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -53,17 +55,30 @@ class Payload:
     gathered parts; every rank uses the same layout (same kind, same k, n).
     """
 
-    __slots__ = ("buf", "k", "kpad", "nb", "bpad", "idx", "vals", "bounds")
+    __slots__ = ("buf", "k", "kpad", "nb", "bpad", "idx", "vals", "bounds", "bounds_area", "peer", "mirrors",
+                 "pushed")
 
-    def __init__(self, k: int, n: int, device, with_bounds: bool = True):
+    def __init__(self, k: int, n: int, device, with_bounds: bool = True, buf: torch.Tensor | None = None):
         self.k = k
         self.kpad = (k + 3) & ~3
-        self.nb = (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1 if with_bounds else 0
+        self.nb = (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1 if (with_bounds or buf is not None) else 0
         self.bpad = (self.nb + 3) & ~3
-        self.buf = torch.empty(2 * self.kpad + self.bpad, dtype=torch.int32, device=device)
+        if buf is None:
+            buf = torch.empty(2 * self.kpad + self.bpad, dtype=torch.int32, device=device)
+        self.buf = buf
         self.idx = self.buf[:self.kpad].view(torch.uint32)
         self.vals = self.buf[self.kpad:2 * self.kpad].view(torch.float32)
-        self.bounds = self.buf[2 * self.kpad:2 * self.kpad + self.nb].view(torch.uint32) if with_bounds else None
+        self.bounds_area = self.buf[2 * self.kpad:2 * self.kpad + self.nb].view(torch.uint32) if self.nb else None
+        # bounds: set when the emit writes them (level-1 Top-k emits do)
+        self.bounds = self.bounds_area if with_bounds else None
+        self.peer = None
+        self.mirrors = None  # nat.EmitMirrors: the peers' receive slots (push exchange)
+        self.pushed = False  # set by the emit once the mirrors hold the full payload
+
+    @staticmethod
+    def words_for(k: int, n: int) -> int:
+        nb = (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1
+        return 2 * ((k + 3) & ~3) + ((nb + 3) & ~3)
 
     @property
     def words(self) -> int:
@@ -114,6 +129,136 @@ def allgather_aggregate(part: SparseGradient, group=None, out: torch.Tensor | No
                            part.original_length, out=out, offs=[r * L for r in range(world)],
                            bounds=bounds, bounds_stride=L)
     return GradientVector._wrap(res)
+
+
+class PeerExchange:
+    """C1 + K7 fused over NVLink peer memory (one node, NCCL process group).
+
+    Every rank owns one symmetric (peer-mapped) buffer:
+        [flags: 64 u32 | parity 0: slot[0..W-1] | parity 1: slot[0..W-1]]
+    Exchange number e uses parity e % 2; slot[r] holds rank r's payload
+    (idx | vals | tile bounds, exchange.Payload layout).
+
+    Push (Top-k level-1 emits, the hot path): the emit writes rank r's payload
+    into slot[r] of its OWN buffer and, through gvc_emit_mirrored, into
+    slot[r] of every peer's buffer while it runs (ordinary stores over
+    NVLink, then a system fence).  gvc_peer_signal posts e into every rank's
+    flags[r]; gvc_aggregate_peers waits for flags[p] >= e and merges the W
+    slots of its own buffer -- local HBM reads only.
+    Pull (any other payload): only the own slot is written; the merge reads
+    slot[p] of rank p's buffer over NVLink.
+
+    Reuse of parity e % 2 by exchange e + 2 needs no second barrier: a rank
+    starts exchange e + 2 only after its merge of e + 1 saw every flag e + 1,
+    and each rank posts e + 1 after its merge of e completed (same stream).
+    All ranks run the same sequence of exchanges because they take identical
+    decisions (C2).
+    """
+
+    FLAG_WORDS = 64
+    _cache: dict = {}
+
+    def __init__(self, group, device):
+        self.group, self.device = group, device
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > nat.MAX_PEERS:
+            raise ValueError(f"peer exchange supports at most {nat.MAX_PEERS} ranks on one node")
+        self.cap = 0
+        self.epoch = 0
+        self.buf = None
+        self.handle = None
+
+    @classmethod
+    def get(cls, group, device) -> "PeerExchange":
+        key = (id(group), device.index)
+        px = cls._cache.get(key)
+        if px is None:
+            px = cls(group, device)
+            cls._cache[key] = px
+        return px
+
+    def _slot_word(self, parity: int, src: int) -> int:
+        return self.FLAG_WORDS + (parity * self.world + src) * self.cap
+
+    def _ensure(self, words: int) -> None:
+        if words <= self.cap:
+            return
+        import torch.distributed._symmetric_memory as symm
+        cap = (words + 1023) & ~1023
+        buf = symm.empty(self.FLAG_WORDS + 2 * self.world * cap, dtype=torch.int32, device=self.device)
+        buf[:self.FLAG_WORDS].zero_()
+        handle = symm.rendezvous(buf, self.group)  # collective: every rank grows together
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)  # every flag array is zero before anyone signals
+        self.buf, self.handle, self.cap, self.epoch = buf, handle, cap, 0
+        self.bases = [int(p) for p in handle.buffer_ptrs]
+        self._flag_ptrs = (ctypes.c_void_p * self.world)(*self.bases)
+
+    def slot(self, k: int, n: int, push: bool = True) -> Payload:
+        """This rank's payload slot of the next exchange.  With ``push`` (a
+        level-1 Top-k emit, which writes the tile bounds) the emit also writes
+        the same slot of every peer; otherwise the bounds are computed at the
+        exchange and the peers pull."""
+        words = Payload.words_for(k, n)
+        self._ensure(words)
+        e = self.epoch + 1
+        base = self._slot_word(e % 2, self.rank)
+        pl = Payload(k, n, self.device, with_bounds=push, buf=self.buf[base:base + words])
+        pl.peer = (self, e, base)
+        if push and self.world > 1:
+            m = nat.EmitMirrors()
+            m.count = self.world - 1
+            for i, q in enumerate(r for r in range(self.world) if r != self.rank):
+                b = self.bases[q] + 4 * base
+                m.idx_dev[i] = b
+                m.vals_dev[i] = b + 4 * pl.kpad
+                m.bounds_dev[i] = b + 8 * pl.kpad
+            pl.mirrors = m
+        return pl
+
+    def aggregate(self, part: SparseGradient, out: torch.Tensor | None = None) -> torch.Tensor:
+        """The rank-ordered fp64 mean of every rank's part (aggregate() semantics)."""
+        n = part.original_length
+        pl = getattr(part, "_payload", None)
+        if pl is None or pl.peer is None or pl.peer[0] is not self or pl.peer[1] != self.epoch + 1 \
+                or pl.vals.data_ptr() != part.vals.data_ptr():
+            pl = self.slot(part.kept, n, push=False)
+            pl.idx[:part.kept].copy_(part.indices)
+            pl.vals[:part.kept].copy_(part.vals)
+            pl.bounds = None
+        _, e, _ = pl.peer
+        lib = nat.load()
+        stream = nat.stream_ptr(self.device)
+        pushed = pl.pushed
+        if not pushed and pl.bounds is None:  # the emit did not write them (level-2 / non-Top-k views)
+            nat.check(lib.gvc_tile_bounds(nat.ptr(pl.idx), part.kept, n, nat.ptr(pl.bounds_area), stream),
+                      "tile_bounds")
+        self.epoch = e
+        nat.check(lib.gvc_peer_signal(self._flag_ptrs, self.world, self.rank, e, stream), "peer_signal")
+        W = self.world
+        own = self.bases[self.rank]
+        # push: every slot is in this rank's buffer; pull: slot p lives in rank p's buffer
+        bases = [own + 4 * self._slot_word(e % 2, p) if pushed else self.bases[p] + 4 * self._slot_word(e % 2, p)
+                 for p in range(W)]
+        idx = (ctypes.c_void_p * W)(*bases)
+        vals = (ctypes.c_void_p * W)(*[b + 4 * pl.kpad for b in bases])
+        bnd = (ctypes.c_void_p * W)(*[b + 8 * pl.kpad for b in bases])
+        counts = (ctypes.c_uint64 * W)(*([part.kept] * W))
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self.device)
+        nat.check(lib.gvc_aggregate_peers(idx, vals, bnd, counts, W, n, nat.ptr(self.buf), e, nat.ptr(out),
+                                          stream), "aggregate_peers")
+        return out
+
+
+def use_peer_exchange(group) -> bool:
+    """The fused NVLink exchange runs for NCCL groups of at most 8 ranks
+    (GVC_EXCHANGE=nccl selects the all-gather + K7 path instead)."""
+    import os
+    return (group is not None and dist.get_backend(group) == "nccl"
+            and os.environ.get("GVC_EXCHANGE", "peer") == "peer"
+            and dist.get_world_size(group) <= nat.MAX_PEERS)
 
 
 def allgather_dense_mean(g: GradientVector, group=None) -> GradientVector:

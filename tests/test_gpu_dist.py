@@ -1,7 +1,7 @@
 """Multi-GPU path (one process per GPU, NCCL): the C2 gain exchange gives every
-rank the reference's worker-ordered decision, and C1 + K7 (all-gather of the
-(idx, val) payload + fp64 rank-ordered average) equals aggregate() over the
-same parts, bit for bit.  Skipped with fewer than 2 GPUs."""
+rank the reference's worker-ordered decision, and C1 + K7 -- fused over NVLink
+peer memory (default) or all-gather + K7 (GVC_EXCHANGE=nccl) -- equals
+aggregate() over the same parts, bit for bit.  Skipped with fewer than 2 GPUs."""
 import os
 import socket
 
@@ -12,7 +12,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, kind, q):
+def _worker(rank, world, port, kind, q, exchange="peer"):
+    os.environ["GVC_EXCHANGE"] = exchange
     import torch.distributed as dist
     import paper_2305_12201_b200 as G
     from paper_2305_12201_b200.exchange import allgather_aggregate, allgather_payload
@@ -45,22 +46,82 @@ def _worker(rank, world, port, kind, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["topk", "dgc"])
-def test_two_rank_step(kind):
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+def _spawn(target, world, *args):
     import torch.multiprocessing as mp
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
-    assert res[0] == res[1]  # identical decisions and gains on both ranks
-    assert all(r[4] for r in res[0])  # fused exchange == aggregate() bit for bit
+    return res
+
+
+def _world():
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    return min(n, 4)
+
+
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+@pytest.mark.parametrize("kind", ["topk", "dgc", "redsync"])
+def test_multi_rank_step(kind, exchange):
+    world = _world()
+    res = _spawn(_step_worker, world, kind, exchange)
+    for r in range(1, world):
+        assert res[r] == res[0]  # identical decisions and gains on every rank
+    assert all(r[4] for r in res[0])  # exchange == aggregate() bit for bit
+
+
+def _step_worker(rank, world, port, kind, exchange, q):
+    _worker(rank, world, port, kind, q, exchange)
+
+
+def _peer_worker(rank, world, port, q):
+    """Many exchanges through the two peer slots (growing k re-allocates the
+    symmetric buffer), each against the fp64 rank-ordered oracle mean."""
+    import torch.distributed as dist
+    from oracle import oracle as O
+    import paper_2305_12201_b200 as G
+    from paper_2305_12201_b200.exchange import PeerExchange
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=dev)
+    px = PeerExchange.get(dist.group.WORLD, dev)
+    ok = []
+    n = 300_007
+    for e, k in enumerate([1, 5000, 5000, 30_001, 30_001, 30_001, 4096, 120_000, 7]):
+        parts = []
+        for r in range(world):
+            rs = np.random.default_rng(1000 * e + r)
+            idx = np.sort(rs.choice(n, k, replace=False)).astype(np.uint32)
+            vals = (rs.standard_normal(k) * (1 + r)).astype(np.float32)
+            if e == 3:
+                vals[::7] = -0.0
+            parts.append((idx, vals))
+        pl = px.slot(k, n, push=False)
+        pl.idx[:k].copy_(torch.from_numpy(parts[rank][0].view(np.int32)).to(dev).view(torch.uint32))
+        pl.vals[:k].copy_(torch.from_numpy(parts[rank][1]).to(dev))
+        pl.bounds = None  # not written by an emit: the exchange computes them
+        part = G.SparseGradient._wrap(pl.idx[:k], pl.vals[:k], n, n / k)
+        part._payload = pl
+        out = px.aggregate(part).cpu().numpy()
+        ref = O.aggregate(parts, n)
+        ok.append(bool(np.array_equal(out.view(np.int32), ref.view(np.int32))))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_peer_exchange_epochs():
+    world = _world()
+    res = _spawn(_peer_worker, world)
+    for r in range(world):
+        assert all(res[r]), res[r]

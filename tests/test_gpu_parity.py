@@ -457,3 +457,39 @@ def test_emit_tile_bounds(G, n, k):
     a = aggregate_packed(idx, vals, [k], n)
     b = aggregate_packed(idx, vals, [k], n, bounds=tb)
     assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 4, 5, 8])
+def test_aggregate_adversarial(G, nparts):
+    """K7 fast paths vs the fp64 oracle on values built to break them: exact
+    cancellation, exponent gaps > 29, sums that overflow fp32 but not fp64,
+    subnormal sums, -0.0, +-inf, and 3+ parts at one position."""
+    rs = np.random.default_rng(77 + nparts)
+    n = 3 * 4096 + 123
+    specials = np.array([0.0, -0.0, 3.0e38, -3.0e38, 1e-40, -1e-40, 1.5e-45, 2.0 ** -126, np.inf, -np.inf,
+                         1.0, 1.0 + 2.0 ** -23, 2.0 ** -30, -1.0, 6.0e37], dtype=np.float32)
+    parts = []
+    for p in range(nparts):
+        k = int(rs.integers(n // 4, n // 2))
+        idx = np.sort(rs.choice(n, k, replace=False)).astype(np.uint32)
+        vals = rs.standard_normal(k).astype(np.float32)
+        pick = rs.random(k) < 0.5
+        vals[pick] = specials[rs.integers(0, len(specials), pick.sum())]
+        parts.append((idx, vals))
+    # a block of positions every part hits: the same special pattern in every
+    # part (3e38 + 3e38 overflows fp32 only, 1 + -1 cancels, ...)
+    common = np.arange(100, 100 + len(specials), dtype=np.uint32)
+    full = []
+    for p, (i, v) in enumerate(parts):
+        keep = ~np.isin(i, common)
+        i2 = np.concatenate([i[keep], common])
+        v2 = np.concatenate([v[keep], np.roll(specials, p % 2)])
+        o = np.argsort(i2, kind="stable")
+        full.append((i2[o].astype(np.uint32), v2[o].astype(np.float32)))
+    parts = full
+    ref = O.aggregate(parts, n)
+    sg = [G.SparseGradient(i, v, n, 1.0) for i, v in parts]
+    out = host(G.aggregate(sg).values)
+    fin = np.isfinite(ref) | np.isinf(ref)
+    assert np.array_equal(bits(out)[fin], bits(ref)[fin])
+    assert np.array_equal(np.isnan(out), np.isnan(ref))
