@@ -238,6 +238,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     # warm-up mirrors the timed loop exactly (the previous step's outputs stay
     # alive while the next one runs), so the caching allocator is warm
     clocks = ClockSampler(local).__enter__()  # started early: its start-up stays out of the timed region
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region (re-enabled right after)
     res = None
     for w in range(args.warmup):
         g = fresh()
@@ -248,9 +251,6 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         dist.barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    import gc
-    gc.collect()
-    gc.disable()  # no collector pauses inside the timed region (re-enabled right after)
     chosen.clear()
     from paper_2305_12201_b200.controller import STATS
     torch.cuda.synchronize()

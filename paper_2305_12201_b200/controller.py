@@ -488,8 +488,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     dev = grads[0].values.device
     peer = None
     if group is not None:
-        from .exchange import PeerExchange, use_peer_exchange
-        if use_peer_exchange(group):
+        from .exchange import PeerExchange, exchange_mode
+        xmode = exchange_mode(group)
+        if xmode != "nccl":
             peer = PeerExchange.get(group, dev)
 
     # ---- one device->host read per iteration: every worker's norms and
@@ -527,7 +528,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
 
     def wire(s, c, bnd):
         if peer is not None:
-            return peer.slot(s.chosen_count(c), length, push=bnd)
+            return peer.slot(s.chosen_count(c), length, push=bnd and xmode == "push")
         from .exchange import new_payload
         return new_payload(s.chosen_count(c), dev, n=length if bnd else None)
 

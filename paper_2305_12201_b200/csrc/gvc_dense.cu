@@ -734,18 +734,14 @@ static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *
     }
     count_launches(1);
     const unsigned g = (unsigned)ntiles;
-    const size_t sm1 = AGG_TILE * 4, sm2 = 2 * sm1, sm4 = 4 * sm1;
-    static bool attr = false;
-    if (!attr) {
-        attr = true;
-        cudaFuncSetAttribute(k_tile_part<1, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-        cudaFuncSetAttribute(k_tile_part<1, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-    }
+    const size_t sm1 = AGG_TILE * 4, sm2 = 2 * sm1;
+    // measured (scripts/merge_bench.py): per-part fp32 tiles win for 1-2 parts,
+    // the single fp64 tile (less shared memory, higher occupancy) above
     if (flags) {
         if (nparts <= 2)
             k_tile_part<1, true, 2><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch);
         else if (nparts <= 4)
-            k_tile_part<1, true, 4><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch);
+            k_tile_merge<2, true, 4><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch);
         else
             k_tile_merge<2, true, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch);
     } else if (!avg) {
@@ -755,7 +751,7 @@ static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *
     } else if (nparts == 2) {
         k_tile_part<1, false, 2><<<g, AGG_THREADS, sm2, s>>>(P, nparts, n, out, nullptr, 0);
     } else if (nparts <= 4) {
-        k_tile_part<1, false, 4><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, nullptr, 0);
+        k_tile_merge<2, false, 4><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0);
     } else {
         k_tile_merge<2, false, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0);
     }

@@ -252,13 +252,21 @@ class PeerExchange:
         return out
 
 
-def use_peer_exchange(group) -> bool:
-    """The fused NVLink exchange runs for NCCL groups of at most 8 ranks
-    (GVC_EXCHANGE=nccl selects the all-gather + K7 path instead)."""
+def exchange_mode(group) -> str:
+    """"push" / "pull" (the NVLink peer-memory exchange) or "nccl" (all-gather
+    + K7).  Peer memory needs an NCCL group of at most 8 ranks on one node.
+    GVC_EXCHANGE overrides; the default pulls (measured on B200: pull 0.383 ms
+    vs push 0.389 ms per step at 2 ranks, 0.543 vs 0.638 at 4 -- every extra
+    destination slows the pushing emit)."""
     import os
-    return (group is not None and dist.get_backend(group) == "nccl"
-            and os.environ.get("GVC_EXCHANGE", "peer") == "peer"
-            and dist.get_world_size(group) <= nat.MAX_PEERS)
+    if group is None or dist.get_backend(group) != "nccl" or dist.get_world_size(group) > nat.MAX_PEERS:
+        return "nccl"
+    mode = os.environ.get("GVC_EXCHANGE", "auto")
+    if mode == "auto":
+        mode = "pull"
+    if mode not in ("push", "pull", "nccl"):
+        raise ValueError(f"GVC_EXCHANGE={mode!r}: expected push, pull, nccl or auto")
+    return mode
 
 
 def allgather_dense_mean(g: GradientVector, group=None) -> GradientVector:

@@ -1,6 +1,6 @@
 """Multi-GPU path (one process per GPU, NCCL): the C2 gain exchange gives every
 rank the reference's worker-ordered decision, and C1 + K7 -- fused over NVLink
-peer memory (default) or all-gather + K7 (GVC_EXCHANGE=nccl) -- equals
+peer memory (GVC_EXCHANGE=push / pull) or all-gather + K7 (nccl) -- equals
 aggregate() over the same parts, bit for bit.  Skipped with fewer than 2 GPUs."""
 import os
 import socket
@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, kind, q, exchange="peer"):
+def _worker(rank, world, port, kind, q, exchange="auto"):
     os.environ["GVC_EXCHANGE"] = exchange
     import torch.distributed as dist
     import paper_2305_12201_b200 as G
@@ -70,7 +70,7 @@ def _world():
     return min(n, 4)
 
 
-@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+@pytest.mark.parametrize("exchange", ["push", "pull", "nccl"])
 @pytest.mark.parametrize("kind", ["topk", "dgc", "redsync"])
 def test_multi_rank_step(kind, exchange):
     world = _world()
