@@ -28,6 +28,7 @@
 //                                 output offsets for EVERY ladder entry
 //   k_emit (gvc_emit)             ordered (idx, val) compaction of one entry,
 //                                 fused residual update
+#include <algorithm>
 #include <mutex>
 #include <stdio.h>
 #include <string>
@@ -639,41 +640,77 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         acc_c[b][threadIdx.x] = 0u;
     }
     uint32_t nan_any = 0;
+    // fast window (hi_0 - 1, lo_1): band 1, in no interval (empty when the
+    // first two intervals touch)
+    const uint32_t f_lo = him1[0];
+    const uint32_t f_hi = nks >= 2 ? lo[1] : 0xffffffffu;
+    double e_b1 = 0.0, a_b1 = 0.0;
+    uint32_t c_b1 = 0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
         const uint32_t cnt = p.seg_cnt[seg];
         uint32_t *mem = p.mem_idx + beg;
         const uint32_t lt = lanemask_lt();
         uint32_t mcount = 0;
+        // register double buffer: the next 128 candidates are in flight while
+        // this group is classified (a warp walks ~8 groups back to back)
+        float4 nfv = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint4 niv = make_uint4(0u, 0u, 0u, 0u);
+        if (cnt) {
+            nfv = *reinterpret_cast<const float4 *>(p.cand_val + beg + lane * 4);
+            if (KM == KEY_HASH)
+                niv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + lane * 4);
+        }
         for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
             const uint32_t t = base + lane * 4;
-            float v[4];
-            uint32_t pos[4], key[4];
+            const float4 fv = nfv;
+            const uint4 iv = niv;
+            if (base + 128 < cnt) {
+                nfv = *reinterpret_cast<const float4 *>(p.cand_val + beg + t + 128);
+                if (KM == KEY_HASH)
+                    niv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t + 128);
+            }
+            float v[4] = {fv.x, fv.y, fv.z, fv.w};
+            uint32_t pos[4] = {iv.x, iv.y, iv.z, iv.w}, key[4];
             bool ok[4];
-            load_cand4<KM>(p, beg, t, cnt, v, pos, key, ok, false);
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                ok[c] = t + c < cnt;
+                key[c] = ok[c] ? cand_key<KM>(p, v[c], pos[c]) : 0u;
+            }
             bool memb[4];
             uint32_t mb[4];
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                int band = 0;
-                bool in = false;
-#pragma unroll
-                for (int j = 0; j < NB; j++) {
-                    const uint32_t d = key[c] - lo[j];
-                    const bool inj = j < nks && d <= wm1[j];
-                    in |= inj;
-                    band += key[c] > him1[j];
-                    if (ok[c] && inj && act[j])
-                        atomicAdd(&p.histl[j * GVC_HL_BINS + (d >> sh[j])], 1u);
-                }
-                memb[c] = ok[c] && in;
                 if (KM == KEY_MAG)
                     nan_any |= (uint32_t)(ok[c] && key[c] > 0x7f800000u);
-                if (ok[c] && !in) {
-                    acc_e[band][threadIdx.x] += (double)v[c] * (double)v[c];
+                memb[c] = false;
+                if (ok[c] && key[c] > f_lo && key[c] < f_hi) {
+                    // the common case: above threshold 0, below interval 1 ->
+                    // band 1, not a member; accumulated in registers
+                    e_b1 += (double)v[c] * (double)v[c];
                     if (ABS)
-                        acc_a[band][threadIdx.x] += fabs((double)v[c]);
-                    acc_c[band][threadIdx.x] += 1u;
+                        a_b1 += fabs((double)v[c]);
+                    c_b1 += 1u;
+                } else if (ok[c]) {
+                    int band = 0;
+                    bool in = false;
+#pragma unroll
+                    for (int j = 0; j < NB; j++) {
+                        const uint32_t d = key[c] - lo[j];
+                        const bool inj = j < nks && d <= wm1[j];
+                        in |= inj;
+                        band += key[c] > him1[j];
+                        if (inj && act[j])
+                            atomicAdd(&p.histl[j * GVC_HL_BINS + (d >> sh[j])], 1u);
+                    }
+                    memb[c] = in;
+                    if (!in) {
+                        acc_e[band][threadIdx.x] += (double)v[c] * (double)v[c];
+                        if (ABS)
+                            acc_a[band][threadIdx.x] += fabs((double)v[c]);
+                        acc_c[band][threadIdx.x] += 1u;
+                    }
                 }
                 mb[c] = __ballot_sync(0xffffffffu, memb[c]);
             }
@@ -689,6 +726,12 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         if (lane == 0)
             p.seg_mcnt[seg] = mcount;
     }
+    // band 1 never reaches the shared accumulator when the fast window is
+    // open, so this is the same fixed-order fp64 sum as before
+    acc_e[1][threadIdx.x] += e_b1;
+    if (ABS)
+        acc_a[1][threadIdx.x] += a_b1;
+    acc_c[1][threadIdx.x] += c_b1;
     __syncwarp();
     nan_any = __any_sync(0xffffffffu, nan_any);
     if (lane == 0 && nan_any)
@@ -893,8 +936,9 @@ __device__ __forceinline__ void block_sum_vec(double (&v)[K], double *sh /* 33*K
     }
     __syncthreads();
     if (threadIdx.x < K) {
+        const int nwarps = (int)(blockDim.x >> 5);
         double r = 0.0;
-        for (int w = 0; w < 32; w++)
+        for (int w = 0; w < nwarps; w++)
             r += sh[w * K + threadIdx.x];
         sh[32 * K + threadIdx.x] = r;
     }
@@ -928,16 +972,18 @@ __device__ __forceinline__ void block_excl_prefix_vec(unsigned long long (&v)[K]
     }
     __syncthreads();
     if (warp == 0) {
+        const int nwarps = (int)(blockDim.x >> 5);
 #pragma unroll
         for (int k = 0; k < K; k++) {
-            unsigned long long w = sh[lane * K + k], wi = w;
+            unsigned long long w = lane < nwarps ? sh[lane * K + k] : 0ull, wi = w;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
                 if (lane >= o)
                     wi += y;
             }
-            sh[lane * K + k] = wi - w;
+            if (lane < nwarps)
+                sh[lane * K + k] = wi - w;
             if (lane == 31)
                 sh[32 * K + k] = wi;
         }
@@ -1061,7 +1107,7 @@ __global__ void __launch_bounds__(1024) k_finish(const Plan p, int)
         for (uint32_t sg = pb * GVC_WARPS_PER_BLOCK; sg < s_end; sg++) {
             const uint64_t beg = (uint64_t)sg * p.seg_len;
             const uint32_t cn = p.seg_cnt[sg];
-            for (uint32_t base = 0; base < cn; base += 1024) {
+            for (uint32_t base = 0; base < cn; base += blockDim.x) {
                 const uint32_t tt = base + t;
                 bool is_tie = false;
                 float v = 0.f;
@@ -1173,7 +1219,7 @@ struct Mirrors {
 template <int KM, bool SMEM_MASK>
 __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
                                                       float *out_val, float *resid, uint32_t *smask, float *sm_out,
-                                                      uint32_t *tile_b, Mirrors mir)
+                                                      uint32_t *tile_b, Mirrors mir, int want_stats)
 {
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
     extern __shared__ uint32_t mwords[];  // [8][seg_len / 32] when SMEM_MASK
@@ -1235,6 +1281,16 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
         uint32_t t_next = (uint32_t)((beg + GVC_AGG_TILE - 1) / GVC_AGG_TILE);
         // 4 coalesced 32-wide sub-groups per trip: loads in flight together,
         // stores stay contiguous across the warp
+        // register double buffer: the next group's loads are issued before
+        // this group is classified and stored
+        float nv[4];
+        uint32_t npos[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const uint32_t t = c * 32 + lane;
+            nv[c] = t < cnt ? p.cand_val[beg + t] : 0.f;
+            npos[c] = t < cnt ? p.cand_idx[beg + t] : 0u;
+        }
         for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
             float v[4];
             uint32_t pos[4], key[4];
@@ -1243,8 +1299,11 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
             for (int c = 0; c < 4; c++) {
                 const uint32_t t = base + c * 32 + lane;
                 ok[c] = t < cnt;
-                v[c] = ok[c] ? p.cand_val[beg + t] : 0.f;
-                pos[c] = ok[c] ? p.cand_idx[beg + t] : 0u;
+                v[c] = nv[c];
+                pos[c] = npos[c];
+                const uint32_t tn = t + 128;
+                nv[c] = tn < cnt ? p.cand_val[beg + tn] : 0.f;
+                npos[c] = tn < cnt ? p.cand_idx[beg + tn] : 0u;
             }
 #pragma unroll
             for (int c = 0; c < 4; c++)
@@ -1255,7 +1314,9 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                 const uint32_t tb = __ballot_sync(0xffffffffu, tie);
                 const bool sel = ok[c] && (key[c] > T || (tie && ties_seen + __popc(tb & lt) < take));
                 const uint32_t sb = __ballot_sync(0xffffffffu, sel);
-                if (tile_b) {
+                // tiles start in this group only if its last selected position
+                // lies in a tile >= t_next (warp-uniform; ~1 group in 13 at CF 10)
+                if (tile_b && sb && __shfl_sync(0xffffffffu, pos[c], 31 - __clz(sb)) / GVC_AGG_TILE >= t_next) {
                     // tiles starting in (previous selected index, this index] begin here
                     const uint32_t prior = sb & lt;
                     const int pl = prior ? 31 - __clz(prior) : 0;
@@ -1296,8 +1357,10 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                         const float ef = idx_map ? resid[gi] : v[c];
                         resid[gi] = __fsub_rn(ef, sv);
                     }
-                    e2 += (double)sv * (double)sv;
-                    ab += fabs((double)sv);
+                    if (want_stats) {
+                        e2 += (double)sv * (double)sv;
+                        ab += fabs((double)sv);
+                    }
                 }
                 ties_seen += __popc(tb);
                 out += __popc(sb);
@@ -1325,6 +1388,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
         for (uint32_t w = lane; w < live; w += 32)
             smask[(beg >> 5) + w] = mw[w];
     }
+    if (!want_stats)
+        return;  // uniform: the sent-value statistics are not requested
     e2 = warp_sum_f64(e2);
     ab = warp_sum_f64(ab);
     if (lane == 0) {
@@ -1453,12 +1518,15 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes)
     launches += 5;
     launch_tail<KM>(p, s);
     launches += 3;
+    // k_finish: 2 blocks per thread; only as many warps as the blocks need
+    // (its block-wide reductions cost per warp)
+    const int fin_threads = (int)std::min<uint32_t>(1024u, std::max<uint32_t>(64u, ((p.B + 1) / 2 + 31) & ~31u));
     switch (nb_for(p.n_ks)) {
-    case 1: k_finish<KM, 1><<<1, 1024, 0, s>>>(p, 0); break;
-    case 2: k_finish<KM, 2><<<1, 1024, 0, s>>>(p, 0); break;
-    case 4: k_finish<KM, 4><<<1, 1024, 0, s>>>(p, 0); break;
-    case 8: k_finish<KM, 8><<<1, 1024, 0, s>>>(p, 0); break;
-    default: k_finish<KM, 16><<<1, 1024, 0, s>>>(p, 0); break;
+    case 1: k_finish<KM, 1><<<1, fin_threads, 0, s>>>(p, 0); break;
+    case 2: k_finish<KM, 2><<<1, fin_threads, 0, s>>>(p, 0); break;
+    case 4: k_finish<KM, 4><<<1, fin_threads, 0, s>>>(p, 0); break;
+    case 8: k_finish<KM, 8><<<1, fin_threads, 0, s>>>(p, 0); break;
+    default: k_finish<KM, 16><<<1, fin_threads, 0, s>>>(p, 0); break;
     }
     return launches + 2;
 }
@@ -1659,17 +1727,17 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         }
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                       sm_out, tile_b, mir);
+                                                                       sm_out, tile_b, mir, stats != nullptr);
         else
             k_emit<KEY_HASH, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
-                                                                        smask, sm_out, tile_b, mir);
+                                                                        smask, sm_out, tile_b, mir, stats != nullptr);
     } else {
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                   sm_out, tile_b, mir);
+                                                                   sm_out, tile_b, mir, stats != nullptr);
         else
             k_emit<KEY_HASH, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
-                                                                    sm_out, tile_b, mir);
+                                                                    sm_out, tile_b, mir, stats != nullptr);
     }
     if (stats)
         k_emit_finish<<<1, 1024, 0, s>>>(p, stats);
