@@ -233,9 +233,12 @@ GVC_API int gvc_tile_bounds(const uint32_t *idx_dev, uint64_t k, uint64_t n, uin
 GVC_API int gvc_aggregate_dense(const float *parts_dev, int nparts, uint64_t n, float *out_dev,
                         void *stream);
 
-/* Measurement hooks (bench.py): when enabled, CUDA events bracket the
- * collect kernel, the whole selection, the emit and the decompress-average on
- * the launching stream; gvc_prof_read synchronises on them, returns per-category
+/* Measurement hooks (bench.py).  on = 1: the selection runs as direct
+ * launches and CUDA events bracket the collect kernel, the whole selection,
+ * the emit and the decompress-average on the launching stream.  on = 2: the
+ * selection keeps running as its CUDA graph, with event-record nodes around
+ * the collect kernel only (its duration inside the timed loop itself).
+ * gvc_prof_read synchronises on the events, returns per-category
  * milliseconds and launch counts (categories: 0 collect, 1 select, 2 emit,
  * 3 aggregate) and resets.  gvc_launch_count is a running count of every
  * kernel this library launched. */

@@ -25,7 +25,8 @@ int set_error(int code, const char *fmt, ...)
 
 // ---------------------------------------------------------------- profiler
 static std::mutex g_prof_mu;
-static bool g_prof_on = false;
+static bool g_prof_on = false;     // mode 1: direct launches bracketed by events
+static bool g_prof_graph = false;  // mode 2: event-record nodes around k_collect inside the select graph
 static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_pending;
 static std::vector<cudaEvent_t> g_prof_free;
 static double g_prof_ms[PROF_NCAT];
@@ -71,6 +72,20 @@ bool prof_enabled()
     return g_prof_on;
 }
 
+bool prof_graph_enabled()
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    return g_prof_graph && !g_prof_on;
+}
+
+void prof_graph_pair(cudaEvent_t *a, cudaEvent_t *b)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    *a = prof_event();
+    *b = prof_event();
+    g_prof_pending.push_back({PROF_COLLECT, {*a, *b}});
+}
+
 static int check_launch(const char *what)
 {
     cudaError_t e = cudaGetLastError();
@@ -94,9 +109,10 @@ int gvc_abi_version(void) { return GVC_ABI_VERSION; }
 void gvc_prof_enable(int on)
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    g_prof_on = on != 0;
+    g_prof_on = on == 1;
+    g_prof_graph = on == 2;
     // pre-create events so the timed region never pays cudaEventCreate
-    while (g_prof_on && g_prof_free.size() < 4096) {
+    while ((g_prof_on || g_prof_graph) && g_prof_free.size() < 4096) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess)
             break;

@@ -1485,8 +1485,10 @@ static void set_attributes()
 
 // The select pipeline on stream s; every kernel takes the plan by value (its
 // fields live in the constant bank).  Returns the number of kernels.
+static cudaEvent_t g_ev_mark[2];  // capture-time placeholders of the collect event nodes
+
 template <int KM>
-static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes)
+static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gprobes)
 {
     ProfScope all(probes ? PROF_SELECT : -1, s);
     const int blocks = (int)p.B;
@@ -1500,6 +1502,8 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes)
     k_sample_resolve<<<1, 1024, 0, s>>>(p, 0);
     {
         ProfScope pc(probes ? PROF_COLLECT : -1, s);
+        if (gprobes)
+            cudaEventRecordWithFlags(g_ev_mark[0], s, cudaEventRecordExternal);
         if (!p.ef)
             k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
         else if (!p.pmask)
@@ -1508,6 +1512,8 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes)
             k_collect<KM, true, 1><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
         else
             k_collect<KM, true, 2><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+        if (gprobes)
+            cudaEventRecordWithFlags(g_ev_mark[1], s, cudaEventRecordExternal);
     }
     k_resolve0<<<1, 1024, 0, s>>>(p, 0);
     if (p.ef)
@@ -1533,14 +1539,15 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes)
 
 static_assert(sizeof(Plan) <= 4000, "the plan is passed as a kernel parameter");
 
-static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *launches)
+static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *launches, bool gprobes = false)
 {
     cudaMemsetAsync(p.st, 0, sizeof(SelState), s);
     cudaMemsetAsync(p.hist0, 0, GVC_H0_BINS * 4, s);
     cudaMemsetAsync(p.histl, 0, GVC_MAX_LADDER * GVC_HL_BINS * 4, s);
     if (p.keymode == KEY_MAG)
         cudaMemsetAsync(p.shist, 0, GVC_SAMPLE_BINS * 4, s);
-    *launches = p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, s, probes) : launch_pipeline<KEY_HASH>(p, s, probes);
+    *launches = p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
+                                     : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
 }
 
 // CUDA graphs of the select pipeline, one per launch shape.  Every kernel has
@@ -1555,6 +1562,7 @@ struct GraphEntry {
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     std::vector<GraphNode> nodes;
+    cudaGraphNode_t ev_nodes[2] = {nullptr, nullptr};  // collect start / end (profiling graphs)
     int launches;
 };
 static std::unordered_map<std::string, GraphEntry> g_graphs;
@@ -1633,7 +1641,8 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
         // measurement mode: direct launches bracketed by CUDA events (bench.py roofline)
         enqueue_select(p, s, true, &launches);
     } else {
-        const std::string key = graph_key(p, ws);
+        const bool gprobes = prof_graph_enabled();
+        const std::string key = graph_key(p, ws) + (gprobes ? "|ev" : "");
         std::lock_guard<std::mutex> glk(g_mu);
         auto it = g_graphs.find(key);
         if (it == g_graphs.end()) {
@@ -1642,8 +1651,12 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
                 cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
             cudaGraph_t graph;
             GraphEntry ge;
+            if (gprobes && !g_ev_mark[0]) {
+                cudaEventCreate(&g_ev_mark[0]);
+                cudaEventCreate(&g_ev_mark[1]);
+            }
             cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
-            enqueue_select(p, cs, false, &ge.launches);
+            enqueue_select(p, cs, false, &ge.launches, gprobes);
             cudaError_t ce = cudaStreamEndCapture(cs, &graph);
             if (ce != cudaSuccess)
                 return set_error(GVC_ERR_CUDA, "select graph capture: %s", cudaGetErrorString(ce));
@@ -1654,6 +1667,12 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             for (cudaGraphNode_t nd : all) {
                 cudaGraphNodeType ty;
                 cudaGraphNodeGetType(nd, &ty);
+                if (ty == cudaGraphNodeTypeEventRecord) {
+                    cudaEvent_t ev;
+                    cudaGraphEventRecordNodeGetEvent(nd, &ev);
+                    ge.ev_nodes[ev == g_ev_mark[0] ? 0 : 1] = nd;
+                    continue;
+                }
                 if (ty != cudaGraphNodeTypeKernel)
                     continue;
                 GraphNode gn;
@@ -1678,6 +1697,12 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             cudaError_t ue = cudaGraphExecKernelNodeSetParams(it->second.exec, gn.node, &kp);
             if (ue != cudaSuccess)
                 return set_error(GVC_ERR_CUDA, "select graph update: %s", cudaGetErrorString(ue));
+        }
+        if (it->second.ev_nodes[0] && it->second.ev_nodes[1]) {
+            cudaEvent_t a, b;
+            prof_graph_pair(&a, &b);
+            cudaGraphExecEventRecordNodeSetEvent(it->second.exec, it->second.ev_nodes[0], a);
+            cudaGraphExecEventRecordNodeSetEvent(it->second.exec, it->second.ev_nodes[1], b);
         }
         cudaGraphLaunch(it->second.exec, s);
         launches = it->second.launches;
