@@ -11,7 +11,16 @@
 // Segments: the input is cut into S contiguous ranges, one per warp of the
 // collect kernel.  S depends only on n (never on the device), so every
 // reduction order is a function of the input size alone.
-#define GVC_SEG_TARGET 4736  // 148 SMs x 4 resident blocks x 8 warps: the collect grid is one full wave
+#ifndef GVC_COLLECT_PREFETCH
+#define GVC_COLLECT_PREFETCH 1
+#endif
+#if GVC_COLLECT_PREFETCH
+#define GVC_COLLECT_BLOCKS 4  // register double buffer: 64 regs
+#else
+#define GVC_COLLECT_BLOCKS 5  // no register buffer: 48 regs, latency hidden by warps
+#endif
+// 148 SMs x resident collect blocks x 8 warps: the collect grid is one full wave
+#define GVC_SEG_TARGET (148 * GVC_COLLECT_BLOCKS * 8)
 #define GVC_SEG_MAX 16384
 #define GVC_SEG_QUANTUM 512  // elements per warp iteration: 32 lanes x 4 float4
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)

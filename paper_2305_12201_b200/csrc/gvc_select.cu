@@ -362,7 +362,7 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // (exactness fallback).  NaN keys are always candidates and are flagged by the
 // candidate passes, not here.
 template <int KM, bool EF, int PM>
-__global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan p, int refill)
+__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int refill)
 {
     __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan p, int re
         uint32_t *cidx = p.cand_idx + beg;
         uint32_t ccount = 0;
         uint32_t i = 0;
+#if GVC_COLLECT_PREFETCH
         // software pipeline over 256-value steps: the next step's g / r loads are
         // in flight while this step is added, reduced and compacted
         constexpr uint32_t STEP = 256;
@@ -413,6 +414,19 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan p, int re
                         nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
                 }
             }
+#else
+        // 256-value steps; latency is hidden by warps (6 resident blocks/SM)
+        constexpr uint32_t STEP = 256;
+        const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
+        for (; i < nfull; i += STEP) {
+            float4 a[2], b[2];
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
+                if (do_ef)
+                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
+            }
+#endif
             if (do_ef) {
                 if (PM) {
                     // the 8 mask words of this step in one load (lanes 0..7), shuffled to
@@ -449,6 +463,7 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan p, int re
                 push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
                           cidx, ccount);
             }
+#if GVC_COLLECT_PREFETCH
             if (more) {
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
@@ -456,6 +471,7 @@ __global__ void __launch_bounds__(GVC_THREADS, 4) k_collect(const Plan p, int re
                     b[u] = nb[u];
                 }
             }
+#endif
         }
         // tail: one value per lane, lane-major order preserved
         for (; i < len; i += 32) {
