@@ -395,6 +395,9 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
         constexpr uint32_t STEP = 256;
         const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
         float4 a[2], b[2];
+        // the step's 8 pending-mask words (lanes 0..7), prefetched with the data:
+        // a mask load issued at its use was the kernel's top stall (ncu)
+        uint32_t wreg = 0u;
         if (nfull) {
 #pragma unroll
             for (int u = 0; u < 2; u++) {
@@ -402,9 +405,12 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
                 if (do_ef)
                     b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + u * 128) + lane);
             }
+            if (do_ef && PM && lane < 8)
+                wreg = mp[lane];
         }
         for (; i < nfull; i += STEP) {
             float4 na[2], nb[2];
+            uint32_t nw = 0u;
             const bool more = i + STEP < nfull;
             if (more) {
 #pragma unroll
@@ -413,6 +419,8 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
                     if (do_ef)
                         nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
                 }
+                if (do_ef && PM && lane < 8)
+                    nw = mp[((i + STEP) >> 5) + lane];
             }
 #else
         // 256-value steps; latency is hidden by warps (6 resident blocks/SM)
@@ -429,9 +437,11 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
 #endif
             if (do_ef) {
                 if (PM) {
-                    // the 8 mask words of this step in one load (lanes 0..7), shuffled to
-                    // the lanes owning their 4-bit slices, cleared after use
+                    // the 8 mask words of this step (lanes 0..7), shuffled to the
+                    // lanes owning their 4-bit slices, cleared after use
+#if !GVC_COLLECT_PREFETCH
                     const uint32_t wreg = lane < 8 ? mp[(i >> 5) + lane] : 0u;
+#endif
 #pragma unroll
                     for (int u = 0; u < 2; u++) {
                         const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
@@ -470,6 +480,7 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
                     a[u] = na[u];
                     b[u] = nb[u];
                 }
+                wreg = nw;
             }
 #endif
         }
