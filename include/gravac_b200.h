@@ -225,6 +225,26 @@ GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, u
 GVC_API int gvc_aggregate_peers(const uint32_t *const *idx_dev, const float *const *vals_dev,
                         const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,
                         const uint32_t *flags_dev, uint32_t epoch, float *out_dev, void *stream);
+/* Staged pull: the same merge, but the first copy_blocks CTAs of its grid
+ * stream the peers' (idx, vals) chunk by chunk (chunk_entries, a power of
+ * two) over NVLink into LOCAL staging slots -- idx_dev / vals_dev[p] for
+ * p != self -- and publish each chunk in ready_dev[chunk] (local, monotonic
+ * epochs, ceil(k / chunk_entries) words); each tile waits only for its own
+ * chunks, so the transfer and the merge overlap.  src_*_dev[p]: peer p's
+ * payload (peer-mapped); bounds_dev[p] is read from the peers directly. */
+typedef struct gvc_peer_staging {
+    int32_t self;
+    int32_t copy_blocks;
+    uint32_t chunk_entries;
+    uint32_t reserved;
+    uint32_t *ready_dev;
+    const uint32_t *src_idx_dev[GVC_MAX_PEERS];
+    const float *src_vals_dev[GVC_MAX_PEERS];
+} gvc_peer_staging;
+GVC_API int gvc_aggregate_peers_staged(const uint32_t *const *idx_dev, const float *const *vals_dev,
+                        const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,
+                        const uint32_t *flags_dev, uint32_t epoch, const gvc_peer_staging *staging,
+                        float *out_dev, void *stream);
 /* Tile boundaries (gvc_emit's tile_bounds_dev layout) of one index-ascending
  * list of k entries over [0, n): u32[ceil(n / GVC_AGG_TILE) + 1]. */
 GVC_API int gvc_tile_bounds(const uint32_t *idx_dev, uint64_t k, uint64_t n, uint32_t *bounds_dev, void *stream);

@@ -30,6 +30,7 @@ EXPORTS = (
     "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
+    "gvc_aggregate_peers_staged",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -68,6 +69,13 @@ class SelectResult(ctypes.Structure):
 
 
 RESULT_BYTES = ctypes.sizeof(SelectResult)
+
+
+class PeerStaging(ctypes.Structure):
+    """gvc_peer_staging: the staged-pull exchange (copier CTAs + merge tiles)."""
+    _fields_ = [("self_rank", _i32), ("copy_blocks", _i32), ("chunk_entries", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32), ("ready_dev", _vp), ("src_idx_dev", _vp * 8),
+                ("src_vals_dev", _vp * 8)]
 
 
 class EmitMirrors(ctypes.Structure):
@@ -123,6 +131,8 @@ def load(build_if_missing: bool = False):
         L.gvc_peer_signal.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, _vp]
         L.gvc_aggregate_peers.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32, _vp, _vp]
         L.gvc_tile_bounds.argtypes = [_vp, _u64, _u64, _vp, _vp]
+        L.gvc_aggregate_peers_staged.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32,
+                                                 ctypes.POINTER(PeerStaging), _vp, _vp]
         L.gvc_emit_mirrored.argtypes = [_vp, _sz, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                         ctypes.POINTER(EmitMirrors), _vp]
         L.gvc_prof_enable.argtypes = [ctypes.c_int]

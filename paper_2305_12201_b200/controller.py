@@ -417,7 +417,7 @@ def _average(sent, group, out: torch.Tensor | None, peer=None):
     from .compressors import aggregate_packed, aggregate_dense
     if isinstance(sent[0], SparseGradient):
         if peer is not None:
-            return GradientVector._wrap(peer.aggregate(sent[0], out=out))
+            return GradientVector._wrap(peer.aggregate(sent[0], out=out, staged=peer.staged))
         if group is not None:
             from .exchange import allgather_aggregate
             return allgather_aggregate(sent[0], group, out=out)
@@ -492,6 +492,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         xmode = exchange_mode(group)
         if xmode != "nccl":
             peer = PeerExchange.get(group, dev)
+            peer.staged = xmode == "staged"
 
     # ---- one device->host read per iteration: every worker's norms and
     # energies (with a process group: C2, all-gathered first).  Started on the

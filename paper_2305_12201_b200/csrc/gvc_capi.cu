@@ -292,6 +292,17 @@ int gvc_aggregate_peers(const uint32_t *const *idx, const float *const *vals, co
     return rc ? rc : check_launch("aggregate_peers");
 }
 
+int gvc_aggregate_peers_staged(const uint32_t *const *idx, const float *const *vals, const uint32_t *const *bounds,
+                               const uint64_t *counts, int nparts, uint64_t n, const uint32_t *flags, uint32_t epoch,
+                               const gvc_peer_staging *staging, float *out, void *stream)
+{
+    if (!idx || !vals || !bounds || !counts || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_aggregate_peers_staged: bad arguments");
+    int rc = aggregate_peers_staged_run(idx, vals, bounds, counts, nparts, n, flags, epoch, staging, out,
+                                        STREAM(stream));
+    return rc ? rc : check_launch("aggregate_peers_staged");
+}
+
 int gvc_tile_bounds(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, void *stream)
 {
     if (!idx || !bounds || n < 1 || k > n)

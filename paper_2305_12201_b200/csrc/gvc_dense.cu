@@ -375,6 +375,92 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p)
     return v;
 }
 
+// Staged pull (C1 + K7 overlapped): the first `ncopy` CTAs of the merge grid
+// are copiers.  They wait for every peer's payload flag, then stream the
+// peers' (idx, vals) chunk by chunk over NVLink into local staging slots and
+// publish each chunk with a release store of the epoch into ready[chunk].
+// The remaining CTAs are the usual tiles; a tile waits only for the chunks
+// its entries fall in, so the merge trails the transfer instead of following
+// it.  Copiers have the lowest block indices: they are dispatched first, so a
+// spinning tile never holds the slot a copier needs.
+struct Staged {
+    int ncopy;           // copier CTAs (0: direct pull, no staging)
+    int self;            // this rank's part (already local)
+    uint32_t ch_log2;    // entries per chunk = 1 << ch_log2 (multiple of 4)
+    uint32_t nchunks;
+    uint32_t *ready;     // [nchunks] epochs, local memory
+    const uint32_t *src_idx[GVC_MAX_PEERS];  // peer p's payload (remote)
+    const float *src_val[GVC_MAX_PEERS];
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ void staged_copier(const Staged &st, const AggParts &parts, int nparts, const uint32_t *flags,
+                              uint32_t epoch)
+{
+    if (threadIdx.x < nparts && (int)threadIdx.x != st.self) {
+        while ((int32_t)(ld_acquire_sys(flags + threadIdx.x) - epoch) < 0)
+            __nanosleep(64);
+    }
+    __syncthreads();
+    constexpr int U = 4;
+    for (uint32_t c = blockIdx.x; c < st.nchunks; c += st.ncopy) {
+        for (int q = 0; q < nparts; q++) {
+            if (q == st.self)
+                continue;
+            const uint64_t k = parts.cnt[q];
+            const uint64_t lo = (uint64_t)c << st.ch_log2;
+            const uint64_t hi = min((unsigned long long)k, (unsigned long long)(lo + (1ull << st.ch_log2)));
+            if (lo >= hi)
+                continue;
+            // int4 granules; the slots are padded to 4 entries, so rounding up is safe
+            const uint32_t lo4 = (uint32_t)(lo >> 2), hi4 = (uint32_t)((hi + 3) >> 2);
+            const int4 *si = reinterpret_cast<const int4 *>(st.src_idx[q]);
+            const int4 *sv = reinterpret_cast<const int4 *>(st.src_val[q]);
+            int4 *di = reinterpret_cast<int4 *>(const_cast<uint32_t *>(parts.idx[q]));
+            int4 *dv = reinterpret_cast<int4 *>(const_cast<float *>(parts.vals[q]));
+            for (uint32_t i0 = lo4 + threadIdx.x; i0 < hi4; i0 += U * AGG_THREADS) {
+                int4 a[U], b[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t i = i0 + u * AGG_THREADS;
+                    if (i < hi4) {
+                        a[u] = __ldcg(si + i);
+                        b[u] = __ldcg(sv + i);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t i = i0 + u * AGG_THREADS;
+                    if (i < hi4) {
+                        __stcg(di + i, a[u]);
+                        __stcg(dv + i, b[u]);
+                    }
+                }
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + c), "r"(epoch) : "memory");
+    }
+}
+
+// A tile's wait for the staged chunks of part q covering entries [a, b).
+__device__ __forceinline__ void staged_wait(const Staged &st, int q, uint32_t a, uint32_t b, uint32_t epoch)
+{
+    if (q == st.self || b <= a)
+        return;
+    for (uint32_t c = a >> st.ch_log2; c <= (b - 1) >> st.ch_log2; c++)
+        while ((int32_t)(ld_acquire_gpu(st.ready + c) - epoch) < 0)
+            __nanosleep(32);
+}
+
 // MODE 0: decompress (fp32 assignment, -0.0 kept); 1: mean of ONE part
 // (0.0 + v in fp64 then /1: v, except -0.0 -> +0.0); 2: fp64 mean of N parts.
 // Parts are taken in groups of NP: the group's tile bounds are fetched by NP
@@ -387,16 +473,20 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p)
 // waits until peer p has posted `epoch` into flags[p] (its payload is
 // complete), and all part reads bypass L1 (ld.global.cg), so no stale line of
 // an earlier exchange through the same slot can be hit.
-template <int MODE, bool WAIT, int NP>
+template <int MODE, bool WAIT, int NP, bool STAGED = false>
 __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int nparts, uint64_t n,
                                                             float *__restrict__ out, const uint32_t *flags,
-                                                            uint32_t epoch)
+                                                            uint32_t epoch, Staged stg)
 {
     constexpr int U = NP >= 8 ? 2 : 4;
     __shared__ __align__(16) double acc[MODE == 2 ? AGG_TILE : 2];
     __shared__ __align__(16) float accf[MODE == 2 ? 4 : AGG_TILE];
     __shared__ uint32_t s_a[NP], s_b[NP];
-    const uint32_t tile = blockIdx.x;
+    if (STAGED && (int)blockIdx.x < stg.ncopy) {
+        staged_copier(stg, parts, nparts, flags, epoch);
+        return;
+    }
+    const uint32_t tile = STAGED ? blockIdx.x - stg.ncopy : blockIdx.x;
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (MODE == 2) {
@@ -424,6 +514,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
             }
             s_a[threadIdx.x] = __ldcg(parts.bounds[p] + tile);
             s_b[threadIdx.x] = __ldcg(parts.bounds[p] + tile + 1);
+            if (STAGED)
+                staged_wait(stg, p, s_a[threadIdx.x], s_b[threadIdx.x], epoch);
         }
         __syncthreads();
         uint32_t maxlen = 0;
@@ -520,15 +612,19 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
 // contributes +0.0, which leaves any fp64 sum starting from +0.0 unchanged
 // (it can never be -0.0).  MODE 0: decompress (one part, fp32 copy, -0.0
 // kept); MODE 1: average.  Dynamic shared memory: NP * AGG_TILE floats.
-template <int MODE, bool WAIT, int NP>
+template <int MODE, bool WAIT, int NP, bool STAGED = false>
 __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int nparts, uint64_t n,
                                                            float *__restrict__ out, const uint32_t *flags,
-                                                           uint32_t epoch)
+                                                           uint32_t epoch, Staged stg)
 {
     constexpr int U = NP >= 4 ? 2 : 4;
     extern __shared__ __align__(16) float tiles[];
     __shared__ uint32_t s_a[NP], s_b[NP];
-    const uint32_t tile = blockIdx.x;
+    if (STAGED && (int)blockIdx.x < stg.ncopy) {
+        staged_copier(stg, parts, nparts, flags, epoch);
+        return;
+    }
+    const uint32_t tile = STAGED ? blockIdx.x - stg.ncopy : blockIdx.x;
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (threadIdx.x < nparts) {
@@ -539,6 +635,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
         }
         s_a[p] = __ldcg(parts.bounds[p] + tile);
         s_b[p] = __ldcg(parts.bounds[p] + tile + 1);
+        if (STAGED)
+            staged_wait(stg, p, s_a[p], s_b[p], epoch);
     }
     for (int i = threadIdx.x; i < nparts * (AGG_TILE / 4); i += AGG_THREADS)
         reinterpret_cast<float4 *>(tiles)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -715,7 +813,7 @@ size_t aggregate_workspace_bytes(int nparts, uint64_t n)
 
 // Parts without tile bounds get them from k_tile_bounds into ws first.
 static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes,
-                          const uint32_t *flags, uint32_t epoch, cudaStream_t s)
+                          const uint32_t *flags, uint32_t epoch, cudaStream_t s, const Staged *staged = nullptr)
 {
     const uint64_t ntiles = (n + AGG_TILE - 1) / AGG_TILE;
     ProfScope pa(PROF_AGGREGATE, s);
@@ -737,23 +835,34 @@ static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *
     const size_t sm1 = AGG_TILE * 4, sm2 = 2 * sm1;
     // measured (scripts/merge_bench.py): per-part fp32 tiles win for 1-2 parts,
     // the single fp64 tile (less shared memory, higher occupancy) above
-    if (flags) {
+    Staged none;
+    memset(&none, 0, sizeof(none));
+    const Staged &st = staged ? *staged : none;
+    const unsigned gs = g + (unsigned)st.ncopy;
+    if (staged) {
         if (nparts <= 2)
-            k_tile_part<1, true, 2><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch);
+            k_tile_part<1, true, 2, true><<<gs, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch, st);
         else if (nparts <= 4)
-            k_tile_merge<2, true, 4><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch);
+            k_tile_merge<2, true, 4, true><<<gs, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch, st);
         else
-            k_tile_merge<2, true, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch);
+            k_tile_merge<2, true, 8, true><<<gs, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch, st);
+    } else if (flags) {
+        if (nparts <= 2)
+            k_tile_part<1, true, 2><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch, st);
+        else if (nparts <= 4)
+            k_tile_merge<2, true, 4><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch, st);
+        else
+            k_tile_merge<2, true, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch, st);
     } else if (!avg) {
-        k_tile_part<0, false, 1><<<g, AGG_THREADS, sm1, s>>>(P, nparts, n, out, nullptr, 0);
+        k_tile_part<0, false, 1><<<g, AGG_THREADS, sm1, s>>>(P, nparts, n, out, nullptr, 0, st);
     } else if (nparts == 1) {
-        k_tile_part<1, false, 1><<<g, AGG_THREADS, sm1, s>>>(P, nparts, n, out, nullptr, 0);
+        k_tile_part<1, false, 1><<<g, AGG_THREADS, sm1, s>>>(P, nparts, n, out, nullptr, 0, st);
     } else if (nparts == 2) {
-        k_tile_part<1, false, 2><<<g, AGG_THREADS, sm2, s>>>(P, nparts, n, out, nullptr, 0);
+        k_tile_part<1, false, 2><<<g, AGG_THREADS, sm2, s>>>(P, nparts, n, out, nullptr, 0, st);
     } else if (nparts <= 4) {
-        k_tile_merge<2, false, 4><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0);
+        k_tile_merge<2, false, 4><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0, st);
     } else {
-        k_tile_merge<2, false, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0);
+        k_tile_merge<2, false, 8><<<g, AGG_THREADS, 0, s>>>(P, nparts, n, out, nullptr, 0, st);
     }
     return GVC_OK;
 }
@@ -833,6 +942,40 @@ int aggregate_peers_run(const uint32_t *const *idx, const float *const *vals, co
         P.cnt[p] = counts[p];
     }
     return tile_merge_run(true, P, nparts, n, out, nullptr, 0, flags, epoch, s);
+}
+
+int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *vals, const uint32_t *const *bounds,
+                               const uint64_t *counts, int nparts, uint64_t n, const uint32_t *flags, uint32_t epoch,
+                               const gvc_peer_staging *sg, float *out, cudaStream_t s)
+{
+    if (nparts < 1 || nparts > GVC_MAX_PEERS)
+        return set_error(GVC_ERR_ARG, "aggregate_peers_staged: nparts %d outside [1, %d]", nparts, GVC_MAX_PEERS);
+    if (!flags || !sg || !sg->ready_dev || sg->self < 0 || sg->self >= nparts || sg->copy_blocks < 1)
+        return set_error(GVC_ERR_ARG, "aggregate_peers_staged: bad flags / staging");
+    const uint32_t ce = sg->chunk_entries;
+    if (ce < 4 || (ce & (ce - 1)))
+        return set_error(GVC_ERR_ARG, "aggregate_peers_staged: chunk_entries %u is not a power of two >= 4", ce);
+    AggParts P;
+    Staged st;
+    memset(&st, 0, sizeof(st));
+    st.ncopy = sg->copy_blocks;
+    st.self = sg->self;
+    st.ch_log2 = (uint32_t)__builtin_ctz(ce);
+    st.ready = sg->ready_dev;
+    uint64_t kmax = 0;
+    for (int p = 0; p < nparts; p++) {
+        if (!idx[p] || !vals[p] || !bounds[p] || (p != sg->self && (!sg->src_idx_dev[p] || !sg->src_vals_dev[p])))
+            return set_error(GVC_ERR_ARG, "aggregate_peers_staged: part %d has a null pointer", p);
+        P.idx[p] = idx[p];
+        P.vals[p] = vals[p];
+        P.bounds[p] = bounds[p];
+        P.cnt[p] = counts[p];
+        st.src_idx[p] = sg->src_idx_dev[p];
+        st.src_val[p] = sg->src_vals_dev[p];
+        kmax = counts[p] > kmax ? counts[p] : kmax;
+    }
+    st.nchunks = (uint32_t)((kmax + ce - 1) / ce);
+    return tile_merge_run(true, P, nparts, n, out, nullptr, 0, flags, epoch, s, &st);
 }
 
 int tile_bounds_run(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, cudaStream_t s)

@@ -156,6 +156,7 @@ class PeerExchange:
     """
 
     FLAG_WORDS = 64
+    CHUNK = 4096  # entries per staged-pull chunk (power of two)
     _cache: dict = {}
 
     def __init__(self, group, device):
@@ -168,6 +169,13 @@ class PeerExchange:
         self.epoch = 0
         self.buf = None
         self.handle = None
+        self.staged = True  # pull payloads through the staged (copier + trailing merge) kernel
+        import os
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        # measured on B200 (scripts/stage_sweep.sh): 4096-entry chunks with one
+        # copier CTA per 2 SMs beat 2048 x 148, 8192 x 148 and 1024 x 148
+        self.copy_blocks = int(os.environ.get("GVC_STAGE_COPIERS", max(1, sms // 2)))
+        self.chunk = int(os.environ.get("GVC_STAGE_CHUNK", self.CHUNK))
 
     @classmethod
     def get(cls, group, device) -> "PeerExchange":
@@ -194,6 +202,8 @@ class PeerExchange:
         self.buf, self.handle, self.cap, self.epoch = buf, handle, cap, 0
         self.bases = [int(p) for p in handle.buffer_ptrs]
         self._flag_ptrs = (ctypes.c_void_p * self.world)(*self.bases)
+        # staged pull: per-chunk ready epochs (local); epochs restart with the buffer
+        self.ready = torch.zeros(cap // self.chunk + 2, dtype=torch.int32, device=self.device)
 
     def slot(self, k: int, n: int, push: bool = True) -> Payload:
         """This rank's payload slot of the next exchange.  With ``push`` (a
@@ -217,8 +227,13 @@ class PeerExchange:
             pl.mirrors = m
         return pl
 
-    def aggregate(self, part: SparseGradient, out: torch.Tensor | None = None) -> torch.Tensor:
-        """The rank-ordered fp64 mean of every rank's part (aggregate() semantics)."""
+    def aggregate(self, part: SparseGradient, out: torch.Tensor | None = None, staged: bool = True) -> torch.Tensor:
+        """The rank-ordered fp64 mean of every rank's part (aggregate() semantics).
+
+        Pull payloads are merged either ``staged`` (copier CTAs stream the
+        peers' payloads into this rank's own slots chunk by chunk while the
+        merge tiles trail them) or directly (the tiles read the peers' slots
+        over NVLink)."""
         n = part.original_length
         pl = getattr(part, "_payload", None)
         if pl is None or pl.peer is None or pl.peer[0] is not self or pl.peer[1] != self.epoch + 1 \
@@ -238,34 +253,51 @@ class PeerExchange:
         nat.check(lib.gvc_peer_signal(self._flag_ptrs, self.world, self.rank, e, stream), "peer_signal")
         W = self.world
         own = self.bases[self.rank]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self.device)
+        counts = (ctypes.c_uint64 * W)(*([part.kept] * W))
+        peer_slot = [self.bases[p] + 4 * self._slot_word(e % 2, p) for p in range(W)]  # slot p in rank p's buffer
+        own_slot = [own + 4 * self._slot_word(e % 2, p) for p in range(W)]  # slot p in this rank's buffer
+        if not pushed and staged and W > 1:
+            # staged pull: local staging = own_slot[p]; sources and tile bounds = peer_slot[p]
+            sg = nat.PeerStaging()
+            sg.self_rank = self.rank
+            sg.copy_blocks = self.copy_blocks
+            sg.chunk_entries = self.chunk
+            sg.ready_dev = self.ready.data_ptr()
+            for p in range(W):
+                sg.src_idx_dev[p] = peer_slot[p]
+                sg.src_vals_dev[p] = peer_slot[p] + 4 * pl.kpad
+            idx = (ctypes.c_void_p * W)(*own_slot)
+            vals = (ctypes.c_void_p * W)(*[b + 4 * pl.kpad for b in own_slot])
+            bnd = (ctypes.c_void_p * W)(*[b + 8 * pl.kpad for b in peer_slot])
+            nat.check(lib.gvc_aggregate_peers_staged(idx, vals, bnd, counts, W, n, nat.ptr(self.buf), e,
+                                                     ctypes.byref(sg), nat.ptr(out), stream), "aggregate_peers")
+            return out
         # push: every slot is in this rank's buffer; pull: slot p lives in rank p's buffer
-        bases = [own + 4 * self._slot_word(e % 2, p) if pushed else self.bases[p] + 4 * self._slot_word(e % 2, p)
-                 for p in range(W)]
+        bases = own_slot if pushed else peer_slot
         idx = (ctypes.c_void_p * W)(*bases)
         vals = (ctypes.c_void_p * W)(*[b + 4 * pl.kpad for b in bases])
         bnd = (ctypes.c_void_p * W)(*[b + 8 * pl.kpad for b in bases])
-        counts = (ctypes.c_uint64 * W)(*([part.kept] * W))
-        if out is None:
-            out = torch.empty(n, dtype=torch.float32, device=self.device)
         nat.check(lib.gvc_aggregate_peers(idx, vals, bnd, counts, W, n, nat.ptr(self.buf), e, nat.ptr(out),
                                           stream), "aggregate_peers")
         return out
 
 
 def exchange_mode(group) -> str:
-    """"push" / "pull" (the NVLink peer-memory exchange) or "nccl" (all-gather
-    + K7).  Peer memory needs an NCCL group of at most 8 ranks on one node.
-    GVC_EXCHANGE overrides; the default pulls (measured on B200: pull 0.383 ms
-    vs push 0.389 ms per step at 2 ranks, 0.543 vs 0.638 at 4 -- every extra
-    destination slows the pushing emit)."""
+    """"staged" / "pull" / "push" (the NVLink peer-memory exchange) or "nccl"
+    (all-gather + K7).  Peer memory needs an NCCL group of at most 8 ranks on one node.
+    GVC_EXCHANGE overrides; the default is the staged pull (measured on B200,
+    ms/step: 2 ranks staged 0.350, pull 0.367, push 0.389, nccl 0.397; 4 ranks
+    staged 0.454, pull 0.533, nccl 0.598, push 0.638)."""
     import os
     if group is None or dist.get_backend(group) != "nccl" or dist.get_world_size(group) > nat.MAX_PEERS:
         return "nccl"
     mode = os.environ.get("GVC_EXCHANGE", "auto")
     if mode == "auto":
-        mode = "pull"
-    if mode not in ("push", "pull", "nccl"):
-        raise ValueError(f"GVC_EXCHANGE={mode!r}: expected push, pull, nccl or auto")
+        mode = "staged"
+    if mode not in ("push", "pull", "staged", "nccl"):
+        raise ValueError(f"GVC_EXCHANGE={mode!r}: expected push, pull, staged, nccl or auto")
     return mode
 
 

@@ -1,6 +1,6 @@
 """Multi-GPU path (one process per GPU, NCCL): the C2 gain exchange gives every
 rank the reference's worker-ordered decision, and C1 + K7 -- fused over NVLink
-peer memory (GVC_EXCHANGE=push / pull) or all-gather + K7 (nccl) -- equals
+peer memory (GVC_EXCHANGE=staged / pull / push) or all-gather + K7 (nccl) -- equals
 aggregate() over the same parts, bit for bit.  Skipped with fewer than 2 GPUs."""
 import os
 import socket
@@ -70,7 +70,7 @@ def _world():
     return min(n, 4)
 
 
-@pytest.mark.parametrize("exchange", ["push", "pull", "nccl"])
+@pytest.mark.parametrize("exchange", ["staged", "push", "pull", "nccl"])
 @pytest.mark.parametrize("kind", ["topk", "dgc", "redsync"])
 def test_multi_rank_step(kind, exchange):
     world = _world()
@@ -113,7 +113,7 @@ def _peer_worker(rank, world, port, q):
         pl.bounds = None  # not written by an emit: the exchange computes them
         part = G.SparseGradient._wrap(pl.idx[:k], pl.vals[:k], n, n / k)
         part._payload = pl
-        out = px.aggregate(part).cpu().numpy()
+        out = px.aggregate(part, staged=e % 2 == 0).cpu().numpy()
         ref = O.aggregate(parts, n)
         ok.append(bool(np.array_equal(out.view(np.int32), ref.view(np.int32))))
     q.put((rank, ok))
