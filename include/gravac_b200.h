@@ -226,12 +226,13 @@ GVC_API int gvc_aggregate_peers(const uint32_t *const *idx_dev, const float *con
                         const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,
                         const uint32_t *flags_dev, uint32_t epoch, float *out_dev, void *stream);
 /* Staged pull: the same merge, but the first copy_blocks CTAs of its grid
- * stream the peers' (idx, vals) chunk by chunk (chunk_entries, a power of
- * two) over NVLink into LOCAL staging slots -- idx_dev / vals_dev[p] for
- * p != self -- and publish each chunk in ready_dev[chunk] (local, monotonic
- * epochs, ceil(k / chunk_entries) words); each tile waits only for its own
- * chunks, so the transfer and the merge overlap.  src_*_dev[p]: peer p's
- * payload (peer-mapped); bounds_dev[p] is read from the peers directly. */
+ * stream the peers' tile bounds, then their (idx, vals) chunk by chunk
+ * (chunk_entries, a power of two), over NVLink into LOCAL staging slots --
+ * idx_dev / vals_dev / bounds_dev[p] for p != self.  ready_dev (local, zeroed
+ * once, copy_blocks + ceil(k / chunk_entries) words of monotonic epochs):
+ * word b < copy_blocks tags bound slice b, word copy_blocks + c chunk c.  Each
+ * tile waits only for its own chunks, so the transfer and the merge overlap.
+ * src_*_dev[p]: peer p's payload (peer-mapped). */
 typedef struct gvc_peer_staging {
     int32_t self;
     int32_t copy_blocks;
@@ -240,6 +241,7 @@ typedef struct gvc_peer_staging {
     uint32_t *ready_dev;
     const uint32_t *src_idx_dev[GVC_MAX_PEERS];
     const float *src_vals_dev[GVC_MAX_PEERS];
+    const uint32_t *src_bounds_dev[GVC_MAX_PEERS];
 } gvc_peer_staging;
 GVC_API int gvc_aggregate_peers_staged(const uint32_t *const *idx_dev, const float *const *vals_dev,
                         const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,

@@ -75,7 +75,7 @@ class PeerStaging(ctypes.Structure):
     """gvc_peer_staging: the staged-pull exchange (copier CTAs + merge tiles)."""
     _fields_ = [("self_rank", _i32), ("copy_blocks", _i32), ("chunk_entries", ctypes.c_uint32),
                 ("reserved", ctypes.c_uint32), ("ready_dev", _vp), ("src_idx_dev", _vp * 8),
-                ("src_vals_dev", _vp * 8)]
+                ("src_vals_dev", _vp * 8), ("src_bounds_dev", _vp * 8)]
 
 
 class EmitMirrors(ctypes.Structure):

@@ -388,9 +388,11 @@ struct Staged {
     int self;            // this rank's part (already local)
     uint32_t ch_log2;    // entries per chunk = 1 << ch_log2 (multiple of 4)
     uint32_t nchunks;
-    uint32_t *ready;     // [nchunks] epochs, local memory
+    uint32_t nb;         // tile-bound words per part (ntiles + 1)
+    uint32_t *ready;     // [b < ncopy]: bound slice b's epoch; [ncopy + c]: chunk c's epoch
     const uint32_t *src_idx[GVC_MAX_PEERS];  // peer p's payload (remote)
     const float *src_val[GVC_MAX_PEERS];
+    const uint32_t *src_bounds[GVC_MAX_PEERS];
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p)
@@ -408,6 +410,23 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
             __nanosleep(64);
     }
     __syncthreads();
+    // first the tile bounds (every tile needs them before it can look for its
+    // chunks): copier b stages slice b of every remote part's bounds
+    {
+        const uint32_t per = (st.nb + st.ncopy - 1) / st.ncopy;
+        const uint32_t b0 = blockIdx.x * per, b1 = min(st.nb, b0 + per);
+        for (int q = 0; q < nparts; q++) {
+            if (q == st.self)
+                continue;
+            uint32_t *dst = const_cast<uint32_t *>(parts.bounds[q]);
+            for (uint32_t i = b0 + threadIdx.x; i < b1; i += AGG_THREADS)
+                __stcg(dst + i, __ldcg(st.src_bounds[q] + i));
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + blockIdx.x), "r"(epoch) : "memory");
+    }
     constexpr int U = 4;
     for (uint32_t c = blockIdx.x; c < st.nchunks; c += st.ncopy) {
         for (int q = 0; q < nparts; q++) {
@@ -447,8 +466,19 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0)
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + c), "r"(epoch) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + st.ncopy + c), "r"(epoch) : "memory");
     }
+}
+
+// A tile's wait for the staged bound slices holding entries t and t + 1.
+__device__ __forceinline__ void staged_wait_bounds(const Staged &st, int q, uint32_t t, uint32_t epoch)
+{
+    if (q == st.self)
+        return;
+    const uint32_t per = (st.nb + st.ncopy - 1) / st.ncopy;
+    for (uint32_t b = t / per; b <= (t + 1) / per; b++)
+        while ((int32_t)(ld_acquire_gpu(st.ready + b) - epoch) < 0)
+            __nanosleep(32);
 }
 
 // A tile's wait for the staged chunks of part q covering entries [a, b).
@@ -457,7 +487,7 @@ __device__ __forceinline__ void staged_wait(const Staged &st, int q, uint32_t a,
     if (q == st.self || b <= a)
         return;
     for (uint32_t c = a >> st.ch_log2; c <= (b - 1) >> st.ch_log2; c++)
-        while ((int32_t)(ld_acquire_gpu(st.ready + c) - epoch) < 0)
+        while ((int32_t)(ld_acquire_gpu(st.ready + st.ncopy + c) - epoch) < 0)
             __nanosleep(32);
 }
 
@@ -512,6 +542,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
                 while ((int32_t)(ld_acquire_sys(flags + p) - epoch) < 0)
                     __nanosleep(64);
             }
+            if (STAGED)
+                staged_wait_bounds(stg, p, tile, epoch);
             s_a[threadIdx.x] = __ldcg(parts.bounds[p] + tile);
             s_b[threadIdx.x] = __ldcg(parts.bounds[p] + tile + 1);
             if (STAGED)
@@ -633,6 +665,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
             while ((int32_t)(ld_acquire_sys(flags + p) - epoch) < 0)
                 __nanosleep(64);
         }
+        if (STAGED)
+            staged_wait_bounds(stg, p, tile, epoch);
         s_a[p] = __ldcg(parts.bounds[p] + tile);
         s_b[p] = __ldcg(parts.bounds[p] + tile + 1);
         if (STAGED)
@@ -972,9 +1006,13 @@ int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *v
         P.cnt[p] = counts[p];
         st.src_idx[p] = sg->src_idx_dev[p];
         st.src_val[p] = sg->src_vals_dev[p];
+        st.src_bounds[p] = sg->src_bounds_dev[p];
+        if (p != sg->self && !sg->src_bounds_dev[p])
+            return set_error(GVC_ERR_ARG, "aggregate_peers_staged: part %d has no source bounds", p);
         kmax = counts[p] > kmax ? counts[p] : kmax;
     }
     st.nchunks = (uint32_t)((kmax + ce - 1) / ce);
+    st.nb = (uint32_t)((n + AGG_TILE - 1) / AGG_TILE + 1);
     return tile_merge_run(true, P, nparts, n, out, nullptr, 0, flags, epoch, s, &st);
 }
 

@@ -203,7 +203,7 @@ class PeerExchange:
         self.bases = [int(p) for p in handle.buffer_ptrs]
         self._flag_ptrs = (ctypes.c_void_p * self.world)(*self.bases)
         # staged pull: per-chunk ready epochs (local); epochs restart with the buffer
-        self.ready = torch.zeros(cap // self.chunk + 2, dtype=torch.int32, device=self.device)
+        self.ready = torch.zeros(self.copy_blocks + cap // self.chunk + 2, dtype=torch.int32, device=self.device)
 
     def slot(self, k: int, n: int, push: bool = True) -> Payload:
         """This rank's payload slot of the next exchange.  With ``push`` (a
@@ -259,7 +259,7 @@ class PeerExchange:
         peer_slot = [self.bases[p] + 4 * self._slot_word(e % 2, p) for p in range(W)]  # slot p in rank p's buffer
         own_slot = [own + 4 * self._slot_word(e % 2, p) for p in range(W)]  # slot p in this rank's buffer
         if not pushed and staged and W > 1:
-            # staged pull: local staging = own_slot[p]; sources and tile bounds = peer_slot[p]
+            # staged pull: local staging = own_slot[p] (payload and tile bounds); sources = peer_slot[p]
             sg = nat.PeerStaging()
             sg.self_rank = self.rank
             sg.copy_blocks = self.copy_blocks
@@ -268,9 +268,10 @@ class PeerExchange:
             for p in range(W):
                 sg.src_idx_dev[p] = peer_slot[p]
                 sg.src_vals_dev[p] = peer_slot[p] + 4 * pl.kpad
+                sg.src_bounds_dev[p] = peer_slot[p] + 8 * pl.kpad
             idx = (ctypes.c_void_p * W)(*own_slot)
             vals = (ctypes.c_void_p * W)(*[b + 4 * pl.kpad for b in own_slot])
-            bnd = (ctypes.c_void_p * W)(*[b + 8 * pl.kpad for b in peer_slot])
+            bnd = (ctypes.c_void_p * W)(*[b + 8 * pl.kpad for b in own_slot])
             nat.check(lib.gvc_aggregate_peers_staged(idx, vals, bnd, counts, W, n, nat.ptr(self.buf), e,
                                                      ctypes.byref(sg), nat.ptr(out), stream), "aggregate_peers")
             return out
