@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
     // x / N == x * (1/N) exactly only for power-of-two N; zeros skip the divide
     const double np = (double)nparts;
     const bool pow2 = (nparts & (nparts - 1)) == 0;
-    const double inv = 1.0 / np;
+    const double inv = (double)(1.0f / (float)nparts);  // exact when it is used (power-of-two N)
     auto mean = [&](double a) -> float {
         if (a == 0.0)
             return 0.0f;
@@ -676,8 +676,10 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
         reinterpret_cast<float4 *>(tiles)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     uint32_t maxlen = 0;
-    for (int q = 0; q < nparts; q++)
-        maxlen = max(maxlen, s_b[q] - s_a[q]);
+#pragma unroll
+    for (int q = 0; q < NP; q++)
+        if (q < nparts)
+            maxlen = max(maxlen, s_b[q] - s_a[q]);
     if (maxlen <= U * AGG_THREADS) {
         // every entry of every part in flight before the first store
         uint32_t r[NP][U];
@@ -738,10 +740,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
     // other output (>= 3 non-zero terms, a tiny sum, non-power-of-two N) takes
     // the fp64 path, as does an fp32 sum that overflowed.  This keeps the fp64 convert/add units -- a fraction of
     // the fp32 rate -- off the common path.
-    const double np = (double)nparts;
     const bool pow2 = (nparts & (nparts - 1)) == 0;
-    const double inv = 1.0 / np;
-    const float invf = (float)inv;
+    const float invf = 1.0f / (float)nparts;  // exact for the power-of-two N the fast path needs
     auto combine = [&](const float (&t)[NP]) -> float {
         if (MODE == 0)
             return t[0];
@@ -767,7 +767,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
                 acc += (double)t[q];
         if (acc == 0.0)
             return 0.0f;
-        return (float)(pow2 ? acc * inv : acc / np);
+        const double np = (double)nparts;
+        return (float)(pow2 ? acc * (1.0 / np) : acc / np);
     };
     // |s| == 0 or 2^-100 <= |s| <= FLT_MAX, on the bits
     auto range_ok = [](float x) -> bool {
