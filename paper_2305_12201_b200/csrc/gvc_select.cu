@@ -60,6 +60,7 @@ struct SelState {
     unsigned long long shortfall;
     JState js[GVC_MAX_LADDER];
     float redsync_mean[GVC_MAX_LADDER];
+    uint32_t fin_done;  // k_finish blocks done (the last one writes the status)
 };
 
 struct Plan {
@@ -802,7 +803,8 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
     __shared__ unsigned long long sh[33];
     __shared__ __align__(16) uint32_t hs[GVC_HL_BINS];
     SelState *st = p.st;
-    for (int j = 0; j < p.n_ks; j++) {
+    // one block per ladder entry: the entries' refinements are independent
+    for (int j = blockIdx.x; j < p.n_ks; j += gridDim.x) {
         if (st->js[j].resolved)
             continue;  // uniform across the block
         uint32_t *h = p.histl + j * GVC_HL_BINS;
@@ -1225,6 +1227,223 @@ __global__ void __launch_bounds__(1024) k_finish(const Plan p, int)
     }
 }
 
+// k_finish, one block per ladder entry j (the entries are independent):
+// tie cut for T_j (lowest-index ties via the per-block prefix), kept energy
+// and |v| sum (gain numerator, Redsync mean), per-block output offsets.  Two
+// barrier phases: [norm, band sums >= j, tie prefix] and then [tie sums,
+// offset prefix].  Block 0 also reports the norm; the last block to finish
+// writes the status (after every entry's consistency check).
+template <int KM>
+__device__ __forceinline__ void finish_pair_sum(double &a, double &b, unsigned long long &c, unsigned long long &ct,
+                                                double *shd, unsigned long long *shu)
+{
+    // deterministic fixed-order sums of a, b (fp64) and an exclusive prefix of c
+    // (total in ct) over the block, sharing the barriers
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (int)(blockDim.x >> 5);
+    a = warp_sum_f64(a);
+    b = warp_sum_f64(b);
+    unsigned long long x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o)
+            x += y;
+    }
+    if (lane == 31) {
+        shd[2 * warp] = a;
+        shd[2 * warp + 1] = b;
+        shu[warp] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < nwarps ? shu[lane] : 0ull, wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o)
+                wi += y;
+        }
+        if (lane < nwarps)
+            shu[lane] = wi - w;
+        if (lane == 31)
+            shu[32] = wi;
+        if (lane == 0) {
+            double ra = 0.0, rb = 0.0;
+            for (int w2 = 0; w2 < nwarps; w2++) {
+                ra += shd[2 * w2];
+                rb += shd[2 * w2 + 1];
+            }
+            shd[64] = ra;
+            shd[65] = rb;
+        }
+    }
+    __syncthreads();
+    a = shd[64];
+    b = shd[65];
+    ct = shu[32];
+    c = shu[warp] + x - c;
+    __syncthreads();
+}
+
+template <int KM>
+__global__ void __launch_bounds__(1024) k_finish_j(const Plan p, int)
+{
+    constexpr int PER = GVC_BLK_MAX / 1024;  // 2 blocks per thread, contiguous
+    __shared__ double shd[66];
+    __shared__ unsigned long long shu[33];
+    __shared__ double shn[66];
+    __shared__ unsigned long long shn_u[33];
+    __shared__ uint32_t part_blk;
+    __shared__ unsigned long long part_take;
+    __shared__ int last;
+    SelState *st = p.st;
+    gvc_select_result *res = p.res;
+    const uint32_t B = p.B;
+    const int nks = p.n_ks;
+    const int j = blockIdx.x;
+    const int t = threadIdx.x;
+    if (j >= nks)
+        return;
+    const uint32_t T = (uint32_t)st->js[j].lo;
+    const unsigned long long q = st->js[j].need;
+    // ---- one load phase: this thread's 2 blocks
+    double nrm = 0.0, be = 0.0, ba = 0.0;
+    uint32_t above[PER], tc[PER];
+    double tie_e2[PER], tie_ab[PER];
+    unsigned long long cabove = 0, tpre = 0;
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+        const uint32_t b = t * PER + i;
+        const bool ok = b < B;
+        above[i] = 0u;
+        if (ok) {
+            if (j == 0)
+                nrm += p.blk_norm[b];
+            for (int band = j; band < nks; band++) {
+                const size_t o = (size_t)band * GVC_BLK_MAX + b;
+                above[i] += p.blk_band_cnt[o];
+                be += p.blk_band_e2[o];
+                ba += p.blk_band_ab[o];
+            }
+        }
+        const size_t oj = (size_t)j * GVC_BLK_MAX + b;
+        tc[i] = ok ? p.blk_tie_cnt[oj] : 0u;
+        tie_e2[i] = ok ? p.blk_tie_e2[oj] : 0.0;
+        tie_ab[i] = ok ? p.blk_tie_ab[oj] : 0.0;
+        cabove += above[i];
+        tpre += tc[i];
+    }
+    if (t == 0)
+        part_blk = 0xffffffffu;
+    // ---- phase 1: norm (block 0), band sums >= j, totals / tie prefix
+    unsigned long long ca_tot, tp_tot;
+    {
+        double nz = 0.0;
+        finish_pair_sum<KM>(nrm, nz, cabove, ca_tot, shn, shn_u);
+    }
+    finish_pair_sum<KM>(be, ba, tpre, tp_tot, shd, shu);
+    // ---- tie cut per block, selected counts
+    double te = 0.0, ta = 0.0;
+    unsigned long long sel[PER], so = 0;
+    {
+        unsigned long long before = tpre;
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            const uint32_t b = t * PER + i;
+            const unsigned long long c = tc[i];
+            const unsigned long long tk = before >= q ? 0 : (q - before < c ? q - before : c);
+            before += c;
+            if (b < B) {
+                p.blk_take[(size_t)j * GVC_BLK_MAX + b] = (uint32_t)tk;
+                if (tk == c && tk > 0) {
+                    te += tie_e2[i];
+                    ta += tie_ab[i];
+                }
+                if (tk > 0 && tk < c) {
+                    part_blk = b;
+                    part_take = tk;
+                }
+            }
+            sel[i] = b < B ? tk + above[i] : 0ull;
+            so += sel[i];
+        }
+    }
+    __syncthreads();
+    // ---- the (rare) partially-taken block: first part_take ties in index order
+    if (part_blk != 0xffffffffu) {
+        unsigned long long seen = 0;
+        const uint32_t pb = part_blk;
+        const uint32_t s_end = min(p.S, (pb + 1) * GVC_WARPS_PER_BLOCK);
+        for (uint32_t sg = pb * GVC_WARPS_PER_BLOCK; sg < s_end; sg++) {
+            const uint64_t beg = (uint64_t)sg * p.seg_len;
+            const uint32_t cn = p.seg_cnt[sg];
+            for (uint32_t base = 0; base < cn; base += blockDim.x) {
+                const uint32_t tt = base + t;
+                bool is_tie = false;
+                float v = 0.f;
+                if (tt < cn) {
+                    v = p.cand_val[beg + tt];
+                    const uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + tt]);
+                    is_tie = key == T;
+                }
+                unsigned long long tot;
+                const unsigned long long rank = seen + block_excl_prefix(is_tie ? 1ull : 0ull, shu, &tot);
+                if (is_tie && rank < part_take) {
+                    te += (double)v * (double)v;
+                    ta += fabs((double)v);
+                }
+                seen += tot;
+            }
+        }
+    }
+    // ---- phase 2: tie sums and the per-block output offsets
+    unsigned long long so_tot;
+    finish_pair_sum<KM>(te, ta, so, so_tot, shd, shu);
+    {
+        unsigned long long off = so;
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            const uint32_t b = t * PER + i;
+            if (b < B)
+                p.blk_off[(size_t)j * GVC_BLK_MAX + b] = (uint32_t)off;
+            off += sel[i];
+        }
+    }
+    if (t == 0) {
+        const unsigned long long k = p.ks[j] - (j == 0 ? st->shortfall : 0ull);
+        const double A = ba + ta;
+        double E = be + te;
+        const float m = (float)(A / (double)k);
+        const unsigned long long nnz = k - ((KM == KEY_MAG && T == 0u) ? q : 0ull);
+        if (p.kind == GVC_REDSYNC)
+            E = (double)nnz * ((double)m * (double)m);
+        st->redsync_mean[j] = m;
+        res->kept_sq[j] = E;
+        res->kept_abs[j] = A;
+        res->threshold_key[j] = T;
+        res->tie_quota[j] = q;
+        res->redsync_mean[j] = m;
+        res->kept_count[j] = so_tot;
+        res->kept_nonzero[j] = nnz;
+        if (ca_tot + q != k || so_tot != k)
+            atomicOr(&st->nan_flag, 2u);  // internal consistency failure
+        if (j == 0) {
+            res->ef_norm_sq = nrm;
+            res->candidates = st->cand_total;
+            res->fallback_used = (int)st->fallback;
+            res->shortfall = st->shortfall;
+        }
+        __threadfence();
+        last = atomicAdd(&st->fin_done, 1u) == (unsigned)nks - 1;
+    }
+    __syncthreads();
+    if (last && t == 0) {
+        __threadfence();
+        const uint32_t f = atomicOr(&st->nan_flag, 0u);
+        res->status = (f & 1u) ? GVC_ERR_NAN : ((f & 2u) ? GVC_ERR_STATE : GVC_OK);
+    }
+}
+
 // -------------------------------------------------------------------- emit
 // One warp per segment: in-block prefix of the 8 segments' tie / selected
 // counts (lanes 0..7), then an ordered 4-wide compaction.
@@ -1472,7 +1691,7 @@ static void launch_tail_nb(const Plan &p, cudaStream_t s)
 {
     const size_t smem = (size_t)(NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4);
     k_pass1<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(p, 0);
-    k_resolve1<KM><<<1, 1024, 0, s>>>(p, 0);
+    k_resolve1<KM><<<NB, 1024, 0, s>>>(p, 0);  // NB (in the graph key) >= n_ks blocks
     k_members<KM, NB, ABS><<<(int)p.B, GVC_THREADS, 0, s>>>(p, 0);
 }
 
@@ -1551,15 +1770,16 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     launches += 5;
     launch_tail<KM>(p, s);
     launches += 3;
-    // k_finish: 2 blocks per thread; only as many warps as the blocks need
-    // (its block-wide reductions cost per warp)
+    // k_finish_j: one block per ladder entry, 2 blocks per thread; only as many
+    // warps as the blocks need (its block-wide reductions cost per warp).
+    // Grid = NB (in the graph key) >= n_ks.
     const int fin_threads = (int)std::min<uint32_t>(1024u, std::max<uint32_t>(64u, ((p.B + 1) / 2 + 31) & ~31u));
     switch (nb_for(p.n_ks)) {
-    case 1: k_finish<KM, 1><<<1, fin_threads, 0, s>>>(p, 0); break;
-    case 2: k_finish<KM, 2><<<1, fin_threads, 0, s>>>(p, 0); break;
-    case 4: k_finish<KM, 4><<<1, fin_threads, 0, s>>>(p, 0); break;
-    case 8: k_finish<KM, 8><<<1, fin_threads, 0, s>>>(p, 0); break;
-    default: k_finish<KM, 16><<<1, fin_threads, 0, s>>>(p, 0); break;
+    case 1: k_finish_j<KM><<<1, fin_threads, 0, s>>>(p, 0); break;
+    case 2: k_finish_j<KM><<<2, fin_threads, 0, s>>>(p, 0); break;
+    case 4: k_finish_j<KM><<<4, fin_threads, 0, s>>>(p, 0); break;
+    case 8: k_finish_j<KM><<<8, fin_threads, 0, s>>>(p, 0); break;
+    default: k_finish_j<KM><<<16, fin_threads, 0, s>>>(p, 0); break;
     }
     return launches + 2;
 }
