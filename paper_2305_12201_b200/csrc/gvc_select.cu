@@ -60,7 +60,8 @@ struct SelState {
     unsigned long long shortfall;
     JState js[GVC_MAX_LADDER];
     float redsync_mean[GVC_MAX_LADDER];
-    uint32_t fin_done;  // k_finish blocks done (the last one writes the status)
+    uint32_t fin_done;     // k_finish blocks done (the last one writes the status)
+    uint32_t sample_done;  // k_sample blocks done (the last one resolves key_est)
 };
 
 struct Plan {
@@ -191,6 +192,8 @@ __device__ __forceinline__ void load_cand4(const Plan &p, uint64_t beg, uint32_t
 // ------------------------------------------------------------------ sample
 // Strided chunks of 128 contiguous values -> 14-bit shared-memory histogram of
 // magnitude keys, merged into global memory once per block.  Reads ~1.5%.
+__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh);
+
 __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
 {
     extern __shared__ uint32_t sh[];
@@ -240,14 +243,24 @@ __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
         if (sh[i])
             atomicAdd(&p.shist[i], sh[i]);
+    // the last block to finish resolves key_est (no separate launch)
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        last = atomicAdd(&p.st->sample_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        sample_resolve_body(p, reinterpret_cast<unsigned long long *>(sh));
+    }
 }
 
 // Chooses key_est (a lower bound for the k_0-th largest key, w.h.p.) and the
 // level-0 bin shift.  Magnitude keys: from the sample histogram.  Hash keys:
 // from the binomial tail (host-computed).
-__global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
+__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh)
 {
-    __shared__ unsigned long long sh[33];
     SelState *st = p.st;
     if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
         if (threadIdx.x == 0) {
@@ -320,6 +333,12 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
         }
         acc += h[i];
     }
+}
+
+__global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
+{
+    __shared__ unsigned long long sh[33];
+    sample_resolve_body(p, sh);
 }
 
 // ----------------------------------------------------------------- collect
@@ -1742,10 +1761,12 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
         uint64_t wb = (p.s_chunks + 31) / 32;
         int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
-        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);
+        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);  // its last block resolves key_est
+        launches++;
+    } else {
+        k_sample_resolve<<<1, 1024, 0, s>>>(p, 0);
         launches++;
     }
-    k_sample_resolve<<<1, 1024, 0, s>>>(p, 0);
     {
         ProfScope pc(probes ? PROF_COLLECT : -1, s);
         if (gprobes)
@@ -1767,7 +1788,7 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     else
         k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     k_resolve0<<<1, 1024, 0, s>>>(p, 1);
-    launches += 5;
+    launches += 4;
     launch_tail<KM>(p, s);
     launches += 3;
     // k_finish_j: one block per ladder entry, 2 blocks per thread; only as many
@@ -1781,7 +1802,7 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     case 8: k_finish_j<KM><<<8, fin_threads, 0, s>>>(p, 0); break;
     default: k_finish_j<KM><<<16, fin_threads, 0, s>>>(p, 0); break;
     }
-    return launches + 2;
+    return launches + 1;
 }
 
 static_assert(sizeof(Plan) <= 4000, "the plan is passed as a kernel parameter");
