@@ -163,8 +163,20 @@ def ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _dev_index(device) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    if isinstance(device, int):
+        return device
+    idx = device.index
+    return torch.cuda.current_device() if idx is None else idx
+
+
 def stream_ptr(device=None):
-    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    """The current CUDA stream of ``device`` as a raw cudaStream_t (the fast
+    accessor: torch.cuda.current_stream() costs tens of microseconds of host
+    time per call in this torch build)."""
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(_dev_index(device)))
 
 
 class Workspace:
@@ -182,8 +194,14 @@ class Workspace:
         return buf
 
 
+_ws_bytes: dict = {}
+
+
 def select_workspace(device, slot: str, kind: int, n: int) -> torch.Tensor:
-    return Workspace.get(device, slot, int(load().gvc_select_workspace_bytes(kind, n)))
+    nb = _ws_bytes.get((kind, n))
+    if nb is None:
+        nb = _ws_bytes[(kind, n)] = int(load().gvc_select_workspace_bytes(kind, n))
+    return Workspace.get(device, slot, nb)
 
 
 PROF_CATS = ("collect", "select", "emit", "aggregate")
@@ -271,7 +289,12 @@ def d2h_start(t: torch.Tensor, ready: "torch.cuda.Event | None" = None) -> Pendi
     host, ev = buf
     side = side_stream(t.device)
     if ready is None:
-        ready = torch.cuda.Event()
+        # one reusable marker per device: the side stream's wait on it is
+        # enqueued before the next record can happen
+        rkey = ("ready", t.device.index)
+        ready = _pinned.get(rkey)
+        if ready is None:
+            ready = _pinned[rkey] = torch.cuda.Event()
         ready.record()
     side.wait_event(ready)
     with torch.cuda.stream(side):

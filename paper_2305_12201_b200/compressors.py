@@ -301,17 +301,21 @@ def aggregate_packed(idx: torch.Tensor, vals: torch.Tensor, counts: Sequence[int
     lib = nat.load()
     nparts = len(counts)
     if offs is None:
-        offs = np.zeros(nparts, dtype=np.uint64)
-        offs[1:] = np.cumsum(np.asarray(counts, dtype=np.uint64))[:-1]
-    else:
-        offs = np.asarray(offs, dtype=np.uint64)
-    cnts = np.asarray(counts, dtype=np.uint64)
+        offs, acc = [], 0
+        for c in counts:
+            offs.append(acc)
+            acc += int(c)
+    offs_c = (ctypes.c_uint64 * nparts)(*[int(o) for o in offs])
+    cnts_c = (ctypes.c_uint64 * nparts)(*[int(c) for c in counts])
     if out is None:
         out = torch.empty(n, dtype=torch.float32, device=dev)
-    ws = nat.Workspace.get(dev, "agg", int(lib.gvc_aggregate_workspace_bytes(nparts, n)))
-    nat.check(lib.gvc_aggregate(nat.ptr(idx), nat.ptr(vals), offs.ctypes.data_as(ctypes.c_void_p),
-                                cnts.ctypes.data_as(ctypes.c_void_p), nparts, n, nat.ptr(out), nat.ptr(ws),
-                                ws.numel(), nat.ptr(bounds), bounds_stride, nat.stream_ptr(dev)), "aggregate")
+    if bounds is None:  # the boundary pass needs scratch
+        ws = nat.Workspace.get(dev, "agg", int(lib.gvc_aggregate_workspace_bytes(nparts, n)))
+        ws_p, ws_n = nat.ptr(ws), ws.numel()
+    else:
+        ws_p, ws_n = None, 0
+    nat.check(lib.gvc_aggregate(nat.ptr(idx), nat.ptr(vals), offs_c, cnts_c, nparts, n, nat.ptr(out), ws_p,
+                                ws_n, nat.ptr(bounds), bounds_stride, nat.stream_ptr(dev)), "aggregate")
     return out
 
 
