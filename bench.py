@@ -35,15 +35,23 @@ sys.path.insert(0, ROOT)
 
 METRIC = "gradient GB/s compressed+allgathered per step, 1/2/4/8 B200; % of HBM roofline"
 WORKLOADS = {
-    # name: (M, theta_min, theta_s (candidate = theta_s * theta_min), extra CFs, description)
+    # name: (M, theta_min, theta_s (candidate = theta_s * theta_min), extra CFs, description[, compressor])
     "resnet101": (44_500_000, 10.0, 10.0, (1000.0,),
                   "ResNet101-size 44.5M fp32 gradient, GraVAC CF search {10,100,1000} with Top-k + EF, "
                   "sparse allgather + fp64 decompress-average (BASELINE configs[1])"),
     "vgg16": (138_000_000, 10.0, 10.0, (1000.0,),
               "VGG16-size 138M fp32 gradient, Top-k + EF + CF search {10,100,1000} (north-star size)"),
     "resnet18": (11_700_000, 100.0, 1.0, (), "ResNet-18-size 11.7M fp32 gradient, Top-k CF100 + EF + gain"),
+    "vgg16-dgc": (138_000_000, 10.0, 10.0, (), "VGG16-size 138M fp32 gradient, DGC sampled-threshold sparsify "
+                  "+ residual, CF {10, 100} (BASELINE configs[2])", "dgc"),
+    "lstm-redsync": (66_000_000, 10.0, 10.0, (), "LSTM-size 66M fp32 gradient, Redsync threshold search + EF, "
+                     "CF {10, 100} (BASELINE configs[3])", "redsync"),
+    "lstm-randomk": (66_000_000, 10.0, 10.0, (), "LSTM-size 66M fp32 gradient, Random-k (counter-based RNG) + EF, "
+                     "CF {10, 100} (BASELINE configs[3])", "randomk"),
 }
 EPSILON = 0.35  # fresh iid N(0,1) gradients give gain(CF10) ~= 0.42 -> the compressed CF10 branch is taken
+# per compressor: gains at CF10 on N(0,1) data are ~0.42 (Top-k, DGC), ~0.33 (Redsync), ~0.1 (Random-k)
+EPSILONS = {"topk": EPSILON, "dgc": EPSILON, "redsync": 0.25, "randomk": 0.05}
 
 
 def peaks():
@@ -135,19 +143,20 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU legs
-def oracle_step(O, g, r, M, theta_min, theta_s, extra, nworkers=1):
-    """One reference-algorithm step on the host: per worker EF, norm, Top-k at
-    theta_min, the ladder via compress_further (compressors.py:226-246), the
-    residual update, then aggregate() over the parts (simworkers.py:242-245)."""
+def oracle_step(O, g, r, M, theta_min, theta_s, extra, nworkers=1, kind="topk"):
+    """One reference-algorithm step on the host: per worker EF, norm, the
+    compressor at theta_min, the ladder via compress_further
+    (compressors.py:226-246), the residual update, then aggregate() over the
+    parts (simworkers.py:242-245)."""
     parts = []
     new_r = []
     for w in range(nworkers):
         ef = O.ef_add(g[w], r[w])
         norm = O.sq_norm(ef)
-        idx, vals, _ = O.compress("topk", ef, theta_min)
+        idx, vals, _ = O.compress(kind, ef, theta_min, seed=7, stream=w)
         gains = [O.sq_norm(vals) / norm]
         for step in (theta_s, *[c / theta_min for c in extra]):
-            _, v2, _ = O.compress_further("topk", idx, vals, M, step)
+            _, v2, _ = O.compress_further(kind, idx, vals, M, step, seed=7, stream=100 + w)
             gains.append(O.sq_norm(v2) / norm)
         new_r.append(O.update_residual(ef, idx, vals))
         parts.append((idx, vals))
@@ -167,10 +176,10 @@ def run_reference(args, M, theta_min, theta_s, extra, desc):
     r = [np.zeros(M, dtype=np.float32) for _ in range(world)]
     warm, steps = min(args.warmup, 1), min(args.steps, 3)
     for _ in range(warm):
-        r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world)
+        r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world, args.kind)
     t0 = time.perf_counter()
     for _ in range(steps):
-        r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world)
+        r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world, args.kind)
     dt = (time.perf_counter() - t0) / steps
     value = world * 4 * M / dt / 1e9
     sample = (f"{steps} timed full steps ({warm} warm-up) of the {M}-element workload, {world} simulated "
@@ -212,8 +221,8 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     def fresh():
         """A new iid N(0,1) gradient per step (drawn before the timed events)."""
         return gbuf.normal_(generator=gen)
-    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=max(1000.0, theta_min), epsilon=EPSILON,
-                             window=1 << 30, compressor=G.CompressorKind("topk"))
+    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=max(1000.0, theta_min), epsilon=EPSILONS[args.kind],
+                             window=1 << 30, compressor=G.CompressorKind(args.kind))
     state = G.ControllerState.fresh(cfg, world)
     state.theta_s = theta_s
     store = G.ResidualStore(M, device=dev)
@@ -391,8 +400,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: a fresh iid N(0,1) fp32 gradient per step and rank (drawn outside the timed events), "
                 "residual carried across steps",
-        "config": {"workload": desc, "M": M, "cf_ladder": [theta_min, theta_min * theta_s, *extra],
-                   "epsilon": EPSILON, "chosen_cf": {str(k): v for k, v in chosen.items()},
+        "config": {"workload": desc, "M": M, "compressor": args.kind,
+                   "cf_ladder": [theta_min, theta_min * theta_s, *extra],
+                   "epsilon": EPSILONS[args.kind], "chosen_cf": {str(k): v for k, v in chosen.items()},
                    "l2": "evicted before every timed step by reading a 256 MiB buffer (L2 126 MB), outside the timed events; inputs (178 MB each) exceed L2",
                    "parallelism": f"dp{world}"},
         "roofline": {"bound": "hbm", "kernel": "k_collect (fused EF add + fp64 norm + candidate compaction)",
@@ -421,11 +431,11 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         O.lib()
         gh = fresh().cpu().numpy()
         rh = np.zeros(M, dtype=np.float32)
-        oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra)  # warm
+        oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra, 1, args.kind)  # warm
         t0 = time.perf_counter()
         n_cpu = 2
         for _ in range(n_cpu):
-            rh = oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra)[0]
+            rh = oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra, 1, args.kind)[0]
         dt = (time.perf_counter() - t0) / n_cpu
         line["cpu_baseline"] = {"value": 4 * M / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
                                 "sample": f"{n_cpu} full steps of the same workload (C oracle, single thread)",
@@ -447,7 +457,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    M, theta_min, theta_s, extra, desc = WORKLOADS[args.workload]
+    M, theta_min, theta_s, extra, desc = WORKLOADS[args.workload][:5]
+    args.kind = WORKLOADS[args.workload][5] if len(WORKLOADS[args.workload]) > 5 else "topk"
     if args.impl == "reference":
         run_reference(args, M, theta_min, theta_s, extra, desc)
     else:
