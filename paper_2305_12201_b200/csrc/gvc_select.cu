@@ -264,11 +264,12 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh)
     SelState *st = p.st;
     if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
         if (threadIdx.x == 0) {
-            const uint32_t est = *p.key_est_dev;
-            st->key_est = est;
-            const uint64_t span = (1ull << 31) - (est < (1u << 31) ? est : (1u << 31) - 1);
-            int shf = bitlen64(span - 1) - 12;
-            st->shift0 = shf < 0 ? 0 : shf;
+            // the k-th largest key sits just above the sampled threshold: fine
+            // level-0 bins there (4096 keys, 1/2048 of an octave; the top bin is
+            // open-ended), so level 1 resolves it.  Bins sized to the whole key
+            // range instead left ~10^5 members for the single-block refinement.
+            st->key_est = *p.key_est_dev;
+            st->shift0 = 12;
         }
         return;
     }
@@ -687,6 +688,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         acc_c[b][threadIdx.x] = 0u;
     }
     uint32_t nan_any = 0;
+    uint32_t hc_bin = 0xffffffffu, hc_cnt = 0;  // level-1 histogram run-length cache
     // fast window (hi_0 - 1, lo_1): band 1, in no interval (empty when the
     // first two intervals touch)
     const uint32_t f_lo = him1[0];
@@ -748,8 +750,19 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
                         const bool inj = j < nks && d <= wm1[j];
                         in |= inj;
                         band += key[c] > him1[j];
-                        if (inj && act[j])
-                            atomicAdd(&p.histl[j * GVC_HL_BINS + (d >> sh[j])], 1u);
+                        if (inj && act[j]) {
+                            // run-length cache: tie-heavy inputs put every member
+                            // in one bin, and one global atomic per member then
+                            // serialises on a single address
+                            const uint32_t bin = j * GVC_HL_BINS + (d >> sh[j]);
+                            if (bin != hc_bin) {
+                                if (hc_cnt)
+                                    atomicAdd(&p.histl[hc_bin], hc_cnt);
+                                hc_bin = bin;
+                                hc_cnt = 0;
+                            }
+                            hc_cnt++;
+                        }
                     }
                     memb[c] = in;
                     if (!in) {
@@ -772,6 +785,13 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         }
         if (lane == 0)
             p.seg_mcnt[seg] = mcount;
+    }
+    // flush the histogram caches: lanes holding the same bin combine first
+    {
+        const unsigned same = __match_any_sync(0xffffffffu, hc_cnt ? hc_bin : 0xffffffffu);
+        const uint32_t tot = __reduce_add_sync(same, hc_cnt);
+        if (hc_cnt && (threadIdx.x & 31) == __ffs(same) - 1)
+            atomicAdd(&p.histl[hc_bin], tot);
     }
     // band 1 never reaches the shared accumulator when the fast window is
     // open, so this is the same fixed-order fp64 sum as before
