@@ -268,6 +268,12 @@ GVC_API void gvc_prof_enable(int on);
 GVC_API int gvc_prof_read(double *ms, unsigned long long *counts, int ncat);
 GVC_API unsigned long long gvc_launch_count(void);
 
+/* DGC's threshold sample (compressors.py:118; parity-unpinned):
+ * s ascending positions of [0, n), one per stratum [j n / s, (j + 1) n / s),
+ * at lo_j + floor(h_j * width_j / 2^32), h_j = Philox4x32-10 word 0 at
+ * counter (pos_base + lo_j, stream), key seed. */
+GVC_API int gvc_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t rng_stream, uint64_t pos_base,
+                           uint32_t *out_pos_dev, void *stream);
 /* DGC helpers (compressors.py:110-137).
  * gvc_gather_ef: out[i] = values at pos[i]: fl32(g + r_true) in EF mode (g_dev and
  *   resid_dev, with the deferred mask of gvc_select_args applied), else values_dev[pos[i]].

@@ -205,6 +205,23 @@ static int cmp_keypos(const void *a, const void *b)
 
 static int cmp_desc_u32(const void *a, const void *b) { return -cmp_u32(a, b); }
 
+/* DGC's threshold sample (compressors.py:118 draws s positions without
+ * replacement with numpy's Generator.choice; parity-unpinned):
+ * [0, n) is cut into s strata [floor(j n / s), floor((j + 1) n / s)) and
+ * stratum j contributes the position lo_j + floor(h_j * width_j / 2^32),
+ * h_j = Philox4x32-10 word 0 at counter (pos_base + lo_j, stream), key seed.
+ * Exactly s distinct, ascending positions; a stratified sample of the same
+ * size as the reference's simple random sample. */
+void orc_dgc_sample_positions(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
+                              uint32_t *out)
+{
+    for (uint64_t j = 0; j < s; j++) {
+        const uint64_t lo = j * n / s, hi = (j + 1) * n / s;
+        const uint32_t h = orc_position_hash(seed, stream, pos_base + lo);
+        out[j] = (uint32_t)(lo + (((uint64_t)h * (hi - lo)) >> 32));
+    }
+}
+
 /* compressors.py:110-137 with the counter-based sample (see header). */
 static int dgc_pick(const float *v, const uint32_t *mk, uint64_t n, uint64_t k, uint64_t seed,
                     uint64_t stream, uint64_t pos_base, double frac, uint32_t *out_idx)
@@ -215,16 +232,14 @@ static int dgc_pick(const float *v, const uint32_t *mk, uint64_t n, uint64_t k, 
         s = n;
     if (s >= n)
         return orc_select_keys(mk, n, k, out_idx);
-    /* sample = the s positions with the smallest hash (ties -> lower position) */
-    uint32_t *hk = (uint32_t *)malloc(n * sizeof(uint32_t));
+    /* sample = one position per stratum (orc_dgc_sample_positions) */
+    uint32_t *hk = (uint32_t *)malloc(1 * sizeof(uint32_t));
     uint32_t *samp = (uint32_t *)malloc(s * sizeof(uint32_t));
     uint32_t *sk = (uint32_t *)malloc(s * sizeof(uint32_t));
     uint8_t *picked = (uint8_t *)calloc(n, 1);
     if (!hk || !samp || !sk || !picked)
         return ORC_ERR_NOMEM;
-    for (uint64_t i = 0; i < n; i++)
-        hk[i] = ~orc_position_hash(seed, stream, pos_base + i);
-    orc_select_keys(hk, n, s, samp);
+    orc_dgc_sample_positions(n, s, seed, stream, pos_base, samp);
     for (uint64_t j = 0; j < s; j++)
         sk[j] = mk[samp[j]];
     qsort(sk, s, sizeof(uint32_t), cmp_desc_u32); /* np.sort(...)[::-1] */

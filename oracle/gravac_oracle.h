@@ -45,6 +45,8 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 
 /* Counter-based position hash used by Random-k and the DGC sample:
  * ctr = (lo(i), hi(i), lo(stream), hi(stream)), key = (lo(seed), hi(seed)) -> out[0]. */
+void orc_dgc_sample_positions(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
+                              uint32_t *out);
 uint32_t orc_position_hash(uint64_t seed, uint64_t stream, uint64_t i);
 
 /* feedback.py:32-36: out = fl32(g + r). */

@@ -303,6 +303,15 @@ int gvc_aggregate_peers_staged(const uint32_t *const *idx, const float *const *v
     return rc ? rc : check_launch("aggregate_peers_staged");
 }
 
+int gvc_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t rng_stream, uint64_t pos_base, uint32_t *out,
+                   void *stream)
+{
+    if (!out)
+        return set_error(GVC_ERR_ARG, "gvc_dgc_sample: null output");
+    int rc = dgc_sample_run(n, s, seed, rng_stream, pos_base, out, STREAM(stream));
+    return rc ? rc : check_launch("dgc_sample");
+}
+
 int gvc_tile_bounds(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, void *stream)
 {
     if (!idx || !bounds || n < 1 || k > n)

@@ -186,6 +186,31 @@ int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const 
 }
 
 // ------------------------------------------------------------ DGC helpers
+// DGC's threshold sample: one position per stratum [j n / s, (j + 1) n / s),
+// offset = Philox word 0 at counter (pos_base + lo_j, stream) scaled to the
+// stratum width (the C-ABI header states the definition).
+__global__ void k_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
+                             uint32_t *__restrict__ out)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < s; j += stride) {
+        const uint64_t lo = j * n / s, hi = (j + 1) * n / s;
+        const uint32_t h = philox_x0(pos_base + lo, stream, seed);
+        out[j] = (uint32_t)(lo + (((uint64_t)h * (hi - lo)) >> 32));
+    }
+}
+
+int dgc_sample_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base, uint32_t *out,
+                   cudaStream_t st)
+{
+    if (s < 1 || s > n)
+        return set_error(GVC_ERR_ARG, "dgc_sample: %llu samples of %llu positions", (unsigned long long)s,
+                         (unsigned long long)n);
+    count_launches(1);
+    k_dgc_sample<<<grid_for(s, 256, 148 * 8), 256, 0, st>>>(n, s, seed, stream, pos_base, out);
+    return GVC_OK;
+}
+
 __global__ void k_gather_ef(const uint32_t *__restrict__ pos, uint64_t k, const float *__restrict__ values,
                             const float *__restrict__ g, const float *__restrict__ resid, const uint32_t *pmask,
                             const float *pm_ptr, int pmode, float *__restrict__ out)

@@ -9,8 +9,9 @@ The reference:
   else: chosen + largest sampled below thr (ties -> lower index) + global top-up  :126-137
 
 This build composes it from the sm_100a primitives:
-  * the sample is the s smallest Philox position hashes (Random-k select over
-    the index space; see DESIGN.md for why it replaces numpy's choice);
+  * the sample is one counter-based (Philox) position per stratum of n / s
+    positions (gvc_dgc_sample; see DESIGN.md for why it replaces numpy's
+    choice);
   * g_ef at the sampled positions is gathered (EF applied on the fly);
   * thr is the exact rank-th largest sampled key (a Top-k select on s values);
   * ONE fused collect pass with the candidate threshold forced to thr yields
@@ -107,9 +108,10 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
         res = sel.result() if (check or want_result) else None
         return (idx, vals, res) if want_result else (idx, vals)
 
-    # sample positions: the s smallest position hashes (Random-k over the index space)
-    sel_s = Selection(CompressorKind("randomk"), [s], values=src, rng=rng, pos_base=pos_base, slot=slot + "s")
-    P, _ = sel_s.emit(0)
+    # sample positions: one per stratum of n / s positions (gvc_dgc_sample)
+    P = torch.empty(s, dtype=torch.int32, device=dev).view(torch.uint32)
+    nat.check(nat.load().gvc_dgc_sample(n, s, rng.seed if rng is not None else 0, rng.stream if rng is not None else 0,
+                                        pos_base, nat.ptr(P), nat.stream_ptr(dev)), "dgc_sample")
     vP = _gather(P, values=values, g=g, resid=resid, pending=pending)
     rank = min(s, max(1, int(round(k * s / n))))
     if rank < s:
