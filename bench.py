@@ -291,6 +291,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     # event-record nodes around k_collect (gvc_prof_enable(2)) -- the kernel's
     # duration inside the real step sequence, kept out of the headline loop
     timed_col = (0.0, 0)
+    timed_prof = None
     if timed_probe:
         nat.load().gvc_prof_enable(2)
         g = fresh()
@@ -303,7 +304,8 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
             cool()
             step(g)
         torch.cuda.synchronize()
-        timed_col = nat.prof_read()["collect"]
+        timed_prof = nat.prof_read()
+        timed_col = timed_prof["collect"]
         nat.prof_enable(False)
     # kernel-level probes: a separate pass of the same step with CUDA events
     # around the collect kernel / select / emit / average (the timed loop above
@@ -389,9 +391,16 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     col_bytes = 12 * M  # read g, read r, write g_ef: the algorithmic bytes of the fused EF pass
     achieved = col_bytes / (col_launch * 1e-3) / 1e9 if col_launch > 0 else None
     k1 = G.keep_count(M, theta_min)
-    sel_ms = prof["select"][0] / max(prof["select"][1], 1)
-    emit_ms = prof["emit"][0] / max(prof["emit"][1], 1)
-    agg_ms = prof["aggregate"][0] / max(prof["aggregate"][1], 1)
+    # stage times from the roofline loop (select: graph event nodes; emit and
+    # average: events around their direct launches) when present, else the
+    # probed pass
+    src = timed_prof if (timed_prof and timed_prof["select"][1]) else prof
+    sel_ms = src["select"][0] / max(src["select"][1], 1)
+    emit_ms = src["emit"][0] / max(src["emit"][1], 1)
+    agg_ms = src["aggregate"][0] / max(src["aggregate"][1], 1)
+    stage_note = ("select: CUDA event-record nodes around the select graph; emit / average: CUDA events around "
+                  "their launches; all inside the roofline loop of the real step" if src is timed_prof else
+                  "per-kernel CUDA events from a probed pass of the same step (direct launches)")
     comp_bytes = 12 * M + 8 * k1
     comp_achieved = comp_bytes / ((sel_ms + emit_ms) * 1e-3) / 1e9 if sel_ms > 0 else None
     line = {
@@ -415,8 +424,8 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         "compress_stage": {"what": "gvc_select (all kernels) + gvc_emit, algorithmic 12M + 8k bytes",
                            "ms": sel_ms + emit_ms, "achieved": comp_achieved,
                            "frac": comp_achieved / peak if comp_achieved else None},
-        "breakdown_ms": {"collect": probed_col, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms,
-                         "note": "per-kernel CUDA events from a probed pass of the same step (direct launches)"},
+        "breakdown_ms": {"collect": col_launch, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms,
+                         "collect_probed_pass": probed_col, "note": stage_note},
         "gpu_launches": int(launches),
         "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms),
                     "argmax": step_ms.index(max(step_ms))},

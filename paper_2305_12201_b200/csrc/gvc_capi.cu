@@ -48,7 +48,9 @@ static cudaEvent_t prof_event()
 ProfScope::ProfScope(int cat, cudaStream_t st) : slot(-1), s(st)
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    if (!g_prof_on || cat < 0)
+    // mode 2 (graph probes) still brackets the directly launched emit / average
+    const bool on = g_prof_on || (g_prof_graph && (cat == PROF_EMIT || cat == PROF_AGGREGATE));
+    if (!on || cat < 0)
         return;
     cudaEvent_t a = prof_event(), b = prof_event();
     cudaEventRecord(a, s);
@@ -78,12 +80,12 @@ bool prof_graph_enabled()
     return g_prof_graph && !g_prof_on;
 }
 
-void prof_graph_pair(cudaEvent_t *a, cudaEvent_t *b)
+void prof_graph_pair(int cat, cudaEvent_t *a, cudaEvent_t *b)
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     *a = prof_event();
     *b = prof_event();
-    g_prof_pending.push_back({PROF_COLLECT, {*a, *b}});
+    g_prof_pending.push_back({cat, {*a, *b}});
 }
 
 static int check_launch(const char *what)

@@ -23,7 +23,7 @@ struct ProfScope {
 void count_launches(int n);
 bool prof_enabled();
 bool prof_graph_enabled();
-void prof_graph_pair(cudaEvent_t *a, cudaEvent_t *b);
+void prof_graph_pair(int cat, cudaEvent_t *a, cudaEvent_t *b);
 
 size_t select_workspace_bytes(int kind, uint64_t n);
 int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,

@@ -1770,7 +1770,7 @@ static void set_attributes()
 
 // The select pipeline on stream s; every kernel takes the plan by value (its
 // fields live in the constant bank).  Returns the number of kernels.
-static cudaEvent_t g_ev_mark[2];  // capture-time placeholders of the collect event nodes
+static cudaEvent_t g_ev_mark[4];  // capture-time placeholders: collect start/end, select start/end
 
 template <int KM>
 static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gprobes)
@@ -1829,6 +1829,8 @@ static_assert(sizeof(Plan) <= 4000, "the plan is passed as a kernel parameter");
 
 static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *launches, bool gprobes = false)
 {
+    if (gprobes)
+        cudaEventRecordWithFlags(g_ev_mark[2], s, cudaEventRecordExternal);
     cudaMemsetAsync(p.st, 0, sizeof(SelState), s);
     cudaMemsetAsync(p.hist0, 0, GVC_H0_BINS * 4, s);
     cudaMemsetAsync(p.histl, 0, GVC_MAX_LADDER * GVC_HL_BINS * 4, s);
@@ -1836,6 +1838,8 @@ static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *laun
         cudaMemsetAsync(p.shist, 0, GVC_SAMPLE_BINS * 4, s);
     *launches = p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
                                      : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
+    if (gprobes)
+        cudaEventRecordWithFlags(g_ev_mark[3], s, cudaEventRecordExternal);
 }
 
 // CUDA graphs of the select pipeline, one per launch shape.  Every kernel has
@@ -1850,7 +1854,7 @@ struct GraphEntry {
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     std::vector<GraphNode> nodes;
-    cudaGraphNode_t ev_nodes[2] = {nullptr, nullptr};  // collect start / end (profiling graphs)
+    cudaGraphNode_t ev_nodes[4] = {nullptr, nullptr, nullptr, nullptr};  // g_ev_mark order (profiling graphs)
     int launches;
 };
 static std::unordered_map<std::string, GraphEntry> g_graphs;
@@ -1940,8 +1944,8 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             cudaGraph_t graph;
             GraphEntry ge;
             if (gprobes && !g_ev_mark[0]) {
-                cudaEventCreate(&g_ev_mark[0]);
-                cudaEventCreate(&g_ev_mark[1]);
+                for (int e = 0; e < 4; e++)
+                    cudaEventCreate(&g_ev_mark[e]);
             }
             cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
             enqueue_select(p, cs, false, &ge.launches, gprobes);
@@ -1958,7 +1962,9 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
                 if (ty == cudaGraphNodeTypeEventRecord) {
                     cudaEvent_t ev;
                     cudaGraphEventRecordNodeGetEvent(nd, &ev);
-                    ge.ev_nodes[ev == g_ev_mark[0] ? 0 : 1] = nd;
+                    for (int e = 0; e < 4; e++)
+                        if (ev == g_ev_mark[e])
+                            ge.ev_nodes[e] = nd;
                     continue;
                 }
                 if (ty != cudaGraphNodeTypeKernel)
@@ -1986,11 +1992,13 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             if (ue != cudaSuccess)
                 return set_error(GVC_ERR_CUDA, "select graph update: %s", cudaGetErrorString(ue));
         }
-        if (it->second.ev_nodes[0] && it->second.ev_nodes[1]) {
-            cudaEvent_t a, b;
-            prof_graph_pair(&a, &b);
-            cudaGraphExecEventRecordNodeSetEvent(it->second.exec, it->second.ev_nodes[0], a);
-            cudaGraphExecEventRecordNodeSetEvent(it->second.exec, it->second.ev_nodes[1], b);
+        for (int e = 0; e < 4; e += 2) {
+            if (it->second.ev_nodes[e] && it->second.ev_nodes[e + 1]) {
+                cudaEvent_t a, b;
+                prof_graph_pair(e == 0 ? PROF_COLLECT : PROF_SELECT, &a, &b);
+                cudaGraphExecEventRecordNodeSetEvent(it->second.exec, it->second.ev_nodes[e], a);
+                cudaGraphExecEventRecordNodeSetEvent(it->second.exec, it->second.ev_nodes[e + 1], b);
+            }
         }
         cudaGraphLaunch(it->second.exec, s);
         launches = it->second.launches;
