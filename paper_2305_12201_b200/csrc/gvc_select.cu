@@ -665,6 +665,9 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
     double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
     uint32_t(*acc_c)[GVC_THREADS] = reinterpret_cast<uint32_t(*)[GVC_THREADS]>(acc_a + (ABS ? NB + 1 : 0));
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][2][NB];
+    constexpr uint32_t P1_Q = 256;  // per-warp ring buffer of queued (slow-path) candidates
+    __shared__ float p1_qv[GVC_WARPS_PER_BLOCK][P1_Q];
+    __shared__ uint32_t p1_qk[GVC_WARPS_PER_BLOCK][P1_Q], p1_qt[GVC_WARPS_PER_BLOCK][P1_Q];
     const SelState *st = p.st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
@@ -701,6 +704,50 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         uint32_t *mem = p.mem_idx + beg;
         const uint32_t lt = lanemask_lt();
         uint32_t mcount = 0;
+        float *q_v = p1_qv[warp];
+        uint32_t *q_k = p1_qk[warp], *q_t = p1_qt[warp];
+        uint32_t qh = 0, qn = 0;  // ring buffer head / count (warp-uniform)
+        // classify queue entries qh .. qh + m - 1 (m <= 32), one per lane, in index order
+        auto classify = [&](uint32_t m) {
+            const bool okq = (uint32_t)lane < m;
+            const uint32_t e = (qh + lane) & (P1_Q - 1);
+            const float vq = okq ? q_v[e] : 0.f;
+            const uint32_t kq = okq ? q_k[e] : 0u;
+            const uint32_t tq = okq ? q_t[e] : 0u;
+            int band = 0;
+            bool in = false;
+#pragma unroll
+            for (int j = 0; j < NB; j++) {
+                const uint32_t d = kq - lo[j];
+                const bool inj = okq && j < nks && d <= wm1[j];
+                in |= inj;
+                band += kq > him1[j];
+                if (inj && act[j]) {
+                    // run-length cache: tie-heavy inputs put every member
+                    // in one bin, and one global atomic per member then
+                    // serialises on a single address
+                    const uint32_t bin = j * GVC_HL_BINS + (d >> sh[j]);
+                    if (bin != hc_bin) {
+                        if (hc_cnt)
+                            atomicAdd(&p.histl[hc_bin], hc_cnt);
+                        hc_bin = bin;
+                        hc_cnt = 0;
+                    }
+                    hc_cnt++;
+                }
+            }
+            if (okq && !in) {
+                acc_e[band][threadIdx.x] += (double)vq * (double)vq;
+                if (ABS)
+                    acc_a[band][threadIdx.x] += fabs((double)vq);
+                acc_c[band][threadIdx.x] += 1u;
+            }
+            const uint32_t mbq = __ballot_sync(0xffffffffu, okq && in);
+            if (okq && in)
+                mem[mcount + __popc(mbq & lt)] = tq;
+            mcount += __popc(mbq);
+            __syncwarp();
+        };
         // register double buffer: the next 128 candidates are in flight while
         // this group is classified (a warp walks ~8 groups back to back)
         float4 nfv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -727,62 +774,49 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
                 ok[c] = t + c < cnt;
                 key[c] = ok[c] ? cand_key<KM>(p, v[c], pos[c]) : 0u;
             }
-            bool memb[4];
-            uint32_t mb[4];
+            // fast window in registers; everything else (band 0, members,
+            // bands >= 2: ~12% at CF 10) is queued in index order and
+            // classified 32 at a time, so the NB-way classification runs on
+            // full warps instead of as predicated code under every candidate
+            bool slow[4];
+            uint32_t sbal[4];
 #pragma unroll
             for (int c = 0; c < 4; c++) {
                 if (KM == KEY_MAG)
                     nan_any |= (uint32_t)(ok[c] && key[c] > 0x7f800000u);
-                memb[c] = false;
-                if (ok[c] && key[c] > f_lo && key[c] < f_hi) {
+                const bool fast = ok[c] && key[c] > f_lo && key[c] < f_hi;
+                if (fast) {
                     // the common case: above threshold 0, below interval 1 ->
                     // band 1, not a member; accumulated in registers
                     e_b1 += (double)v[c] * (double)v[c];
                     if (ABS)
                         a_b1 += fabs((double)v[c]);
                     c_b1 += 1u;
-                } else if (ok[c]) {
-                    int band = 0;
-                    bool in = false;
-#pragma unroll
-                    for (int j = 0; j < NB; j++) {
-                        const uint32_t d = key[c] - lo[j];
-                        const bool inj = j < nks && d <= wm1[j];
-                        in |= inj;
-                        band += key[c] > him1[j];
-                        if (inj && act[j]) {
-                            // run-length cache: tie-heavy inputs put every member
-                            // in one bin, and one global atomic per member then
-                            // serialises on a single address
-                            const uint32_t bin = j * GVC_HL_BINS + (d >> sh[j]);
-                            if (bin != hc_bin) {
-                                if (hc_cnt)
-                                    atomicAdd(&p.histl[hc_bin], hc_cnt);
-                                hc_bin = bin;
-                                hc_cnt = 0;
-                            }
-                            hc_cnt++;
-                        }
-                    }
-                    memb[c] = in;
-                    if (!in) {
-                        acc_e[band][threadIdx.x] += (double)v[c] * (double)v[c];
-                        if (ABS)
-                            acc_a[band][threadIdx.x] += fabs((double)v[c]);
-                        acc_c[band][threadIdx.x] += 1u;
-                    }
                 }
-                mb[c] = __ballot_sync(0xffffffffu, memb[c]);
+                slow[c] = ok[c] && !fast;
+                sbal[c] = __ballot_sync(0xffffffffu, slow[c]);
             }
-            uint32_t o = mcount + __popc(mb[0] & lt) + __popc(mb[1] & lt) + __popc(mb[2] & lt) + __popc(mb[3] & lt);
+            uint32_t o = qh + qn + __popc(sbal[0] & lt) + __popc(sbal[1] & lt) + __popc(sbal[2] & lt) +
+                         __popc(sbal[3] & lt);
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                if (memb[c])
-                    mem[o] = t + c;
-                o += memb[c];
+                if (slow[c]) {
+                    q_v[o & (P1_Q - 1)] = v[c];
+                    q_k[o & (P1_Q - 1)] = key[c];
+                    q_t[o & (P1_Q - 1)] = t + c;
+                    o++;
+                }
             }
-            mcount += __popc(mb[0]) + __popc(mb[1]) + __popc(mb[2]) + __popc(mb[3]);
+            qn += __popc(sbal[0]) + __popc(sbal[1]) + __popc(sbal[2]) + __popc(sbal[3]);
+            __syncwarp();
+            while (qn >= 32) {
+                classify(32);
+                qh += 32;
+                qn -= 32;
+            }
         }
+        if (qn)
+            classify(qn);
         if (lane == 0)
             p.seg_mcnt[seg] = mcount;
     }
