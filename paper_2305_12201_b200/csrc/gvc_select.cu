@@ -1022,284 +1022,6 @@ __global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan p, int)
     }
 }
 
-// K-wide versions of the block reductions: every ladder entry / band is
-// reduced in the same barrier phase (one block of 1024 threads).
-template <int K>
-__device__ __forceinline__ void block_sum_vec(double (&v)[K], double *sh /* 33*K */)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int k = 0; k < K; k++)
-        v[k] = warp_sum_f64(v[k]);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < K; k++)
-            sh[warp * K + k] = v[k];
-    }
-    __syncthreads();
-    if (threadIdx.x < K) {
-        const int nwarps = (int)(blockDim.x >> 5);
-        double r = 0.0;
-        for (int w = 0; w < nwarps; w++)
-            r += sh[w * K + threadIdx.x];
-        sh[32 * K + threadIdx.x] = r;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; k++)
-        v[k] = sh[32 * K + k];
-    __syncthreads();
-}
-
-template <int K>
-__device__ __forceinline__ void block_excl_prefix_vec(unsigned long long (&v)[K], unsigned long long (&tot)[K],
-                                                      unsigned long long *sh /* 33*K */)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long x[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        x[k] = v[k];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long y = __shfl_up_sync(0xffffffffu, x[k], o);
-            if (lane >= o)
-                x[k] += y;
-        }
-    }
-    if (lane == 31) {
-#pragma unroll
-        for (int k = 0; k < K; k++)
-            sh[warp * K + k] = x[k];
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const int nwarps = (int)(blockDim.x >> 5);
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            unsigned long long w = lane < nwarps ? sh[lane * K + k] : 0ull, wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o)
-                    wi += y;
-            }
-            if (lane < nwarps)
-                sh[lane * K + k] = wi - w;
-            if (lane == 31)
-                sh[32 * K + k] = wi;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        tot[k] = sh[32 * K + k];
-        v[k] = sh[warp * K + k] + x[k] - v[k];
-    }
-    __syncthreads();
-}
-
-// Gains, tie cut and per-block output offsets for every ladder entry (one
-// block; all entries reduced together, ~10 barrier phases in total).
-template <int KM, int NB>
-__global__ void __launch_bounds__(1024) k_finish(const Plan p, int)
-{
-    constexpr int PER = GVC_BLK_MAX / 1024;  // 2 blocks per thread, contiguous
-    __shared__ unsigned long long shu[33 * NB];
-    __shared__ double shd[33 * (2 * NB + 1)];
-    __shared__ uint32_t part_blk[NB];
-    __shared__ unsigned long long part_take[NB];
-    SelState *st = p.st;
-    gvc_select_result *res = p.res;
-    const uint32_t B = p.B;
-    const int nks = p.n_ks;
-    const int t = threadIdx.x;
-    uint32_t T[NB];
-    unsigned long long q[NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        T[j] = j < nks ? (uint32_t)st->js[j].lo : 0xffffffffu;
-        q[j] = j < nks ? st->js[j].need : 0ull;
-    }
-    // ---- one load phase: this thread's 2 blocks, every band / entry
-    double nrm = 0.0;
-    double be[NB], ba[NB], te[NB], ta[NB];
-    uint32_t bc[PER][NB], tc[PER][NB];
-    double tie_e2[PER][NB], tie_ab[PER][NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        be[j] = ba[j] = te[j] = ta[j] = 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < PER; i++) {
-        const uint32_t b = t * PER + i;
-        const bool ok = b < B;
-        nrm += ok ? p.blk_norm[b] : 0.0;
-#pragma unroll
-        for (int j = 0; j < NB; j++) {
-            const bool okj = ok && j < nks;
-            const size_t o = (size_t)j * GVC_BLK_MAX + b;
-            bc[i][j] = okj ? p.blk_band_cnt[o] : 0u;
-            tc[i][j] = okj ? p.blk_tie_cnt[o] : 0u;
-            be[j] += okj ? p.blk_band_e2[o] : 0.0;
-            ba[j] += okj ? p.blk_band_ab[o] : 0.0;
-            tie_e2[i][j] = okj ? p.blk_tie_e2[o] : 0.0;
-            tie_ab[i][j] = okj ? p.blk_tie_ab[o] : 0.0;
-        }
-    }
-    // ---- totals: norm and per-band energies / |v| sums
-    double sums[2 * NB + 1];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        sums[j] = be[j];
-        sums[NB + j] = ba[j];
-    }
-    sums[2 * NB] = nrm;
-    block_sum_vec<2 * NB + 1>(sums, shd);
-    unsigned long long cnt[NB], cnt_tot[NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++)
-        cnt[j] = (unsigned long long)bc[0][j] + (PER > 1 ? bc[PER - 1][j] : 0u);
-    block_excl_prefix_vec<NB>(cnt, cnt_tot, shu);  // only the totals are used
-    // ---- tie cut per entry: exclusive prefix of per-block tie counts
-    unsigned long long tp[NB], tp_tot[NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++)
-        tp[j] = (unsigned long long)tc[0][j] + (PER > 1 ? tc[PER - 1][j] : 0u);
-    if (t < NB)
-        part_blk[t] = 0xffffffffu;
-    block_excl_prefix_vec<NB>(tp, tp_tot, shu);
-    unsigned long long sel[PER][NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        unsigned long long before = tp[j];
-#pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const uint32_t b = t * PER + i;
-            const unsigned long long c = tc[i][j];
-            const unsigned long long tk = before >= q[j] ? 0 : (q[j] - before < c ? q[j] - before : c);
-            before += c;
-            if (b < B && j < nks) {
-                p.blk_take[(size_t)j * GVC_BLK_MAX + b] = (uint32_t)tk;
-                if (tk == c && tk > 0) {
-                    te[j] += tie_e2[i][j];
-                    ta[j] += tie_ab[i][j];
-                }
-                if (tk > 0 && tk < c) {
-                    part_blk[j] = b;
-                    part_take[j] = tk;
-                }
-            }
-            unsigned long long s_ = tk;
-#pragma unroll
-            for (int band = 0; band < NB; band++)
-                if (band >= j)
-                    s_ += bc[i][band];
-            sel[i][j] = (b < B && j < nks) ? s_ : 0ull;
-        }
-    }
-    __syncthreads();
-    // ---- the (rare) partially-taken block of an entry: first part_take ties in index order
-    for (int j = 0; j < nks; j++) {
-        if (part_blk[j] == 0xffffffffu)
-            continue;  // uniform
-        unsigned long long seen = 0;
-        const uint32_t pb = part_blk[j];
-        const uint32_t s_end = min(p.S, (pb + 1) * GVC_WARPS_PER_BLOCK);
-        for (uint32_t sg = pb * GVC_WARPS_PER_BLOCK; sg < s_end; sg++) {
-            const uint64_t beg = (uint64_t)sg * p.seg_len;
-            const uint32_t cn = p.seg_cnt[sg];
-            for (uint32_t base = 0; base < cn; base += blockDim.x) {
-                const uint32_t tt = base + t;
-                bool is_tie = false;
-                float v = 0.f;
-                if (tt < cn) {
-                    v = p.cand_val[beg + tt];
-                    uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + tt]);
-                    is_tie = key == T[j];
-                }
-                unsigned long long tot;
-                unsigned long long rank = seen + block_excl_prefix(is_tie ? 1ull : 0ull, shu, &tot);
-                if (is_tie && rank < part_take[j]) {
-#pragma unroll
-                    for (int jj = 0; jj < NB; jj++)
-                        if (jj == j) {
-                            te[jj] += (double)v * (double)v;
-                            ta[jj] += fabs((double)v);
-                        }
-                }
-                seen += tot;
-            }
-        }
-    }
-    double tsum[2 * NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        tsum[j] = te[j];
-        tsum[NB + j] = ta[j];
-    }
-    block_sum_vec<2 * NB>(tsum, shd);
-    // ---- per-block output offsets for every entry
-    unsigned long long so[NB], so_tot[NB];
-#pragma unroll
-    for (int j = 0; j < NB; j++)
-        so[j] = sel[0][j] + (PER > 1 ? sel[PER - 1][j] : 0ull);
-    block_excl_prefix_vec<NB>(so, so_tot, shu);
-#pragma unroll
-    for (int j = 0; j < NB; j++) {
-        unsigned long long off = so[j];
-#pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const uint32_t b = t * PER + i;
-            if (b < B && j < nks)
-                p.blk_off[(size_t)j * GVC_BLK_MAX + b] = (uint32_t)off;
-            off += sel[i][j];
-        }
-    }
-    if (t == 0) {
-        unsigned bad = 0;
-#pragma unroll
-        for (int j = 0; j < NB; j++) {
-            if (j >= nks)
-                continue;
-            double e_above = 0.0, a_above = 0.0;
-            unsigned long long c_above = 0;
-#pragma unroll
-            for (int band = 0; band < NB; band++) {
-                if (band >= j && band < nks) {
-                    e_above += sums[band];
-                    a_above += sums[NB + band];
-                    c_above += cnt_tot[band];
-                }
-            }
-            const unsigned long long k = p.ks[j] - (j == 0 ? st->shortfall : 0ull);
-            const double A = a_above + tsum[NB + j];
-            double E = e_above + tsum[j];
-            const float m = (float)(A / (double)k);
-            const unsigned long long nnz = k - ((KM == KEY_MAG && T[j] == 0u) ? q[j] : 0ull);
-            if (p.kind == GVC_REDSYNC)
-                E = (double)nnz * ((double)m * (double)m);
-            st->redsync_mean[j] = m;
-            res->kept_sq[j] = E;
-            res->kept_abs[j] = A;
-            res->threshold_key[j] = T[j];
-            res->tie_quota[j] = q[j];
-            res->redsync_mean[j] = m;
-            res->kept_count[j] = so_tot[j];
-            res->kept_nonzero[j] = nnz;
-            if (c_above + q[j] != k || so_tot[j] != k)
-                bad = 1;
-        }
-        if (bad)
-            st->nan_flag |= 2u;  // internal consistency failure
-        res->ef_norm_sq = sums[2 * NB];
-        res->candidates = st->cand_total;
-        res->status = (st->nan_flag & 1u) ? GVC_ERR_NAN : ((st->nan_flag & 2u) ? GVC_ERR_STATE : GVC_OK);
-        res->fallback_used = (int)st->fallback;
-        res->shortfall = st->shortfall;
-    }
-}
-
 // k_finish, one block per ladder entry j (the entries are independent):
 // tie cut for T_j (lowest-index ties via the per-block prefix), kept energy
 // and |v| sum (gain numerator, Redsync mean), per-block output offsets.  Two
