@@ -403,6 +403,20 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
                   "per-kernel CUDA events from a probed pass of the same step (direct launches)")
     comp_bytes = 12 * M + 8 * k1
     comp_achieved = comp_bytes / ((sel_ms + emit_ms) * 1e-3) / 1e9 if sel_ms > 0 else None
+    # exchange (N > 1): every rank receives the other ranks' 8k-byte payloads;
+    # the fused kernel's time (signal + pull + decompress-average) against the
+    # NVLink 5 per-direction peak
+    nvlink = None
+    if world > 1 and agg_ms > 0:
+        kc = max(chosen, key=chosen.get) if chosen else theta_min
+        ksent = int(M // kc)
+        recv = (world - 1) * 8 * ksent
+        nv_ach = recv / (agg_ms * 1e-3) / 1e9
+        nvlink = {"what": "fused exchange: flag signal + staged NVLink pull of the peers' (idx, val) payloads + "
+                          "fp64 decompress-average, one kernel (time includes the merge)",
+                  "bytes_received_per_rank": recv, "ms": agg_ms, "achieved": nv_ach, "peak": 900.0,
+                  "peak_kind": "NVLink 5 per-direction spec", "unit": "GB/s", "frac": nv_ach / 900.0,
+                  "measured_p2p_read_GBps": 560}
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -424,6 +438,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         "compress_stage": {"what": "gvc_select (all kernels) + gvc_emit, algorithmic 12M + 8k bytes",
                            "ms": sel_ms + emit_ms, "achieved": comp_achieved,
                            "frac": comp_achieved / peak if comp_achieved else None},
+        "nvlink": nvlink,
         "breakdown_ms": {"collect": col_launch, "select_total": sel_ms, "emit": emit_ms, "aggregate": agg_ms,
                          "collect_probed_pass": probed_col, "note": stage_note},
         "gpu_launches": int(launches),
