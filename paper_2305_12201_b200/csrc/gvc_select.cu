@@ -1654,8 +1654,8 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.res = res;
     const uint64_t n = a->n, k0 = a->ks[0];
     if (p.keymode == KEY_MAG) {
-        // sample ~n/64 values in 128-value chunks (everything when n is small)
-        uint64_t want = n <= 65536 ? n : (n / 64 > 65536 ? n / 64 : 65536);
+        // sample ~n/128 values in 128-value chunks (everything when n is small)
+        uint64_t want = n <= 65536 ? n : (n / 128 > 65536 ? n / 128 : 65536);
         uint64_t chunks = (want + 127) / 128;
         uint64_t stride = n / chunks;
         stride &= ~(uint64_t)3;
