@@ -32,8 +32,9 @@ M = int(os.environ.get("GVC_M", "44500000"))
 gen = torch.Generator(device=dev)
 gen.manual_seed(1000 * rank + 1)
 g = torch.empty(M, device=dev)
+KIND = os.environ.get("GVC_KIND", "topk")
 cfg = G.ControllerConfig(theta_min=10.0, theta_max=1000.0, epsilon=0.35, window=1 << 30,
-                         compressor=G.CompressorKind("topk"))
+                         compressor=G.CompressorKind(KIND))
 state = G.ControllerState.fresh(cfg, world)
 state.theta_s = 10.0
 store = G.ResidualStore(M, device=dev)
@@ -50,8 +51,10 @@ for it in range(60):
         dist.barrier()
     CT.TIMELINE = [] if it >= 10 else None
     h0 = time.perf_counter()
-    G.run_iteration(state, G.GradientVector._wrap(g), store, cost, rng, extra_cfs=(1000.0,), group=pg,
-                    average=True, average_out=avg)
+    if CT.TIMELINE is not None:
+        CT._mark("step")
+    G.run_iteration(state, G.GradientVector._wrap(g), store, cost, rng, extra_cfs=(1000.0,) if KIND == "topk" else (),
+                    group=pg, average=True, average_out=avg)
     torch.cuda.synchronize()
     if CT.TIMELINE:
         t0 = CT.TIMELINE[0][1]
