@@ -1257,11 +1257,20 @@ struct Mirrors {
     uint32_t *tb[GVC_MAX_PEERS];
 };
 
-template <int KM, bool SMEM_MASK>
+// LEAN: the hot level-1 emit (no idx_map, no direct residual, no Redsync
+// substitution, no statistics, no mirrors) compiled without those paths --
+// uniform runtime flags still cost predicated instructions per candidate.
+template <int KM, bool SMEM_MASK, bool LEAN = false>
 __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint32_t *idx_map, uint32_t *out_idx,
                                                       float *out_val, float *resid, uint32_t *smask, float *sm_out,
                                                       uint32_t *tile_b, Mirrors mir, int want_stats)
 {
+    if (LEAN) {
+        idx_map = nullptr;
+        resid = nullptr;
+        mir.n = 0;
+        want_stats = 0;
+    }
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
     extern __shared__ uint32_t mwords[];  // [8][seg_len / 32] when SMEM_MASK
     const uint32_t nwords = p.seg_len >> 5;
@@ -1277,7 +1286,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
     const SelState *st = p.st;
     const uint32_t T = (uint32_t)st->js[j].lo;
     const float m = st->redsync_mean[j];
-    const bool redsync = p.kind == GVC_REDSYNC;
+    const bool redsync = !LEAN && p.kind == GVC_REDSYNC;
     const int nks = p.n_ks;
     // per-segment counts of this block in lanes 0..7
     uint32_t my_tie = 0, my_above = 0;
@@ -1384,21 +1393,23 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                     const uint32_t gi = idx_map ? idx_map[pos[c]] : pos[c];
                     out_idx[w] = gi;
                     out_val[w] = sv;
-                    for (int q = 0; q < mir.n; q++) {
-                        mir.idx[q][w] = gi;
-                        mir.val[q][w] = sv;
+                    if (!LEAN) {
+                        for (int q = 0; q < mir.n; q++) {
+                            mir.idx[q][w] = gi;
+                            mir.val[q][w] = sv;
+                        }
                     }
                     if (SMEM_MASK)
                         atomicOr(&mw[(pos[c] - (uint32_t)beg) >> 5], 1u << (pos[c] & 31));
                     else if (smask)
                         atomicOr(&smask[gi >> 5], 1u << (gi & 31));
-                    if (resid) {
+                    if (!LEAN && resid) {
                         // level-1 emits: the candidate value IS g_ef; a second-level
                         // emit (idx_map) carries level-1 SENT values, so read g_ef back
                         const float ef = idx_map ? resid[gi] : v[c];
                         resid[gi] = __fsub_rn(ef, sv);
                     }
-                    if (want_stats) {
+                    if (!LEAN && want_stats) {
                         e2 += (double)sv * (double)sv;
                         ab += fabs((double)sv);
                     }
@@ -1800,9 +1811,14 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         if (!attr) {
             cudaFuncSetAttribute(k_emit<KEY_MAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(k_emit<KEY_MAG, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             attr = true;
         }
-        if (p.keymode == KEY_MAG)
+        const bool lean = !idx_map && !resid && mir.n == 0 && !stats && p.kind != GVC_REDSYNC;
+        if (p.keymode == KEY_MAG && lean)
+            k_emit<KEY_MAG, true, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
+                                                                             smask, sm_out, tile_b, mir, 0);
+        else if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
                                                                        sm_out, tile_b, mir, stats != nullptr);
         else
