@@ -382,9 +382,12 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // `values`.  REFILL re-collects from the already-written g_ef with key_est = 0
 // (exactness fallback).  NaN keys are always candidates and are flagged by the
 // candidate passes, not here.
-template <int KM, bool EF, int PM>
-__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int refill)
+template <int KM, bool EF, int PM, bool REFILL = false>
+__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int)
 {
+    // compile-time: a runtime flag would leave predicated refill / no-refill
+    // code under every value of the hot loop
+    constexpr bool refill = REFILL;
     __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
     if (refill && !p.st->fallback)
@@ -1571,9 +1574,9 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     }
     k_resolve0<<<1, 1024, 0, s>>>(p, 0);
     if (p.ef)
-        k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
+        k_collect<KM, true, 0, true><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     else
-        k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
+        k_collect<KM, false, 0, true><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
     k_resolve0<<<1, 1024, 0, s>>>(p, 1);
     launches += 4;
     launch_tail<KM>(p, s);
