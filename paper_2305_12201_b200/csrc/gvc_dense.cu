@@ -711,28 +711,33 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
         // every entry of every part in flight before the first store
         uint32_t r[NP][U];
         float v[NP][U];
+        // per part: this thread's first entry and how many it may take
+        // (pointers formed once; the U loads use immediate offsets)
+        int left[NP];
 #pragma unroll
         for (int q = 0; q < NP; q++) {
+            left[q] = 0;
             if (q < nparts) {
-                const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
+                const uint32_t a = s_a[q] + threadIdx.x;
+                left[q] = (int)s_b[q] - (int)a;
+                const uint32_t *pi = parts.idx[q] + a;
+                const float *pv = parts.vals[q] + a;
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    if (a + u * AGG_THREADS < b) {
-                        r[q][u] = __ldcg(parts.idx[q] + a + u * AGG_THREADS) - (uint32_t)lo;
-                        v[q][u] = __ldcg(parts.vals[q] + a + u * AGG_THREADS);
+                    if (u * AGG_THREADS < left[q]) {
+                        r[q][u] = __ldcg(pi + u * AGG_THREADS) - (uint32_t)lo;
+                        v[q][u] = __ldcg(pv + u * AGG_THREADS);
                     }
                 }
             }
         }
 #pragma unroll
         for (int q = 0; q < NP; q++) {
-            if (q < nparts) {
-                const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
+            float *tq = tiles + q * AGG_TILE;
 #pragma unroll
-                for (int u = 0; u < U; u++)
-                    if (a + u * AGG_THREADS < b)
-                        tiles[q * AGG_TILE + r[q][u]] = v[q][u];
-            }
+            for (int u = 0; u < U; u++)
+                if (u * AGG_THREADS < left[q])
+                    tq[r[q][u]] = v[q][u];
         }
     } else {
         for (int q = 0; q < nparts; q++) {
