@@ -583,17 +583,20 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
         if (maxlen <= U * AGG_THREADS) {
             uint32_t r[NP][U];
             float v[NP][U];
+            int left[NP];
 #pragma unroll
             for (int q = 0; q < NP; q++) {
+                left[q] = 0;
                 if (q < np) {
-                    const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
-                    const uint32_t *pi = parts.idx[p0 + q];
-                    const float *pv = parts.vals[p0 + q];
+                    const uint32_t a = s_a[q] + threadIdx.x;
+                    left[q] = (int)s_b[q] - (int)a;
+                    const uint32_t *pi = parts.idx[p0 + q] + a;
+                    const float *pv = parts.vals[p0 + q] + a;
 #pragma unroll
                     for (int u = 0; u < U; u++) {
-                        if (a + u * AGG_THREADS < b) {
-                            r[q][u] = __ldcg(pi + a + u * AGG_THREADS) - (uint32_t)lo;
-                            v[q][u] = __ldcg(pv + a + u * AGG_THREADS);
+                        if (u * AGG_THREADS < left[q]) {
+                            r[q][u] = __ldcg(pi + u * AGG_THREADS) - (uint32_t)lo;
+                            v[q][u] = __ldcg(pv + u * AGG_THREADS);
                         }
                     }
                 }
@@ -601,10 +604,9 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
 #pragma unroll
             for (int q = 0; q < NP; q++) {
                 if (q < np) {
-                    const uint32_t a = s_a[q] + threadIdx.x, b = s_b[q];
 #pragma unroll
                     for (int u = 0; u < U; u++)
-                        if (a + u * AGG_THREADS < b)
+                        if (u * AGG_THREADS < left[q])
                             put(r[q][u], v[q][u]);
                     if (MODE == 2)
                         __syncthreads();  // worker order per position (compressors.py:266-269)
