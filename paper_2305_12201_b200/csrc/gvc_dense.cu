@@ -1,7 +1,6 @@
 // gvc_dense.cu -- dense-side kernels of the GraVAC step (sm_100a):
 // error-feedback add, fp64 norm, residual scatter, decompress and the
 // shared-memory-tiled fp64 decompress-average of N sparse parts.
-#include <cstdlib>
 
 #include "gvc_common.cuh"
 #include "gvc_internal.h"
@@ -908,22 +907,7 @@ static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *
     memset(&none, 0, sizeof(none));
     const Staged &st = staged ? *staged : none;
     const unsigned gs = g + (unsigned)st.ncopy;
-    // 3-4 parts: per-part fp32 tiles (64 KB smem) or the single fp64 tile;
-    // GVC_K7_PART4=1 selects the former (measurement switch)
-    static const bool part4 = getenv("GVC_K7_PART4") && getenv("GVC_K7_PART4")[0] == '1';
-    if (part4) {
-        static bool attr = false;
-        if (!attr) {
-            attr = true;
-            cudaFuncSetAttribute(k_tile_part<1, true, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (int)sm1);
-            cudaFuncSetAttribute(k_tile_part<1, false, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (int)sm1);
-        }
-    }
-    if (staged && part4 && nparts > 2 && nparts <= 4) {
-        k_tile_part<1, true, 4, true><<<gs, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch, st);
-    } else if (!staged && !flags && avg && part4 && nparts > 2 && nparts <= 4) {
-        k_tile_part<1, false, 4, false><<<g, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, nullptr, 0, st);
-    } else if (staged) {
+    if (staged) {
         if (nparts <= 2)
             k_tile_part<1, true, 2, true><<<gs, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch, st);
         else if (nparts <= 4)
