@@ -1668,8 +1668,12 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.res = res;
     const uint64_t n = a->n, k0 = a->ks[0];
     if (p.keymode == KEY_MAG) {
-        // sample ~n/128 values in 128-value chunks (everything when n is small)
+        // sample ~n/128 values (at most 2^19) in 128-value chunks (everything
+        // when n is small): past ~10^5 sampled candidates the 5-sigma margin is
+        // already a few tenths of a percent of k_0, and the sample pass is pure latency
         uint64_t want = n <= 65536 ? n : (n / 128 > 65536 ? n / 128 : 65536);
+        if (want > (1ull << 19))
+            want = 1ull << 19;
         uint64_t chunks = (want + 127) / 128;
         uint64_t stride = n / chunks;
         stride &= ~(uint64_t)3;
