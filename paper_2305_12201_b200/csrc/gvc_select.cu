@@ -382,6 +382,148 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // `values`.  REFILL re-collects from the already-written g_ef with key_est = 0
 // (exactness fallback).  NaN keys are always candidates and are flagged by the
 // candidate passes, not here.
+// One warp's pass over segment `seg` (k_collect's body; also the inline
+// exactness refill of k_resolve0).  Adds the warp's fp64 squares to nacc.
+template <int KM, bool EF, int PM, bool REFILL>
+__device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int lane, uint32_t *h, uint32_t dummy,
+                                                uint32_t key_est, int shift0, float pm, double &nacc)
+{
+    constexpr bool refill = REFILL;
+    const bool do_ef = EF && !refill;
+    const uint64_t beg = (uint64_t)seg * p.seg_len;
+    const uint32_t len = (uint32_t)(min(p.n, beg + p.seg_len) - beg);
+    const float *src = (EF ? (refill ? p.resid : p.g) : p.values) + beg;
+    float *rp = p.resid + beg;
+    const uint32_t *mp = p.pmask + (beg >> 5);
+    float *cval = p.cand_val + beg;
+    uint32_t *cidx = p.cand_idx + beg;
+    uint32_t ccount = 0;
+    uint32_t i = 0;
+#if GVC_COLLECT_PREFETCH
+    // software pipeline over 256-value steps: the next step's g / r loads are
+    // in flight while this step is added, reduced and compacted
+    constexpr uint32_t STEP = 256;
+    const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
+    float4 a[2], b[2];
+    // the step's 8 pending-mask words (lanes 0..7), prefetched with the data:
+    // a mask load issued at its use was the kernel's top stall (ncu)
+    uint32_t wreg = 0u;
+    if (nfull) {
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            a[u] = ld_stream(reinterpret_cast<const float4 *>(src + u * 128) + lane);
+            if (do_ef)
+                b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + u * 128) + lane);
+        }
+        if (do_ef && PM && lane < 8)
+            wreg = mp[lane];
+    }
+    for (; i < nfull; i += STEP) {
+        float4 na[2], nb[2];
+        uint32_t nw = 0u;
+        const bool more = i + STEP < nfull;
+        if (more) {
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                na[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + STEP + u * 128) + lane);
+                if (do_ef)
+                    nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
+            }
+            if (do_ef && PM && lane < 8)
+                nw = mp[((i + STEP) >> 5) + lane];
+        }
+#else
+    // 256-value steps; latency is hidden by warps (6 resident blocks/SM)
+    constexpr uint32_t STEP = 256;
+    const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
+    for (; i < nfull; i += STEP) {
+        float4 a[2], b[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
+            if (do_ef)
+                b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
+        }
+#endif
+        if (do_ef) {
+            if (PM) {
+                // the 8 mask words of this step (lanes 0..7), shuffled to the
+                // lanes owning their 4-bit slices, cleared after use
+#if !GVC_COLLECT_PREFETCH
+                const uint32_t wreg = lane < 8 ? mp[(i >> 5) + lane] : 0u;
+#endif
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
+                    b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
+                    b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
+                    b[u].z = (bits & 4u) ? pending_resid(b[u].z, PM, pm) : b[u].z;
+                    b[u].w = (bits & 8u) ? pending_resid(b[u].w, PM, pm) : b[u].w;
+                }
+                if (wreg)
+                    p.pmask[(beg >> 5) + (i >> 5) + lane] = 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                a[u].x = __fadd_rn(a[u].x, b[u].x);
+                a[u].y = __fadd_rn(a[u].y, b[u].y);
+                a[u].z = __fadd_rn(a[u].z, b[u].z);
+                a[u].w = __fadd_rn(a[u].w, b[u].w);
+                st_stream(reinterpret_cast<float4 *>(rp + i + u * 128) + lane, a[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+            if (!refill) {
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    nacc = __fma_rn((double)v[c], (double)v[c], nacc);
+            }
+            push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
+                      cidx, ccount);
+        }
+#if GVC_COLLECT_PREFETCH
+        if (more) {
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                a[u] = na[u];
+                b[u] = nb[u];
+            }
+            wreg = nw;
+        }
+#endif
+    }
+    // tail: one value per lane, lane-major order preserved
+    for (; i < len; i += 32) {
+        const uint32_t t = i + lane;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t valid = t < len ? 1u : 0u;
+        if (valid) {
+            float x = src[t];
+            if (do_ef) {
+                float r = rp[t];
+                if (PM) {
+                    const uint64_t gpos = beg + t;
+                    const uint32_t bit = 1u << (gpos & 31);
+                    if (p.pmask[gpos >> 5] & bit) {
+                        r = pending_resid(r, PM, pm);
+                        atomicAnd(&p.pmask[gpos >> 5], ~bit);
+                    }
+                }
+                x = __fadd_rn(x, r);
+                rp[t] = x;
+            }
+            v[0] = x;
+            if (!refill)
+                nacc = __fma_rn((double)x, (double)x, nacc);
+        }
+        push4<KM>(p, v, (uint32_t)beg + t, valid, key_est, shift0, h, dummy, cval, cidx, ccount);
+    }
+    if (lane == 0)
+        p.seg_cnt[seg] = ccount;
+}
+
 template <int KM, bool EF, int PM, bool REFILL = false>
 __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int)
 {
@@ -399,144 +541,11 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
     const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
     const uint32_t key_est = refill ? 0u : p.st->key_est;
     const int shift0 = refill ? (KM == KEY_MAG ? 19 : 20) : p.st->shift0;
-    const bool do_ef = EF && !refill;
     const float pm = (EF && PM == 2 && !refill) ? *p.pm : 0.f;
     const uint32_t dummy = GVC_H0_BINS + lane;
     double nacc = 0.0;
-    if (seg < p.S) {
-        const uint64_t beg = (uint64_t)seg * p.seg_len;
-        const uint32_t len = (uint32_t)(min(p.n, beg + p.seg_len) - beg);
-        const float *src = (EF ? (refill ? p.resid : p.g) : p.values) + beg;
-        float *rp = p.resid + beg;
-        const uint32_t *mp = p.pmask + (beg >> 5);
-        float *cval = p.cand_val + beg;
-        uint32_t *cidx = p.cand_idx + beg;
-        uint32_t ccount = 0;
-        uint32_t i = 0;
-#if GVC_COLLECT_PREFETCH
-        // software pipeline over 256-value steps: the next step's g / r loads are
-        // in flight while this step is added, reduced and compacted
-        constexpr uint32_t STEP = 256;
-        const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
-        float4 a[2], b[2];
-        // the step's 8 pending-mask words (lanes 0..7), prefetched with the data:
-        // a mask load issued at its use was the kernel's top stall (ncu)
-        uint32_t wreg = 0u;
-        if (nfull) {
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + u * 128) + lane);
-                if (do_ef)
-                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + u * 128) + lane);
-            }
-            if (do_ef && PM && lane < 8)
-                wreg = mp[lane];
-        }
-        for (; i < nfull; i += STEP) {
-            float4 na[2], nb[2];
-            uint32_t nw = 0u;
-            const bool more = i + STEP < nfull;
-            if (more) {
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    na[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + STEP + u * 128) + lane);
-                    if (do_ef)
-                        nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
-                }
-                if (do_ef && PM && lane < 8)
-                    nw = mp[((i + STEP) >> 5) + lane];
-            }
-#else
-        // 256-value steps; latency is hidden by warps (6 resident blocks/SM)
-        constexpr uint32_t STEP = 256;
-        const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
-        for (; i < nfull; i += STEP) {
-            float4 a[2], b[2];
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
-                if (do_ef)
-                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
-            }
-#endif
-            if (do_ef) {
-                if (PM) {
-                    // the 8 mask words of this step (lanes 0..7), shuffled to the
-                    // lanes owning their 4-bit slices, cleared after use
-#if !GVC_COLLECT_PREFETCH
-                    const uint32_t wreg = lane < 8 ? mp[(i >> 5) + lane] : 0u;
-#endif
-#pragma unroll
-                    for (int u = 0; u < 2; u++) {
-                        const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
-                        b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
-                        b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
-                        b[u].z = (bits & 4u) ? pending_resid(b[u].z, PM, pm) : b[u].z;
-                        b[u].w = (bits & 8u) ? pending_resid(b[u].w, PM, pm) : b[u].w;
-                    }
-                    if (wreg)
-                        p.pmask[(beg >> 5) + (i >> 5) + lane] = 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    a[u].x = __fadd_rn(a[u].x, b[u].x);
-                    a[u].y = __fadd_rn(a[u].y, b[u].y);
-                    a[u].z = __fadd_rn(a[u].z, b[u].z);
-                    a[u].w = __fadd_rn(a[u].w, b[u].w);
-                    st_stream(reinterpret_cast<float4 *>(rp + i + u * 128) + lane, a[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
-                if (!refill) {
-#pragma unroll
-                    for (int c = 0; c < 4; c++)
-                        nacc = __fma_rn((double)v[c], (double)v[c], nacc);
-                }
-                push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
-                          cidx, ccount);
-            }
-#if GVC_COLLECT_PREFETCH
-            if (more) {
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    a[u] = na[u];
-                    b[u] = nb[u];
-                }
-                wreg = nw;
-            }
-#endif
-        }
-        // tail: one value per lane, lane-major order preserved
-        for (; i < len; i += 32) {
-            const uint32_t t = i + lane;
-            float v[4] = {0.f, 0.f, 0.f, 0.f};
-            const uint32_t valid = t < len ? 1u : 0u;
-            if (valid) {
-                float x = src[t];
-                if (do_ef) {
-                    float r = rp[t];
-                    if (PM) {
-                        const uint64_t gpos = beg + t;
-                        const uint32_t bit = 1u << (gpos & 31);
-                        if (p.pmask[gpos >> 5] & bit) {
-                            r = pending_resid(r, PM, pm);
-                            atomicAnd(&p.pmask[gpos >> 5], ~bit);
-                        }
-                    }
-                    x = __fadd_rn(x, r);
-                    rp[t] = x;
-                }
-                v[0] = x;
-                if (!refill)
-                    nacc = __fma_rn((double)x, (double)x, nacc);
-            }
-            push4<KM>(p, v, (uint32_t)beg + t, valid, key_est, shift0, h, dummy, cval, cidx, ccount);
-        }
-        if (lane == 0)
-            p.seg_cnt[seg] = ccount;
-    }
+    if (seg < p.S)
+        collect_segment<KM, EF, PM, REFILL>(p, seg, lane, h, dummy, key_est, shift0, pm, nacc);
     nacc = warp_sum_f64(nacc);
     if (lane == 0)
         red[warp] = nacc;
@@ -589,13 +598,9 @@ __device__ __forceinline__ void find_crossings(const uint32_t *h, unsigned long 
 }
 
 // Level 0: candidate total, fallback decision, first interval per ladder entry.
-__global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int pass)
+__device__ void resolve_level0(const Plan &p, int pass, unsigned long long *sh, unsigned long long *need)
 {
-    __shared__ unsigned long long sh[33];
-    __shared__ unsigned long long need[GVC_MAX_LADDER];
     SelState *st = p.st;
-    if (pass == 1 && !st->fallback)
-        return;
     if (threadIdx.x < p.n_ks)
         need[threadIdx.x] = p.ks[threadIdx.x];
     __syncthreads();
@@ -647,6 +652,37 @@ __global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int pass)
             pend += !st->js[j].resolved;
         st->pending = pend;
     }
+}
+
+// Level 0 (one block): candidate total, first interval per ladder entry.  If
+// the sampled estimate overshot (fewer than k_0 candidates) the same block
+// re-collects every segment with key_est = 0 -- the exactness refill, taken
+// with probability ~1e-7 per step, so it lives here instead of as two
+// early-exit launches in every select graph -- and resolves level 0 again.
+template <int KM, bool EF>
+__global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int)
+{
+    __shared__ unsigned long long sh[33];
+    __shared__ unsigned long long need[GVC_MAX_LADDER];
+    __shared__ uint32_t hs[GVC_H0_BINS + 32];
+    resolve_level0(p, 0, sh, need);
+    __syncthreads();
+    if (!*(volatile uint32_t *)&p.st->fallback)
+        return;
+    for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += blockDim.x)
+        hs[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int shift = KM == KEY_MAG ? 19 : 20;
+    double nacc = 0.0;  // the refill does not re-accumulate the norm
+    for (uint32_t seg = warp; seg < p.S; seg += blockDim.x >> 5)
+        collect_segment<KM, EF, 0, true>(p, seg, lane, hs, GVC_H0_BINS + lane, 0u, shift, 0.f, nacc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < GVC_H0_BINS; i += blockDim.x)
+        p.hist0[i] = hs[i];
+    __threadfence();
+    __syncthreads();
+    resolve_level0(p, 1, sh, need);
 }
 
 // ------------------------------------------------------- candidate pass
@@ -1572,13 +1608,11 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[1], s, cudaEventRecordExternal);
     }
-    k_resolve0<<<1, 1024, 0, s>>>(p, 0);
     if (p.ef)
-        k_collect<KM, true, 0, true><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
+        k_resolve0<KM, true><<<1, 1024, 0, s>>>(p, 0);
     else
-        k_collect<KM, false, 0, true><<<blocks, GVC_THREADS, 0, s>>>(p, 1);
-    k_resolve0<<<1, 1024, 0, s>>>(p, 1);
-    launches += 4;
+        k_resolve0<KM, false><<<1, 1024, 0, s>>>(p, 0);
+    launches += 2;
     launch_tail<KM>(p, s);
     launches += 3;
     // k_finish_j: one block per ladder entry, 2 blocks per thread; only as many
