@@ -36,6 +36,16 @@ enum KeyMode { KEY_MAG = 0, KEY_HASH = 1 };
 
 // |x| as an order-preserving integer: clear the sign bit (-0 -> 0).  Monotone
 // for every non-NaN float; NaN keys are > 0x7f800000.
+// Programmatic dependent launch: a select kernel lets its successor launch
+// as soon as all its CTAs are running, and waits for its predecessor's
+// completion (and memory) before touching its outputs.  Both are no-ops when
+// the kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_enter()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
 
 // Philox4x32-10 (Salmon et al. SC'11), output word 0.  Counter-based position

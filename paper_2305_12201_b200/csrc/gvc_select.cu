@@ -196,6 +196,7 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh);
 
 __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
 {
+    pdl_enter();
     extern __shared__ uint32_t sh[];
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
         sh[i] = 0;
@@ -338,6 +339,7 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh)
 
 __global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
 {
+    pdl_enter();
     __shared__ unsigned long long sh[33];
     sample_resolve_body(p, sh);
 }
@@ -527,6 +529,7 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
 template <int KM, bool EF, int PM, bool REFILL = false>
 __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int)
 {
+    pdl_enter();
     // compile-time: a runtime flag would leave predicated refill / no-refill
     // code under every value of the hot loop
     constexpr bool refill = REFILL;
@@ -662,6 +665,7 @@ __device__ void resolve_level0(const Plan &p, int pass, unsigned long long *sh, 
 template <int KM, bool EF>
 __global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int)
 {
+    pdl_enter();
     __shared__ unsigned long long sh[33];
     __shared__ unsigned long long need[GVC_MAX_LADDER];
     __shared__ uint32_t hs[GVC_H0_BINS + 32];
@@ -699,6 +703,7 @@ __global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int)
 template <int KM, int NB, bool ABS>
 __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
 {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char fsm[];
     double(*acc_e)[GVC_THREADS] = reinterpret_cast<double(*)[GVC_THREADS]>(fsm);
     double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
@@ -912,6 +917,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
 template <int KM>
 __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
 {
+    pdl_enter();
     __shared__ unsigned long long sh[33];
     __shared__ __align__(16) uint32_t hs[GVC_HL_BINS];
     SelState *st = p.st;
@@ -966,6 +972,7 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
 template <int KM, int NB, bool ABS>
 __global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan p, int)
 {
+    pdl_enter();
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
     __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
     const SelState *st = p.st;
@@ -1122,6 +1129,7 @@ __device__ __forceinline__ void finish_pair_sum(double &a, double &b, unsigned l
 template <int KM>
 __global__ void __launch_bounds__(1024) k_finish_j(const Plan p, int)
 {
+    pdl_enter();
     constexpr int PER = GVC_BLK_MAX / 1024;  // 2 blocks per thread, contiguous
     __shared__ double shd[66];
     __shared__ unsigned long long shu[33];
@@ -1531,26 +1539,48 @@ size_t select_workspace_bytes(int kind, uint64_t n)
 
 static int nb_for(int n_ks) { return n_ks <= 1 ? 1 : n_ks <= 2 ? 2 : n_ks <= 4 ? 4 : n_ks <= 8 ? 8 : 16; }
 
+// Launch with programmatic stream serialization (PDL) when `pdl`.
+template <typename Kern>
+static void launch_k(Kern kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const Plan &p,
+                     int aux)
+{
+    if (!pdl) {
+        kernel<<<grid, block, smem, s>>>(p, aux);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, p, aux);
+}
+
 template <int KM, int NB, bool ABS>
-static void launch_tail_nb(const Plan &p, cudaStream_t s)
+static void launch_tail_nb(const Plan &p, cudaStream_t s, bool pdl)
 {
     const size_t smem = (size_t)(NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4);
-    k_pass1<KM, NB, ABS><<<(int)p.B, GVC_THREADS, smem, s>>>(p, 0);
-    k_resolve1<KM><<<NB, 1024, 0, s>>>(p, 0);  // NB (in the graph key) >= n_ks blocks
-    k_members<KM, NB, ABS><<<(int)p.B, GVC_THREADS, 0, s>>>(p, 0);
+    launch_k(k_pass1<KM, NB, ABS>, dim3((unsigned)p.B), dim3(GVC_THREADS), smem, s, pdl, p, 0);
+    launch_k(k_resolve1<KM>, dim3(NB), dim3(1024), 0, s, pdl, p, 0);  // NB (in the graph key) >= n_ks blocks
+    launch_k(k_members<KM, NB, ABS>, dim3((unsigned)p.B), dim3(GVC_THREADS), 0, s, pdl, p, 0);
 }
 
 // |v| sums are only consumed by Redsync's mean (compressors.py:188)
 template <int KM>
-static void launch_tail(const Plan &p, cudaStream_t s)
+static void launch_tail(const Plan &p, cudaStream_t s, bool pdl)
 {
     const bool abs_sums = p.kind == GVC_REDSYNC;
     switch (nb_for(p.n_ks)) {
-    case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, s) : launch_tail_nb<KM, 1, false>(p, s); break;
-    case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, s) : launch_tail_nb<KM, 2, false>(p, s); break;
-    case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, s) : launch_tail_nb<KM, 4, false>(p, s); break;
-    case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, s) : launch_tail_nb<KM, 8, false>(p, s); break;
-    default: abs_sums ? launch_tail_nb<KM, 16, true>(p, s) : launch_tail_nb<KM, 16, false>(p, s); break;
+    case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, s, pdl) : launch_tail_nb<KM, 1, false>(p, s, pdl); break;
+    case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, s, pdl) : launch_tail_nb<KM, 2, false>(p, s, pdl); break;
+    case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, s, pdl) : launch_tail_nb<KM, 4, false>(p, s, pdl); break;
+    case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, s, pdl) : launch_tail_nb<KM, 8, false>(p, s, pdl); break;
+    default: abs_sums ? launch_tail_nb<KM, 16, true>(p, s, pdl) : launch_tail_nb<KM, 16, false>(p, s, pdl); break;
     }
 }
 
@@ -1581,6 +1611,7 @@ static cudaEvent_t g_ev_mark[4];  // capture-time placeholders: collect start/en
 template <int KM>
 static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gprobes)
 {
+    const bool pdl = !probes;  // direct probe launches keep plain stream order
     ProfScope all(probes ? PROF_SELECT : -1, s);
     const int blocks = (int)p.B;
     int launches = 0;
@@ -1597,35 +1628,30 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
         ProfScope pc(probes ? PROF_COLLECT : -1, s);
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[0], s, cudaEventRecordExternal);
+        const bool cpdl = pdl && !gprobes;
         if (!p.ef)
-            k_collect<KM, false, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+            launch_k(k_collect<KM, false, 0>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else if (!p.pmask)
-            k_collect<KM, true, 0><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+            launch_k(k_collect<KM, true, 0>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else if (p.pmode == 1)
-            k_collect<KM, true, 1><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+            launch_k(k_collect<KM, true, 1>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else
-            k_collect<KM, true, 2><<<blocks, GVC_THREADS, 0, s>>>(p, 0);
+            launch_k(k_collect<KM, true, 2>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[1], s, cudaEventRecordExternal);
     }
     if (p.ef)
-        k_resolve0<KM, true><<<1, 1024, 0, s>>>(p, 0);
+        launch_k(k_resolve0<KM, true>, dim3(1), dim3(1024), 0, s, pdl && !gprobes, p, 0);
     else
-        k_resolve0<KM, false><<<1, 1024, 0, s>>>(p, 0);
+        launch_k(k_resolve0<KM, false>, dim3(1), dim3(1024), 0, s, pdl && !gprobes, p, 0);
     launches += 2;
-    launch_tail<KM>(p, s);
+    launch_tail<KM>(p, s, pdl);
     launches += 3;
     // k_finish_j: one block per ladder entry, 2 blocks per thread; only as many
     // warps as the blocks need (its block-wide reductions cost per warp).
     // Grid = NB (in the graph key) >= n_ks.
     const int fin_threads = (int)std::min<uint32_t>(1024u, std::max<uint32_t>(64u, ((p.B + 1) / 2 + 31) & ~31u));
-    switch (nb_for(p.n_ks)) {
-    case 1: k_finish_j<KM><<<1, fin_threads, 0, s>>>(p, 0); break;
-    case 2: k_finish_j<KM><<<2, fin_threads, 0, s>>>(p, 0); break;
-    case 4: k_finish_j<KM><<<4, fin_threads, 0, s>>>(p, 0); break;
-    case 8: k_finish_j<KM><<<8, fin_threads, 0, s>>>(p, 0); break;
-    default: k_finish_j<KM><<<16, fin_threads, 0, s>>>(p, 0); break;
-    }
+    launch_k(k_finish_j<KM>, dim3(nb_for(p.n_ks)), dim3(fin_threads), 0, s, pdl, p, 0);
     return launches + 1;
 }
 
