@@ -492,7 +492,10 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
         xmode = exchange_mode(group)
         if xmode != "nccl":
             peer = PeerExchange.get(group, dev)
-            peer.staged = xmode == "staged"
+            if peer.ok:
+                peer.staged = xmode == "staged"
+            else:  # no peer access: the all-gather exchange
+                peer, xmode = None, "nccl"
 
     # ---- one device->host read per iteration: every worker's norms and
     # energies (with a process group: C2, all-gathered first).  Started on the

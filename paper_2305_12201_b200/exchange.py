@@ -170,6 +170,7 @@ class PeerExchange:
         self.buf = None
         self.handle = None
         self.staged = True  # pull payloads through the staged (copier + trailing merge) kernel
+        self.ok = True
         import os
         sms = torch.cuda.get_device_properties(device).multi_processor_count
         # measured on B200 (scripts/stage_sweep.sh): 4096-entry chunks with one
@@ -183,8 +184,22 @@ class PeerExchange:
         px = cls._cache.get(key)
         if px is None:
             px = cls(group, device)
+            px.ok = px._probe()
             cls._cache[key] = px
         return px
+
+    def _probe(self) -> bool:
+        """Can every rank map the others' memory?  A first (small) symmetric
+        buffer is allocated and exchanged; the ranks agree on the outcome, so
+        a node without peer access falls back to the NCCL exchange everywhere."""
+        ok = 1
+        try:
+            self._ensure(4096)
+        except Exception:  # no symmetric-memory backend / peer access on this node
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(flag.item())
 
     def _slot_word(self, parity: int, src: int) -> int:
         return self.FLAG_WORDS + (parity * self.world + src) * self.cap
