@@ -350,8 +350,14 @@ class _DgcStep:
         else:
             self.identity_level1 = False
             pending = store._take_pending()
+            # the level-1 emit also builds its sent mask (taken if level 1 is sent)
+            self._mask1 = store._spare_buf()
+            if self.n > 400_000_000:
+                # past ~4.6e8 values the emit ORs mask bits in global memory
+                # instead of writing every word from shared memory
+                self._mask1.zero_()
             idx, vals, res = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
-                                        slot=slot + "a", want_result=True)
+                                        slot=slot + "a", want_result=True, sent_mask=self._mask1)
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
             self.norm = res.ef_norm_sq
         if k2 < self.g_min.kept:
@@ -385,6 +391,9 @@ class _DgcStep:
             nat.check(nat.load().gvc_update_residual(nat.ptr(store._resid), nat.ptr(part.indices),
                                                      nat.ptr(part.vals), part.kept, self.n, nat.ptr(store._resid),
                                                      nat.stream_ptr(store._resid.device)), "update_residual")
+            return part
+        if not candidate or self.g_c is self.g_min:
+            store._adopt_mask(self._mask1)  # built by the level-1 emit
             return part
         mask = store._mask_buf()
         nat.check(nat.load().gvc_mark_sent(nat.ptr(part.indices), part.kept, nat.ptr(mask),

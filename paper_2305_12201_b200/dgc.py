@@ -88,13 +88,15 @@ def _largest(keys: torch.Tensor, kk: int, slot: str) -> torch.Tensor:
 
 def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0,
                idx_map: torch.Tensor | None = None, check: bool = True, *, g: torch.Tensor | None = None,
-               resid: torch.Tensor | None = None, pending=None, slot: str = "dgc", want_result: bool = False):
+               resid: torch.Tensor | None = None, pending=None, slot: str = "dgc", want_result: bool = False,
+               sent_mask: torch.Tensor | None = None):
     """(ascending indices, values) of the DGC selection of k entries.
 
     Plain mode: ``values``.  EF mode: ``g`` + ``resid`` (+ ``pending``): g_ef is
     computed in the fused pass and written over ``resid``.  With ``want_result``
     also returns the gvc_select_result of the fused pass (its ef_norm_sq is
-    ||g_ef||^2).
+    ||g_ef||^2).  ``sent_mask`` (level 1, no idx_map): also write the bit mask
+    of the selected positions there, every word of it.
     """
     from .compressors import CompressorKind, Selection
     src = values if values is not None else g
@@ -104,7 +106,7 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
     s = min(n, max(256, int(round(kind.dgc_sample_fraction * n))))
     if s >= n:  # full sample: threshold estimation degenerates to exact selection (:113-115)
         sel = Selection(topk, [k], values=values, g=g, resid=resid, pending=pending, slot=slot + "c")
-        idx, vals = sel.emit(0, idx_map=idx_map)
+        idx, vals = sel.emit(0, idx_map=idx_map, sent_mask=sent_mask)
         res = sel.result() if (check or want_result) else None
         return (idx, vals, res) if want_result else (idx, vals)
 
@@ -127,7 +129,7 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
     res = sel_c.result()  # host decision point: did the threshold overshoot?
     short = int(res.shortfall)
     if short == 0:
-        idx, vals = sel_c.emit(0, idx_map=idx_map)
+        idx, vals = sel_c.emit(0, idx_map=idx_map, sent_mask=sent_mask)
         return (idx, vals, res) if want_result else (idx, vals)
 
     # overshoot (:126-137): keep all of `chosen`, pad from the sample below thr,
@@ -151,6 +153,8 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
         _mark(_largest(keysE, rest, slot + "u"), mask)
     idx = _compact(mask, n, k)
     vals = _gather(idx, values=e)
+    if sent_mask is not None:
+        sent_mask.copy_(mask)
     if idx_map is not None:
         idx = _take_u32(idx_map, idx)
     return (idx, vals, res) if want_result else (idx, vals)
