@@ -27,6 +27,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _native as nat
@@ -135,13 +137,20 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
     # overshoot (:126-137): keep all of `chosen`, pad from the sample below thr,
     # then top up globally; re-order the union by position
     e = values if values is not None else resid  # g_ef now lives in resid (EF mode)
-    mask = _mask_for(n, dev)
     nchosen = k - short
-    if nchosen:
-        ci, _ = sel_c.emit(0, count=nchosen)
-        _mark(ci, mask)
+    if nchosen and idx_map is None:
+        # `chosen` straight into a complete mask (every word written by the emit)
+        # (past ~4.6e8 values the emit ORs bits in global memory: start from zero)
+        mask = (_mask_for(n, dev) if n > 400_000_000 else
+                torch.empty((n + 31) // 32, dtype=torch.int32, device=dev).view(torch.uint32))
+        sel_c.emit(0, count=nchosen, sent_mask=mask)
+    else:
+        mask = _mask_for(n, dev)
+        if nchosen:
+            ci, _ = sel_c.emit(0, count=nchosen)
+            _mark(ci, mask)
     keysP, cntP = _below_keys(vP, thr_u)
-    nb = int(cntP.item())
+    nb = int(np.frombuffer(nat.d2h_bytes(cntP), dtype=np.int64)[0])
     take = min(short, nb)
     if take:
         _mark(_take_u32(P, _largest(keysP, take, slot + "p")), mask)
