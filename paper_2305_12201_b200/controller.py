@@ -223,8 +223,16 @@ class _WorkerStep:
         else:
             self.ladder = [k1]
             self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a", pending=pending)
-            idx, vals = self.sel1.emit(0)
+            # the level-1 emit also builds its sent mask (every word, in the spare
+            # buffer), the Redsync mean and the K7 tile bounds; taken if level 1 is sent
+            self._mask1 = store._spare_buf()
+            if self.n > 400_000_000:
+                self._mask1.zero_()  # the emit ORs bits in global memory there
+            bounds = torch.empty((self.n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1, dtype=torch.int32,
+                                 device=g.device).view(torch.uint32)
+            idx, vals = self.sel1.emit(0, sent_mask=self._mask1, sent_m=store._pm, tile_bounds=bounds)
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
+            self._bounds1 = bounds
             if k2 < k1:
                 self.sel2 = Selection(kind, [k2], values=vals, rng=rng1, slot=slot + "b")
 
@@ -287,7 +295,8 @@ class _WorkerStep:
         part = self._emit(candidate, payload)
         if payload is not None and part.vals.data_ptr() == payload.vals.data_ptr():
             part._payload = payload
-        part._bounds = self._tile_bounds
+        if self._tile_bounds is not None:
+            part._bounds = self._tile_bounds
         return part
 
     def _emit(self, candidate: bool, payload: torch.Tensor | None) -> SparseGradient:
@@ -317,11 +326,10 @@ class _WorkerStep:
             part = SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
         else:
             part = self.g_min
-            nat.check(lib.gvc_mark_sent(nat.ptr(part.indices), part.kept, nat.ptr(mask),
-                                        nat.stream_ptr(self.resid.device)), "mark_sent")
-            if mode == 2:  # the level-1 Redsync mean, straight from the device result
-                off = nat.SelectResult.redsync_mean.offset
-                store._pm.copy_(self.sel1.res_dev[off:off + 4].view(torch.float32))
+            part._bounds = self._bounds1
+            # mask, Redsync mean (in store._pm) and bounds came with the level-1 emit
+            store._adopt_mask(self._mask1, mode)
+            return part
         store._pmode = mode
         return part
 
@@ -517,7 +525,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     pending = rows = None
     if group is not None:
         import torch.distributed as dist
-        if dist.get_backend(group) == "nccl":
+        if dist.get_backend(group) == "nccl" and peer is not None:
+            # C2 on a side stream: the peer-memory exchange issues no other NCCL
+            # work this step, so the collective cannot be reordered against one
             ready = torch.cuda.Event()
             ready.record()
             side = nat.side_stream(dev)
@@ -527,6 +537,13 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
                 dist.all_gather_into_tensor(gathered, flat, group=group)
                 pending = nat.d2h_start(gathered)
                 _mark("c2_read", side)
+        elif dist.get_backend(group) == "nccl":
+            # NCCL exchange: every collective of this communicator on one stream
+            # (collectives on two streams may execute in different orders on
+            # different ranks and deadlock)
+            gathered = torch.empty((dist.get_world_size(group), flat.numel()), dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(gathered, flat, group=group)
+            pending = nat.d2h_start(gathered)
         else:
             from .exchange import allgather_stats
             rows = allgather_stats(flat.cpu(), group)

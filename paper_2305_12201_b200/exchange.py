@@ -208,6 +208,9 @@ class PeerExchange:
         if words <= self.cap:
             return
         import torch.distributed._symmetric_memory as symm
+        # the step's C2 all-gather may still be in flight on the side stream:
+        # finish it before this rank issues the collectives below
+        torch.cuda.synchronize(self.device)
         cap = (words + 1023) & ~1023
         buf = symm.empty(self.FLAG_WORDS + 2 * self.world * cap, dtype=torch.int32, device=self.device)
         buf[:self.FLAG_WORDS].zero_()
