@@ -401,16 +401,18 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
     uint32_t *cidx = p.cand_idx + beg;
     uint32_t ccount = 0;
     uint32_t i = 0;
-#if GVC_COLLECT_PREFETCH
-    // software pipeline over 256-value steps: the next step's g / r loads are
-    // in flight while this step is added, reduced and compacted
+    // 256-value steps.  PF (magnitude keys): software pipeline -- the next
+    // step's g / r loads and mask words are in flight while this step is
+    // added, reduced and compacted.  Hash keys are Philox-bound, and the
+    // register double buffer there only costs spills.
+    constexpr bool PF = GVC_COLLECT_PREFETCH != 0 && KM == KEY_MAG;
     constexpr uint32_t STEP = 256;
     const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
     float4 a[2], b[2];
-    // the step's 8 pending-mask words (lanes 0..7), prefetched with the data:
-    // a mask load issued at its use was the kernel's top stall (ncu)
+    // the step's 8 pending-mask words (lanes 0..7), prefetched with the data
+    // when PF: a mask load issued at its use was the kernel's top stall (ncu)
     uint32_t wreg = 0u;
-    if (nfull) {
+    if (PF && nfull) {
 #pragma unroll
         for (int u = 0; u < 2; u++) {
             a[u] = ld_stream(reinterpret_cast<const float4 *>(src + u * 128) + lane);
@@ -424,36 +426,31 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
         float4 na[2], nb[2];
         uint32_t nw = 0u;
         const bool more = i + STEP < nfull;
-        if (more) {
+        if (PF) {
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    na[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + STEP + u * 128) + lane);
+                    if (do_ef)
+                        nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
+                }
+                if (do_ef && PM && lane < 8)
+                    nw = mp[((i + STEP) >> 5) + lane];
+            }
+        } else {
 #pragma unroll
             for (int u = 0; u < 2; u++) {
-                na[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + STEP + u * 128) + lane);
+                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
                 if (do_ef)
-                    nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
+                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
             }
             if (do_ef && PM && lane < 8)
-                nw = mp[((i + STEP) >> 5) + lane];
+                wreg = mp[(i >> 5) + lane];
         }
-#else
-    // 256-value steps; latency is hidden by warps (6 resident blocks/SM)
-    constexpr uint32_t STEP = 256;
-    const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
-    for (; i < nfull; i += STEP) {
-        float4 a[2], b[2];
-#pragma unroll
-        for (int u = 0; u < 2; u++) {
-            a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
-            if (do_ef)
-                b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
-        }
-#endif
         if (do_ef) {
             if (PM) {
                 // the 8 mask words of this step (lanes 0..7), shuffled to the
                 // lanes owning their 4-bit slices, cleared after use
-#if !GVC_COLLECT_PREFETCH
-                const uint32_t wreg = lane < 8 ? mp[(i >> 5) + lane] : 0u;
-#endif
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
                     const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
@@ -485,8 +482,7 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
             push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
                       cidx, ccount);
         }
-#if GVC_COLLECT_PREFETCH
-        if (more) {
+        if (PF && more) {
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 a[u] = na[u];
@@ -494,7 +490,6 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
             }
             wreg = nw;
         }
-#endif
     }
     // tail: one value per lane, lane-major order preserved
     for (; i < len; i += 32) {
