@@ -460,10 +460,12 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         gh = fresh().cpu().numpy()
         rh = np.zeros(M, dtype=np.float32)
         oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra, 1, args.kind)  # warm
+        # a bounded sample of ~10 s of host work: whole steps until 10 s pass (at least 2)
         t0 = time.perf_counter()
-        n_cpu = 2
-        for _ in range(n_cpu):
+        n_cpu = 0
+        while n_cpu < 2 or (time.perf_counter() - t0 < 10.0 and n_cpu < 50):
             rh = oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra, 1, args.kind)[0]
+            n_cpu += 1
         dt = (time.perf_counter() - t0) / n_cpu
         line["cpu_baseline"] = {"value": 4 * M / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
                                 "sample": f"{n_cpu} full steps of the same workload (C oracle, single thread)",
