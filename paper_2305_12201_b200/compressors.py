@@ -129,7 +129,7 @@ class Selection:
                  g: torch.Tensor | None = None, resid: torch.Tensor | None = None,
                  rng: SeededRng | None = None, pos_base: int = 0, slot: str = "sel0",
                  force_exact: int = 0, pending=None, key_est: torch.Tensor | None = None,
-                 allow_short: bool = False):
+                 allow_short: bool = False, persist_res: bool = False):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -138,7 +138,10 @@ class Selection:
         self.device = src.device
         lib = nat.load()
         self.ws = nat.select_workspace(self.device, slot, kind.kind_id, self.n)
-        self.res_dev = torch.empty(nat.RESULT_BYTES, dtype=torch.uint8, device=self.device)
+        # persist_res: the slot's result buffer is reused (the controller reads
+        # it back within the step), so an unchanged plan needs no graph update
+        self.res_dev = (nat.Workspace.get(self.device, slot + "/res", nat.RESULT_BYTES)[:nat.RESULT_BYTES]
+                        if persist_res else torch.empty(nat.RESULT_BYTES, dtype=torch.uint8, device=self.device))
         a = nat.SelectArgs()
         a.kind = kind.kind_id
         a.n_ks = len(self.ks)

@@ -219,7 +219,7 @@ class _WorkerStep:
             # F2: nested Top-k == exact top-k2 of the whole vector -> one sweep
             self.ladder = [k1, k2] + list(extra_ks)
             self.sel1 = Selection(kind, self.ladder, g=g, resid=resid, rng=rng0, slot=slot + "a",
-                                  pending=pending)
+                                  pending=pending, persist_res=True)
         else:
             self.ladder = [k1]
             self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a", pending=pending)

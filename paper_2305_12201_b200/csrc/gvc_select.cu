@@ -1681,6 +1681,8 @@ struct GraphEntry {
     std::vector<GraphNode> nodes;
     cudaGraphNode_t ev_nodes[4] = {nullptr, nullptr, nullptr, nullptr};  // g_ev_mark order (profiling graphs)
     int launches;
+    Plan last;  // the plan the nodes currently hold
+    bool has_last = false;
 };
 static std::unordered_map<std::string, GraphEntry> g_graphs;
 
@@ -1710,9 +1712,12 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.values = a->values_dev;
     p.g = a->g_dev;
     p.resid = a->resid_dev;
-    p.seed = a->seed;
-    p.stream = a->rng_stream;
-    p.pos_base = a->pos_base;
+    // the hash inputs only matter for hash keys; zero otherwise so that an
+    // unchanged magnitude-key plan is bit-identical call to call
+    const bool hashk = a->kind == GVC_RANDOMK;
+    p.seed = hashk ? a->seed : 0;
+    p.stream = hashk ? a->rng_stream : 0;
+    p.pos_base = hashk ? a->pos_base : 0;
     p.key_est_dev = a->key_est_dev;
     p.allow_short = a->key_est_dev ? a->allow_short : 0;
     p.pmask = p.ef ? a->pending_mask_dev : nullptr;
@@ -1812,14 +1817,20 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
                 return set_error(GVC_ERR_CUDA, "select graph instantiate: %s", cudaGetErrorString(ce));
             it = g_graphs.emplace(key, std::move(ge)).first;
         }
-        for (GraphNode &gn : it->second.nodes) {
-            int aux = gn.aux;
-            void *args[2] = {(void *)&p, (void *)&aux};
-            cudaKernelNodeParams kp = gn.kp;
-            kp.kernelParams = args;
-            cudaError_t ue = cudaGraphExecKernelNodeSetParams(it->second.exec, gn.node, &kp);
-            if (ue != cudaSuccess)
-                return set_error(GVC_ERR_CUDA, "select graph update: %s", cudaGetErrorString(ue));
+        // the node arguments change only when the plan does (steady state: the
+        // same tensors every step) -- skip the per-node updates then
+        if (!it->second.has_last || memcmp(&it->second.last, &p, sizeof(Plan)) != 0) {
+            for (GraphNode &gn : it->second.nodes) {
+                int aux = gn.aux;
+                void *args[2] = {(void *)&p, (void *)&aux};
+                cudaKernelNodeParams kp = gn.kp;
+                kp.kernelParams = args;
+                cudaError_t ue = cudaGraphExecKernelNodeSetParams(it->second.exec, gn.node, &kp);
+                if (ue != cudaSuccess)
+                    return set_error(GVC_ERR_CUDA, "select graph update: %s", cudaGetErrorString(ue));
+            }
+            it->second.last = p;
+            it->second.has_last = true;
         }
         for (int e = 0; e < 4; e += 2) {
             if (it->second.ev_nodes[e] && it->second.ev_nodes[e + 1]) {
