@@ -196,8 +196,10 @@ class _WorkerStep:
         self.g_min: SparseGradient | None = None
         self.sel2: Selection | None = None
         self.identity1 = k1 >= self.n
-        rng0 = rng.split(i, w, _STAGE_MIN)
-        rng1 = rng.split(i, w, _STAGE_STEP)
+        # the per-stage streams only feed Random-k (Top-k and Redsync draw nothing)
+        needs_rng = kind.name not in (TOPK, "redsync")
+        rng0 = rng.split(i, w, _STAGE_MIN) if needs_rng else None
+        rng1 = rng.split(i, w, _STAGE_STEP) if needs_rng else None
         slot = f"step{w}"
         if self.identity1:
             # theta_min == 1: level 1 keeps everything; g_ef by the EF kernel
