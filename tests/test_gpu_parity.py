@@ -493,3 +493,30 @@ def test_aggregate_adversarial(G, nparts):
     fin = np.isfinite(ref) | np.isinf(ref)
     assert np.array_equal(bits(out)[fin], bits(ref)[fin])
     assert np.array_equal(np.isnan(out), np.isnan(ref))
+
+
+def test_integration_ctypes_stub(G):
+    """The reference-side binding of INTEGRATION.md §2 (raw C-ABI through
+    ctypes: gvc_select + gvc_emit) equals the oracle's Top-k."""
+    import ctypes
+    from paper_2305_12201_b200 import _native as nat
+    lib = nat.load()
+    x_np = np.random.default_rng(5).standard_normal(300_001).astype(np.float32)
+    k = 3_000
+    x = torch.from_numpy(x_np).cuda()
+    n = x.numel()
+    ws = torch.empty(lib.gvc_select_workspace_bytes(0, n), dtype=torch.uint8, device="cuda")
+    res = torch.empty(nat.RESULT_BYTES, dtype=torch.uint8, device="cuda")
+    a = nat.SelectArgs(kind=0, n_ks=1, n=n, values_dev=x.data_ptr())
+    a.ks[0] = k
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.check(lib.gvc_select(ctypes.byref(a), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                             ctypes.c_void_p(res.data_ptr()), stream))
+    idx = torch.empty(k, dtype=torch.int32, device="cuda").view(torch.uint32)
+    val = torch.empty(k, dtype=torch.float32, device="cuda")
+    nat.check(lib.gvc_emit(ctypes.c_void_p(ws.data_ptr()), ws.numel(), 0, None,
+                           ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(val.data_ptr()),
+                           None, None, None, None, None, stream))
+    oi = O.topk_indices(x_np, k)
+    assert np.array_equal(host(idx).astype(np.int64), np.asarray(oi, dtype=np.int64))
+    assert np.array_equal(bits(host(val)), bits(x_np[oi]))
