@@ -735,8 +735,12 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
     // first two intervals touch)
     const uint32_t f_lo = him1[0];
     const uint32_t f_hi = nks >= 2 ? lo[1] : 0xffffffffu;
-    double e_b1 = 0.0, a_b1 = 0.0;
-    uint32_t c_b1 = 0;
+    // second fast window (hi_1 - 1, lo_2): band 2 (the entries kept at the
+    // candidate CF as well, ~10% of the candidates of a x10 ladder step)
+    const uint32_t f2_lo = nks >= 2 ? him1[NB >= 2 ? 1 : 0] : 0xffffffffu;
+    const uint32_t f2_hi = nks >= 3 ? lo[NB >= 3 ? 2 : 0] : 0xffffffffu;
+    double e_b1 = 0.0, a_b1 = 0.0, e_b2 = 0.0, a_b2 = 0.0;
+    uint32_t c_b1 = 0, c_b2 = 0;
     if (seg < p.S) {
         const uint64_t beg = (uint64_t)seg * p.seg_len;
         const uint32_t cnt = p.seg_cnt[seg];
@@ -789,21 +793,30 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         };
         // register double buffer: the next 128 candidates are in flight while
         // this group is classified (a warp walks ~8 groups back to back)
-        float4 nfv = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint4 niv = make_uint4(0u, 0u, 0u, 0u);
+        // (two groups in flight: one warp per segment and ~5 warps per SM
+        // quadrant leave too few bytes in flight with a single group)
+        float4 nfv = make_float4(0.f, 0.f, 0.f, 0.f), nfv2 = nfv;
+        uint4 niv = make_uint4(0u, 0u, 0u, 0u), niv2 = niv;
         if (cnt) {
             nfv = *reinterpret_cast<const float4 *>(p.cand_val + beg + lane * 4);
             if (KM == KEY_HASH)
                 niv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + lane * 4);
         }
+        if (cnt > 128) {
+            nfv2 = *reinterpret_cast<const float4 *>(p.cand_val + beg + 128 + lane * 4);
+            if (KM == KEY_HASH)
+                niv2 = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + 128 + lane * 4);
+        }
         for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
             const uint32_t t = base + lane * 4;
             const float4 fv = nfv;
             const uint4 iv = niv;
-            if (base + 128 < cnt) {
-                nfv = *reinterpret_cast<const float4 *>(p.cand_val + beg + t + 128);
+            nfv = nfv2;
+            niv = niv2;
+            if (base + 256 < cnt) {
+                nfv2 = *reinterpret_cast<const float4 *>(p.cand_val + beg + t + 256);
                 if (KM == KEY_HASH)
-                    niv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t + 128);
+                    niv2 = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t + 256);
             }
             float v[4] = {fv.x, fv.y, fv.z, fv.w};
             uint32_t pos[4] = {iv.x, iv.y, iv.z, iv.w}, key[4];
@@ -832,7 +845,14 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
                         a_b1 += fabs((double)v[c]);
                     c_b1 += 1u;
                 }
-                slow[c] = ok[c] && !fast;
+                const bool fast2 = NB >= 2 && ok[c] && key[c] > f2_lo && key[c] < f2_hi;
+                if (fast2) {
+                    e_b2 += (double)v[c] * (double)v[c];
+                    if (ABS)
+                        a_b2 += fabs((double)v[c]);
+                    c_b2 += 1u;
+                }
+                slow[c] = ok[c] && !fast && !fast2;
                 sbal[c] = __ballot_sync(0xffffffffu, slow[c]);
             }
             uint32_t o = qh + qn + __popc(sbal[0] & lt) + __popc(sbal[1] & lt) + __popc(sbal[2] & lt) +
@@ -872,6 +892,12 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
     if (ABS)
         acc_a[1][threadIdx.x] += a_b1;
     acc_c[1][threadIdx.x] += c_b1;
+    if (NB >= 2) {
+        acc_e[NB >= 2 ? 2 : 0][threadIdx.x] += e_b2;
+        if (ABS)
+            acc_a[NB >= 2 ? 2 : 0][threadIdx.x] += a_b2;
+        acc_c[NB >= 2 ? 2 : 0][threadIdx.x] += c_b2;
+    }
     __syncwarp();
     nan_any = __any_sync(0xffffffffu, nan_any);
     if (lane == 0 && nan_any)
