@@ -245,11 +245,14 @@ __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
         if (sh[i])
             atomicAdd(&p.shist[i], sh[i]);
     // the last block to finish resolves key_est (no separate launch)
+    // (the block's histogram atomics are ordered before thread 0's device-scope
+    // fence by the barrier -- fence cumulativity -- so one thread fences)
     __shared__ int last;
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+        __threadfence();
         last = atomicAdd(&p.st->sample_done, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (last) {
         __threadfence();
