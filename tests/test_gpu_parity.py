@@ -520,3 +520,32 @@ def test_integration_ctypes_stub(G):
     oi = O.topk_indices(x_np, k)
     assert np.array_equal(host(idx).astype(np.int64), np.asarray(oi, dtype=np.int64))
     assert np.array_equal(bits(host(val)), bits(x_np[oi]))
+
+
+@pytest.mark.parametrize("kind", ["topk", "randomk"])
+@pytest.mark.parametrize("dist", ["gauss", "ties", "layered"])
+@pytest.mark.parametrize("ladder", [(10.0,), (10.0, 10.0), (10.0, 100.0), (2.0, 2.0, 2.0),
+                                    (10.0, 100.0, 1000.0, 1.001), (1.5, 3.0, 10.0, 30.0, 100.0, 300.0),
+                                    (10.0, 10.5, 11.0, 12.0, 20.0, 40.0, 80.0, 160.0, 320.0)])
+def test_ladder_shapes_vs_oracle(G, kind, dist, ladder):
+    """Every entry of ladders of 1-9 CFs (coinciding, adjacent and far-apart
+    thresholds: k_pass1's register band windows, its slow queue and the member
+    path of every NB instantiation) against the oracle's exact selection."""
+    from paper_2305_12201_b200.compressors import Selection
+    K = G.CompressorKind(kind)
+    n = 1_500_007
+    x = _vec(dist, n, 11)
+    ks = [G.keep_count(n, ladder[0])]
+    for cf in ladder[1:]:
+        ks.append(G.keep_count(ks[-1], cf))
+    rng = G.SeededRng(5).split(0, 1, 2)
+    sel = Selection(K, ks, values=torch.from_numpy(x).cuda(), rng=rng, slot="lad")
+    res = sel.result()
+    assert res.fallback_used == 0
+    for j, k in enumerate(ks):
+        oi, ov = O.select(kind, x, k, seed=rng.seed, stream=rng.stream)
+        idx, vals = sel.emit(j)
+        assert np.array_equal(host(idx), oi), (j, k)
+        assert np.array_equal(bits(host(vals)), bits(x[oi]))
+        assert res.kept_sq[j] == pytest.approx(O.sq_norm(x[oi]), rel=1e-9)
+        assert res.kept_count[j] == k
