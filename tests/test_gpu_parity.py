@@ -549,3 +549,24 @@ def test_ladder_shapes_vs_oracle(G, kind, dist, ladder):
         assert np.array_equal(bits(host(vals)), bits(x[oi]))
         assert res.kept_sq[j] == pytest.approx(O.sq_norm(x[oi]), rel=1e-9)
         assert res.kept_count[j] == k
+
+
+@pytest.mark.parametrize("dist", ["gauss", "ties"])
+@pytest.mark.parametrize("ladder", [(10.0, 10.0), (10.0, 100.0, 1000.0), (1.5, 3.0, 10.0, 30.0, 100.0)])
+def test_redsync_ladder_vs_oracle(G, dist, ladder):
+    """Redsync over multi-CF ladders: k_pass1's |v| band sums (the mean) for
+    every entry -- support bit-exact, substituted values within 1e-6."""
+    from paper_2305_12201_b200.compressors import Selection
+    K = G.CompressorKind("redsync")
+    n = 1_500_007
+    x = _vec(dist, n, 13)
+    ks = [G.keep_count(n, ladder[0])]
+    for cf in ladder[1:]:
+        ks.append(G.keep_count(ks[-1], cf))
+    sel = Selection(K, ks, values=torch.from_numpy(x).cuda(), slot="lrs")
+    assert sel.result().fallback_used == 0
+    for j, k in enumerate(ks):
+        oi, ov = O.select("redsync", x, k)
+        idx, vals = sel.emit(j)
+        assert np.array_equal(host(idx), oi), (j, k)
+        np.testing.assert_allclose(host(vals), ov, rtol=1e-6, atol=0)
