@@ -268,6 +268,11 @@ GVC_API void gvc_prof_enable(int on);
 GVC_API int gvc_prof_read(double *ms, unsigned long long *counts, int ncat);
 GVC_API unsigned long long gvc_launch_count(void);
 
+/* Diagnostic: the %globaltimer stamps (ns) the last gvc_select on `ws`
+ * recorded at its phase boundaries (collect start, sample barriers, pass end,
+ * level-0 resolve, ...); synchronous.  Development aid for the roofline work. */
+GVC_API int gvc_select_phase_times(void *ws, unsigned long long *out, int n);
+
 /* DGC's threshold sample (compressors.py:118; parity-unpinned):
  * s ascending positions of [0, n), one per stratum [j n / s, (j + 1) n / s),
  * at lo_j + floor(h_j * width_j / 2^32), h_j = Philox4x32-10 word 0 at

@@ -56,6 +56,7 @@ def lib():
         L.orc_aggregate.argtypes = [vp, vp, vp, i32, u64, vp]
         L.orc_aggregate_dense.argtypes = [vp, i32, u64, vp]
         L.orc_update_residual.argtypes = [vp, vp, vp, u64, u64, vp]
+        L.orc_dgc_sample_positions.argtypes = [u64, u64, u64, u64, u64, vp]
         _lib = L
     return _lib
 
@@ -148,6 +149,28 @@ def select(kind, values: np.ndarray, k: int, seed: int = 0, stream: int = 0,
     _check(lib().orc_select(kind, _p(values), n, k, seed & _MASK64, stream & _MASK64,
                             pos_base, dgc_sample_fraction, _p(idx), _p(vals)))
     return idx, vals
+
+
+def dgc_sample_positions(n: int, s: int, seed: int, stream: int, pos_base: int = 0) -> np.ndarray:
+    """The s stratified sample positions of the DGC threshold estimate (gravac_oracle.c)."""
+    out = np.empty(s, dtype=np.uint32)
+    lib().orc_dgc_sample_positions(n, s, seed & _MASK64, stream & _MASK64, pos_base, _p(out))
+    return out
+
+
+def dgc_overshoots(values: np.ndarray, k: int, seed: int, stream: int, frac: float = 0.01) -> bool:
+    """Which branch compressors.py:123-137 takes: True when fewer than k entries
+    reach the sampled threshold (the pad + top-up branch)."""
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    n = values.size
+    s = min(n, max(256, round(frac * n)))
+    if s >= n:
+        return False
+    mk = values.view(np.uint32) & np.uint32(0x7FFFFFFF)
+    sk = np.sort(mk[dgc_sample_positions(n, s, seed, stream).astype(np.int64)])[::-1]
+    rank = min(s, max(1, round(k * s / n)))
+    thr = sk[rank - 1]
+    return int(np.count_nonzero(mk >= thr)) < k
 
 
 def topk_indices(values: np.ndarray, k: int) -> np.ndarray:

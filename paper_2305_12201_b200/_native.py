@@ -30,7 +30,7 @@ EXPORTS = (
     "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
-    "gvc_aggregate_peers_staged", "gvc_dgc_sample",
+    "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_select_phase_times",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -140,6 +140,7 @@ def load(build_if_missing: bool = False):
         L.gvc_prof_enable.restype = None
         L.gvc_prof_read.argtypes = [_vp, _vp, ctypes.c_int]
         L.gvc_launch_count.restype = ctypes.c_ulonglong
+        L.gvc_select_phase_times.argtypes = [_vp, _vp, ctypes.c_int]
         if L.gvc_abi_version() != 1:
             raise ImportError("libgravac_b200 ABI version mismatch")
         _lib = L

@@ -179,11 +179,17 @@ class IterationResult:
 
 # ------------------------------------------------------------ fused step
 class _WorkerStep:
-    """Device-side work of one worker for one iteration (level 1 + level 2)."""
+    """Device-side work of one worker for one iteration (level 1 + level 2).
+
+    Top-k evaluates every keep count of the step -- k1 (theta_min), k2 (the
+    candidate) and the extra CFs' counts -- as ONE descending, de-duplicated
+    ladder; ``slot[k]`` is the ladder entry holding keep count k.  Counts >= n
+    keep everything (gain 1, no ladder entry)."""
 
     def __init__(self, kind: CompressorKind, g: torch.Tensor, store: ResidualStore, k1: int, k2: int,
                  extra_ks: Sequence[int], rng: SeededRng, i: int, w: int):
         self.kind, self.k1, self.k2 = kind, k1, k2
+        self.extra_ks = list(extra_ks)
         self.store = store
         if k1 >= g.numel():
             resid = store.residual  # materialise any deferred update first
@@ -201,6 +207,11 @@ class _WorkerStep:
         rng0 = rng.split(i, w, _STAGE_MIN) if needs_rng else None
         rng1 = rng.split(i, w, _STAGE_STEP) if needs_rng else None
         slot = f"step{w}"
+        if kind.name == TOPK:
+            self.ladder = sorted({k for k in [k1, k2, *self.extra_ks] if k < self.n}, reverse=True)
+        else:
+            self.ladder = [k1] if k1 < self.n else []
+        self.slot = {k: j for j, k in enumerate(self.ladder)}
         if self.identity1:
             # theta_min == 1: level 1 keeps everything; g_ef by the EF kernel
             nat.check(nat.load().gvc_ef_add(nat.ptr(g), nat.ptr(resid), nat.ptr(resid), self.n,
@@ -209,17 +220,14 @@ class _WorkerStep:
             self.sel1 = None
             from .gradcore import squared_l2_norm_dev
             self._norm_dev = squared_l2_norm_dev(resid)
-            self.ladder = [k2] + list(extra_ks)
             if kind.name == TOPK:
-                ks = [k for k in self.ladder if k < self.n]
-                self.sel2 = Selection(kind, ks or [self.n - 1], values=resid, slot=slot + "b") if ks else None
+                self.sel2 = Selection(kind, self.ladder, values=resid, slot=slot + "b") if self.ladder else None
             else:
                 self.sel2 = (Selection(kind, [k2], values=self.g_min.vals, rng=rng1, slot=slot + "b")
                              if k2 < self.n else None)
             return
         if kind.name == TOPK:
             # F2: nested Top-k == exact top-k2 of the whole vector -> one sweep
-            self.ladder = [k1, k2] + list(extra_ks)
             self.sel1 = Selection(kind, self.ladder, g=g, resid=resid, rng=rng0, slot=slot + "a",
                                   pending=pending, persist_res=True)
         else:
@@ -262,28 +270,23 @@ class _WorkerStep:
                 raise ValueError("NaN in gradient: compression order undefined")
             if r.status != nat.GVC_OK:
                 raise RuntimeError(f"selection consistency failure (status {r.status})")
-        if self.identity1:
-            norm = norm_host
-            e_min = norm
-            if self.kind.name == TOPK:
-                extra_e = []
-                ks = [k for k in self.ladder if k < self.n]
-                e_by_k = {k: r2.kept_sq[j] for j, k in enumerate(ks)} if r2 is not None else {}
-                e_c = e_by_k.get(self.k2, norm)
-                extra_e = [e_by_k.get(k, norm) for k in self.ladder[1:]]
-                return norm, e_min, e_c, extra_e
-            e_c = r2.kept_sq[0] if r2 is not None else norm
-            return norm, e_min, e_c, []
-        norm = r1.ef_norm_sq
+        norm = norm_host if self.identity1 else r1.ef_norm_sq
         if self.kind.name == TOPK:
-            return norm, r1.kept_sq[0], r1.kept_sq[1], [r1.kept_sq[2 + j] for j in range(len(self.ladder) - 2)]
+            res = r2 if self.identity1 else r1
+
+            def energy(k):  # a count >= n keeps everything: E = ||g_ef||^2
+                return res.kept_sq[self.slot[k]] if k in self.slot else norm
+            return norm, energy(self.k1), energy(self.k2), [energy(k) for k in self.extra_ks]
+        if self.identity1:
+            return norm, norm, (r2.kept_sq[0] if r2 is not None else norm), []
         e_min = r1.kept_sq[0]
         e_c = r2.kept_sq[0] if r2 is not None else e_min
         return norm, e_min, e_c, []
 
     def chosen_count(self, candidate: bool) -> int:
-        if self.kind.name == TOPK and not self.identity1:
-            return self.ladder[1 if candidate else 0]
+        if self.kind.name == TOPK:
+            k = self.k2 if candidate else self.k1
+            return k if k in self.slot else self.n
         return self.k2 if (candidate and self.sel2 is not None) else self.g_min.kept
 
     def emit(self, candidate: bool, payload=None, bounds: bool = False) -> SparseGradient:
@@ -307,9 +310,11 @@ class _WorkerStep:
         mode = 2 if self.kind.name == "redsync" else 1
         if self.identity1:
             # theta_min == 1 (level 1 keeps everything): direct update, no mask
-            if candidate and self.sel2 is not None:
-                idx, vals = self.sel2.emit(0, idx_map=self.g_min.indices, resid=self.resid)
+            if candidate and self.sel2 is not None and (self.kind.name != TOPK or self.k2 in self.slot):
+                j = self.slot[self.k2] if self.kind.name == TOPK else 0
+                idx, vals = self.sel2.emit(j, idx_map=self.g_min.indices, resid=self.resid)
                 return SparseGradient._wrap(idx, vals, self.n, self.n / self.k2)
+            # theta_s == 1 too (k2 >= n): the whole g_ef is sent, as compress_further copies
             part = self.g_min
             nat.check(lib.gvc_update_residual(nat.ptr(self.resid), nat.ptr(part.indices), nat.ptr(part.vals),
                                               part.kept, self.n, nat.ptr(self.resid),
@@ -317,9 +322,8 @@ class _WorkerStep:
             return part
         mask = store._mask_buf()
         if self.kind.name == TOPK:
-            j = 1 if candidate else 0
-            k = self.ladder[j]
-            idx, vals = self.sel1.emit(j, sent_mask=mask, sent_m=store._pm, payload=payload,
+            k = self.k2 if candidate else self.k1
+            idx, vals = self.sel1.emit(self.slot[k], sent_mask=mask, sent_m=store._pm, payload=payload,
                                        tile_bounds=self._tile_bounds)
             part = SparseGradient._wrap(idx, vals, self.n, self.n / k)
         elif candidate and self.sel2 is not None:
@@ -462,9 +466,11 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     With ``group`` (a torch.distributed process group), this process is ONE
     worker -- worker index = rank -- and the per-worker gain ratios are
     all-gathered so every rank takes the same decision in the reference's
-    worker order.  ``extra_cfs``: more CFs (>= theta_min) whose gains the Top-k
-    sweep evaluates in the same pass; reported in ``ladder_gains`` but never
-    fed to the EWMA trackers.  ``average=True`` also performs the
+    worker order.  ``extra_cfs``: more CFs whose gains the Top-k sweep
+    evaluates in the same pass (any order, any value >= 1: a CF >= theta_min
+    is nested under level 1 like compress_further, a smaller one is a plain
+    compress); reported in ``ladder_gains`` but never fed to the EWMA
+    trackers.  ``average=True`` also performs the
     step's exchange and mean (what the reference's simworkers does after
     run_iteration, simworkers.py:242-245) into ``IterationResult.averaged``;
     it is enqueued behind the speculative emit, so the device never waits for
@@ -491,7 +497,9 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     k1 = keep_count(length, theta_min)
     k2 = keep_count(k1, state.theta_s)
     extra = [float(c) for c in extra_cfs if kind.name == TOPK]
-    extra_ks = [keep_count(k1, c / theta_min) for c in extra]
+    # an extra CF >= theta_min nests under level 1 (compress_further from k1);
+    # one below theta_min is a plain compress of the whole gradient (larger k)
+    extra_ks = [keep_count(k1, c / theta_min) if c >= theta_min else keep_count(length, c) for c in extra]
 
     steps = []
     for w, (g, store) in enumerate(zip(grads, stores)):

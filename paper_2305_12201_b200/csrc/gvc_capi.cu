@@ -147,6 +147,13 @@ int gvc_prof_read(double *ms, unsigned long long *counts, int ncat)
 
 unsigned long long gvc_launch_count(void) { return g_launches.load(); }
 
+int gvc_select_phase_times(void *ws, unsigned long long *out, int n)
+{
+    if (!ws || !out || n < 1)
+        return set_error(GVC_ERR_ARG, "gvc_select_phase_times: bad arguments");
+    return select_phase_times(ws, out, n);
+}
+
 size_t gvc_select_workspace_bytes(int kind, uint64_t n) { return select_workspace_bytes(kind, n); }
 
 int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res, void *stream)

@@ -26,8 +26,6 @@
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)
 #define GVC_HL_BINS 4096     // refinement histogram per ladder entry (global)
 #define GVC_BLK_MAX (GVC_SEG_MAX / GVC_WARPS_PER_BLOCK)
-#define GVC_SAMPLE_BINS 16384  // shared-memory sample histogram (64 KB)
-#define GVC_SAMPLE_SHIFT 17    // 31-bit magnitude key >> 17 -> 14-bit bin (1/64 octave)
 #define GVC_MAX_LEVELS 3
 
 namespace gvc {
@@ -164,6 +162,66 @@ __device__ __forceinline__ float pending_resid(float r, int mode, float m)
         return __fsub_rn(r, __fmul_rn(sg, m));
     }
     return __fsub_rn(r, r);
+}
+
+// ------------------------------------------------------- grid barriers
+// For cooperative launches only (every CTA is resident, so a CTA spinning here
+// cannot starve one that has not started).  The counters live in the select
+// state, which is zeroed before every launch, so each barrier instance is
+// used once.  Spins are bounded: after ~4 s the barrier gives up and sets
+// bit 4 of *err (reported as GVC_ERR_STATE) instead of hanging the GPU.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+#define GVC_SPIN_LIMIT (1ll << 33)  // clock64 ticks (~4 s at 1.9 GHz)
+
+// All CTAs arrive; the CTA that arrives last runs `last_fn()` (whole block)
+// before the others are released, so its global writes are visible to every
+// CTA after the barrier (read them with ld_cg / volatile: L1 is not coherent).
+template <typename F>
+__device__ __forceinline__ void grid_sync_last(uint32_t *bar, uint32_t nblocks, uint32_t *err, F last_fn)
+{
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&bar[0], 1u) == nblocks - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        last_fn();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_u32(&bar[1], 1u);
+        }
+    } else if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire_u32(&bar[1]) == 0u) {
+            __nanosleep(40);
+            if (clock64() - t0 > GVC_SPIN_LIMIT) {
+                atomicOr(err, 4u);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_cg(const T *p)
+{
+    return __ldcg(p);
 }
 
 // Streaming loads / stores: the gradient and residual are touched once per

@@ -28,6 +28,7 @@ void prof_graph_pair(int cat, cudaEvent_t *a, cudaEvent_t *b);
 size_t select_workspace_bytes(int kind, uint64_t n);
 int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_result *res,
                cudaStream_t s);
+int select_phase_times(void *ws, unsigned long long *out, int n);
 int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t *out_idx, float *out_val,
              float *resid, uint32_t *smask, float *sm_out, uint32_t *tile_b, double *stats,
              const gvc_emit_mirrors *mirrors, cudaStream_t s);

@@ -1,0 +1,219 @@
+"""GPU parity at the sizes the benchmark measures, and the adaptive controller
+with an extra-CF ladder.
+
+BASELINE configs: C2 (ResNet101, 44.5M, Top-k CF search {10,100,1000}), C4
+(LSTM, 66M, Redsync and Random-k, CF {10,100}), C3 / north star (VGG16, 138M,
+Top-k ladder and DGC in both of its branches).  Each step runs through the
+drop-in ``run_iteration`` (EF, fused select, decision, emit, deferred residual,
+decompress-average) and is replayed on the C oracle: indices, chosen CF,
+averaged gradient and residual bit-exact; gains within 1e-6 (fp64 summation
+order only); Redsync values within 1e-6 (their fp64 mean is summed in a
+different order, compressors.py:188).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from tests.conftest import bits  # noqa: E402
+
+RTOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2305_12201_b200 as G
+    from paper_2305_12201_b200 import _native
+    _native.load()
+    return G
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def _gauss(n, seed):
+    return np.random.default_rng(seed).standard_normal(n, dtype=np.float32)
+
+
+def _ladder_k(n, k1, theta_min, c):
+    """Keep count of an extra CF (controller.run_iteration's nesting rule)."""
+    return O.keep_count(k1, c / theta_min) if c >= theta_min else O.keep_count(n, c)
+
+
+def _replay_step(kind, ef, k1, theta_s, it, w, rng):
+    """(i1, v1), (i2, v2): level 1 and the nested candidate of one worker (controller.py:232-250)."""
+    n = ef.size
+    s0, s1 = rng.split(it, w, 0), rng.split(it, w, 1)
+    if kind == "topk":
+        i1 = O.topk_indices(ef, k1)
+        v1 = ef[i1.astype(np.int64)]
+    else:
+        i1, v1 = O.select(kind, ef, k1, seed=s0.seed, stream=s0.stream)
+    i2, v2, _ = O.compress_further(kind, i1, v1, n, theta_s, seed=s1.seed, stream=s1.stream)
+    return (i1, v1), (i2, v2)
+
+
+def _run_chain(G, kind, n, steps, *, theta_min=10.0, theta_s=10.0, extra=(), epsilon=0.35, seed0=0):
+    """`steps` chained run_iteration steps of one worker vs the oracle replay."""
+    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=1000.0, epsilon=epsilon, window=1 << 30,
+                             compressor=G.CompressorKind(kind))
+    state = G.ControllerState.fresh(cfg, 1)
+    state.theta_s = theta_s
+    store = G.ResidualStore(n)
+    cost = G.CostModelParams(workers=1)
+    rng = G.SeededRng(7)
+    r_host = np.zeros(n, dtype=np.float32)
+    seen = []
+    for it in range(1, steps + 1):
+        g = _gauss(n, seed0 + it)
+        k1 = O.keep_count(n, state.theta_min)
+        ts = state.theta_s
+        res = G.run_iteration(state, G.GradientVector(g), store, cost, rng, extra_cfs=extra, average=True)
+        ef = O.ef_add(g, r_host)
+        norm = O.sq_norm(ef)
+        (i1, v1), (i2, v2) = _replay_step(kind, ef, k1, ts, it, 0, rng)
+        assert res.gain_min_raw == pytest.approx(min(1.0, O.sq_norm(v1) / norm), rel=RTOL)
+        assert res.gain_c_raw == pytest.approx(min(1.0, O.sq_norm(v2) / norm), rel=RTOL)
+        for c in extra:
+            kc = _ladder_k(n, k1, theta_min, c)
+            want = min(1.0, O.sq_norm(ef[O.topk_indices(ef, kc).astype(np.int64)]) / norm)
+            assert res.ladder_gains[c] == pytest.approx(want, rel=RTOL), (it, c)
+        seen.append(res.decision.choice)
+        assert res.decision.choice != "dense", (it, res.decision)
+        ci, cv = (i2, v2) if res.decision.choice == "candidate" else (i1, v1)
+        part = res.sent[0]
+        assert np.array_equal(host(part.indices), ci), it
+        if kind == "redsync":
+            np.testing.assert_allclose(host(part.vals), cv, rtol=RTOL)
+        else:
+            assert np.array_equal(bits(host(part.vals)), bits(cv)), it
+        # the step's average (one worker: fp64 sum / 1 -> fp32, simworkers.py:242-245)
+        want_avg = O.aggregate([(host(part.indices), host(part.vals))], n)
+        assert np.array_equal(bits(host(res.averaged.values)), bits(want_avg)), it
+        r_host = O.update_residual(ef, ci, host(part.vals))
+        assert np.array_equal(bits(host(store.residual)), bits(r_host)), it
+    return seen
+
+
+@pytest.mark.slow
+def test_resnet101_topk_ladder_44M(G):
+    """C2: 44.5M, Top-k with the CF search {10, 100, 1000} in one sweep, EF, 3 chained steps."""
+    seen = _run_chain(G, "topk", 44_500_000, 3, extra=(1000.0,))
+    assert seen
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind,eps", [("redsync", 0.25), ("randomk", 0.05)])
+def test_lstm_66M(G, kind, eps):
+    """C4: 66M, Redsync and Random-k at CF {10, 100}, EF, 2 chained steps."""
+    _run_chain(G, kind, 66_000_000, 2, epsilon=eps)
+
+
+@pytest.mark.slow
+def test_vgg16_topk_ladder_138M(G):
+    """North star: 138M, Top-k ladder {10, 100, 1000} + EF, 2 chained steps."""
+    _run_chain(G, "topk", 138_000_000, 2, extra=(1000.0,), seed0=20)
+
+
+@pytest.mark.slow
+def test_vgg16_dgc_138M_both_branches(G):
+    """C3: DGC at 138M in both branches of compressors.py:123-137 (seeds chosen
+    with the oracle so that one takes the exact branch and one the overshoot
+    pad + top-up branch), bit-exact against the oracle."""
+    n = 138_000_000
+    x = _gauss(n, 0)
+    g = G.GradientVector(x)
+    K = G.CompressorKind("dgc")
+    branches = set()
+    for cf, seed in ((10.0, 0), (10.0, 1), (100.0, 0), (100.0, 1)):
+        k = O.keep_count(n, cf)
+        rng = G.SeededRng(seed)
+        branches.add(O.dgc_overshoots(x, k, rng.seed, rng.stream))
+        s, _ = G.compress(K, g, cf, rng)
+        oi, ov = O.select("dgc", x, k, seed=rng.seed, stream=rng.stream)
+        assert np.array_equal(host(s.indices), oi), (cf, seed)
+        assert np.array_equal(bits(host(s.vals)), bits(ov)), (cf, seed)
+    assert branches == {True, False}
+
+
+@pytest.mark.slow
+def test_vgg16_dgc_run_iteration_138M(G):
+    """C3 through run_iteration: DGC level 1 over g_ef + level 2, EF, 2 chained steps."""
+    _run_chain(G, "dgc", 138_000_000, 2, seed0=40)
+
+
+# ------------------------------------------------- adaptive run + extra CFs
+@pytest.mark.parametrize("workers", [1, 2])
+def test_adaptive_run_with_extra_cfs(G, workers):
+    """The exponential policy with window 2 escalates theta_min and grows
+    theta_s while extra CFs on both sides of theta_min ride in the same sweep
+    (controller.py:85-105, 137-171): no error, and every ladder gain, the
+    chosen CF, the sent entries and the residual match the oracle."""
+    n = 400_003
+    extra = (20.0, 100.0, 160.0, 1000.0)
+    cfg = G.ControllerConfig(theta_min=10.0, theta_max=1000.0, epsilon=0.2, omega=0.9, window=2,
+                             policy="exponential", compressor=G.CompressorKind("topk"))
+    state = G.ControllerState.fresh(cfg, workers)
+    cost = G.CostModelParams(workers=workers)
+    rng = G.SeededRng(5)
+    stores = [G.ResidualStore(n) for _ in range(workers)]
+    r_host = [np.zeros(n, dtype=np.float32) for _ in range(workers)]
+    tmins = set()
+    for it in range(1, 15):
+        gs = [_gauss(n, 1000 * w + it) for w in range(workers)]
+        tmin, ts = state.theta_min, state.theta_s
+        tmins.add(tmin)
+        k1 = O.keep_count(n, tmin)
+        res = G.run_iteration(state, [G.GradientVector(x) for x in gs], stores, cost, rng, extra_cfs=extra)
+        efs = [O.ef_add(gs[w], r_host[w]) for w in range(workers)]
+        norms = [O.sq_norm(e) for e in efs]
+        want = {}
+        for c in (tmin, tmin * ts, *extra):
+            kc = k1 if c == tmin else (O.keep_count(k1, ts) if c == tmin * ts else _ladder_k(n, k1, tmin, c))
+            gains = [min(1.0, O.sq_norm(e[O.topk_indices(e, kc).astype(np.int64)]) / nv) if kc < n else 1.0
+                     for e, nv in zip(efs, norms)]
+            want[c] = sum(gains) / workers
+        for c in extra:
+            assert res.ladder_gains[c] == pytest.approx(want[c], rel=RTOL), (it, c)
+        assert res.gain_min_raw == pytest.approx(want[tmin], rel=RTOL)
+        assert res.gain_c_raw == pytest.approx(want[tmin * ts], rel=RTOL)
+        for w in range(workers):
+            if res.decision.choice == "dense":
+                r_host[w] = np.zeros(n, dtype=np.float32)
+                continue
+            kc = k1 if res.decision.choice == "minimum" else O.keep_count(k1, ts)
+            ci = O.topk_indices(efs[w], kc)
+            cv = efs[w][ci.astype(np.int64)]
+            assert np.array_equal(host(res.sent[w].indices), ci), (it, w)
+            assert np.array_equal(bits(host(res.sent[w].vals)), bits(cv)), (it, w)
+            r_host[w] = O.update_residual(efs[w], ci, cv)
+            assert np.array_equal(bits(host(stores[w].residual)), bits(r_host[w])), (it, w)
+    assert len(tmins) > 1, tmins  # theta_min escalated at least once
+
+
+def test_identity_level1_with_extra_cfs(G):
+    """theta_min == 1 with extra CFs: at policy step 0 the candidate is CF 1 too
+    (k2 == n), so the candidate sends all of g_ef (compress_further copies,
+    compressors.py:239-240) and the residual becomes zero; the extra CFs' gains
+    are still reported."""
+    n = 200_001
+    cfg = G.ControllerConfig(theta_min=1.0, theta_max=1000.0, epsilon=0.5, window=1 << 30,
+                             compressor=G.CompressorKind("topk"))
+    state = G.ControllerState.fresh(cfg, 1)
+    store = G.ResidualStore(n)
+    cost = G.CostModelParams(workers=1)
+    g = _gauss(n, 3)
+    res = G.run_iteration(state, G.GradientVector(g), store, cost, G.SeededRng(1), extra_cfs=(10.0, 100.0))
+    assert res.decision.choice == "candidate" and res.decision.cf == 1.0
+    assert res.floats_sent == n and res.sent[0].kept == n
+    assert np.array_equal(bits(host(res.sent[0].vals)), bits(g))
+    assert not host(store.residual).any()
+    for c in (10.0, 100.0):
+        k = O.keep_count(n, c)
+        want = O.sq_norm(g[O.topk_indices(g, k).astype(np.int64)]) / O.sq_norm(g)
+        assert res.ladder_gains[c] == pytest.approx(want, rel=RTOL)
