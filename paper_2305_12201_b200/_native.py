@@ -140,7 +140,8 @@ def load(build_if_missing: bool = False):
         L.gvc_prof_enable.restype = None
         L.gvc_prof_read.argtypes = [_vp, _vp, ctypes.c_int]
         L.gvc_launch_count.restype = ctypes.c_ulonglong
-        L.gvc_select_phase_times.argtypes = [_vp, _vp, ctypes.c_int]
+        if hasattr(L, "gvc_select_phase_times"):  # diagnostic
+            L.gvc_select_phase_times.argtypes = [_vp, _vp, ctypes.c_int]
         if L.gvc_abi_version() != 1:
             raise ImportError("libgravac_b200 ABI version mismatch")
         _lib = L

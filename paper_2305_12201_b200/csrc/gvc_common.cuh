@@ -26,6 +26,8 @@
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)
 #define GVC_HL_BINS 4096     // refinement histogram per ladder entry (global)
 #define GVC_BLK_MAX (GVC_SEG_MAX / GVC_WARPS_PER_BLOCK)
+#define GVC_SAMPLE_BINS 16384  // shared-memory sample histogram (64 KB)
+#define GVC_SAMPLE_SHIFT 17    // 31-bit magnitude key >> 17 -> 14-bit bin (1/64 octave)
 #define GVC_MAX_LEVELS 3
 
 namespace gvc {
@@ -184,31 +186,37 @@ __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v)
 
 #define GVC_SPIN_LIMIT (1ll << 33)  // clock64 ticks (~4 s at 1.9 GHz)
 
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // All CTAs arrive; the CTA that arrives last runs `last_fn()` (whole block)
 // before the others are released, so its global writes are visible to every
-// CTA after the barrier (read them with ld_cg / volatile: L1 is not coherent).
+// CTA after the barrier.  Release/acquire at gpu scope by one thread per CTA
+// (bar.sync orders the rest of the block); read what other CTAs wrote with
+// ld_cg, ideally once per CTA (a line every thread of the grid polls is an L2
+// hot spot).
 template <typename F>
 __device__ __forceinline__ void grid_sync_last(uint32_t *bar, uint32_t nblocks, uint32_t *err, F last_fn)
 {
     __shared__ int s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_acq_rel_gpu();
         s_last = atomicAdd(&bar[0], 1u) == nblocks - 1;
+        if (s_last)
+            fence_acq_rel_gpu();
     }
     __syncthreads();
     if (s_last) {
-        __threadfence();
         last_fn();
         __syncthreads();
         if (threadIdx.x == 0) {
-            __threadfence();
+            fence_acq_rel_gpu();
             st_release_u32(&bar[1], 1u);
         }
     } else if (threadIdx.x == 0) {
         const long long t0 = clock64();
         while (ld_acquire_u32(&bar[1]) == 0u) {
-            __nanosleep(40);
+            __nanosleep(32);
             if (clock64() - t0 > GVC_SPIN_LIMIT) {
                 atomicOr(err, 4u);
                 break;
@@ -222,6 +230,19 @@ template <typename T>
 __device__ __forceinline__ T ld_cg(const T *p)
 {
     return __ldcg(p);
+}
+
+// One L2 read per CTA of a value another CTA wrote, broadcast through shared
+// memory (contains a __syncthreads).
+template <typename T>
+__device__ __forceinline__ T bcast_cg(const T *p)
+{
+    __shared__ T v;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        v = __ldcg(p);
+    __syncthreads();
+    return v;
 }
 
 // Streaming loads / stores: the gradient and residual are touched once per

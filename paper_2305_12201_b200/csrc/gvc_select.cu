@@ -29,6 +29,7 @@
 //   k_emit (gvc_emit)             ordered (idx, val) compaction of one entry,
 //                                 fused residual update
 #include <algorithm>
+#include <type_traits>
 #include <mutex>
 #include <stdio.h>
 #include <string>
@@ -61,10 +62,8 @@ struct SelState {
     JState js[GVC_MAX_LADDER];
     float redsync_mean[GVC_MAX_LADDER];
     uint32_t fin_done;     // k_finish blocks done (the last one writes the status)
-    uint32_t s_bin;        // sample: coarse bin holding the target rank (~0u: exact path)
-    unsigned long long s_above;  // sample: sampled keys above that bin
-    uint32_t bar[8][2];    // grid barriers of the cooperative kernels (arrive, release)
-    unsigned long long t_phase[16];  // %globaltimer at phase boundaries (gvc_select_phase_times)
+    uint32_t sample_done;  // k_sample blocks done (the last one resolves key_est)
+    unsigned long long t_phase[32];  // %globaltimer at kernel boundaries (gvc_select_phase_times)
 };
 
 struct Plan {
@@ -83,9 +82,8 @@ struct Plan {
     uint32_t *pmask;
     const float *pm;
     int pmode;
-    // sample: the head of every segment (k_collect_coop), target rank in it
-    uint64_t s_target;
-    int sample_head;  // k_collect_coop samples its first step and resolves key_est in-kernel
+    // sample
+    uint64_t s_chunks, s_stride, s_target;
     uint32_t hash_key_est;
     // workspace
     SelState *st;
@@ -135,7 +133,7 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
     q->st = (SelState *)take(sizeof(SelState));
     q->hist0 = (uint32_t *)take(GVC_H0_BINS * 4);
     q->histl = (uint32_t *)take(L * GVC_HL_BINS * 4);
-    q->shist = (uint32_t *)take(2 * GVC_H0_BINS * 4);  // coarse + fine sample histograms
+    q->shist = (uint32_t *)take(GVC_SAMPLE_BINS * 4);
     q->seg_cnt = (uint32_t *)take(SM * 4);
     q->seg_mcnt = (uint32_t *)take(SM * 4);
     q->seg_band = (uint32_t *)take(L * SM * 4);
@@ -193,6 +191,172 @@ __device__ __forceinline__ void load_cand4(const Plan &p, uint64_t beg, uint32_t
     }
 }
 
+// ------------------------------------------------------------------ sample
+// Strided chunks of 128 contiguous values -> 14-bit shared-memory histogram of
+// magnitude keys, merged into global memory once per block.  Reads ~1.5%.
+__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh);
+
+__global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
+{
+    pdl_enter();
+    extern __shared__ uint32_t sh[];
+    for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
+        sh[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * 32;
+    const float pm = (p.pmask && p.pmode == 2) ? *p.pm : 0.f;
+    uint32_t kmax = 0;
+    for (uint64_t c = blockIdx.x * 32 + (threadIdx.x >> 5); c < p.s_chunks; c += warps) {
+        const uint64_t base = c * p.s_stride;
+        float v[4];
+        bool ok[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint64_t i = base + (uint64_t)q * 32 + lane;
+            ok[q] = i < p.n && i < base + 128;
+            if (ok[q]) {
+                if (p.ef) {
+                    float r = p.resid[i];
+                    if (p.pmask && ((p.pmask[i >> 5] >> (i & 31)) & 1u))
+                        r = pending_resid(r, p.pmode, pm);
+                    v[q] = __fadd_rn(p.g[i], r);
+                } else {
+                    v[q] = p.values[i];
+                }
+            } else {
+                v[q] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint32_t k = mag_key(v[q]);
+            if (ok[q] && k <= 0x7f800000u) {
+                atomicAdd(&sh[k >> GVC_SAMPLE_SHIFT], 1u);
+                kmax = max(kmax, k);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    // one global atomic per block: a per-warp atomicMax serialises thousands of
+    // updates on one line
+    __shared__ uint32_t s_kmax;
+    if (threadIdx.x == 0)
+        s_kmax = 0;
+    __syncthreads();
+    if (lane == 0 && kmax)
+        atomicMax(&s_kmax, kmax);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_kmax)
+        atomicMax(&p.st->max_key, s_kmax);
+    for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
+        if (sh[i])
+            atomicAdd(&p.shist[i], sh[i]);
+    // the last block to finish resolves key_est (no separate launch)
+    // (the block's histogram atomics are ordered before thread 0's device-scope
+    // fence by the barrier -- fence cumulativity -- so one thread fences)
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&p.st->sample_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        sample_resolve_body(p, reinterpret_cast<unsigned long long *>(sh));
+    }
+}
+
+// Chooses key_est (a lower bound for the k_0-th largest key, w.h.p.) and the
+// level-0 bin shift.  Magnitude keys: from the sample histogram.  Hash keys:
+// from the binomial tail (host-computed).
+__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh)
+{
+    SelState *st = p.st;
+    if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
+        if (threadIdx.x == 0) {
+            // the k-th largest key sits just above the sampled threshold: fine
+            // level-0 bins there (4096 keys, 1/2048 of an octave; the top bin is
+            // open-ended), so level 1 resolves it.  Bins sized to the whole key
+            // range instead left ~10^5 members for the single-block refinement.
+            st->key_est = *p.key_est_dev;
+            st->shift0 = 12;
+        }
+        return;
+    }
+    if (p.force_exact == 2) {  // test hook: an estimate that must miss -> exercises the refill path
+        if (threadIdx.x == 0) {
+            st->key_est = 0xffffffffu;
+            st->shift0 = 0;
+        }
+        return;
+    }
+    if (p.keymode == KEY_HASH) {
+        if (threadIdx.x == 0) {
+            uint32_t est = p.force_exact ? 0u : p.hash_key_est;
+            st->key_est = est;
+            uint64_t span = (1ull << 32) - est;
+            int shf = bitlen64(span - 1) - 12;
+            st->shift0 = shf < 0 ? 0 : shf;
+        }
+        return;
+    }
+    if (p.force_exact || p.s_target == 0) {
+        if (threadIdx.x == 0) {
+            st->key_est = 0;
+            st->shift0 = 19;  // 31-bit keys over 4096 bins
+        }
+        return;
+    }
+    constexpr int PER = GVC_SAMPLE_BINS / 1024;  // 16 bins per thread
+    const int t = threadIdx.x;
+    uint32_t h[PER];
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.shist + t * PER);
+    unsigned long long local = 0;
+#pragma unroll
+    for (int q = 0; q < PER / 4; q++) {
+        uint4 x = src[q];
+        h[4 * q] = x.x;
+        h[4 * q + 1] = x.y;
+        h[4 * q + 2] = x.z;
+        h[4 * q + 3] = x.w;
+        local += (unsigned long long)x.x + x.y + x.z + x.w;
+    }
+    unsigned long long total;
+    unsigned long long pre = block_excl_prefix(local, sh, &total);
+    unsigned long long acc = total - pre - local;  // keys in bins above my range
+    const unsigned long long target = p.s_target;
+    if (total < target) {  // too few sampled values (e.g. NaN-only): exact path
+        if (t == 0) {
+            st->key_est = 0;
+            st->shift0 = 19;
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = PER - 1; i >= 0; i--) {
+        if (acc < target && acc + h[i] >= target) {
+            uint32_t est = (uint32_t)(t * PER + i) << GVC_SAMPLE_SHIFT;
+            st->key_est = est;
+            uint32_t mk = st->max_key;
+            uint64_t span = mk > est ? (uint64_t)(mk - est) : 0;
+            int shf = bitlen64(span) - 12;
+            st->shift0 = shf < 0 ? 0 : shf;
+        }
+        acc += h[i];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
+{
+    pdl_enter();
+    __shared__ unsigned long long sh[33];
+    sample_resolve_body(p, sh);
+}
+
 // ----------------------------------------------------------------- collect
 // Candidate compaction for 4 consecutive values of one lane (lane-major index
 // order within the warp).  Straight-line so the ballots stay convergent; the
@@ -227,88 +391,17 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
     ccount += __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
 }
 
-// Step 0 of a segment, EF applied and stored: what k_collect_coop's sample
-// head keeps in registers across its barriers (the next steps were prefetched
-// into L2, so they cost no registers while the grid waits).
-struct Head {
-    float4 a[2];  // step 0: g_ef (or the plain values)
-};
-
-// L2 prefetch of `bytes` (multiple of 16) at p: one bulk request, no registers.
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// The 256-value step at `at`: g (or values) into x, r into y, the step's 8
-// pending-mask words into w (lanes 0..7).
-template <bool EF, int PM>
-__device__ __forceinline__ void load_step(const float *src, const float *rp, const uint32_t *mp, uint32_t at,
-                                          int lane, float4 (&x)[2], float4 (&y)[2], uint32_t &w)
-{
-#pragma unroll
-    for (int u = 0; u < 2; u++) {
-        x[u] = ld_stream(reinterpret_cast<const float4 *>(src + at + u * 128) + lane);
-        if (EF)
-            y[u] = ld_stream(reinterpret_cast<const float4 *>(rp + at + u * 128) + lane);
-    }
-    if (EF && PM && lane < 8)
-        w = mp[(at >> 5) + lane];
-}
-
-// EF on one loaded step: the deferred residual update of the previous step
-// (mask bits, cleared after use), g_ef = fl32(g + r) stored over r.
-template <int PM>
-__device__ __forceinline__ void ef_step(const Plan &p, uint64_t beg, float *rp, uint32_t at, int lane, float pm,
-                                        float4 (&a)[2], float4 (&b)[2], uint32_t wreg)
-{
-    if (PM) {
-        // the 8 mask words of this step (lanes 0..7), shuffled to the
-        // lanes owning their 4-bit slices, cleared after use
-#pragma unroll
-        for (int u = 0; u < 2; u++) {
-            const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
-            b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
-            b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
-            b[u].z = (bits & 4u) ? pending_resid(b[u].z, PM, pm) : b[u].z;
-            b[u].w = (bits & 8u) ? pending_resid(b[u].w, PM, pm) : b[u].w;
-        }
-        if (wreg)
-            p.pmask[(beg >> 5) + (at >> 5) + lane] = 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 2; u++) {
-        a[u].x = __fadd_rn(a[u].x, b[u].x);
-        a[u].y = __fadd_rn(a[u].y, b[u].y);
-        a[u].z = __fadd_rn(a[u].z, b[u].z);
-        a[u].w = __fadd_rn(a[u].w, b[u].w);
-        st_stream(reinterpret_cast<float4 *>(rp + at + u * 128) + lane, a[u]);
-    }
-}
-
-__device__ __forceinline__ void norm_step(const float4 (&a)[2], double &nacc)
-{
-#pragma unroll
-    for (int u = 0; u < 2; u++) {
-        const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
-#pragma unroll
-        for (int c = 0; c < 4; c++)
-            nacc = __fma_rn((double)v[c], (double)v[c], nacc);
-    }
-}
-
 // One warp per segment.  EF: v = fl32(g + r_true) written back over r (the only
 // full-size write of the step), where r_true applies the previous step's
 // deferred residual update (PM = pending mode, 0 none); !EF: v read from
 // `values`.  REFILL re-collects from the already-written g_ef with key_est = 0
 // (exactness fallback).  NaN keys are always candidates and are flagged by the
-// candidate passes, not here.  HEAD: step 0 was already loaded, EF'd, stored
-// and normed by the sample head (hd), and step 1's loads are in flight there.
-// Adds the warp's fp64 squares to nacc.
+// candidate passes, not here.
+// One warp's pass over segment `seg` (k_collect's body; also the inline
+// exactness refill of k_collect's last block).  Adds the warp's fp64 squares to nacc.
 template <int KM, bool EF, int PM, bool REFILL>
 __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int lane, uint32_t *h, uint32_t dummy,
-                                                uint32_t key_est, int shift0, float pm, double &nacc,
-                                                const Head *hd = nullptr)
+                                                uint32_t key_est, int shift0, float pm, double &nacc)
 {
     constexpr bool refill = REFILL;
     const bool do_ef = EF && !refill;
@@ -332,37 +425,73 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
     // the step's 8 pending-mask words (lanes 0..7), prefetched with the data
     // when PF: a mask load issued at its use was the kernel's top stall (ncu)
     uint32_t wreg = 0u;
-    if (PF && !REFILL && hd) {
-        if (nfull) {  // nfull >= 512: step 1 exists
+    if (PF && nfull) {
 #pragma unroll
-            for (int u = 0; u < 2; u++) {
-                const float v[4] = {hd->a[u].x, hd->a[u].y, hd->a[u].z, hd->a[u].w};
-                push4<KM>(p, v, (uint32_t)beg + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval, cidx,
-                          ccount);
-            }
-            i = STEP;
-            load_step<EF, PM>(src, rp, mp, STEP, lane, a, b, wreg);  // prefetched into L2 by the head
+        for (int u = 0; u < 2; u++) {
+            a[u] = ld_stream(reinterpret_cast<const float4 *>(src + u * 128) + lane);
+            if (do_ef)
+                b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + u * 128) + lane);
         }
-    } else if (PF && nfull) {
-        load_step<EF && !REFILL, PM>(src, rp, mp, 0, lane, a, b, wreg);
+        if (do_ef && PM && lane < 8)
+            wreg = mp[lane];
     }
     for (; i < nfull; i += STEP) {
         float4 na[2], nb[2];
         uint32_t nw = 0u;
         const bool more = i + STEP < nfull;
         if (PF) {
-            if (more)
-                load_step<EF && !REFILL, PM>(src, rp, mp, i + STEP, lane, na, nb, nw);
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    na[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + STEP + u * 128) + lane);
+                    if (do_ef)
+                        nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
+                }
+                if (do_ef && PM && lane < 8)
+                    nw = mp[((i + STEP) >> 5) + lane];
+            }
         } else {
-            load_step<EF && !REFILL, PM>(src, rp, mp, i, lane, a, b, wreg);
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                a[u] = ld_stream(reinterpret_cast<const float4 *>(src + i + u * 128) + lane);
+                if (do_ef)
+                    b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + u * 128) + lane);
+            }
+            if (do_ef && PM && lane < 8)
+                wreg = mp[(i >> 5) + lane];
         }
-        if (do_ef)
-            ef_step<PM>(p, beg, rp, i, lane, pm, a, b, wreg);
-        if (!refill)
-            norm_step(a, nacc);
+        if (do_ef) {
+            if (PM) {
+                // the 8 mask words of this step (lanes 0..7), shuffled to the
+                // lanes owning their 4-bit slices, cleared after use
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
+                    b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
+                    b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
+                    b[u].z = (bits & 4u) ? pending_resid(b[u].z, PM, pm) : b[u].z;
+                    b[u].w = (bits & 8u) ? pending_resid(b[u].w, PM, pm) : b[u].w;
+                }
+                if (wreg)
+                    p.pmask[(beg >> 5) + (i >> 5) + lane] = 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                a[u].x = __fadd_rn(a[u].x, b[u].x);
+                a[u].y = __fadd_rn(a[u].y, b[u].y);
+                a[u].z = __fadd_rn(a[u].z, b[u].z);
+                a[u].w = __fadd_rn(a[u].w, b[u].w);
+                st_stream(reinterpret_cast<float4 *>(rp + i + u * 128) + lane, a[u]);
+            }
+        }
 #pragma unroll
         for (int u = 0; u < 2; u++) {
             const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+            if (!refill) {
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    nacc = __fma_rn((double)v[c], (double)v[c], nacc);
+            }
             push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
                       cidx, ccount);
         }
@@ -405,6 +534,44 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
         p.seg_cnt[seg] = ccount;
 }
 
+template <int KM, bool EF, int PM, bool REFILL = false>
+__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int)
+{
+    pdl_enter();
+    // compile-time: a runtime flag would leave predicated refill / no-refill
+    // code under every value of the hot loop
+    constexpr bool refill = REFILL;
+    __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
+    __shared__ double red[GVC_WARPS_PER_BLOCK];
+    if (refill && !p.st->fallback)
+        return;
+    for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += GVC_THREADS)
+        h[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
+    const uint32_t key_est = refill ? 0u : p.st->key_est;
+    const int shift0 = refill ? (KM == KEY_MAG ? 19 : 20) : p.st->shift0;
+    const float pm = (EF && PM == 2 && !refill) ? *p.pm : 0.f;
+    const uint32_t dummy = GVC_H0_BINS + lane;
+    double nacc = 0.0;
+    if (seg < p.S)
+        collect_segment<KM, EF, PM, REFILL>(p, seg, lane, h, dummy, key_est, shift0, pm, nacc);
+    nacc = warp_sum_f64(nacc);
+    if (lane == 0)
+        red[warp] = nacc;
+    __syncthreads();
+    if (threadIdx.x == 0 && !refill) {
+        double b = 0.0;
+        for (int w = 0; w < GVC_WARPS_PER_BLOCK; w++)
+            b += red[w];
+        p.blk_norm[blockIdx.x] = b;
+    }
+    for (int i = threadIdx.x; i < GVC_H0_BINS; i += GVC_THREADS)
+        if (h[i])
+            atomicAdd(&p.hist0[i], h[i]);
+}
+
 // ----------------------------------------------------------------- resolve
 __device__ void set_jstate(JState &js, unsigned long long lo, unsigned long long hi, unsigned long long above,
                            unsigned long long need)
@@ -431,30 +598,51 @@ __device__ __forceinline__ void find_crossings(const uint32_t *h, unsigned long 
     const int t = threadIdx.x;
     uint32_t c[PER];
     unsigned long long local = 0;
+    if constexpr (PER % 4 == 0) {
 #pragma unroll
-    for (int q = 0; q < PER / 4; q++) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(h) + t * (PER / 4) + q;
-        const uint4 x = CG ? ld_cg(src) : *src;
-        c[4 * q] = x.x;
-        c[4 * q + 1] = x.y;
-        c[4 * q + 2] = x.z;
-        c[4 * q + 3] = x.w;
-        local += (unsigned long long)x.x + x.y + x.z + x.w;
+        for (int q = 0; q < PER / 4; q++) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(h) + t * (PER / 4) + q;
+            const uint4 x = CG ? ld_cg(src) : *src;
+            c[4 * q] = x.x;
+            c[4 * q + 1] = x.y;
+            c[4 * q + 2] = x.z;
+            c[4 * q + 3] = x.w;
+            local += (unsigned long long)x.x + x.y + x.z + x.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            c[q] = CG ? ld_cg(h + t * PER + q) : h[t * PER + q];
+            local += c[q];
+        }
     }
     unsigned long long total;
     unsigned long long pre = block_excl_prefix(local, sh, &total);
-    unsigned long long acc = total - pre - local;
-    for (int i = PER - 1; i >= 0; i--) {
-        for (int j = 0; j < nneed; j++)
-            if (acc < need[j] && acc + c[i] >= need[j])
-                fn(j, PER * t + i, acc);
-        acc += c[i];
+    // count strictly above my bins / including them: a need crosses here iff
+    // acc_lo < need <= acc_hi (one load per need, the bin scan only where it crosses)
+    const unsigned long long acc_lo = total - pre - local, acc_hi = total - pre;
+    for (int j = 0; j < nneed; j++) {
+        const unsigned long long nd = need[j];
+        if (acc_lo < nd && nd <= acc_hi) {
+            unsigned long long acc = acc_lo;
+            int hit = -1;
+            unsigned long long hit_acc = 0;
+#pragma unroll
+            for (int i = PER - 1; i >= 0; i--) {
+                if (hit < 0 && acc + c[i] >= nd) {
+                    hit = i;
+                    hit_acc = acc;
+                }
+                acc += c[i];
+            }
+            fn(j, PER * t + hit, hit_acc);
+        }
     }
 }
 
 // Level 0: candidate total, fallback decision, first interval per ladder entry.
 // PER = 4096 / blockDim bins per thread.
-template <int PER = 4>
+template <int PER>
 __device__ void resolve_level0(const Plan &p, int pass, unsigned long long *sh, unsigned long long *need)
 {
     SelState *st = p.st;
@@ -518,237 +706,36 @@ __device__ void resolve_level0(const Plan &p, int pass, unsigned long long *sh, 
     }
 }
 
-// ------------------------------------------ cooperative collect (+ sample)
-// Sample head: the first step (256 values) of every segment of a CTA's first
-// block of segments -- data the pass reads anyway -- histogrammed by 31-bit
-// magnitude key >> 19 (4096 coarse bins, 1/16 octave), then the coarse bin
-// holding the target rank is refined by (key >> 7) & 4095.  Two grid
-// barriers; the CTA arriving last at each resolves.
-#define GVC_COARSE_SHIFT 19
-#define GVC_FINE_SHIFT 7
-
-__device__ __forceinline__ unsigned long long gtime()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#define GVC_TMARK(i)                                                                                          \
-    do {                                                                                                      \
-        if (threadIdx.x == 0)                                                                                 \
-            st->t_phase[i] = gtime();                                                                         \
-    } while (0)
-
-// key_est / shift0 when there is no sample to take (plan-derived, identical in every CTA).
-__device__ __forceinline__ void plan_key_est(const Plan &p, uint32_t &key_est, int &shift0)
-{
-    if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
-        // fine level-0 bins just above the threshold (4096 keys, 1/2048 of an
-        // octave; the top bin is open-ended), so level 1 resolves the k-th key
-        key_est = *p.key_est_dev;
-        shift0 = 12;
-    } else if (p.force_exact == 2) {  // test hook: an estimate that must miss -> the refill path
-        key_est = 0xffffffffu;
-        shift0 = 0;
-    } else if (p.keymode == KEY_HASH) {
-        key_est = p.force_exact ? 0u : p.hash_key_est;
-        const uint64_t span = (1ull << 32) - key_est;
-        const int shf = bitlen64(span - 1) - 12;
-        shift0 = shf < 0 ? 0 : shf;
-    } else {  // exact path: every value is a candidate
-        key_est = 0u;
-        shift0 = 19;  // 31-bit keys over 4096 bins
-    }
-}
-
-// Merge a CTA's shared-memory histogram (4096 bins) into global memory.
-__device__ __forceinline__ void merge_hist(const uint32_t *h, uint32_t *g)
-{
-    for (int i = threadIdx.x; i < GVC_H0_BINS; i += blockDim.x)
-        if (h[i])
-            atomicAdd(&g[i], h[i]);
-}
-
-__device__ __forceinline__ void zero_hist(uint32_t *h)
-{
-    __syncthreads();
-    for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += blockDim.x)
-        h[i] = 0;
-    __syncthreads();
-}
-
-// One cooperative launch (every CTA resident; grid <= B, CTAs stride over the
-// blocks of 8 segments): [sample head + key_est] -> the streaming pass of
-// k_collect -> level-0 resolve by the last CTA -> (rare) exactness refill by
-// every CTA + level-0 resolve again.  Replaces k_sample + k_collect + k_resolve0.
-template <int KM, bool EF, int PM>
-__global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect_coop(const Plan p, int)
+// Level 0 (one block): candidate total, first interval per ladder entry.  If
+// the sampled estimate overshot (fewer than k_0 candidates) the same block
+// re-collects every segment with key_est = 0 -- the exactness refill, taken
+// with probability ~1e-7 per step, so it lives here instead of as two
+// early-exit launches in every select graph -- and resolves level 0 again.
+template <int KM, bool EF>
+__global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int)
 {
     pdl_enter();
-    constexpr int PER = GVC_H0_BINS / GVC_THREADS;  // histogram bins per thread in the resolves
-    __shared__ uint32_t h[GVC_H0_BINS + 32];        // + per-lane dummy bins
-    __shared__ double red[GVC_WARPS_PER_BLOCK];
-    __shared__ unsigned long long shs[33];
+    __shared__ unsigned long long sh[33];
     __shared__ unsigned long long need[GVC_MAX_LADDER];
-    SelState *st = p.st;
-    uint32_t *err = &st->nan_flag;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t nblk = gridDim.x;
-    if (blockIdx.x == 0)
-        GVC_TMARK(0);
-    zero_hist(h);
-    const float pm = (EF && PM == 2) ? *p.pm : 0.f;
-    const uint32_t dummy = GVC_H0_BINS + lane;
-    uint32_t key_est;
-    int shift0;
-    Head hd;
-    bool head = false;
-    double nacc = 0.0;
-    if (KM == KEY_MAG && p.sample_head) {
-        const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
-        if (seg < p.S) {
-            const uint64_t beg = (uint64_t)seg * p.seg_len;
-            const uint32_t len = (uint32_t)(min(p.n, beg + p.seg_len) - beg);
-            if (len >= GVC_SEG_QUANTUM) {  // a whole 512-chunk: steps 0 and 1 exist
-                const float *src = (EF ? p.g : p.values) + beg;
-                float *rp = p.resid + beg;
-                const uint32_t *mp = p.pmask + (beg >> 5);
-                float4 b[2];
-                uint32_t w = 0u;
-                load_step<EF, PM>(src, rp, mp, 0, lane, hd.a, b, w);
-                // steps 1..3 into L2 while the grid resolves the sample
-                const uint32_t pf = min(len, 4u * 256u) - 256u;
-                if (lane == 0)
-                    prefetch_l2(src + 256, pf * 4);
-                if (EF && lane == 1)
-                    prefetch_l2(rp + 256, pf * 4);
-                if (EF)
-                    ef_step<PM>(p, beg, rp, 0, lane, pm, hd.a, b, w);
-                norm_step(hd.a, nacc);
-                head = true;
-            }
-        }
-        uint32_t kmax = 0;
-        if (head) {
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                const float v[4] = {hd.a[u].x, hd.a[u].y, hd.a[u].z, hd.a[u].w};
-#pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    const uint32_t k = mag_key(v[c]);
-                    if (k <= 0x7f800000u) {
-                        atomicAdd(&h[k >> GVC_COARSE_SHIFT], 1u);
-                        kmax = max(kmax, k);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-        if (lane == 0 && kmax)
-            atomicMax(&st->max_key, kmax);
-        __syncthreads();
-        merge_hist(h, p.shist);
-        grid_sync_last(st->bar[0], nblk, err, [&] {
-            GVC_TMARK(1);
-            if (threadIdx.x == 0) {  // defaults: too few sampled values -> exact path
-                st->s_bin = 0xffffffffu;
-                st->key_est = 0u;
-                st->shift0 = 19;
-            }
-            __syncthreads();
-            const unsigned long long tgt = p.s_target;
-            find_crossings<PER, true>(p.shist, shs, 1, &tgt, [&](int, int b, unsigned long long above) {
-                st->s_bin = (uint32_t)b;
-                st->s_above = above;
-            });
-            GVC_TMARK(2);
-        });
-        const uint32_t bstar = ld_cg(&st->s_bin);
-        if (bstar != 0xffffffffu) {  // uniform across the grid
-            zero_hist(h);
-            if (head) {
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    const float v[4] = {hd.a[u].x, hd.a[u].y, hd.a[u].z, hd.a[u].w};
-#pragma unroll
-                    for (int c = 0; c < 4; c++) {
-                        const uint32_t k = mag_key(v[c]);
-                        if ((k >> GVC_COARSE_SHIFT) == bstar)
-                            atomicAdd(&h[(k >> GVC_FINE_SHIFT) & (GVC_H0_BINS - 1)], 1u);
-                    }
-                }
-            }
-            __syncthreads();
-            merge_hist(h, p.shist + GVC_H0_BINS);
-            grid_sync_last(st->bar[1], nblk, err, [&] {
-                GVC_TMARK(3);
-                const unsigned long long tgt = p.s_target - ld_cg(&st->s_above);
-                find_crossings<PER, true>(p.shist + GVC_H0_BINS, shs, 1, &tgt,
-                                          [&](int, int f, unsigned long long) {
-                                              const uint32_t est = (bstar << GVC_COARSE_SHIFT) |
-                                                                   ((uint32_t)f << GVC_FINE_SHIFT);
-                                              const uint32_t mk = ld_cg(&st->max_key);
-                                              const uint64_t span = mk > est ? (uint64_t)(mk - est) : 0;
-                                              const int shf = bitlen64(span) - 12;
-                                              st->key_est = est;
-                                              st->shift0 = shf < 0 ? 0 : shf;
-                                          });
-                GVC_TMARK(4);
-            });
-        }
-        key_est = ld_cg(&st->key_est);
-        shift0 = ld_cg(&st->shift0);
-        zero_hist(h);
-    } else {
-        plan_key_est(p, key_est, shift0);
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            st->key_est = key_est;
-            st->shift0 = shift0;
-        }
-    }
-    // ---- the streaming pass (g_ef, norm, candidates, level-0 histogram)
-    for (uint32_t b = blockIdx.x; b < p.B; b += nblk) {
-        const uint32_t seg = b * GVC_WARPS_PER_BLOCK + warp;
-        if (seg < p.S)
-            collect_segment<KM, EF, PM, false>(p, seg, lane, h, dummy, key_est, shift0, pm, nacc,
-                                               (head && b == blockIdx.x) ? &hd : nullptr);
-        const double wsum = warp_sum_f64(nacc);
-        nacc = 0.0;
-        if (lane == 0)
-            red[warp] = wsum;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < GVC_WARPS_PER_BLOCK; w++)
-                t += red[w];
-            p.blk_norm[b] = t;
-        }
-        __syncthreads();
-    }
-    if (blockIdx.x == 0)
-        GVC_TMARK(7);
-    merge_hist(h, p.hist0);
-    // ---- level 0 by the last CTA; the (rare) exactness refill by every CTA
-    grid_sync_last(st->bar[2], nblk, err, [&] {
-        GVC_TMARK(5);
-        resolve_level0<PER>(p, 0, shs, need);
-        GVC_TMARK(6);
-    });
-    if (!ld_cg(&st->fallback))
-        return;
-    zero_hist(h);
-    const int rshift = KM == KEY_MAG ? 19 : 20;
-    for (uint32_t b = blockIdx.x; b < p.B; b += nblk) {
-        const uint32_t seg = b * GVC_WARPS_PER_BLOCK + warp;
-        double unused = 0.0;  // the refill does not re-accumulate the norm
-        if (seg < p.S)
-            collect_segment<KM, EF, 0, true>(p, seg, lane, h, dummy, 0u, rshift, 0.f, unused);
-    }
+    __shared__ uint32_t hs[GVC_H0_BINS + 32];
+    resolve_level0<4>(p, 0, sh, need);
     __syncthreads();
-    merge_hist(h, p.hist0);
-    grid_sync_last(st->bar[3], nblk, err, [&] { resolve_level0<PER>(p, 1, shs, need); });
+    if (!*(volatile uint32_t *)&p.st->fallback)
+        return;
+    for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += blockDim.x)
+        hs[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int shift = KM == KEY_MAG ? 19 : 20;
+    double nacc = 0.0;  // the refill does not re-accumulate the norm
+    for (uint32_t seg = warp; seg < p.S; seg += blockDim.x >> 5)
+        collect_segment<KM, EF, 0, true>(p, seg, lane, hs, GVC_H0_BINS + lane, 0u, shift, 0.f, nacc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < GVC_H0_BINS; i += blockDim.x)
+        p.hist0[i] = hs[i];
+    __threadfence();
+    __syncthreads();
+    resolve_level0<4>(p, 1, sh, need);
 }
 
 // ------------------------------------------------------- candidate pass
@@ -772,8 +759,10 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
     uint32_t(*acc_c)[GVC_THREADS] = reinterpret_cast<uint32_t(*)[GVC_THREADS]>(acc_a + (ABS ? NB + 1 : 0));
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][2][NB];
     constexpr uint32_t P1_Q = 256;  // per-warp ring buffer of queued (slow-path) candidates
-    __shared__ float p1_qv[GVC_WARPS_PER_BLOCK][P1_Q];
-    __shared__ uint32_t p1_qk[GVC_WARPS_PER_BLOCK][P1_Q], p1_qt[GVC_WARPS_PER_BLOCK][P1_Q];
+    // (+ 32 per-lane dummy slots: the branch-free queue stores of non-queued candidates)
+    // one array per warp, [value bits | key | offset][slot]: the three stores
+    // of a queued candidate share one address (constant offsets)
+    __shared__ uint32_t p1_q[GVC_WARPS_PER_BLOCK][3][P1_Q + 32];
     const SelState *st = p.st;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t seg = blockIdx.x * GVC_WARPS_PER_BLOCK + warp;
@@ -806,6 +795,9 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
     // candidate CF as well, ~10% of the candidates of a x10 ladder step)
     const uint32_t f2_lo = nks >= 2 ? him1[NB >= 2 ? 1 : 0] : 0xffffffffu;
     const uint32_t f2_hi = nks >= 3 ? lo[NB >= 3 ? 2 : 0] : 0xffffffffu;
+    // (lo, hi) exclusive as base + unsigned width: key - base < width
+    const uint32_t f1_base = f_lo + 1u, f1_w = f_hi > f_lo ? f_hi - f_lo - 1u : 0u;
+    const uint32_t f2_base = f2_lo + 1u, f2_w = f2_hi > f2_lo ? f2_hi - f2_lo - 1u : 0u;
     double e_b1 = 0.0, a_b1 = 0.0, e_b2 = 0.0, a_b2 = 0.0;
     uint32_t c_b1 = 0, c_b2 = 0;
     if (seg < p.S) {
@@ -814,8 +806,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         uint32_t *mem = p.mem_idx + beg;
         const uint32_t lt = lanemask_lt();
         uint32_t mcount = 0;
-        float *q_v = p1_qv[warp];
-        uint32_t *q_k = p1_qk[warp], *q_t = p1_qt[warp];
+        float *q_v = reinterpret_cast<float *>(p1_q[warp][0]);
+        uint32_t *q_k = p1_q[warp][1], *q_t = p1_q[warp][2];
         uint32_t qh = 0, qn = 0;  // ring buffer head / count (warp-uniform)
         // classify queue entries qh .. qh + m - 1 (m <= 32), one per lane, in index order
         auto classify = [&](uint32_t m) {
@@ -885,55 +877,51 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
                 if (KM == KEY_HASH)
                     niv2 = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t + 256);
             }
-            float v[4] = {fv.x, fv.y, fv.z, fv.w};
-            uint32_t pos[4] = {iv.x, iv.y, iv.z, iv.w}, key[4];
-            bool ok[4];
+            const float v[4] = {fv.x, fv.y, fv.z, fv.w};
+            const uint32_t pos[4] = {iv.x, iv.y, iv.z, iv.w};
+            // fast windows in registers; everything else (band 0, members,
+            // bands >= 3: ~3% at CF 10) is queued and classified 32 at a time,
+            // so the NB-way classification runs on full warps instead of as
+            // predicated code under every candidate.  Branch-free: a window is
+            // one unsigned range test, the sums add +0.0 outside it (x + 0.0
+            // == x: the same fp64 sums as adding the window's candidates
+            // alone), and a non-queued candidate's queue stores go to a
+            // per-lane dummy slot.  Whole groups skip the bounds tests.
+            auto group = [&](auto FULL) {
+                constexpr bool full = decltype(FULL)::value;
 #pragma unroll
-            for (int c = 0; c < 4; c++) {
-                ok[c] = t + c < cnt;
-                key[c] = ok[c] ? cand_key<KM>(p, v[c], pos[c]) : 0u;
-            }
-            // fast window in registers; everything else (band 0, members,
-            // bands >= 2: ~12% at CF 10) is queued in index order and
-            // classified 32 at a time, so the NB-way classification runs on
-            // full warps instead of as predicated code under every candidate
-            bool slow[4];
-            uint32_t sbal[4];
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                if (KM == KEY_MAG)
-                    nan_any |= (uint32_t)(ok[c] && key[c] > 0x7f800000u);
-                const bool fast = ok[c] && key[c] > f_lo && key[c] < f_hi;
-                if (fast) {
-                    // the common case: above threshold 0, below interval 1 ->
-                    // band 1, not a member; accumulated in registers
-                    e_b1 += (double)v[c] * (double)v[c];
-                    if (ABS)
-                        a_b1 += fabs((double)v[c]);
-                    c_b1 += 1u;
+                for (int c = 0; c < 4; c++) {
+                    const bool okc = full || t + c < cnt;
+                    const uint32_t k = okc ? cand_key<KM>(p, v[c], pos[c]) : 0u;
+                    if (KM == KEY_MAG)
+                        nan_any |= (uint32_t)(okc & (k > 0x7f800000u));
+                    const bool fast = okc & (k - f1_base < f1_w);
+                    const bool fast2 = NB >= 2 && (okc & (k - f2_base < f2_w));
+                    const double d = (double)v[c];
+                    const double dd = d * d;
+                    e_b1 += fast ? dd : 0.0;
+                    c_b1 += fast ? 1u : 0u;
+                    if (NB >= 2) {
+                        e_b2 += fast2 ? dd : 0.0;
+                        c_b2 += fast2 ? 1u : 0u;
+                    }
+                    if (ABS) {
+                        a_b1 += fast ? fabs(d) : 0.0;
+                        a_b2 += fast2 ? fabs(d) : 0.0;
+                    }
+                    const bool slow = okc & !fast & !fast2;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, slow);
+                    const uint32_t slot = slow ? ((qh + qn + __popc(bal & lt)) & (P1_Q - 1)) : P1_Q + lane;
+                    q_v[slot] = v[c];
+                    q_k[slot] = k;
+                    q_t[slot] = t + c;
+                    qn += __popc(bal);
                 }
-                const bool fast2 = NB >= 2 && ok[c] && key[c] > f2_lo && key[c] < f2_hi;
-                if (fast2) {
-                    e_b2 += (double)v[c] * (double)v[c];
-                    if (ABS)
-                        a_b2 += fabs((double)v[c]);
-                    c_b2 += 1u;
-                }
-                slow[c] = ok[c] && !fast && !fast2;
-                sbal[c] = __ballot_sync(0xffffffffu, slow[c]);
-            }
-            uint32_t o = qh + qn + __popc(sbal[0] & lt) + __popc(sbal[1] & lt) + __popc(sbal[2] & lt) +
-                         __popc(sbal[3] & lt);
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                if (slow[c]) {
-                    q_v[o & (P1_Q - 1)] = v[c];
-                    q_k[o & (P1_Q - 1)] = key[c];
-                    q_t[o & (P1_Q - 1)] = t + c;
-                    o++;
-                }
-            }
-            qn += __popc(sbal[0]) + __popc(sbal[1]) + __popc(sbal[2]) + __popc(sbal[3]);
+            };
+            if (base + 128 <= cnt)
+                group(std::true_type{});
+            else
+                group(std::false_type{});
             __syncwarp();
             while (qn >= 32) {
                 classify(32);
@@ -1679,6 +1667,7 @@ static void set_attributes()
     if (done)
         return;
     done = true;
+    cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
 #define GVC_PASS1_ATTR(KM, NB, ABS)                                                                          \
     cudaFuncSetAttribute(k_pass1<KM, NB, ABS>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
                          (int)((NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4)));
@@ -1695,85 +1684,43 @@ static void set_attributes()
 // fields live in the constant bank).  Returns the number of kernels.
 static cudaEvent_t g_ev_mark[4];  // capture-time placeholders: collect start/end, select start/end
 
-// Cooperative launch (every CTA resident at once: the grid barriers of
-// k_collect_coop rely on it).  Its grid is capped at what the device keeps
-// resident, per device and kernel (CTAs then stride over the blocks).
-static int coop_capacity(const void *fn)
-{
-    static std::mutex mu;
-    static std::unordered_map<std::string, int> cache;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    char key[64];
-    snprintf(key, sizeof(key), "%d|%p", dev, fn);
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end())
-        return it->second;
-    int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GVC_THREADS, 0);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int cap = std::max(1, per_sm * sms);
-    cache.emplace(key, cap);
-    return cap;
-}
-
-template <typename Kern>
-static void launch_coop(Kern kernel, int grid, cudaStream_t s, const Plan &p, int aux)
-{
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(GVC_THREADS);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kernel, p, aux);
-}
-
-// The cooperative collect instantiation of a plan.
-template <int KM>
-static const void *collect_fn(const Plan &p)
-{
-    if (!p.ef)
-        return (const void *)k_collect_coop<KM, false, 0>;
-    if (!p.pmask)
-        return (const void *)k_collect_coop<KM, true, 0>;
-    return p.pmode == 1 ? (const void *)k_collect_coop<KM, true, 1> : (const void *)k_collect_coop<KM, true, 2>;
-}
-
-static int collect_grid(const Plan &p)
-{
-    const void *fn = p.keymode == KEY_MAG ? collect_fn<KEY_MAG>(p) : collect_fn<KEY_HASH>(p);
-    return std::min<int>((int)p.B, coop_capacity(fn));
-}
-
 template <int KM>
 static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gprobes)
 {
     const bool pdl = !probes;  // direct probe launches keep plain stream order
     ProfScope all(probes ? PROF_SELECT : -1, s);
+    const int blocks = (int)p.B;
     int launches = 0;
+    if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
+        uint64_t wb = (p.s_chunks + 31) / 32;
+        int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
+        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);  // its last block resolves key_est
+        launches++;
+    } else {
+        k_sample_resolve<<<1, 1024, 0, s>>>(p, 0);
+        launches++;
+    }
     {
         ProfScope pc(probes ? PROF_COLLECT : -1, s);
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[0], s, cudaEventRecordExternal);
-        const int grid = collect_grid(p);
+        const bool cpdl = pdl && !gprobes;
         if (!p.ef)
-            launch_coop(k_collect_coop<KM, false, 0>, grid, s, p, 0);
+            launch_k(k_collect<KM, false, 0>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else if (!p.pmask)
-            launch_coop(k_collect_coop<KM, true, 0>, grid, s, p, 0);
+            launch_k(k_collect<KM, true, 0>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else if (p.pmode == 1)
-            launch_coop(k_collect_coop<KM, true, 1>, grid, s, p, 0);
+            launch_k(k_collect<KM, true, 1>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else
-            launch_coop(k_collect_coop<KM, true, 2>, grid, s, p, 0);
+            launch_k(k_collect<KM, true, 2>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[1], s, cudaEventRecordExternal);
-        launches++;
     }
+    if (p.ef)
+        launch_k(k_resolve0<KM, true>, dim3(1), dim3(1024), 0, s, pdl && !gprobes, p, 0);
+    else
+        launch_k(k_resolve0<KM, false>, dim3(1), dim3(1024), 0, s, pdl && !gprobes, p, 0);
+    launches += 2;
     launch_tail<KM>(p, s, pdl);
     launches += 3;
     // k_finish_j: one block per ladder entry, 2 blocks per thread; only as many
@@ -1793,8 +1740,8 @@ static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *laun
     cudaMemsetAsync(p.st, 0, sizeof(SelState), s);
     cudaMemsetAsync(p.hist0, 0, GVC_H0_BINS * 4, s);
     cudaMemsetAsync(p.histl, 0, GVC_MAX_LADDER * GVC_HL_BINS * 4, s);
-    if (p.sample_head)  // coarse + fine sample histograms
-        cudaMemsetAsync(p.shist, 0, 2 * GVC_H0_BINS * 4, s);
+    if (p.keymode == KEY_MAG)
+        cudaMemsetAsync(p.shist, 0, GVC_SAMPLE_BINS * 4, s);
     *launches = p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
                                      : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
     if (gprobes)
@@ -1823,11 +1770,10 @@ static std::unordered_map<std::string, GraphEntry> g_graphs;
 static std::string graph_key(const Plan &p, const void *ws)
 {
     char buf[256];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    snprintf(buf, sizeof(buf), "%d|%p|%llu|%d|%d|%d|%d|%d|%d|%d|%d", dev, ws, (unsigned long long)p.n, p.keymode,
-             p.ef, p.pmask ? p.pmode : 0, nb_for(p.n_ks), p.kind == GVC_REDSYNC, p.force_exact, p.sample_head,
-             p.key_est_dev != nullptr);
+    snprintf(buf, sizeof(buf), "%p|%llu|%d|%d|%d|%d|%d|%d|%d|%d|%d", ws, (unsigned long long)p.n, p.keymode, p.ef,
+             p.pmask ? p.pmode : 0, nb_for(p.n_ks), p.kind == GVC_REDSYNC, p.force_exact,
+             (int)(p.keymode == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev),
+             p.key_est_dev != nullptr, (int)p.s_chunks);
     return std::string(buf);
 }
 
@@ -1863,22 +1809,28 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.res = res;
     const uint64_t n = a->n, k0 = a->ks[0];
     if (p.keymode == KEY_MAG) {
-        // the sample head of k_collect_coop: the first 256 values of every
-        // segment (with a whole 512-chunk) of the CTAs' first blocks; target
-        // rank padded by 2% + 5 sigma so key_est sits below the k_0-th key w.h.p.
-        // (a miss only costs the refill).  Small inputs take the exact path.
-        p.sample_head = 0;
-        if (n >= (1ull << 17) && !p.force_exact && !p.key_est_dev) {
-            const uint64_t segs = std::min<uint64_t>(p.S, (uint64_t)collect_grid(p) * GVC_WARPS_PER_BLOCK);
-            const uint64_t last_len = n - (uint64_t)(p.S - 1) * p.seg_len;
-            const uint64_t full = (segs == p.S && last_len < GVC_SEG_QUANTUM) ? segs - 1 : segs;
-            const uint64_t sampled = full * 256;
-            const double mu = (double)k0 * (double)sampled / (double)n;
-            const double t = mu * 1.02 + 5.0 * sqrt(mu) + 32.0;
-            if (sampled > 0 && t < (double)sampled) {
-                p.s_target = (uint64_t)ceil(t);
-                p.sample_head = 1;
-            }
+        // sample ~n/128 values (at most 2^19) in 128-value chunks (everything
+        // when n is small): past ~10^5 sampled candidates the 5-sigma margin is
+        // already a few tenths of a percent of k_0, and the sample pass is pure latency
+        uint64_t want = n <= 65536 ? n : (n / 128 > 65536 ? n / 128 : 65536);
+        if (want > (1ull << 19))
+            want = 1ull << 19;
+        uint64_t chunks = (want + 127) / 128;
+        uint64_t stride = n / chunks;
+        stride &= ~(uint64_t)3;
+        if (stride < 128)
+            stride = 128;
+        chunks = (n + stride - 1) / stride;
+        const uint64_t last = (chunks - 1) * stride;
+        const uint64_t sampled = (chunks - 1) * 128 + (n - last < 128 ? n - last : 128);
+        p.s_chunks = chunks;
+        p.s_stride = stride;
+        if (sampled >= n) {
+            p.s_target = k0;  // the sample is the whole vector: exact bin
+        } else {
+            double mu = (double)k0 * (double)sampled / (double)n;
+            double t = mu * 1.02 + 5.0 * sqrt(mu) + 32.0;
+            p.s_target = t >= (double)sampled ? 0 : (uint64_t)ceil(t);
         }
     } else {
         double mu = (double)k0 + 8.0 * sqrt((double)k0) + 64.0;
@@ -1983,7 +1935,7 @@ int select_phase_times(void *ws, unsigned long long *out, int n)
     Plan p;
     memset(&p, 0, sizeof(p));
     carve(&p, (char *)ws, 1);
-    const int m = n < 16 ? n : 16;
+    const int m = n < 32 ? n : 32;
     cudaError_t e = cudaMemcpy(out, p.st->t_phase, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return e == cudaSuccess ? GVC_OK : set_error(GVC_ERR_CUDA, "phase times: %s", cudaGetErrorString(e));
 }
