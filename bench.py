@@ -54,6 +54,92 @@ EPSILON = 0.35  # fresh iid N(0,1) gradients give gain(CF10) ~= 0.42 -> the comp
 EPSILONS = {"topk": EPSILON, "dgc": EPSILON, "redsync": 0.25, "randomk": 0.05}
 
 
+SPEC_HBM_GBPS = 8000.0  # B200 HBM3e, DGX spec (the north star's "~8 TB/s")
+NORTH_STAR = "vgg16"     # the north star's 138M Top-k + EF + multi-CF select, reported in every default run
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload_config(name: str, world: int) -> dict:
+    """The `config` both arms print (identical dicts: the driver compares them)."""
+    M, theta_min, theta_s, extra, desc = WORKLOADS[name][:5]
+    kind = WORKLOADS[name][5] if len(WORKLOADS[name]) > 5 else "topk"
+    return {"workload": desc, "M": M, "compressor": kind, "cf_ladder": [theta_min, theta_min * theta_s, *extra],
+            "epsilon": EPSILONS[kind],
+            "l2": "evicted before every timed step by reading a 256 MiB buffer (L2 126 MB), outside the timed "
+                  "events; inputs (4M bytes each) exceed L2",
+            "parallelism": f"dp{world}"}
+
+
+def true_residual(r, mask, pm, pmode):
+    """The residual a ResidualStore presents, from its raw buffers: positions in
+    the deferred sent mask hold g_ef and become fl32(r - f(r)) (feedback.py:39-51;
+    f(r) = r, or sign(r) * m for Redsync)."""
+    r = np.array(r, dtype=np.float32, copy=True)
+    if not pmode:
+        return r
+    bits = np.unpackbits(np.ascontiguousarray(mask).view(np.uint8), bitorder="little")[:r.size].astype(bool)
+    x = r[bits]
+    if pmode == 2:
+        sg = np.sign(x).astype(np.float32)
+        r[bits] = (x - (sg * np.float32(pm)).astype(np.float32)).astype(np.float32)
+    else:
+        r[bits] = (x - x).astype(np.float32)
+    return r
+
+
+def replay_step(O, snap_in, snap_out, res, M, theta_min, theta_s, extra, world, kind):
+    """Re-check one timed step of run_iteration against the C oracle: chosen
+    entries and residual bit-exact, gains within 1e-6 (fp64 summation order),
+    the averaged gradient bit-exact (one rank).  Returns "ok" or the mismatch."""
+    g, r_raw, mask, pm, pmode = snap_in
+    idx, vals, avg, r2_raw, mask2, pm2, pmode2 = snap_out
+    ef = O.ef_add(g, true_residual(r_raw, mask, pm, pmode))
+    norm = O.sq_norm(ef)
+    k1 = O.keep_count(M, theta_min)
+    kc = O.keep_count(k1, theta_s)
+    problems = []
+
+    def top(k):
+        return O.topk_indices(ef, k) if kind == "topk" else None
+    i1 = top(k1)
+    ic = top(kc) if kc != k1 else i1
+    if kind == "topk" and world == 1:
+        for name, want, got in (("gain_min", O.sq_norm(ef[i1.astype(np.int64)]) / norm, res.gain_min_raw),
+                                ("gain_c", O.sq_norm(ef[ic.astype(np.int64)]) / norm, res.gain_c_raw)):
+            if abs(got - min(1.0, want)) > 1e-6 * min(1.0, want):
+                problems.append(f"{name} {got} vs {want}")
+        for c in extra:
+            kx = O.keep_count(k1, c / theta_min)
+            want = min(1.0, O.sq_norm(ef[O.topk_indices(ef, kx).astype(np.int64)]) / norm)
+            if abs(res.ladder_gains[c] - want) > 1e-6 * want:
+                problems.append(f"gain_{c} {res.ladder_gains[c]} vs {want}")
+    if kind == "topk" and res.decision.choice != "dense":
+        want_idx = ic if res.decision.choice == "candidate" else i1
+        if not np.array_equal(idx, want_idx):
+            problems.append("sent indices")
+        want_vals = ef[want_idx.astype(np.int64)]
+        if not np.array_equal(vals.view(np.uint32), want_vals.view(np.uint32)):
+            problems.append("sent values")
+        r_want = O.update_residual(ef, want_idx, want_vals)
+        if not np.array_equal(true_residual(r2_raw, mask2, pm2, pmode2).view(np.uint32), r_want.view(np.uint32)):
+            problems.append("residual")
+        if world == 1 and avg is not None:
+            a_want = O.aggregate([(want_idx, want_vals)], M)
+            if not np.array_equal(avg.view(np.uint32), a_want.view(np.uint32)):
+                problems.append("averaged gradient")
+    return "ok" if not problems else "FAIL: " + ", ".join(problems)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -174,26 +260,109 @@ def run_reference(args, M, theta_min, theta_s, extra, desc):
     rng = np.random.default_rng(1234)
     g = [rng.standard_normal(M, dtype=np.float32) for _ in range(world)]
     r = [np.zeros(M, dtype=np.float32) for _ in range(world)]
-    warm, steps = min(args.warmup, 1), min(args.steps, 3)
+    # the same K / W as our arm, bounded to ~4 minutes of host time in total
+    t0 = time.perf_counter()
+    r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world, args.kind)
+    per = time.perf_counter() - t0
+    budget = 240.0
+    warm = max(0, min(args.warmup - 1, int(budget / 4 / per)))
+    steps = max(1, min(args.steps, int((budget - per * (warm + 1)) / per)))
     for _ in range(warm):
         r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world, args.kind)
     t0 = time.perf_counter()
     for _ in range(steps):
         r = oracle_step(O, g, r, M, theta_min, theta_s, extra, world, args.kind)
     dt = (time.perf_counter() - t0) / steps
+    warm += 1
     value = world * 4 * M / dt / 1e9
     sample = (f"{steps} timed full steps ({warm} warm-up) of the {M}-element workload, {world} simulated "
-              f"worker(s) run sequentially as the reference does (controller.py:232-250)")
+              f"worker(s) run sequentially as the reference does (controller.py:232-250); the reference is "
+              f"single-threaded (numpy), so is its port")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": steps, "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) fp32 gradients",
-            "config": {"workload": desc, "M": M, "parallelism": f"dp{world} (simulated, host)"},
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "port", "sample": sample},
+            "config": workload_config(args.workload, world),
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model(), "host_cores": len(os.sched_getaffinity(0))},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # -------------------------------------------------------------- GPU leg
+def north_star(args, G, nat, O, dev):
+    """The north star's target measured in the default run: the fused Top-k +
+    error-feedback + multi-CF gain select (every select kernel) on a VGG16-size
+    138M gradient on 1 B200, against the HBM roofline, the whole step beside it,
+    and the last step re-checked against the oracle."""
+    import torch
+    M, theta_min, theta_s, extra, desc = WORKLOADS[NORTH_STAR][:5]
+    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=1000.0, epsilon=EPSILONS["topk"], window=1 << 30)
+    state = G.ControllerState.fresh(cfg, 1)
+    state.theta_s = theta_s
+    store = G.ResidualStore(M, device=dev)
+    cost = G.CostModelParams(workers=1)
+    rng = G.SeededRng(7)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321)
+    gbuf = torch.empty(M, device=dev, dtype=torch.float32)
+    avg = torch.empty(M, dtype=torch.float32, device=dev)
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flush_out = torch.empty((), dtype=torch.float32, device=dev)
+
+    def step():
+        return G.run_iteration(state, G.GradientVector._wrap(gbuf), store, cost, rng, extra_cfs=extra,
+                               average=True, average_out=avg)
+    for _ in range(3):
+        gbuf.normal_(generator=gen)
+        step()
+    torch.cuda.synchronize()
+    # select / collect: CUDA event-record nodes inside the real step's select graph
+    nat.load().gvc_prof_enable(2)
+    gbuf.normal_(generator=gen)
+    step()
+    torch.cuda.synchronize()
+    nat.prof_read()
+    n = max(3, min(args.steps, 10))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    snap_in = None
+    for s in range(n):
+        gbuf.normal_(generator=gen)
+        if s == n - 1:
+            snap_in = (gbuf.clone(), store._resid.clone(), None if store._mask is None else store._mask.clone(),
+                       None if store._pm is None else store._pm.clone(), int(store._pmode))
+        torch.sum(flush, dim=0, out=flush_out)
+        ev[s][0].record()
+        res = step()
+        ev[s][1].record()
+    torch.cuda.synchronize()
+    prof = nat.prof_read()
+    nat.prof_enable(False)
+    last = res.sent[0]
+    snap_out = (last.indices.clone(), last.vals.clone(), avg.clone(), store._resid.clone(),
+                None if store._mask is None else store._mask.clone(),
+                None if store._pm is None else store._pm.clone(), int(store._pmode))
+    host = [t.cpu().numpy() if isinstance(t, torch.Tensor) else t for t in snap_in]
+    host[3] = None if host[3] is None else float(host[3][0])
+    host_out = [t.cpu().numpy() if isinstance(t, torch.Tensor) else t for t in snap_out]
+    host_out[5] = None if host_out[5] is None else float(host_out[5][0])
+    parity = replay_step(O, host, host_out, res, M, theta_min, theta_s, extra, 1, "topk")
+    peak, peak_kind = peaks()
+    sel_ms = prof["select"][0] / max(prof["select"][1], 1)
+    col_ms = prof["collect"][0] / max(prof["collect"][1], 1)
+    step_ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    sel_gbs = 12 * M / (sel_ms * 1e-3) / 1e9
+    col_gbs = 12 * M / (col_ms * 1e-3) / 1e9
+    return {"workload": desc, "M": M, "cf_ladder": [theta_min, theta_min * theta_s, *extra],
+            "target": ">= 0.60 of the HBM roofline for the fused Top-k + EF + multi-CF gain pass (north star)",
+            "select_stage": {"ms": sel_ms, "achieved": sel_gbs, "unit": "GB/s", "peak": peak, "peak_kind": peak_kind,
+                             "frac": sel_gbs / peak, "frac_of_spec": sel_gbs / SPEC_HBM_GBPS,
+                             "algorithmic_bytes": 12 * M,
+                             "timing": f"CUDA event-record nodes around the select graph, {prof['select'][1]} steps"},
+            "collect": {"ms": col_ms, "achieved": col_gbs, "frac": col_gbs / peak},
+            "ms_per_step": step_ms, "step_gbps": 4 * M / (step_ms * 1e-3) / 1e9,
+            "chosen_cf": res.decision.cf, "parity": parity}
+
+
 def run_ours(args, M, theta_min, theta_s, extra, desc):
     import torch
     import torch.distributed as dist
@@ -275,10 +444,21 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     chosen.clear()
     for key in STATS:
         STATS[key] = 0
+    def raw_state():
+        """The store's raw buffers (residual, deferred sent mask, Redsync mean, mode): copies,
+        so the step itself runs unchanged (reading .residual would apply the mask)."""
+        return (store._resid.clone(), None if store._mask is None else store._mask.clone(),
+                None if store._pm is None else store._pm.clone(), int(store._pmode))
+
     launches0 = nat.launch_count()
     clocks.mark("t0")
+    snap_in = None
     for s in range(args.steps):
         g = fresh()
+        if s == args.steps - 1:  # inputs of the last timed step, for the oracle re-check (untimed)
+            launches_snap = nat.launch_count()
+            snap_in = (g.clone(),) + raw_state()
+            launches0 += nat.launch_count() - launches_snap
         cool()  # evict L2 (outside the timed events)
         ev[s][0].record()
         res, _ = step(g)
@@ -287,6 +467,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     clocks.mark("t1")
     clocks.__exit__(None, None, None)
     launches = nat.launch_count() - launches0
+    last = res.sent[0]
+    snap_out = (last.indices.clone(), last.vals.clone(), avg.clone()) + raw_state()
+    last_res = res
     # roofline timing: the same loop again, the select graph now carrying CUDA
     # event-record nodes around k_collect (gvc_prof_enable(2)) -- the kernel's
     # duration inside the real step sequence, kept out of the headline loop
@@ -370,6 +553,21 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     e2e_step = float(t.item()) / n_e2e
     e2e_value = world * 4 * M / (e2e_step * 1e-3) / 1e9
 
+    # ---- parity: the last timed step re-checked against the C oracle (untimed)
+    from oracle import oracle as O
+    O.lib()
+    host = [t.cpu().numpy() if isinstance(t, torch.Tensor) else t for t in snap_in]
+    host_out = [t.cpu().numpy() if isinstance(t, torch.Tensor) else t for t in snap_out]
+    host[3] = None if host[3] is None else float(host[3][0])
+    host_out[5] = None if host_out[5] is None else float(host_out[5][0])
+    parity = replay_step(O, host, host_out, last_res, M, theta_min, theta_s, extra, world, args.kind)
+
+    north = None
+    if world == 1 and args.workload == "resnet101" and not args.no_north_star:
+        del gbuf, avg, flush, store, snap_in, snap_out
+        torch.cuda.empty_cache()
+        north = north_star(args, G, nat, O, dev)
+
     if rank != 0:
         if pg is not None:
             dist.barrier()
@@ -423,14 +621,16 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: a fresh iid N(0,1) fp32 gradient per step and rank (drawn outside the timed events), "
                 "residual carried across steps",
-        "config": {"workload": desc, "M": M, "compressor": args.kind,
-                   "cf_ladder": [theta_min, theta_min * theta_s, *extra],
-                   "epsilon": EPSILONS[args.kind], "chosen_cf": {str(k): v for k, v in chosen.items()},
-                   "l2": "evicted before every timed step by reading a 256 MiB buffer (L2 126 MB), outside the timed events; inputs (178 MB each) exceed L2",
-                   "parallelism": f"dp{world}"},
+        "config": workload_config(args.workload, world),
+        "chosen_cf": {str(k): v for k, v in chosen.items()},
+        "parity": parity,
+        "parity_what": ("the last timed step re-run on the C oracle (oracle/, checked against the reference's "
+                        "golden vectors): sent indices, values and residual bit-exact, gains within 1e-6"
+                        + (", averaged gradient bit-exact" if world == 1 else " (this rank's part)")),
         "roofline": {"bound": "hbm", "kernel": "k_collect (fused EF add + fp64 norm + candidate compaction)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "frac": achieved / peak if achieved else None,
+                     "frac_of_spec": achieved / SPEC_HBM_GBPS if achieved else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": col_bytes, "launch_ms": col_launch,
                      "launch_timing": ("CUDA event-record nodes around k_collect inside the timed loop's select graph, "
                                        f"{col_n} launches") if timed_col[1] else "probed pass (direct launches)",
@@ -438,7 +638,9 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         "select_stage": {"what": "the fused EF + Top-k + multi-CF gain select (every select kernel, graph-timed), "
                                  "algorithmic 12M bytes -- the north star's >= 60% target",
                          "ms": sel_ms, "achieved": 12 * M / (sel_ms * 1e-3) / 1e9 if sel_ms > 0 else None,
-                         "frac": (12 * M / (sel_ms * 1e-3) / 1e9) / peak if sel_ms > 0 else None},
+                         "frac": (12 * M / (sel_ms * 1e-3) / 1e9) / peak if sel_ms > 0 else None,
+                         "frac_of_spec": (12 * M / (sel_ms * 1e-3) / 1e9) / SPEC_HBM_GBPS if sel_ms > 0 else None},
+        "north_star": north,
         "compress_stage": {"what": "gvc_select (all kernels) + gvc_emit, algorithmic 12M + 8k bytes",
                            "ms": sel_ms + emit_ms, "achieved": comp_achieved,
                            "frac": comp_achieved / peak if comp_achieved else None},
@@ -455,9 +657,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
                 "d2h_bytes_per_step": nat.RESULT_BYTES, "ms_per_step": e2e_step},
     }
     if world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-        O.lib()
-        gh = fresh().cpu().numpy()
+        gh = np.random.default_rng(5).standard_normal(M, dtype=np.float32)
         rh = np.zeros(M, dtype=np.float32)
         oracle_step(O, [gh], [rh], M, theta_min, theta_s, extra, 1, args.kind)  # warm
         # a bounded sample of ~10 s of host work: whole steps until 10 s pass (at least 2)
@@ -469,7 +669,8 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         dt = (time.perf_counter() - t0) / n_cpu
         line["cpu_baseline"] = {"value": 4 * M / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
                                 "sample": f"{n_cpu} full steps of the same workload (C oracle, single thread)",
-                                "ms_per_step": dt * 1e3}
+                                "ms_per_step": dt * 1e3, "cpu_model": cpu_model(),
+                                "host_cores": len(os.sched_getaffinity(0))}
     print(json.dumps(line), flush=True)
     if pg is not None:
         dist.barrier()
@@ -484,6 +685,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="resnet101")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true",
+                    help="skip the 138M north-star select measurement of the default run")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
