@@ -101,6 +101,16 @@ typedef struct {
                                      them ALL (DGC overshoot, compressors.py:126-128) and report
                                      the shortfall in gvc_select_result.shortfall              */
     int32_t reserved2;
+    /* DGC in one selection, both branches of compressors.py:123-137 (no host
+     * decision): with dgc_thr_dev (the sampled threshold key, device u32) and
+     * dgc_sampled_dev (bit i set = position i is in the threshold sample,
+     * u32[ceil(n/32)]) every value gets the composite key
+     *     (|v| >= thr || sampled(i)) ? 0x80000000 | |v| : |v|
+     * whose top-k IS the DGC pick: if k entries reach thr, the k largest of
+     * them; otherwise all of them, then the largest sampled values below thr,
+     * then the largest of the rest (global top-up), ties to the lower index. */
+    const uint32_t *dgc_thr_dev;
+    const uint32_t *dgc_sampled_dev;
 } gvc_select_args;
 
 GVC_API const char *gvc_last_error(void);

@@ -129,7 +129,8 @@ class Selection:
                  g: torch.Tensor | None = None, resid: torch.Tensor | None = None,
                  rng: SeededRng | None = None, pos_base: int = 0, slot: str = "sel0",
                  force_exact: int = 0, pending=None, key_est: torch.Tensor | None = None,
-                 allow_short: bool = False, persist_res: bool = False):
+                 allow_short: bool = False, persist_res: bool = False,
+                 dgc_thr: torch.Tensor | None = None, dgc_bits: torch.Tensor | None = None):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -159,7 +160,10 @@ class Selection:
         if key_est is not None:  # forced candidate threshold (DGC), a device u32/i32 scalar
             a.key_est_dev = key_est.data_ptr()
             a.allow_short = 1 if allow_short else 0
-        self._keep = (key_est,)  # keep device scalars alive until the stream consumed them
+        if dgc_thr is not None:  # DGC in one selection: composite keys (gvc_select_args.dgc_thr_dev)
+            a.dgc_thr_dev = dgc_thr.data_ptr()
+            a.dgc_sampled_dev = dgc_bits.data_ptr()
+        self._keep = (key_est, dgc_thr, dgc_bits)  # device inputs stay alive until the stream consumed them
         if pending is not None:  # (mask, m, mode): deferred residual update of the previous step
             a.pending_mask_dev = pending[0].data_ptr()
             a.pending_m_dev = pending[1].data_ptr()

@@ -342,7 +342,9 @@ class _WorkerStep:
 
 class _DgcStep:
     """DGC worker step: level 1 over g_ef (fused EF pass with the sampled
-    threshold), level 2 over the level-1 values (compressors.py:226-246)."""
+    threshold), level 2 over the level-1 values (compressors.py:226-246).
+    Both levels are device-only (dgc.py): the norms, kept energies and the
+    selects' statuses travel in the controller's one read-back."""
 
     def __init__(self, kind: CompressorKind, g: torch.Tensor, store: ResidualStore, k1: int, k2: int,
                  rng: SeededRng, i: int, w: int):
@@ -351,6 +353,7 @@ class _DgcStep:
         self.kind, self.k1, self.k2, self.store = kind, k1, k2, store
         self.n = g.numel()
         self.identity1 = False
+        self._res = []
         rng0 = rng.split(i, w, _STAGE_MIN)
         rng1 = rng.split(i, w, _STAGE_STEP)
         slot = f"dgc{w}"
@@ -370,26 +373,34 @@ class _DgcStep:
                 # past ~4.6e8 values the emit ORs mask bits in global memory
                 # instead of writing every word from shared memory
                 self._mask1.zero_()
-            idx, vals, res = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
-                                        slot=slot + "a", want_result=True, sent_mask=self._mask1)
+            idx, vals, sel1 = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
+                                         slot=slot + "a", want_result=True, sent_mask=self._mask1, check=False)
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
-            self.norm = res.ef_norm_sq
+            self.norm = sel1.res_dev[:8].view(torch.float64)  # ||g_ef||^2 of the fused pass, on the device
+            self._res.append(sel1.res_dev)
         if k2 < self.g_min.kept:
-            idx2, vals2 = dgc_select(kind, self.g_min.vals, k2, rng1, idx_map=self.g_min.indices, slot=slot + "b")
+            idx2, vals2, sel2 = dgc_select(kind, self.g_min.vals, k2, rng1, idx_map=self.g_min.indices,
+                                           slot=slot + "b", want_result=True, check=False)
             self.g_c = SparseGradient._wrap(idx2, vals2, self.n, self.n / k2)
+            self._res.append(sel2.res_dev)
         else:
             self.g_c = self.g_min
         # (E_min, E_c, ||g_ef||^2) as device scalars: every rank's row travels the same way in C2
-        norm_dev = (squared_l2_norm_dev(store._resid) if self.norm is None
-                    else torch.full((), self.norm, dtype=torch.float64, device=g.device))
-        self.stats = torch.stack([squared_l2_norm_dev(self.g_min.vals), squared_l2_norm_dev(self.g_c.vals),
-                                  norm_dev])
+        norm_dev = squared_l2_norm_dev(store._resid).reshape(1) if self.norm is None else self.norm
+        self.stats = torch.cat([squared_l2_norm_dev(self.g_min.vals).reshape(1),
+                                squared_l2_norm_dev(self.g_c.vals).reshape(1), norm_dev.reshape(1)])
 
     def stats_dev(self) -> list[torch.Tensor]:
-        return [self.stats]
+        return [self.stats] + self._res
 
     def gains_from(self, raw: list[bytes], norm_host=None):
         import numpy as np
+        for b in raw[1:]:  # the DGC selects' statuses (NaN, consistency)
+            r = nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES])
+            if r.status == nat.GVC_ERR_NAN:
+                raise ValueError("NaN in gradient: compression order undefined")
+            if r.status != nat.GVC_OK:
+                raise RuntimeError(f"selection consistency failure (status {r.status})")
         e_min, e_c, norm = (float(x) for x in np.frombuffer(raw[0], dtype=np.float64))
         if self.identity_level1:  # theta_min == 1: the level-1 gain is exactly 1 (same sum)
             e_min = norm

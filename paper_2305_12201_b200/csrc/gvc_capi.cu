@@ -162,8 +162,12 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
         return set_error(GVC_ERR_ARG, "gvc_select: null argument");
     if (a->kind < GVC_TOPK || a->kind > GVC_RANDOMK)
         return set_error(GVC_ERR_ARG, "unknown compressor kind %d", a->kind);
-    if (a->kind == GVC_DGC)
-        return set_error(GVC_ERR_ARG, "dgc is composed from gvc_select (kind topk, key_est_dev) and the DGC helpers");
+    if (a->kind == GVC_DGC && !a->dgc_thr_dev)
+        return set_error(GVC_ERR_ARG, "dgc selects need dgc_thr_dev and dgc_sampled_dev (gvc_dgc_sample + gvc_select "
+                                      "over the sample give the threshold)");
+    if (a->dgc_thr_dev && (!a->dgc_sampled_dev || a->n_ks != 1 || a->key_est_dev || a->force_exact ||
+                           a->kind == GVC_RANDOMK || a->kind == GVC_REDSYNC))
+        return set_error(GVC_ERR_ARG, "dgc_thr_dev needs dgc_sampled_dev, one ladder entry and no forced threshold");
     if (a->allow_short && (!a->key_est_dev || a->n_ks != 1 || a->kind != GVC_TOPK))
         return set_error(GVC_ERR_ARG, "allow_short needs key_est_dev, one ladder entry and magnitude keys");
     if (a->n < 1 || a->n >= (1ull << 32))

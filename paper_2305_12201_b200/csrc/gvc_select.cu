@@ -77,6 +77,9 @@ struct Plan {
     uint64_t ks[GVC_MAX_LADDER];
     // forced candidate threshold (DGC)
     const uint32_t *key_est_dev;
+    // KEY_DGC: the sampled threshold key and the sample's position bitmap
+    const uint32_t *dgc_thr;
+    const uint32_t *dgc_bits;
     int allow_short;
     // deferred residual update of the previous step (EF mode)
     uint32_t *pmask;
@@ -163,41 +166,33 @@ __device__ __forceinline__ uint32_t cand_key(const Plan &p, float v, uint32_t po
 {
     if (KM == KEY_MAG)
         return mag_key(v);
+    if (KM == KEY_DGC) {
+        // DGC's pick as one top-k (gvc_select_args.dgc_thr_dev): chosen (|v| >=
+        // thr) and sampled values in the upper half ordered by |v| -- chosen
+        // first since they are larger -- the rest below them
+        const uint32_t m = mag_key(v);
+        const bool hi = m >= __ldg(p.dgc_thr) || ((__ldg(p.dgc_bits + (pos >> 5)) >> (pos & 31)) & 1u);
+        return hi ? (0x80000000u | m) : m;
+    }
     return hash_key(p.pos_base + pos, p.stream, p.seed);
 }
 
-// Four consecutive candidates of a segment (lane-major groups of 128):
-// values, positions and keys.  Entries at t >= cnt are invalid.
+// NaN magnitude in a key (the selection order is undefined, reference F8)
 template <int KM>
-__device__ __forceinline__ void load_cand4(const Plan &p, uint64_t beg, uint32_t t, uint32_t cnt, float (&v)[4],
-                                           uint32_t (&pos)[4], uint32_t (&key)[4], bool (&ok)[4], bool need_pos)
+__device__ __forceinline__ bool key_nan(uint32_t key)
 {
-    float4 fv = *reinterpret_cast<const float4 *>(p.cand_val + beg + t);
-    v[0] = fv.x;
-    v[1] = fv.y;
-    v[2] = fv.z;
-    v[3] = fv.w;
-    if (need_pos || KM == KEY_HASH) {
-        uint4 iv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t);
-        pos[0] = iv.x;
-        pos[1] = iv.y;
-        pos[2] = iv.z;
-        pos[3] = iv.w;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; c++) {
-        ok[c] = t + c < cnt;
-        key[c] = ok[c] ? cand_key<KM>(p, v[c], pos[c]) : 0u;
-    }
+    return KM != KEY_HASH && (key & 0x7fffffffu) > 0x7f800000u;
 }
 
 // ------------------------------------------------------------------ sample
 // Strided chunks of 128 contiguous values -> 14-bit shared-memory histogram of
 // magnitude keys, merged into global memory once per block.  Reads ~1.5%.
-__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh);
+__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh, int shift);
 
+template <int KM>
 __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
 {
+    constexpr int SHIFT = KM == KEY_DGC ? GVC_SAMPLE_SHIFT + 1 : GVC_SAMPLE_SHIFT;  // 32- / 31-bit keys
     pdl_enter();
     extern __shared__ uint32_t sh[];
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
@@ -230,9 +225,9 @@ __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
         }
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-            uint32_t k = mag_key(v[q]);
-            if (ok[q] && k <= 0x7f800000u) {
-                atomicAdd(&sh[k >> GVC_SAMPLE_SHIFT], 1u);
+            const uint32_t k = ok[q] ? cand_key<KM>(p, v[q], (uint32_t)(base + (uint64_t)q * 32 + lane)) : 0u;
+            if (ok[q] && !key_nan<KM>(k)) {
+                atomicAdd(&sh[k >> SHIFT], 1u);
                 kmax = max(kmax, k);
             }
         }
@@ -266,14 +261,14 @@ __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
     __syncthreads();
     if (last) {
         __threadfence();
-        sample_resolve_body(p, reinterpret_cast<unsigned long long *>(sh));
+        sample_resolve_body(p, reinterpret_cast<unsigned long long *>(sh), SHIFT);
     }
 }
 
 // Chooses key_est (a lower bound for the k_0-th largest key, w.h.p.) and the
 // level-0 bin shift.  Magnitude keys: from the sample histogram.  Hash keys:
 // from the binomial tail (host-computed).
-__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh)
+__device__ void sample_resolve_body(const Plan &p, unsigned long long *sh, int shift)
 {
     SelState *st = p.st;
     if (p.key_est_dev) {  // DGC: the candidates are exactly {key >= sampled threshold}
@@ -339,7 +334,7 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh)
 #pragma unroll
     for (int i = PER - 1; i >= 0; i--) {
         if (acc < target && acc + h[i] >= target) {
-            uint32_t est = (uint32_t)(t * PER + i) << GVC_SAMPLE_SHIFT;
+            uint32_t est = (uint32_t)(t * PER + i) << shift;
             st->key_est = est;
             uint32_t mk = st->max_key;
             uint64_t span = mk > est ? (uint64_t)(mk - est) : 0;
@@ -354,7 +349,7 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
 {
     pdl_enter();
     __shared__ unsigned long long sh[33];
-    sample_resolve_body(p, sh);
+    sample_resolve_body(p, sh, GVC_SAMPLE_SHIFT);
 }
 
 // ----------------------------------------------------------------- collect
@@ -858,12 +853,12 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         uint4 niv = make_uint4(0u, 0u, 0u, 0u), niv2 = niv;
         if (cnt) {
             nfv = *reinterpret_cast<const float4 *>(p.cand_val + beg + lane * 4);
-            if (KM == KEY_HASH)
+            if (KM != KEY_MAG)
                 niv = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + lane * 4);
         }
         if (cnt > 128) {
             nfv2 = *reinterpret_cast<const float4 *>(p.cand_val + beg + 128 + lane * 4);
-            if (KM == KEY_HASH)
+            if (KM != KEY_MAG)
                 niv2 = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + 128 + lane * 4);
         }
         for (uint32_t base = 0; base < cnt; base += 128) {  // warp-uniform trip count
@@ -874,7 +869,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
             niv = niv2;
             if (base + 256 < cnt) {
                 nfv2 = *reinterpret_cast<const float4 *>(p.cand_val + beg + t + 256);
-                if (KM == KEY_HASH)
+                if (KM != KEY_MAG)
                     niv2 = *reinterpret_cast<const uint4 *>(p.cand_idx + beg + t + 256);
             }
             const float v[4] = {fv.x, fv.y, fv.z, fv.w};
@@ -893,8 +888,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
                 for (int c = 0; c < 4; c++) {
                     const bool okc = full || t + c < cnt;
                     const uint32_t k = okc ? cand_key<KM>(p, v[c], pos[c]) : 0u;
-                    if (KM == KEY_MAG)
-                        nan_any |= (uint32_t)(okc & (k > 0x7f800000u));
+                    if (KM != KEY_HASH)
+                        nan_any |= (uint32_t)(okc & key_nan<KM>(k));
                     const bool fast = okc & (k - f1_base < f1_w);
                     const bool fast2 = NB >= 2 && (okc & (k - f2_base < f2_w));
                     const double d = (double)v[c];
@@ -1332,7 +1327,7 @@ __global__ void __launch_bounds__(1024) k_finish_j(const Plan p, int)
         const double A = ba + ta;
         double E = be + te;
         const float m = (float)(A / (double)k);
-        const unsigned long long nnz = k - ((KM == KEY_MAG && T == 0u) ? q : 0ull);
+        const unsigned long long nnz = k - ((KM != KEY_HASH && (T & 0x7fffffffu) == 0u) ? q : 0ull);
         if (p.kind == GVC_REDSYNC)
             E = (double)nnz * ((double)m * (double)m);
         st->redsync_mean[j] = m;
@@ -1650,13 +1645,19 @@ static void launch_tail_nb(const Plan &p, cudaStream_t s, bool pdl)
 template <int KM>
 static void launch_tail(const Plan &p, cudaStream_t s, bool pdl)
 {
-    const bool abs_sums = p.kind == GVC_REDSYNC;
-    switch (nb_for(p.n_ks)) {
-    case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, s, pdl) : launch_tail_nb<KM, 1, false>(p, s, pdl); break;
-    case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, s, pdl) : launch_tail_nb<KM, 2, false>(p, s, pdl); break;
-    case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, s, pdl) : launch_tail_nb<KM, 4, false>(p, s, pdl); break;
-    case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, s, pdl) : launch_tail_nb<KM, 8, false>(p, s, pdl); break;
-    default: abs_sums ? launch_tail_nb<KM, 16, true>(p, s, pdl) : launch_tail_nb<KM, 16, false>(p, s, pdl); break;
+    if constexpr (KM == KEY_DGC) {  // DGC picks one keep count at a time
+        launch_tail_nb<KM, 1, false>(p, s, pdl);
+    } else {
+        const bool abs_sums = p.kind == GVC_REDSYNC;
+        switch (nb_for(p.n_ks)) {
+        case 1: abs_sums ? launch_tail_nb<KM, 1, true>(p, s, pdl) : launch_tail_nb<KM, 1, false>(p, s, pdl); break;
+        case 2: abs_sums ? launch_tail_nb<KM, 2, true>(p, s, pdl) : launch_tail_nb<KM, 2, false>(p, s, pdl); break;
+        case 4: abs_sums ? launch_tail_nb<KM, 4, true>(p, s, pdl) : launch_tail_nb<KM, 4, false>(p, s, pdl); break;
+        case 8: abs_sums ? launch_tail_nb<KM, 8, true>(p, s, pdl) : launch_tail_nb<KM, 8, false>(p, s, pdl); break;
+        default:
+            abs_sums ? launch_tail_nb<KM, 16, true>(p, s, pdl) : launch_tail_nb<KM, 16, false>(p, s, pdl);
+            break;
+        }
     }
 }
 
@@ -1667,7 +1668,8 @@ static void set_attributes()
     if (done)
         return;
     done = true;
-    cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
+    cudaFuncSetAttribute(k_sample<KEY_MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
+    cudaFuncSetAttribute(k_sample<KEY_DGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
 #define GVC_PASS1_ATTR(KM, NB, ABS)                                                                          \
     cudaFuncSetAttribute(k_pass1<KM, NB, ABS>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
                          (int)((NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4)));
@@ -1678,6 +1680,7 @@ static void set_attributes()
     GVC_PASS1_ATTR(KM, 16, true)
     GVC_PASS1_ATTR_KM(KEY_MAG)
     GVC_PASS1_ATTR_KM(KEY_HASH)
+    GVC_PASS1_ATTR(KEY_DGC, 1, false)
 }
 
 // The select pipeline on stream s; every kernel takes the plan by value (its
@@ -1691,10 +1694,10 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     ProfScope all(probes ? PROF_SELECT : -1, s);
     const int blocks = (int)p.B;
     int launches = 0;
-    if (KM == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
+    if (KM != KEY_HASH && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
         uint64_t wb = (p.s_chunks + 31) / 32;
         int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
-        k_sample<<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);  // its last block resolves key_est
+        k_sample<KM><<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);  // its last block resolves key_est
         launches++;
     } else {
         k_sample_resolve<<<1, 1024, 0, s>>>(p, 0);
@@ -1740,10 +1743,11 @@ static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *laun
     cudaMemsetAsync(p.st, 0, sizeof(SelState), s);
     cudaMemsetAsync(p.hist0, 0, GVC_H0_BINS * 4, s);
     cudaMemsetAsync(p.histl, 0, GVC_MAX_LADDER * GVC_HL_BINS * 4, s);
-    if (p.keymode == KEY_MAG)
+    if (p.keymode != KEY_HASH)
         cudaMemsetAsync(p.shist, 0, GVC_SAMPLE_BINS * 4, s);
-    *launches = p.keymode == KEY_MAG ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
-                                     : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
+    *launches = p.keymode == KEY_MAG   ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
+                : p.keymode == KEY_DGC ? launch_pipeline<KEY_DGC>(p, s, probes, gprobes)
+                                       : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
     if (gprobes)
         cudaEventRecordWithFlags(g_ev_mark[3], s, cudaEventRecordExternal);
 }
@@ -1772,7 +1776,7 @@ static std::string graph_key(const Plan &p, const void *ws)
     char buf[256];
     snprintf(buf, sizeof(buf), "%p|%llu|%d|%d|%d|%d|%d|%d|%d|%d|%d", ws, (unsigned long long)p.n, p.keymode, p.ef,
              p.pmask ? p.pmode : 0, nb_for(p.n_ks), p.kind == GVC_REDSYNC, p.force_exact,
-             (int)(p.keymode == KEY_MAG && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev),
+             (int)(p.keymode != KEY_HASH && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev),
              p.key_est_dev != nullptr, (int)p.s_chunks);
     return std::string(buf);
 }
@@ -1787,7 +1791,9 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.n = a->n;
     p.n_ks = a->n_ks;
     p.kind = a->kind;
-    p.keymode = a->kind == GVC_RANDOMK ? KEY_HASH : KEY_MAG;
+    p.keymode = a->kind == GVC_RANDOMK ? KEY_HASH : (a->dgc_thr_dev ? KEY_DGC : KEY_MAG);
+    p.dgc_thr = a->dgc_thr_dev;
+    p.dgc_bits = a->dgc_sampled_dev;
     p.ef = a->g_dev != nullptr;
     p.force_exact = a->force_exact;
     p.values = a->values_dev;
@@ -1808,7 +1814,7 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
         p.ks[j] = a->ks[j];
     p.res = res;
     const uint64_t n = a->n, k0 = a->ks[0];
-    if (p.keymode == KEY_MAG) {
+    if (p.keymode != KEY_HASH) {
         // sample ~n/128 values (at most 2^19) in 128-value chunks (everything
         // when n is small): past ~10^5 sampled candidates the 5-sigma margin is
         // already a few tenths of a percent of k_0, and the sample pass is pure latency
@@ -1975,6 +1981,7 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         if (!attr) {
             cudaFuncSetAttribute(k_emit<KEY_MAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(k_emit<KEY_DGC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_MAG, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             attr = true;
         }
@@ -1985,12 +1992,18 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         else if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
                                                                        sm_out, tile_b, mir, stats != nullptr);
+        else if (p.keymode == KEY_DGC)
+            k_emit<KEY_DGC, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                       sm_out, tile_b, mir, stats != nullptr);
         else
             k_emit<KEY_HASH, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
                                                                         smask, sm_out, tile_b, mir, stats != nullptr);
     } else {
         if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                   sm_out, tile_b, mir, stats != nullptr);
+        else if (p.keymode == KEY_DGC)
+            k_emit<KEY_DGC, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
                                                                    sm_out, tile_b, mir, stats != nullptr);
         else
             k_emit<KEY_HASH, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
