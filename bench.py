@@ -97,44 +97,52 @@ def true_residual(r, mask, pm, pmode):
     return r
 
 
-def replay_step(O, snap_in, snap_out, res, M, theta_min, theta_s, extra, world, kind):
-    """Re-check one timed step of run_iteration against the C oracle: chosen
-    entries and residual bit-exact, gains within 1e-6 (fp64 summation order),
-    the averaged gradient bit-exact (one rank).  Returns "ok" or the mismatch."""
+def replay_step(O, snap_in, snap_out, res, M, theta_min, theta_s, extra, world, kind, rng=None, it=0, w=0):
+    """Re-check one timed step of run_iteration against the C oracle
+    (controller.py:192-281 replayed on one worker): the sent entries and the
+    residual bit-exact (Redsync values and the residual they leave within
+    1e-6), gains within 1e-6 (fp64 summation order), the averaged gradient
+    bit-exact (one rank).  Returns "ok" or the mismatches."""
     g, r_raw, mask, pm, pmode = snap_in
     idx, vals, avg, r2_raw, mask2, pm2, pmode2 = snap_out
     ef = O.ef_add(g, true_residual(r_raw, mask, pm, pmode))
     norm = O.sq_norm(ef)
     k1 = O.keep_count(M, theta_min)
-    kc = O.keep_count(k1, theta_s)
     problems = []
-
-    def top(k):
-        return O.topk_indices(ef, k) if kind == "topk" else None
-    i1 = top(k1)
-    ic = top(kc) if kc != k1 else i1
-    if kind == "topk" and world == 1:
-        for name, want, got in (("gain_min", O.sq_norm(ef[i1.astype(np.int64)]) / norm, res.gain_min_raw),
-                                ("gain_c", O.sq_norm(ef[ic.astype(np.int64)]) / norm, res.gain_c_raw)):
-            if abs(got - min(1.0, want)) > 1e-6 * min(1.0, want):
+    if kind == "topk":
+        i1 = O.topk_indices(ef, k1)
+        v1 = ef[i1.astype(np.int64)]
+    else:
+        s0 = rng.split(it, w, 0)
+        i1, v1 = O.select(kind, ef, k1, seed=s0.seed, stream=s0.stream)
+    s1 = rng.split(it, w, 1) if rng is not None else None
+    i2, v2, _ = O.compress_further(kind, i1, v1, M, theta_s, seed=s1.seed if s1 else 0,
+                                   stream=s1.stream if s1 else 0)
+    if world == 1:
+        for name, want, got in (("gain_min", min(1.0, O.sq_norm(v1) / norm), res.gain_min_raw),
+                                ("gain_c", min(1.0, O.sq_norm(v2) / norm), res.gain_c_raw)):
+            if abs(got - want) > 1e-6 * want:
                 problems.append(f"{name} {got} vs {want}")
-        for c in extra:
+        for c in (extra if kind == "topk" else ()):
             kx = O.keep_count(k1, c / theta_min)
             want = min(1.0, O.sq_norm(ef[O.topk_indices(ef, kx).astype(np.int64)]) / norm)
             if abs(res.ladder_gains[c] - want) > 1e-6 * want:
                 problems.append(f"gain_{c} {res.ladder_gains[c]} vs {want}")
-    if kind == "topk" and res.decision.choice != "dense":
-        want_idx = ic if res.decision.choice == "candidate" else i1
+    if res.decision.choice != "dense":
+        want_idx, want_vals = (i2, v2) if res.decision.choice == "candidate" else (i1, v1)
         if not np.array_equal(idx, want_idx):
             problems.append("sent indices")
-        want_vals = ef[want_idx.astype(np.int64)]
-        if not np.array_equal(vals.view(np.uint32), want_vals.view(np.uint32)):
+        exact = kind != "redsync"
+        if exact and not np.array_equal(vals.view(np.uint32), want_vals.view(np.uint32)):
             problems.append("sent values")
-        r_want = O.update_residual(ef, want_idx, want_vals)
-        if not np.array_equal(true_residual(r2_raw, mask2, pm2, pmode2).view(np.uint32), r_want.view(np.uint32)):
+        if not exact and not np.allclose(vals, want_vals, rtol=1e-6, atol=0):
+            problems.append("sent values (1e-6)")
+        r_want = O.update_residual(ef, want_idx, vals)
+        r_got = true_residual(r2_raw, mask2, pm2, pmode2)
+        if not np.array_equal(r_got.view(np.uint32), r_want.view(np.uint32)):
             problems.append("residual")
         if world == 1 and avg is not None:
-            a_want = O.aggregate([(want_idx, want_vals)], M)
+            a_want = O.aggregate([(want_idx, vals)], M)
             if not np.array_equal(avg.view(np.uint32), a_want.view(np.uint32)):
                 problems.append("averaged gradient")
     return "ok" if not problems else "FAIL: " + ", ".join(problems)
@@ -345,7 +353,7 @@ def north_star(args, G, nat, O, dev):
     host[3] = None if host[3] is None else float(host[3][0])
     host_out = [t.cpu().numpy() if isinstance(t, torch.Tensor) else t for t in snap_out]
     host_out[5] = None if host_out[5] is None else float(host_out[5][0])
-    parity = replay_step(O, host, host_out, res, M, theta_min, theta_s, extra, 1, "topk")
+    parity = replay_step(O, host, host_out, res, M, theta_min, theta_s, extra, 1, "topk", rng, state.iteration, 0)
     peak, peak_kind = peaks()
     sel_ms = prof["select"][0] / max(prof["select"][1], 1)
     col_ms = prof["collect"][0] / max(prof["collect"][1], 1)
@@ -560,7 +568,8 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     host_out = [t.cpu().numpy() if isinstance(t, torch.Tensor) else t for t in snap_out]
     host[3] = None if host[3] is None else float(host[3][0])
     host_out[5] = None if host_out[5] is None else float(host_out[5][0])
-    parity = replay_step(O, host, host_out, last_res, M, theta_min, theta_s, extra, world, args.kind)
+    parity = replay_step(O, host, host_out, last_res, M, theta_min, theta_s, extra, world, args.kind, rng,
+                         state.iteration, rank)
 
     north = None
     if world == 1 and args.workload == "resnet101" and not args.no_north_star:

@@ -232,6 +232,24 @@ GVC_API int gvc_emit_mirrored(void *ws_dev, size_t ws_bytes, int j, const uint32
              uint32_t *sent_mask_dev, float *sent_m_dev, uint32_t *tile_bounds_dev,
              double *sent_stats_dev, const gvc_emit_mirrors *mirrors, void *stream);
 GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, uint32_t epoch, void *stream);
+
+/* ---- dense fallback over peer memory (C3) ----
+ * The dense message of a step whose decision is DENSE (controller.py:217-230,
+ * 259-264) and its mean, aggregate_dense (compressors.py:274-285), as one
+ * fused reduce-scatter + all-gather over NVLink.  peer_bufs[q]: rank q's
+ * peer-mapped buffer holding its dense input (n floats, 16-byte aligned,
+ * room for n rounded up to 4).  After every rank posted `epoch` into flags
+ * (gvc_peer_signal), gvc_dense_mean_peers makes rank `rank` sum its range
+ * [n4*rank/W, n4*(rank+1)/W) of float4s (n4 = ceil(n/4)) over the W inputs in
+ * fp64 in rank order, divide by W, round to fp32, and write the result range
+ * into every rank's buffer.  Once every rank has posted a second epoch
+ * (signal after gvc_dense_mean_peers), gvc_dense_collect copies the full mean
+ * from this rank's buffer to out_dev.  Waits are bounded (~4 s): a timeout
+ * sets bit 4 of *err_dev instead of hanging. */
+GVC_API int gvc_dense_mean_peers(float *const *peer_bufs, int nranks, int rank, uint64_t n, const uint32_t *flags,
+                                 uint32_t epoch, uint32_t *err_dev, void *stream);
+GVC_API int gvc_dense_collect(const float *own_dev, float *out_dev, uint64_t n, const uint32_t *flags, int nranks,
+                              uint32_t epoch, uint32_t *err_dev, void *stream);
 GVC_API int gvc_aggregate_peers(const uint32_t *const *idx_dev, const float *const *vals_dev,
                         const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,
                         const uint32_t *flags_dev, uint32_t epoch, float *out_dev, void *stream);

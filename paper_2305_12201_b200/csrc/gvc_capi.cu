@@ -341,6 +341,22 @@ int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, 
     return rc ? rc : check_launch("aggregate_dense");
 }
 
+int gvc_dense_mean_peers(float *const *peer_bufs, int nranks, int rank, uint64_t n, const uint32_t *flags,
+                         uint32_t epoch, uint32_t *err_dev, void *stream)
+{
+    if (!peer_bufs)
+        return set_error(GVC_ERR_ARG, "gvc_dense_mean_peers: null buffer table");
+    int rc = dense_mean_peers_run(peer_bufs, nranks, rank, n, flags, epoch, err_dev, STREAM(stream));
+    return rc ? rc : check_launch("dense_mean_peers");
+}
+
+int gvc_dense_collect(const float *own_dev, float *out_dev, uint64_t n, const uint32_t *flags, int nranks,
+                      uint32_t epoch, uint32_t *err_dev, void *stream)
+{
+    int rc = dense_collect_run(own_dev, out_dev, n, flags, nranks, epoch, err_dev, STREAM(stream));
+    return rc ? rc : check_launch("dense_collect");
+}
+
 int gvc_gather_ef(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,
                   const uint32_t *pmask, const float *pm, int pmode, float *out, void *stream)
 {

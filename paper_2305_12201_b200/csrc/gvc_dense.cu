@@ -1082,6 +1082,116 @@ int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, 
     return GVC_OK;
 }
 
+// ------------------------------------------------ C3 over peer memory
+// The dense fallback's exchange + mean (controller.py:259-264 -> aggregate_dense,
+// compressors.py:274-285) as a reduce-scatter + all-gather fused over NVLink:
+// every rank's dense input sits in its peer-mapped buffer; rank `rank` owns
+// the float4 range [lo4, hi4), sums the W inputs there in fp64 in rank order,
+// divides by W and rounds to fp32 -- aggregate_dense's arithmetic -- and
+// writes the result range into EVERY rank's buffer, over the inputs (only the
+// owner reads that range).  Each rank moves 2 (W-1)/W of the vector over
+// NVLink instead of receiving W-1 whole vectors.
+struct DensePeers {
+    float *buf[GVC_MAX_PEERS];
+};
+
+// Bounded wait for flags[q] >= epoch (q < W); bit 4 of *err on timeout.
+__device__ __forceinline__ void wait_peer_flags(const uint32_t *flags, int W, uint32_t epoch, uint32_t *err)
+{
+    if (threadIdx.x < W) {
+        const long long t0 = clock64();
+        while ((int32_t)(ld_acquire_sys(flags + threadIdx.x) - epoch) < 0) {
+            __nanosleep(64);
+            if (clock64() - t0 > (1ll << 33)) {  // ~4 s: a rank died or diverged
+                atomicOr(err, 4u);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_dense_mean_peers(DensePeers P, int W, uint64_t lo4, uint64_t hi4,
+                                                          const uint32_t *flags, uint32_t epoch, uint32_t *err)
+{
+    wait_peer_flags(flags, W, epoch, err);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const double inv = 1.0 / (double)W;
+    (void)inv;
+    for (uint64_t i = lo4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi4; i += stride) {
+        float4 x[GVC_MAX_PEERS];
+#pragma unroll
+        for (int q = 0; q < GVC_MAX_PEERS; q++)
+            if (q < W)
+                x[q] = __ldcg(reinterpret_cast<const float4 *>(P.buf[q]) + i);
+        double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+#pragma unroll
+        for (int q = 0; q < GVC_MAX_PEERS; q++) {
+            if (q < W) {
+                a += (double)x[q].x;
+                b += (double)x[q].y;
+                c += (double)x[q].z;
+                d += (double)x[q].w;
+            }
+        }
+        const float4 o = make_float4((float)(a / (double)W), (float)(b / (double)W), (float)(c / (double)W),
+                                     (float)(d / (double)W));
+#pragma unroll
+        for (int q = 0; q < GVC_MAX_PEERS; q++)
+            if (q < W)
+                __stcg(reinterpret_cast<float4 *>(P.buf[q]) + i, o);
+    }
+    __threadfence_system();  // the result ranges are visible at every peer before this rank signals
+}
+
+// Wait until every rank wrote its result range into this buffer, then copy the
+// mean out of the peer-mapped buffer.
+__global__ void __launch_bounds__(256) k_dense_collect(const float *own, float *out, uint64_t n, const uint32_t *flags,
+                                                       int W, uint32_t epoch, uint32_t *err)
+{
+    wait_peer_flags(flags, W, epoch, err);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t n4 = n / 4;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+        __stcs(reinterpret_cast<float4 *>(out) + i, __ldcg(reinterpret_cast<const float4 *>(own) + i));
+    for (uint64_t i = n4 * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = __ldcg(own + i);
+}
+
+int dense_mean_peers_run(float *const *bufs, int nranks, int rank, uint64_t n, const uint32_t *flags,
+                         uint32_t epoch, uint32_t *err, cudaStream_t s)
+{
+    if (nranks < 1 || nranks > GVC_MAX_PEERS || rank < 0 || rank >= nranks || !flags || !err)
+        return set_error(GVC_ERR_ARG, "dense_mean_peers: rank %d of %d", rank, nranks);
+    DensePeers P;
+    for (int q = 0; q < nranks; q++) {
+        if (!bufs[q] || ((uintptr_t)bufs[q] & 15))
+            return set_error(GVC_ERR_ARG, "dense_mean_peers: buffer of rank %d null or not 16-byte aligned", q);
+        P.buf[q] = bufs[q];
+    }
+    const uint64_t n4 = (n + 3) / 4;  // the buffers hold n rounded up to 4 floats
+    const uint64_t lo4 = n4 * rank / nranks, hi4 = n4 * (rank + 1) / nranks;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    count_launches(1);
+    k_dense_mean_peers<<<grid_for(hi4 - lo4, 256, sms * 8), 256, 0, s>>>(P, nranks, lo4, hi4, flags, epoch, err);
+    return GVC_OK;
+}
+
+int dense_collect_run(const float *own, float *out, uint64_t n, const uint32_t *flags, int nranks, uint32_t epoch,
+                      uint32_t *err, cudaStream_t s)
+{
+    if (!own || !out || !flags || !err || nranks < 1 || nranks > GVC_MAX_PEERS)
+        return set_error(GVC_ERR_ARG, "dense_collect: bad arguments");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    count_launches(1);
+    k_dense_collect<<<grid_for(n / 4 + 1, 256, sms * 8), 256, 0, s>>>(own, out, n, flags, nranks, epoch, err);
+    return GVC_OK;
+}
+
 __global__ void k_iota(uint32_t *out, uint64_t n)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

@@ -57,6 +57,10 @@ int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, 
                   int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *bounds,
                   uint64_t bounds_stride, cudaStream_t s);
 int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, cudaStream_t s);
+int dense_mean_peers_run(float *const *bufs, int nranks, int rank, uint64_t n, const uint32_t *flags,
+                         uint32_t epoch, uint32_t *err, cudaStream_t s);
+int dense_collect_run(const float *own, float *out, uint64_t n, const uint32_t *flags, int nranks, uint32_t epoch,
+                      uint32_t *err, cudaStream_t s);
 int iota_run(uint32_t *out, uint64_t n, cudaStream_t s);
 int gather_ef_run(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,
                   const uint32_t *pmask, const float *pm, int pmode, float *out, cudaStream_t s);

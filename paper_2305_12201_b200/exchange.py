@@ -320,6 +320,89 @@ def exchange_mode(group) -> str:
     return mode
 
 
+class DenseExchange:
+    """C3 -- the dense fallback's exchange + mean -- fused over NVLink peer memory.
+
+    Every rank owns one symmetric buffer [flags: 64 u32 | parity 0: n | parity 1: n]
+    (floats).  Exchange x: each rank copies its dense message into its own
+    parity-x%2 region and posts 2x - 1; gvc_dense_mean_peers makes it the owner
+    of 1/W of the positions: it sums the W inputs there in fp64 in rank order
+    (aggregate_dense's arithmetic, compressors.py:274-285) and writes the mean
+    into that range of every rank's region; after everyone posted 2x, the full
+    mean is copied out.  Per rank 2 (W - 1) / W of the vector crosses NVLink
+    (the all-gather fallback receives W - 1 whole vectors).  A region is reused
+    two exchanges later, after every rank posted 2x + 1 -- which it does only
+    after its own copy-out of x.
+    """
+
+    FLAG_WORDS = 64
+    _cache: dict = {}
+
+    def __init__(self, group, device):
+        self.group, self.device = group, device
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.cap = 0
+        self.x = 0
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+
+    @classmethod
+    def get(cls, group, device) -> "DenseExchange":
+        key = (id(group), device.index)
+        dx = cls._cache.get(key)
+        if dx is None:
+            dx = cls._cache[key] = cls(group, device)
+        return dx
+
+    def _ensure(self, n: int) -> None:
+        if n <= self.cap:
+            return
+        import torch.distributed._symmetric_memory as symm
+        torch.cuda.synchronize(self.device)
+        cap = (n + 1023) & ~1023
+        buf = symm.empty(self.FLAG_WORDS + 2 * cap, dtype=torch.int32, device=self.device)
+        buf[:self.FLAG_WORDS].zero_()
+        handle = symm.rendezvous(buf, self.group)  # collective: every rank grows together
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        self.buf, self.handle, self.cap, self.x = buf, handle, cap, 0
+        self.bases = [int(p) for p in handle.buffer_ptrs]
+        self._flag_ptrs = (ctypes.c_void_p * self.world)(*self.bases)
+
+    def mean(self, g: GradientVector, out: torch.Tensor | None = None) -> torch.Tensor:
+        n = g.length
+        self._ensure(n)
+        x = self.x + 1
+        base = self.FLAG_WORDS + (x % 2) * self.cap  # words
+        own = self.buf[base:base + n].view(torch.float32)
+        own.copy_(g.values)
+        lib = nat.load()
+        stream = nat.stream_ptr(self.device)
+        W = self.world
+        nat.check(lib.gvc_peer_signal(self._flag_ptrs, W, self.rank, 2 * x - 1, stream), "peer_signal")
+        regions = (ctypes.c_void_p * W)(*[b + 4 * base for b in self.bases])
+        nat.check(lib.gvc_dense_mean_peers(regions, W, self.rank, n, nat.ptr(self.buf), 2 * x - 1,
+                                           nat.ptr(self.err), stream), "dense_mean_peers")
+        nat.check(lib.gvc_peer_signal(self._flag_ptrs, W, self.rank, 2 * x, stream), "peer_signal")
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self.device)
+        nat.check(lib.gvc_dense_collect(nat.ptr(own), nat.ptr(out), n, nat.ptr(self.buf), W, 2 * x,
+                                        nat.ptr(self.err), stream), "dense_collect")
+        self.x = x
+        return out
+
+
+def dense_mean(g: GradientVector, group=None) -> GradientVector:
+    """C3 with the reference's fp64 rank-ordered mean: fused over peer memory
+    (DenseExchange) on an NCCL group of one node, else all-gather + mean."""
+    if (group is not None and dist.get_backend(group) == "nccl" and dist.get_world_size(group) <= nat.MAX_PEERS
+            and exchange_mode(group) != "nccl"):
+        px = PeerExchange.get(group, g.values.device)
+        if px.ok:  # symmetric memory works on this node (probed once, agreed by every rank)
+            return GradientVector._wrap(DenseExchange.get(group, g.values.device).mean(g), g.layer_offsets)
+    return allgather_dense_mean(g, group)
+
+
 def allgather_dense_mean(g: GradientVector, group=None) -> GradientVector:
     """C3: dense fallback with the reference's fp64 rank-ordered mean."""
     from .compressors import aggregate_dense

@@ -46,21 +46,35 @@ def _worker(rank, world, port, kind, q, exchange="auto"):
     dist.destroy_process_group()
 
 
-def _spawn(target, world, *args):
+def _spawn(target, world, *args, attempts=3):
+    """Run target on `world` ranks; a rendezvous port taken between choosing it
+    and binding it (EADDRINUSE) is retried on a fresh port."""
+    import queue
+
     import torch.multiprocessing as mp
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=300) for _ in procs)
-    for p in procs:
-        p.join(60)
-        assert p.exitcode == 0
-    return res
+    for attempt in range(attempts):
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        procs = [ctx.Process(target=target, args=(r, world, port) + args + (q,)) for r in range(world)]
+        for p in procs:
+            p.start()
+        try:
+            res = dict(q.get(timeout=300) for _ in procs)
+        except queue.Empty:
+            for p in procs:
+                p.join(30)
+                if p.is_alive():
+                    p.kill()
+            if attempt + 1 < attempts:
+                continue
+            raise
+        for p in procs:
+            p.join(60)
+            assert p.exitcode == 0
+        return res
 
 
 def _world():
@@ -123,5 +137,56 @@ def _peer_worker(rank, world, port, q):
 def test_peer_exchange_epochs():
     world = _world()
     res = _spawn(_peer_worker, world)
+    for r in range(world):
+        assert all(res[r]), res[r]
+
+
+def _dense_worker(rank, world, port, exchange, q):
+    """The dense fallback (every decision DENSE at epsilon 0.99) through
+    run_iteration: the averaged gradient equals aggregate_dense over every
+    rank's g_ef, bit for bit; then DenseExchange alone on odd lengths (float4
+    tails, buffer growth, both parities) against the oracle's fp64 mean."""
+    os.environ["GVC_EXCHANGE"] = exchange
+    import torch.distributed as dist
+    from oracle import oracle as O
+    import paper_2305_12201_b200 as G
+    from paper_2305_12201_b200.exchange import DenseExchange, allgather_dense_mean
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=dev)
+    n = 300_007
+    cfg = G.ControllerConfig(theta_min=10.0, theta_max=1000.0, epsilon=0.99, window=1 << 30,
+                             compressor=G.CompressorKind("topk"))
+    state = G.ControllerState.fresh(cfg, world)
+    store = G.ResidualStore(n)
+    ok = []
+    for it in range(1, 4):
+        g = np.random.default_rng(10 * it + rank).standard_normal(n).astype(np.float32) * (1 + rank)
+        r_before = store.residual.clone()
+        res = G.run_iteration(state, G.GradientVector(g), store, G.CostModelParams(workers=world), G.SeededRng(1),
+                              group=dist.group.WORLD, average=True)
+        ef = G.apply_feedback(G.GradientVector(g), G.ResidualStore(n)).values + r_before
+        ref = allgather_dense_mean(G.GradientVector._wrap(ef), dist.group.WORLD).values
+        ok.append(res.decision.choice == "dense" and bool(torch.equal(res.averaged.values.view(torch.int32),
+                                                                     ref.view(torch.int32))))
+    if exchange != "nccl":
+        dx = DenseExchange.get(dist.group.WORLD, dev)
+        for e, m in enumerate([1, 5, 4099, 300_007, 1_000_001, 17]):
+            xs = [np.random.default_rng(100 * e + r).standard_normal(m).astype(np.float32) * (1 + r)
+                  for r in range(world)]
+            if e == 2:
+                xs[0][::3] = -0.0
+            out = dx.mean(G.GradientVector(xs[rank])).cpu().numpy()
+            ok.append(bool(np.array_equal(out.view(np.int32), O.aggregate_dense(xs).view(np.int32))))
+        ok.append(int(dx.err.item()) == 0)
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["staged", "nccl"])
+def test_dense_fallback_multi_rank(exchange):
+    world = _world()
+    res = _spawn(_dense_worker, world, exchange)
     for r in range(world):
         assert all(res[r]), res[r]
