@@ -233,6 +233,22 @@ GVC_API int gvc_emit_mirrored(void *ws_dev, size_t ws_bytes, int j, const uint32
              double *sent_stats_dev, const gvc_emit_mirrors *mirrors, void *stream);
 GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, uint32_t epoch, void *stream);
 
+/* ---- layerwise compression (compressors.py:204-217) as one segmented selection ----
+ * Segment q = [seg_offsets[q], seg_offsets[q + 1]) keeps seg_k[q] entries
+ * (keep_count of its length) by the compressor's key -- |v| for Top-k, the
+ * Philox position hash of the global position for Random-k -- ties to the
+ * lower index; out = the segments' (global index, value) lists concatenated
+ * in segment order (sum seg_k entries; a segment with seg_k >= its length
+ * keeps everything).  seg_offsets / seg_k are HOST arrays.  Every segment is
+ * resolved by the same 11 launches (4 radix passes of 8 key bits over all
+ * segments at once, counts, one scan, an ordered compaction) however many
+ * segments there are.  *status_dev |= 1 on a NaN magnitude. */
+GVC_API size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg);
+GVC_API int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
+                                 const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream,
+                                 uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev, size_t ws_bytes,
+                                 uint32_t *status_dev, void *stream);
+
 /* ---- dense fallback over peer memory (C3) ----
  * The dense message of a step whose decision is DENSE (controller.py:217-230,
  * 259-264) and its mean, aggregate_dense (compressors.py:274-285), as one

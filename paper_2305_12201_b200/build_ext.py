@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgravac_b200.so")
-SOURCES = ["gvc_capi.cu", "gvc_select.cu", "gvc_dense.cu"]
+SOURCES = ["gvc_capi.cu", "gvc_select.cu", "gvc_dense.cu", "gvc_segsel.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -236,6 +236,63 @@ def _select(kind: CompressorKind, values: torch.Tensor, k: int, rng: SeededRng |
     return out
 
 
+def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf: float, rng):
+    """compressors.py:204-217: per segment keep_count(len, cf) by the kind's
+    rule, indices offset by the segment start, concatenated in order.  Top-k
+    and Random-k: one segmented selection over every segment
+    (gvc_segmented_select); DGC and Redsync: one selection per segment,
+    enqueued back to back, statuses read once at the end."""
+    n = values.numel()
+    bounds = [sl for sl in g.layer_slices() if sl.stop > sl.start]
+    ks = [keep_count(sl.stop - sl.start, cf) for sl in bounds]
+    if kind.name in (RANDOMK, DGC) and rng is None:
+        raise ValueError(f"{kind.name} compression requires an rng")
+    dev = values.device
+    lib = nat.load()
+    if kind.name in (TOPK, RANDOMK):
+        total = sum(min(k, sl.stop - sl.start) for k, sl in zip(ks, bounds))
+        offs = (ctypes.c_uint64 * (len(bounds) + 1))()
+        kk = (ctypes.c_uint64 * len(bounds))(*ks)
+        for q, sl in enumerate(bounds):
+            offs[q] = sl.start
+        offs[len(bounds)] = bounds[-1].stop
+        # (segments are contiguous in GradientVector: each starts where the previous ended)
+        contiguous = all(bounds[q].stop == bounds[q + 1].start for q in range(len(bounds) - 1))
+        if contiguous:
+            idx = torch.empty(total, dtype=torch.int32, device=dev).view(torch.uint32)
+            vals = torch.empty(total, dtype=torch.float32, device=dev)
+            ws = nat.Workspace.get(dev, "segsel", int(lib.gvc_segmented_select_workspace_bytes(n, len(bounds))))
+            status = torch.zeros(1, dtype=torch.int32, device=dev)
+            nat.check(lib.gvc_segmented_select(kind.kind_id, nat.ptr(values), n, offs, kk, len(bounds),
+                                               rng.seed if rng is not None else 0, rng.stream if rng is not None else 0,
+                                               nat.ptr(idx), nat.ptr(vals), nat.ptr(ws), ws.numel(), nat.ptr(status),
+                                               nat.stream_ptr(dev)), "segmented_select")
+            if int(status.item()) & 1:
+                raise ValueError("NaN in gradient: compression order undefined")
+            return idx, vals
+    idx_parts, val_parts, checks = [], [], []
+    for sl, k in zip(bounds, ks):
+        seg = values[sl.start:sl.stop]
+        if seg.data_ptr() % 16:
+            seg = seg.clone()
+        m = sl.stop - sl.start
+        if k >= m:
+            i, v = _iota(m, dev), seg.clone()
+        elif kind.name == DGC:
+            from .dgc import dgc_select
+            i, v, sel = dgc_select(kind, seg, k, rng, pos_base=sl.start, check=False, want_result=True)
+            checks.append(sel)
+        else:
+            sel = Selection(kind, [k], values=seg, rng=rng, pos_base=sl.start)
+            i, v = sel.emit(0)
+            checks.append(sel)
+        idx_parts.append(i.to(torch.int64) + sl.start)
+        val_parts.append(v)
+    for sel in checks:  # one read-back each, after every segment was enqueued
+        sel.result()
+    return torch.cat(idx_parts).to(torch.uint32), torch.cat(val_parts)
+
+
 def compress(kind: CompressorKind, g: GradientVector, cf: float, rng: SeededRng | None = None,
              latency: LatencyFn | None = None, layerwise: bool = False) -> tuple[SparseGradient, float]:
     """Compress a dense gradient to factor cf (compressors.py:193-223).
@@ -248,18 +305,7 @@ def compress(kind: CompressorKind, g: GradientVector, cf: float, rng: SeededRng 
     nat.require_cuda(values)
     n = values.numel()
     if layerwise and len(g.layer_offsets) > 1:
-        idx_parts, val_parts = [], []
-        for sl in g.layer_slices():
-            if sl.stop <= sl.start:
-                continue
-            seg = values[sl.start:sl.stop]
-            if seg.data_ptr() % 16:
-                seg = seg.clone()
-            i, v = _select(kind, seg, keep_count(sl.stop - sl.start, cf), rng, pos_base=sl.start)
-            idx_parts.append(i.to(torch.int64) + sl.start)
-            val_parts.append(v)
-        indices = torch.cat(idx_parts).to(torch.uint32)
-        vals = torch.cat(val_parts)
+        indices, vals = _layerwise(kind, values, g, cf, rng)
         kept = vals.numel()
     else:
         kept = keep_count(n, cf)

@@ -341,6 +341,23 @@ int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, 
     return rc ? rc : check_launch("aggregate_dense");
 }
 
+size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg) { return segsel_workspace_bytes(n, nseg); }
+
+int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
+                         const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream, uint32_t *out_idx_dev,
+                         float *out_val_dev, void *ws_dev, size_t ws_bytes, uint32_t *status_dev, void *stream)
+{
+    if (kind != GVC_TOPK && kind != GVC_RANDOMK)
+        return set_error(GVC_ERR_ARG, "segmented select: Top-k and Random-k (DGC / Redsync go per segment)");
+    if (!values_dev || !seg_offsets || !seg_k || nseg < 1 || !out_idx_dev || !out_val_dev || !ws_dev || !status_dev)
+        return set_error(GVC_ERR_ARG, "segmented select: null argument or no segment");
+    if (n >= (1ull << 32))
+        return set_error(GVC_ERR_ARG, "segmented select: length %llu >= 2^32", (unsigned long long)n);
+    int rc = segsel_run(kind, values_dev, n, seg_offsets, seg_k, nseg, seed, rng_stream, out_idx_dev, out_val_dev,
+                        ws_dev, ws_bytes, status_dev, STREAM(stream));
+    return rc ? rc : check_launch("segmented_select");
+}
+
 int gvc_dense_mean_peers(float *const *peer_bufs, int nranks, int rank, uint64_t n, const uint32_t *flags,
                          uint32_t epoch, uint32_t *err_dev, void *stream)
 {

@@ -62,6 +62,10 @@ int dense_mean_peers_run(float *const *bufs, int nranks, int rank, uint64_t n, c
 int dense_collect_run(const float *own, float *out, uint64_t n, const uint32_t *flags, int nranks, uint32_t epoch,
                       uint32_t *err, cudaStream_t s);
 int iota_run(uint32_t *out, uint64_t n, cudaStream_t s);
+size_t segsel_workspace_bytes(uint64_t n, int nseg);
+int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
+               uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
+               uint32_t *status, cudaStream_t s);
 int gather_ef_run(const uint32_t *pos, uint64_t k, const float *values, const float *g, const float *resid,
                   const uint32_t *pmask, const float *pm, int pmode, float *out, cudaStream_t s);
 int below_keys_run(const float *v, const uint32_t *pos, uint64_t n, const uint32_t *thr, const uint32_t *excl,

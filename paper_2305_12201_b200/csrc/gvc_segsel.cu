@@ -1,0 +1,356 @@
+// gvc_segsel.cu -- layerwise compression as ONE segmented selection (sm_100a).
+//
+// compressors.compress(..., layerwise=True) (compressors.py:204-217) keeps
+// k_s = keep_count(len_s, cf) entries of every layer segment s, chosen inside
+// the segment by the compressor's rule (ties to the lower index), offsets
+// them by the segment start and concatenates the segments in order.  A
+// ResNet-101 gradient has ~300 segments; instead of one selection pipeline per
+// segment, every segment is resolved at once:
+//   * work items = (segment, chunk of <= SS_CHUNK values), one CTA each;
+//   * 4 radix passes of 8 key bits, most significant first: every CTA
+//     histograms the keys of its chunk that match its segment's resolved
+//     prefix (256 shared-memory bins, merged into the segment's global bins);
+//     one warp per segment then picks the digit where the count from the top
+//     reaches the segment's remaining rank -> after 4 passes each segment has
+//     its exact threshold key T_s and tie quota q_s;
+//   * counts per item (> T, == T), one CTA scans them into per-item output
+//     offsets and tie quotas (the segments' outputs are contiguous and in
+//     order, so one exclusive scan over the items gives every offset);
+//   * an ordered compaction writes (global index, value) per item.
+// Keys: 31-bit |v| (Top-k) or the Philox position hash of the global
+// position (Random-k, the counter-based sampler with pos_base = segment start,
+// DESIGN.md).  11 launches whatever the number of segments.
+#include <vector>
+
+#include "gvc_common.cuh"
+#include "gvc_internal.h"
+
+namespace gvc {
+
+#define SS_CHUNK 16384
+#define SS_THREADS 256
+#define SS_PER (SS_CHUNK / SS_THREADS)  // values per thread in a chunk, contiguous
+
+struct SegState {
+    uint32_t prefix;     // resolved key bits (most significant first)
+    uint32_t all;        // k >= len: every value is kept
+    unsigned long long need;  // rank still to take at/below the resolved prefix
+};
+
+struct SegPlan {
+    const float *values;
+    uint64_t n;
+    int nseg, nitems, keymode;
+    uint64_t seed, stream;
+    const uint64_t *seg_lo;   // [nseg]
+    const uint64_t *seg_k;    // [nseg]
+    const uint32_t *item_seg;  // [nitems]
+    const uint64_t *item_lo;   // [nitems] global start of the item
+    const uint32_t *item_len;  // [nitems]
+    SegState *seg;             // [nseg]
+    uint32_t *hist;            // [4][nseg][256]
+    uint32_t *item_gt, *item_eq;  // [nitems]
+    uint32_t *item_take;          // [nitems] ties this item keeps
+    unsigned long long *item_out; // [nitems] output offset
+    unsigned long long *item_E;   // [nitems] exclusive scan of the == counts
+    const uint32_t *seg_first;    // [nseg] first item of the segment
+    uint32_t *status;             // bit 1: NaN
+};
+
+__device__ __forceinline__ uint32_t ss_key(const SegPlan &P, float v, uint64_t pos)
+{
+    return P.keymode == KEY_HASH ? hash_key(pos, P.stream, P.seed) : mag_key(v);
+}
+
+// Pass d: histogram of digit d of the keys matching the segment's prefix.
+__global__ void __launch_bounds__(SS_THREADS) k_ss_hist(SegPlan P, int d)
+{
+    __shared__ uint32_t h[256];
+    const int it = blockIdx.x;
+    const uint32_t s = P.item_seg[it];
+    const SegState st = P.seg[s];
+    for (int i = threadIdx.x; i < 256; i += SS_THREADS)
+        h[i] = 0;
+    __syncthreads();
+    if (!st.all) {
+        const uint64_t lo = P.item_lo[it];
+        const uint32_t len = P.item_len[it];
+        const int shift = 24 - 8 * d;
+        const uint32_t pmask = d ? (0xffffffffu << (32 - 8 * d)) : 0u;
+        uint32_t nan = 0;
+        for (uint32_t i = threadIdx.x; i < len; i += SS_THREADS) {
+            const float v = P.values[lo + i];
+            const uint32_t key = ss_key(P, v, lo + i);
+            if (d == 0 && P.keymode == KEY_MAG)
+                nan |= key > 0x7f800000u;
+            if ((key & pmask) == st.prefix)
+                atomicAdd(&h[(key >> shift) & 255u], 1u);
+        }
+        if (d == 0 && __any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0)
+            atomicOr(P.status, 1u);
+    }
+    __syncthreads();
+    uint32_t *g = P.hist + ((size_t)d * P.nseg + s) * 256;
+    for (int i = threadIdx.x; i < 256; i += SS_THREADS)
+        if (h[i])
+            atomicAdd(&g[i], h[i]);
+}
+
+// One warp per segment: the digit where the count from the top reaches `need`.
+__global__ void __launch_bounds__(SS_THREADS) k_ss_resolve(SegPlan P, int d)
+{
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (SS_THREADS / 32) + (threadIdx.x >> 5);
+    if (s >= P.nseg)
+        return;
+    SegState st = P.seg[s];
+    if (st.all)
+        return;
+    const uint32_t *g = P.hist + ((size_t)d * P.nseg + s) * 256;
+    // lane l holds bins 255 - 8l .. 248 - 8l (descending digits)
+    uint32_t c[8];
+    unsigned long long local = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        c[i] = g[255 - 8 * lane - i];
+        local += c[i];
+    }
+    unsigned long long incl = local;  // inclusive prefix over lanes (from the top digit)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o)
+            incl += y;
+    }
+    const unsigned long long before = incl - local;
+    const unsigned long long nd = st.need;
+    const bool here = before < nd && nd <= incl;
+    if (here) {
+        unsigned long long acc = before;
+        for (int i = 0; i < 8; i++) {
+            if (acc + c[i] >= nd) {
+                const uint32_t digit = 255u - 8u * lane - i;
+                st.prefix |= digit << (24 - 8 * d);
+                st.need = nd - acc;
+                P.seg[s] = st;
+                break;
+            }
+            acc += c[i];
+        }
+    }
+}
+
+// Per item: keys above the threshold and equal to it.
+__global__ void __launch_bounds__(SS_THREADS) k_ss_count(SegPlan P)
+{
+    __shared__ uint32_t sgt, seq;
+    const int it = blockIdx.x;
+    const SegState st = P.seg[P.item_seg[it]];
+    if (threadIdx.x == 0)
+        sgt = seq = 0;
+    __syncthreads();
+    const uint64_t lo = P.item_lo[it];
+    const uint32_t len = P.item_len[it];
+    uint32_t gt = 0, eq = 0;
+    for (uint32_t i = threadIdx.x; i < len; i += SS_THREADS) {
+        const uint32_t key = ss_key(P, P.values[lo + i], lo + i);
+        gt += st.all || key > st.prefix;
+        eq += !st.all && key == st.prefix;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gt += __shfl_xor_sync(0xffffffffu, gt, o);
+        eq += __shfl_xor_sync(0xffffffffu, eq, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sgt, gt);
+        atomicAdd(&seq, eq);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        P.item_gt[it] = sgt;
+        P.item_eq[it] = seq;
+    }
+}
+
+// One CTA: per item the ties it keeps (the first q_s ties of its segment in
+// index order: E = exclusive scan of the == counts, ties before the item =
+// E[item] - E[first item of the segment]) and its output offset (exclusive
+// scan of the kept counts: the segments' outputs are contiguous and in order).
+__global__ void __launch_bounds__(1024) k_ss_scan(SegPlan P)
+{
+    __shared__ unsigned long long sh[33];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0)
+        carry = 0;
+    __syncthreads();
+    for (int base = 0; base < P.nitems; base += blockDim.x) {
+        const int it = base + threadIdx.x;
+        const unsigned long long eq = it < P.nitems ? P.item_eq[it] : 0ull;
+        const unsigned long long c0 = carry;  // read before thread 0 advances it
+        unsigned long long tot;
+        const unsigned long long pre = block_excl_prefix(eq, sh, &tot) + c0;
+        if (it < P.nitems)
+            P.item_E[it] = pre;
+        if (threadIdx.x == 0)
+            carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        carry = 0;
+    __syncthreads();
+    for (int base = 0; base < P.nitems; base += blockDim.x) {
+        const int it = base + threadIdx.x;
+        const bool ok = it < P.nitems;
+        unsigned long long kept = 0, tk = 0;
+        if (ok) {
+            const uint32_t s = P.item_seg[it];
+            const SegState st = P.seg[s];
+            const unsigned long long before = P.item_E[it] - P.item_E[P.seg_first[s]];
+            const unsigned long long eq = P.item_eq[it];
+            tk = st.all || before >= st.need ? 0ull : (st.need - before < eq ? st.need - before : eq);
+            kept = P.item_gt[it] + tk;
+        }
+        const unsigned long long c0 = carry;
+        unsigned long long tot;
+        const unsigned long long out = block_excl_prefix(kept, sh, &tot) + c0;
+        if (ok) {
+            P.item_take[it] = (uint32_t)tk;
+            P.item_out[it] = out;
+        }
+        if (threadIdx.x == 0)
+            carry += tot;
+        __syncthreads();
+    }
+}
+
+// Ordered compaction of one item: thread t owns values [t*PER, (t+1)*PER) of
+// the chunk; kept = key > T, or key == T among the item's first take ties.
+__global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *out_idx, float *out_val)
+{
+    __shared__ unsigned long long sh[33];
+    const int it = blockIdx.x;
+    const SegState st = P.seg[P.item_seg[it]];
+    const uint64_t lo = P.item_lo[it];
+    const uint32_t len = P.item_len[it];
+    const uint32_t take = P.item_take[it];
+    const uint32_t b = threadIdx.x * SS_PER, e = min(len, b + SS_PER);
+    uint32_t gt = 0, eq = 0;
+    for (uint32_t i = b; i < e; i++) {
+        const uint32_t key = ss_key(P, P.values[lo + i], lo + i);
+        gt += st.all || key > st.prefix;
+        eq += !st.all && key == st.prefix;
+    }
+    const unsigned long long eq_pre = block_excl_prefix(eq, sh);
+    // ties this thread keeps: the item's first `take` ties
+    const uint32_t tk = eq_pre >= take ? 0u : min((uint32_t)(take - eq_pre), eq);
+    unsigned long long o = P.item_out[it] + block_excl_prefix(gt + tk, sh);
+    uint32_t ties = 0;
+    for (uint32_t i = b; i < e; i++) {
+        const float v = P.values[lo + i];
+        const uint32_t key = ss_key(P, v, lo + i);
+        bool keep = st.all || key > st.prefix;
+        if (!st.all && key == st.prefix) {
+            keep = ties < tk;
+            ties++;
+        }
+        if (keep) {
+            out_idx[o] = (uint32_t)(lo + i);
+            out_val[o] = v;
+            o++;
+        }
+    }
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t segsel_workspace_bytes(uint64_t n, int nseg)
+{
+    const uint64_t items = n / SS_CHUNK + (uint64_t)nseg + 1;
+    return al256(nseg * sizeof(SegState)) + al256((size_t)4 * nseg * 256 * 4) + al256(nseg * 8) * 2 +
+           al256(nseg * 4) + al256(items * 4) * 6 + al256(items * 8) * 3 + 256;
+}
+
+int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
+               uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
+               uint32_t *status, cudaStream_t s)
+{
+    // host: the work items and the segment table
+    std::vector<uint32_t> iseg, ilen, sfirst(nseg, 0);
+    std::vector<uint64_t> ilo, slo(nseg), sk(nseg);
+    std::vector<SegState> sst(nseg);
+    for (int q = 0; q < nseg; q++) {
+        const uint64_t a = seg_off[q], b = seg_off[q + 1];
+        if (b < a || b > n)
+            return set_error(GVC_ERR_ARG, "segmented select: segment %d [%llu, %llu) outside [0, %llu)", q,
+                             (unsigned long long)a, (unsigned long long)b, (unsigned long long)n);
+        slo[q] = a;
+        sk[q] = seg_k[q];
+        sst[q].prefix = 0;
+        sst[q].all = (b - a == 0) || seg_k[q] >= b - a;
+        sst[q].need = seg_k[q];
+        if (b - a && seg_k[q] < 1)
+            return set_error(GVC_ERR_ARG, "segmented select: keep count 0 in segment %d", q);
+        sfirst[q] = (uint32_t)iseg.size();
+        for (uint64_t c = a; c < b; c += SS_CHUNK) {
+            iseg.push_back((uint32_t)q);
+            ilo.push_back(c);
+            ilen.push_back((uint32_t)(b - c < SS_CHUNK ? b - c : SS_CHUNK));
+        }
+    }
+    const int nitems = (int)iseg.size();
+    if (nitems == 0)
+        return GVC_OK;
+    if (segsel_workspace_bytes(n, nseg) > ws_bytes)
+        return set_error(GVC_ERR_WORKSPACE, "segmented select workspace too small");
+    char *w = (char *)ws;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *q = w + off;
+        off += al256(bytes);
+        return q;
+    };
+    SegPlan P;
+    P.values = values;
+    P.n = n;
+    P.nseg = nseg;
+    P.nitems = nitems;
+    P.keymode = kind == GVC_RANDOMK ? KEY_HASH : KEY_MAG;
+    P.seed = seed;
+    P.stream = stream;
+    P.seg = (SegState *)take(nseg * sizeof(SegState));
+    P.hist = (uint32_t *)take((size_t)4 * nseg * 256 * 4);
+    P.seg_lo = (const uint64_t *)take(nseg * 8);
+    P.seg_k = (const uint64_t *)take(nseg * 8);
+    P.item_seg = (const uint32_t *)take(nitems * 4);
+    P.item_len = (const uint32_t *)take(nitems * 4);
+    P.item_gt = (uint32_t *)take(nitems * 4);
+    P.item_eq = (uint32_t *)take(nitems * 4);
+    P.item_take = (uint32_t *)take(nitems * 4);
+    P.item_lo = (const uint64_t *)take(nitems * 8);
+    P.item_out = (unsigned long long *)take(nitems * 8);
+    P.item_E = (unsigned long long *)take(nitems * 8);
+    P.seg_first = (const uint32_t *)take(nseg * 4);
+    P.status = status;
+    cudaMemcpyAsync(P.seg, sst.data(), nseg * sizeof(SegState), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.seg_lo, slo.data(), nseg * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.seg_k, sk.data(), nseg * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.item_seg, iseg.data(), nitems * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.item_len, ilen.data(), nitems * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.item_lo, ilo.data(), nitems * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.seg_first, sfirst.data(), nseg * 4, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(P.hist, 0, (size_t)4 * nseg * 256 * 4, s);
+    // (the host vectors are pageable: the copies complete before the calls return)
+    const int rgrid = (nseg + SS_THREADS / 32 - 1) / (SS_THREADS / 32);
+    for (int d = 0; d < 4; d++) {
+        k_ss_hist<<<nitems, SS_THREADS, 0, s>>>(P, d);
+        k_ss_resolve<<<rgrid, SS_THREADS, 0, s>>>(P, d);
+    }
+    k_ss_count<<<nitems, SS_THREADS, 0, s>>>(P);
+    k_ss_scan<<<1, 1024, 0, s>>>(P);
+    k_ss_write<<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
+    count_launches(11);
+    return GVC_OK;
+}
+
+}  // namespace gvc

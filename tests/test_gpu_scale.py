@@ -217,3 +217,62 @@ def test_identity_level1_with_extra_cfs(G):
         k = O.keep_count(n, c)
         want = O.sq_norm(g[O.topk_indices(g, k).astype(np.int64)]) / O.sq_norm(g)
         assert res.ladder_gains[c] == pytest.approx(want, rel=RTOL)
+
+
+# ------------------------------------------------------------- layerwise
+def _resnet101_offsets():
+    """Parameter tensor sizes of ResNet-101 (torchvision layout: conv, BN weight
+    and bias, downsample, fc), as GradientVector layer offsets: ~314 segments,
+    44.5M values."""
+    sizes = [64 * 3 * 7 * 7, 64, 64]
+    inplanes = 64
+    for planes, blocks in ((64, 3), (128, 4), (256, 23), (512, 3)):
+        for b in range(blocks):
+            sizes += [inplanes * planes, planes, planes, planes * planes * 9, planes, planes,
+                      planes * planes * 4, planes * 4, planes * 4]
+            if b == 0:
+                sizes += [inplanes * planes * 4, planes * 4, planes * 4]
+            inplanes = planes * 4
+    sizes += [2048 * 1000, 1000]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    return offs, int(np.sum(sizes))
+
+
+@pytest.mark.parametrize("kind", ["topk", "randomk"])
+def test_layerwise_resnet101_segments(G, kind):
+    """compressors.py:204-217 on ResNet-101's ~314 layer segments (44.5M values)
+    as one segmented selection: every segment's keep count, order and values
+    bit-exact against the oracle's per-segment compress."""
+    offs, n = _resnet101_offsets()
+    assert len(offs) > 300 and abs(n - 44_500_000) < 200_000
+    x = _gauss(n, 11)
+    for a, b in zip(offs[:40:3], offs[1:41:3]):  # layer-scaled segments, heavy ties in some
+        x[a:b] *= np.float32(10.0 ** (-(a % 7) / 3))
+    x[offs[5]:offs[6]] = np.round(x[offs[5]:offs[6]] * 2) / 2
+    rng = G.SeededRng(9)
+    g = G.GradientVector(x, tuple(int(o) for o in offs))
+    for cf in (10.0, 100.0):
+        s, _ = G.compress(G.CompressorKind(kind), g, cf, rng, layerwise=True)
+        oi, ov, _ = O.compress(kind, x, cf, seed=rng.seed, stream=rng.stream, layer_offsets=offs, layerwise=True)
+        assert np.array_equal(host(s.indices), oi), cf
+        assert np.array_equal(bits(host(s.vals)), bits(ov)), cf
+
+
+@pytest.mark.parametrize("kind", ["topk", "randomk", "redsync", "dgc"])
+def test_layerwise_edge_segments(G, kind):
+    """Segments of length 1, segments where keep_count keeps everything
+    (cf 1), tie-only segments and -0.0, for every compressor."""
+    x = _gauss(70_001, 3)
+    x[100:400] = 0.5
+    x[400:410] = -0.0
+    offs = (0, 1, 2, 100, 400, 410, 5000, 5001, 69_000)
+    g = G.GradientVector(x, offs)
+    rng = G.SeededRng(4).split(2)
+    for cf in (1.0, 3.0, 10.0):
+        s, _ = G.compress(G.CompressorKind(kind), g, cf, rng, layerwise=True)
+        oi, ov, _ = O.compress(kind, x, cf, seed=rng.seed, stream=rng.stream, layer_offsets=offs, layerwise=True)
+        assert np.array_equal(host(s.indices), oi), (kind, cf)
+        if kind == "redsync":
+            np.testing.assert_allclose(host(s.vals), ov, rtol=RTOL)
+        else:
+            assert np.array_equal(bits(host(s.vals)), bits(ov)), (kind, cf)
