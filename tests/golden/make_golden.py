@@ -27,6 +27,8 @@ outputs; float arrays are stored as float32 so bit patterns survive):
   compressors.py:112-115): position-exact.
 * ``run_iteration.npz`` -- controller.run_iteration traces (controller.py:192-281)
   for Top-k and Redsync with 1 and 3 workers: chosen CF, raw gains, theta_min.
+* ``training.npz`` -- simworkers.run_training in every mode (simworkers.py:174-304)
+  on tests/fixture_tasks.NoisyBowl: trace columns, final weights, JSON lines.
 """
 
 from __future__ import annotations
@@ -307,6 +309,33 @@ def _cases_run_iteration(gravac):
     return out
 
 
+def _cases_training(gravac):
+    """simworkers.run_training (simworkers.py:174-304) in every mode on the
+    tests' NoisyBowl task (tests/fixture_tasks.py)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from tests.fixture_tasks import CHOICES, TRACE_COLUMNS, TRAINING_CASES, NoisyBowl
+    from gravac.compressors import CompressorKind
+    from gravac.controller import ControllerConfig
+    from gravac.costmodel import CostModelParams
+    from gravac.gradcore import GradientVector
+    from gravac.simworkers import OptimizerState, run_training
+    out = {}
+    for i, (mode, kind, cf, tmin, eps, workers, size, iters, lr, mom) in enumerate(TRAINING_CASES):
+        task = NoisyBowl(size, GradientVector, seed=i)
+        cfg = (ControllerConfig(theta_min=tmin, theta_max=256.0, epsilon=eps, omega=0.05, window=3,
+                                compressor=CompressorKind(kind)) if mode == "gravac" else None)
+        opt = OptimizerState(np.zeros(size), lr=lr, momentum=mom, weight_decay=1e-4, lr_decay_iters=(iters - 2,))
+        res = run_training(task, opt, CostModelParams(workers=workers), mode, iters, seed=100 + i,
+                           controller_config=cfg, compressor=CompressorKind(kind) if kind else None, static_cf=cf)
+        out[f"{i}/trace"] = np.array([[getattr(r, c) for c in TRACE_COLUMNS] for r in res.trace], dtype=np.float64)
+        out[f"{i}/choice"] = np.array([CHOICES[r.choice] for r in res.trace], dtype=np.int64)
+        out[f"{i}/weights"] = res.weights
+        out[f"{i}/metric"] = np.float64(res.metric_value)
+        out[f"{i}/jsonl"] = np.array(res.trace.to_jsonl())
+    out["n_cases"] = np.int64(len(TRAINING_CASES))
+    return out
+
+
 def main():
     gravac = _import_reference()
     families = {
@@ -319,6 +348,7 @@ def main():
         "dgc_small": lambda: _cases_dgc_small(gravac),
         "dgc_stats": lambda: _cases_dgc_stats(gravac),
         "run_iteration": lambda: _cases_run_iteration(gravac),
+        "training": lambda: _cases_training(gravac),
     }
     only = set(sys.argv[1:])
     for name, fn in families.items():
