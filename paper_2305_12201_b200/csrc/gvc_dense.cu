@@ -419,6 +419,7 @@ struct Staged {
     const uint32_t *src_idx[GVC_MAX_PEERS];  // peer p's payload (remote)
     const float *src_val[GVC_MAX_PEERS];
     const uint32_t *src_bounds[GVC_MAX_PEERS];
+    uint32_t *err;  // the flag area's error word (bounded waits)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p)
@@ -428,13 +429,38 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p)
     return v;
 }
 
+// Peer waits are bounded.  `err` is a word of this rank's peer-buffer flag
+// area (GVC_FLAG_ERR_WORD): a wait that times out (~4 s -- a rank died or
+// diverged) sets bit 4 there, and every later wait of the exchange sees it and
+// stops waiting, so a dead peer costs seconds instead of a hung GPU.  The
+// host (exchange.PeerExchange) reads the word back every few exchanges.
+#define GVC_FLAG_ERR_WORD 63
+__device__ __forceinline__ void wait_epoch(const uint32_t *word, uint32_t epoch, bool sys, uint32_t *err)
+{
+    long long t0 = 0;
+    while ((int32_t)((sys ? ld_acquire_sys(word) : ld_acquire_gpu(word)) - epoch) < 0) {
+        if (*(volatile uint32_t *)err)
+            return;
+        if (t0 == 0) {
+            t0 = clock64();
+        } else if (clock64() - t0 > (1ll << 33)) {
+            atomicOr(err, 4u);
+            return;
+        }
+        __nanosleep(64);
+    }
+}
+
+__device__ __forceinline__ uint32_t *flag_err(const uint32_t *flags)
+{
+    return const_cast<uint32_t *>(flags) + GVC_FLAG_ERR_WORD;
+}
+
 __device__ void staged_copier(const Staged &st, const AggParts &parts, int nparts, const uint32_t *flags,
                               uint32_t epoch)
 {
-    if (threadIdx.x < nparts && (int)threadIdx.x != st.self) {
-        while ((int32_t)(ld_acquire_sys(flags + threadIdx.x) - epoch) < 0)
-            __nanosleep(64);
-    }
+    if (threadIdx.x < nparts && (int)threadIdx.x != st.self)
+        wait_epoch(flags + threadIdx.x, epoch, true, st.err);
     __syncthreads();
     // first the tile bounds (every tile needs them before it can look for its
     // chunks): copier b stages slice b of every remote part's bounds
@@ -503,8 +529,7 @@ __device__ __forceinline__ void staged_wait_bounds(const Staged &st, int q, uint
         return;
     const uint32_t per = (st.nb + st.ncopy - 1) / st.ncopy;
     for (uint32_t b = t / per; b <= (t + 1) / per; b++)
-        while ((int32_t)(ld_acquire_gpu(st.ready + b) - epoch) < 0)
-            __nanosleep(32);
+        wait_epoch(st.ready + b, epoch, false, st.err);
 }
 
 // A tile's wait for the staged chunks of part q covering entries [a, b).
@@ -513,8 +538,7 @@ __device__ __forceinline__ void staged_wait(const Staged &st, int q, uint32_t a,
     if (q == st.self || b <= a)
         return;
     for (uint32_t c = a >> st.ch_log2; c <= (b - 1) >> st.ch_log2; c++)
-        while ((int32_t)(ld_acquire_gpu(st.ready + st.ncopy + c) - epoch) < 0)
-            __nanosleep(32);
+        wait_epoch(st.ready + st.ncopy + c, epoch, false, st.err);
 }
 
 // MODE 0: decompress (fp32 assignment, -0.0 kept); 1: mean of ONE part
@@ -564,10 +588,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
         const int np = min(NP, nparts - p0);
         if (threadIdx.x < np) {
             const int p = p0 + threadIdx.x;
-            if (WAIT) {
-                while ((int32_t)(ld_acquire_sys(flags + p) - epoch) < 0)
-                    __nanosleep(64);
-            }
+            if (WAIT)
+                wait_epoch(flags + p, epoch, true, flag_err(flags));
             if (STAGED)
                 staged_wait_bounds(stg, p, tile, epoch);
             s_a[threadIdx.x] = __ldcg(parts.bounds[p] + tile);
@@ -689,10 +711,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (threadIdx.x < nparts) {
         const int p = threadIdx.x;
-        if (WAIT) {
-            while ((int32_t)(ld_acquire_sys(flags + p) - epoch) < 0)
-                __nanosleep(64);
-        }
+        if (WAIT)
+            wait_epoch(flags + p, epoch, true, flag_err(flags));
         if (STAGED)
             staged_wait_bounds(stg, p, tile, epoch);
         s_a[p] = __ldcg(parts.bounds[p] + tile);
@@ -1030,6 +1050,7 @@ int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *v
     st.self = sg->self;
     st.ch_log2 = (uint32_t)__builtin_ctz(ce);
     st.ready = sg->ready_dev;
+    st.err = const_cast<uint32_t *>(flags) + GVC_FLAG_ERR_WORD;
     uint64_t kmax = 0;
     for (int p = 0; p < nparts; p++) {
         if (!idx[p] || !vals[p] || !bounds[p] || (p != sg->self && (!sg->src_idx_dev[p] || !sg->src_vals_dev[p])))

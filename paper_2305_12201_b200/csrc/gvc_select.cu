@@ -1661,13 +1661,24 @@ static void launch_tail(const Plan &p, cudaStream_t s, bool pdl)
     }
 }
 
-// One-time kernel attributes (outside any stream capture).
+static int current_device()
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+// One-time kernel attributes per device (cudaFuncSetAttribute is per device),
+// outside any stream capture.
 static void set_attributes()
 {
-    static bool done = false;
-    if (done)
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    const int dev = current_device();
+    if (std::find(done.begin(), done.end(), dev) != done.end())
         return;
-    done = true;
+    done.push_back(dev);
     cudaFuncSetAttribute(k_sample<KEY_MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
     cudaFuncSetAttribute(k_sample<KEY_DGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
 #define GVC_PASS1_ATTR(KM, NB, ABS)                                                                          \
@@ -1774,7 +1785,8 @@ static std::unordered_map<std::string, GraphEntry> g_graphs;
 static std::string graph_key(const Plan &p, const void *ws)
 {
     char buf[256];
-    snprintf(buf, sizeof(buf), "%p|%llu|%d|%d|%d|%d|%d|%d|%d|%d|%d", ws, (unsigned long long)p.n, p.keymode, p.ef,
+    snprintf(buf, sizeof(buf), "%d|%p|%llu|%d|%d|%d|%d|%d|%d|%d|%d|%d", current_device(), ws,
+             (unsigned long long)p.n, p.keymode, p.ef,
              p.pmask ? p.pmode : 0, nb_for(p.n_ks), p.kind == GVC_REDSYNC, p.force_exact,
              (int)(p.keymode != KEY_HASH && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev),
              p.key_est_dev != nullptr, (int)p.s_chunks);
@@ -1859,7 +1871,9 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
         std::lock_guard<std::mutex> glk(g_mu);
         auto it = g_graphs.find(key);
         if (it == g_graphs.end()) {
-            static cudaStream_t cs = nullptr;
+            // the capture stream belongs to a device: one per device
+            static std::unordered_map<int, cudaStream_t> capture_streams;
+            cudaStream_t &cs = capture_streams[current_device()];
             if (!cs)
                 cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
             cudaGraph_t graph;
@@ -1977,14 +1991,17 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
     const size_t mbytes = (size_t)GVC_WARPS_PER_BLOCK * (p.seg_len >> 5) * 4;
     const bool smem_mask = smask && !idx_map && mbytes <= 96 * 1024;
     if (smem_mask) {
-        static bool attr = false;
-        if (!attr) {
+        static std::vector<int> attr_done;  // per device (under g_mu)
+        std::unique_lock<std::mutex> lk(g_mu);
+        const int dev = current_device();
+        if (std::find(attr_done.begin(), attr_done.end(), dev) == attr_done.end()) {
+            attr_done.push_back(dev);
             cudaFuncSetAttribute(k_emit<KEY_MAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_DGC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_MAG, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            attr = true;
         }
+        lk.unlock();
         const bool lean = !idx_map && !resid && mir.n == 0 && !stats && p.kind != GVC_REDSYNC;
         if (p.keymode == KEY_MAG && lean)
             k_emit<KEY_MAG, true, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,

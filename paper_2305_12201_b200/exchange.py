@@ -218,10 +218,31 @@ class PeerExchange:
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)  # every flag array is zero before anyone signals
         self.buf, self.handle, self.cap, self.epoch = buf, handle, cap, 0
+        self._err_check = None
         self.bases = [int(p) for p in handle.buffer_ptrs]
         self._flag_ptrs = (ctypes.c_void_p * self.world)(*self.bases)
         # staged pull: per-chunk ready epochs (local); epochs restart with the buffer
         self.ready = torch.zeros(self.copy_blocks + cap // self.chunk + 2, dtype=torch.int32, device=self.device)
+
+    ERR_WORD = 63  # GVC_FLAG_ERR_WORD: set by a bounded peer wait that timed out
+    ERR_EVERY = 64
+
+    def _check_err(self, e: int) -> None:
+        """Every ERR_EVERY exchanges, read the flag area's error word back
+        asynchronously (no stream sync); a timed-out wait of an earlier exchange
+        -- a rank died or diverged -- raises here."""
+        pend = self._err_check
+        if pend is not None and pend[1].query():
+            if int(pend[0][0]):
+                raise RuntimeError("peer exchange: a wait for another rank timed out (a rank died or diverged); "
+                                   "the exchanged averages since then are invalid")
+            self._err_check = pend = None
+        if pend is None and e % self.ERR_EVERY == 1:
+            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            host.copy_(self.buf[self.ERR_WORD:self.ERR_WORD + 1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._err_check = (host, ev)
 
     def slot(self, k: int, n: int, push: bool = True) -> Payload:
         """This rank's payload slot of the next exchange.  With ``push`` (a
@@ -261,6 +282,7 @@ class PeerExchange:
             pl.vals[:part.kept].copy_(part.vals)
             pl.bounds = None
         _, e, _ = pl.peer
+        self._check_err(e)
         lib = nat.load()
         stream = nat.stream_ptr(self.device)
         pushed = pl.pushed
