@@ -49,6 +49,12 @@ WORKLOADS = {
     "lstm-randomk": (66_000_000, 10.0, 10.0, (), "LSTM-size 66M fp32 gradient, Random-k (counter-based RNG) + EF, "
                      "CF {10, 100} (BASELINE configs[3])", "randomk"),
 }
+# compress-API workloads (run_api_workload): no controller
+WORKLOADS["resnet101-layerwise"] = (44_500_000, 10.0, 1.0, (), "ResNet-101 gradient, layerwise Top-k CF10 over its "
+                                    "314 parameter tensors (compressors.py:204-217) + decompress-average")
+WORKLOADS["sweep"] = (0, 10.0, 1.0, (), "Compressor sweep: M 1M..1B x CF {10,100,1000}, compress + "
+                      "decompress-average (BASELINE configs[4])")
+API_WORKLOADS = ("resnet101-layerwise", "sweep")
 EPSILON = 0.35  # fresh iid N(0,1) gradients give gain(CF10) ~= 0.42 -> the compressed CF10 branch is taken
 # per compressor: gains at CF10 on N(0,1) data are ~0.42 (Top-k, DGC), ~0.33 (Redsync), ~0.1 (Random-k)
 EPSILONS = {"topk": EPSILON, "dgc": EPSILON, "redsync": 0.25, "randomk": 0.05}
@@ -686,6 +692,114 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         dist.destroy_process_group()
 
 
+def resnet101_offsets():
+    """Layer offsets of ResNet-101's parameter tensors (torchvision layout: conv,
+    BN weight and bias, downsample, fc): 314 segments, 44.5M values."""
+    sizes = [64 * 3 * 7 * 7, 64, 64]
+    inplanes = 64
+    for planes, blocks in ((64, 3), (128, 4), (256, 23), (512, 3)):
+        for b in range(blocks):
+            sizes += [inplanes * planes, planes, planes, planes * planes * 9, planes, planes,
+                      planes * planes * 4, planes * 4, planes * 4]
+            if b == 0:
+                sizes += [inplanes * planes * 4, planes * 4, planes * 4]
+            inplanes = planes * 4
+    sizes += [2048 * 1000, 1000]
+    return tuple(int(x) for x in np.concatenate([[0], np.cumsum(sizes)[:-1]])), int(sum(sizes))
+
+
+def run_api_workload(args):
+    """Workloads through the compress API (no controller), one rank:
+      resnet101-layerwise -- compress(topk, g, 10, layerwise=True) over
+        ResNet-101's 314 layer segments (compressors.py:204-217) + the
+        decompress-average of the part, the last step re-checked on the oracle;
+      sweep (BASELINE configs[4]) -- compress + decompress-average for M in
+        1M..1B and CF in {10, 100, 1000}: GB/s and fractions of the HBM roofline."""
+    import torch
+
+    import paper_2305_12201_b200 as G
+    from paper_2305_12201_b200 import _native as nat
+    from oracle import oracle as O
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    nat.load()
+    peak, peak_kind = peaks()
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flush_out = torch.empty((), dtype=torch.float32, device=dev)
+    K = G.CompressorKind("topk")
+
+    def timed(fn, steps, warm):
+        for _ in range(warm):
+            fn()
+        ms = []
+        for _ in range(steps):
+            torch.sum(flush, dim=0, out=flush_out)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = fn()
+            b.record()
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return statistics.median(ms), out
+
+    clocks = ClockSampler(0).__enter__()
+    launches0 = nat.launch_count()
+    clocks.mark("t0")
+    if args.workload == "resnet101-layerwise":
+        offs, M = resnet101_offsets()
+        x = torch.randn(M, device=dev, generator=torch.Generator(device=dev).manual_seed(3))
+        g = G.GradientVector._wrap(x, offs)
+
+        def step():
+            s, _ = G.compress(K, g, 10.0, layerwise=True)
+            return s, G.aggregate([s])
+        ms, (s, avg) = timed(step, args.steps, args.warmup)
+        clocks.mark("t1")
+        xh = x.cpu().numpy()
+        oi, ov, _ = O.compress("topk", xh, 10.0, layer_offsets=offs, layerwise=True)
+        ok = (np.array_equal(s.indices.cpu().numpy(), oi) and
+              np.array_equal(s.vals.cpu().numpy().view(np.uint32), ov.view(np.uint32)) and
+              np.array_equal(avg.values.cpu().numpy().view(np.uint32), O.aggregate([(oi, ov)], M).view(np.uint32)))
+        value = 4 * M / (ms * 1e-3) / 1e9
+        extra_keys = {"segments": len(offs), "kept": s.kept}
+        config = {"workload": WORKLOADS[args.workload][4], "M": M, "compressor": "topk", "cf": 10.0,
+                  "segments": len(offs), "parallelism": "dp1"}
+        parity = "ok" if ok else "FAIL: layerwise entries or average"
+    else:  # sweep
+        rows = []
+        sizes = [1 << 20, 1 << 22, 1 << 24, 1 << 26, 1 << 28, 1 << 30]
+        for M in sizes:
+            x = torch.randn(M, device=dev, generator=torch.Generator(device=dev).manual_seed(M & 0xffff))
+            g = G.GradientVector._wrap(x)
+            for cf in (10.0, 100.0, 1000.0):
+                def step():
+                    s, _ = G.compress(K, g, cf)
+                    return G.aggregate([s])
+                ms, _ = timed(step, max(3, min(args.steps, 5)), 2)
+                # plain select: read the values once (collect), candidates written and re-read
+                # (~8 B each, 1.03 k), the part written (8k), the dense mean written (4M) and the part read (8k)
+                byts = 8 * M + 24 * (M // int(cf))
+                rows.append({"M": M, "cf": cf, "ms": ms, "gbps": 4 * M / (ms * 1e-3) / 1e9,
+                             "hbm_frac": byts / (ms * 1e-3) / 1e9 / peak})
+            del x, g
+            torch.cuda.empty_cache()
+        clocks.mark("t1")
+        top = max(rows, key=lambda r: (r["M"], -r["cf"]))
+        ms, M, value = top["ms"], top["M"], top["gbps"]
+        extra_keys = {"sweep": rows}
+        config = {"workload": WORKLOADS[args.workload][4], "M": "1M..1B", "compressor": "topk",
+                  "cf": [10.0, 100.0, 1000.0], "parallelism": "dp1"}
+        parity = "not re-checked (the parity suite covers the select at every size up to 138M)"
+    clocks.__exit__(None, None, None)
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) fp32 gradient, L2 evicted before every step",
+            "config": config, "parity": parity, "gpu_launches": int(nat.launch_count() - launches0),
+            "clocks": clocks.summary(), "peak": peak, "peak_kind": peak_kind}
+    line.update(extra_keys)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -699,6 +813,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.workload in API_WORKLOADS:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "the API workloads are measured against the "
+                                                                   "oracle inside the GPU arm"}))
+            return
+        run_api_workload(args)
+        return
     M, theta_min, theta_s, extra, desc = WORKLOADS[args.workload][:5]
     args.kind = WORKLOADS[args.workload][5] if len(WORKLOADS[args.workload]) > 5 else "topk"
     if args.impl == "reference":
