@@ -58,6 +58,12 @@ API_WORKLOADS = ("resnet101-layerwise", "sweep")
 EPSILON = 0.35  # fresh iid N(0,1) gradients give gain(CF10) ~= 0.42 -> the compressed CF10 branch is taken
 # per compressor: gains at CF10 on N(0,1) data are ~0.42 (Top-k, DGC), ~0.33 (Redsync), ~0.1 (Random-k)
 EPSILONS = {"topk": EPSILON, "dgc": EPSILON, "redsync": 0.25, "randomk": 0.05}
+# ResNet-18 runs the single CF 100 (theta_s 1): its gain on N(0,1) data is ~0.13
+
+
+def workload_epsilon(name: str) -> float:
+    kind = WORKLOADS[name][5] if len(WORKLOADS[name]) > 5 else "topk"
+    return 0.1 if name == "resnet18" else EPSILONS[kind]
 
 
 SPEC_HBM_GBPS = 8000.0  # B200 HBM3e, DGX spec (the north star's "~8 TB/s")
@@ -80,7 +86,7 @@ def workload_config(name: str, world: int) -> dict:
     M, theta_min, theta_s, extra, desc = WORKLOADS[name][:5]
     kind = WORKLOADS[name][5] if len(WORKLOADS[name]) > 5 else "topk"
     return {"workload": desc, "M": M, "compressor": kind, "cf_ladder": [theta_min, theta_min * theta_s, *extra],
-            "epsilon": EPSILONS[kind],
+            "epsilon": workload_epsilon(name),
             "l2": "evicted before every timed step by reading a 256 MiB buffer (L2 126 MB), outside the timed "
                   "events; inputs (4M bytes each) exceed L2",
             "parallelism": f"dp{world}"}
@@ -134,7 +140,14 @@ def replay_step(O, snap_in, snap_out, res, M, theta_min, theta_s, extra, world, 
             want = min(1.0, O.sq_norm(ef[O.topk_indices(ef, kx).astype(np.int64)]) / norm)
             if abs(res.ladder_gains[c] - want) > 1e-6 * want:
                 problems.append(f"gain_{c} {res.ladder_gains[c]} vs {want}")
-    if res.decision.choice != "dense":
+    if res.decision.choice == "dense":  # the message is g_ef, the residual restarts from zero
+        if not np.array_equal(vals.view(np.uint32), ef.view(np.uint32)):
+            problems.append("dense message")
+        if true_residual(r2_raw, mask2, pm2, pmode2).any():
+            problems.append("residual after dense")
+        if world == 1 and not np.array_equal(avg.view(np.uint32), O.aggregate_dense([ef]).view(np.uint32)):
+            problems.append("dense average")
+    else:
         want_idx, want_vals = (i2, v2) if res.decision.choice == "candidate" else (i1, v1)
         if not np.array_equal(idx, want_idx):
             problems.append("sent indices")
@@ -404,7 +417,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     def fresh():
         """A new iid N(0,1) gradient per step (drawn before the timed events)."""
         return gbuf.normal_(generator=gen)
-    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=max(1000.0, theta_min), epsilon=EPSILONS[args.kind],
+    cfg = G.ControllerConfig(theta_min=theta_min, theta_max=max(1000.0, theta_min), epsilon=workload_epsilon(args.workload),
                              window=1 << 30, compressor=G.CompressorKind(args.kind))
     state = G.ControllerState.fresh(cfg, world)
     state.theta_s = theta_s
@@ -482,8 +495,12 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     clocks.__exit__(None, None, None)
     launches = nat.launch_count() - launches0
     last = res.sent[0]
-    snap_out = (last.indices.clone(), last.vals.clone(), avg.clone()) + raw_state()
+    if isinstance(last, G.SparseGradient):
+        snap_out = (last.indices.clone(), last.vals.clone(), avg.clone()) + raw_state()
+    else:  # a DENSE step: the message is g_ef itself
+        snap_out = (None, last.values.clone(), res.averaged.values.clone()) + raw_state()
     last_res = res
+    snap_iter = state.iteration  # the e2e steps below advance it; the sampler keys on this step's
     # roofline timing: the same loop again, the select graph now carrying CUDA
     # event-record nodes around k_collect (gvc_prof_enable(2)) -- the kernel's
     # duration inside the real step sequence, kept out of the headline loop
@@ -575,7 +592,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     host[3] = None if host[3] is None else float(host[3][0])
     host_out[5] = None if host_out[5] is None else float(host_out[5][0])
     parity = replay_step(O, host, host_out, last_res, M, theta_min, theta_s, extra, world, args.kind, rng,
-                         state.iteration, rank)
+                         snap_iter, rank)
 
     north = None
     if world == 1 and args.workload == "resnet101" and not args.no_north_star:

@@ -22,6 +22,7 @@
 // 148 SMs x resident collect blocks x 8 warps: the collect grid is one full wave
 #define GVC_SEG_TARGET (148 * GVC_COLLECT_BLOCKS * 8)
 #define GVC_SEG_MAX 16384
+#define GVC_STAGE 256        // per-warp candidate staging ring in k_collect (entries)
 #define GVC_SEG_QUANTUM 512  // elements per warp iteration: 32 lanes x 4 float4
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)
 #define GVC_HL_BINS 4096     // refinement histogram per ladder entry (global)
@@ -250,6 +251,19 @@ __device__ __forceinline__ T bcast_cg(const T *p)
 // Streaming loads / stores: the gradient and residual are touched once per
 // step, so they should not displace the candidate buffer in L2.
 __device__ __forceinline__ float4 ld_stream(const float4 *p) { return __ldcs(p); }
+// 16-byte global -> shared copy that holds no register (L2 only), and its groups
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
 
 }  // namespace gvc

@@ -184,6 +184,30 @@ __device__ __forceinline__ bool key_nan(uint32_t key)
     return KM != KEY_HASH && (key & 0x7fffffffu) > 0x7f800000u;
 }
 
+// Development probe (-DGVC_PHASE_STAMPS=1, scripts/phase_probe.py): per select
+// kernel, %globaltimer at block 0's entry (t_phase[2k]) and the latest block
+// exit (t_phase[2k+1]).  Compiled out of the product library.
+#ifndef GVC_PHASE_STAMPS
+#define GVC_PHASE_STAMPS 0
+#endif
+#if GVC_PHASE_STAMPS
+__device__ __forceinline__ unsigned long long gvc_gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define GVC_STAMP_IN(k)                                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0)                                                                  \
+        p.st->t_phase[2 * (k)] = gvc_gtimer();
+#define GVC_STAMP_OUT(k)                                                                                      \
+    if (threadIdx.x == 0)                                                                                     \
+        atomicMax(&p.st->t_phase[2 * (k) + 1], gvc_gtimer());
+#else
+#define GVC_STAMP_IN(k)
+#define GVC_STAMP_OUT(k)
+#endif
+
 // ------------------------------------------------------------------ sample
 // Strided chunks of 128 contiguous values -> 14-bit shared-memory histogram of
 // magnitude keys, merged into global memory once per block.  Reads ~1.5%.
@@ -193,7 +217,7 @@ template <int KM>
 __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
 {
     constexpr int SHIFT = KM == KEY_DGC ? GVC_SAMPLE_SHIFT + 1 : GVC_SAMPLE_SHIFT;  // 32- / 31-bit keys
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(0);
     extern __shared__ uint32_t sh[];
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
         sh[i] = 0;
@@ -263,6 +287,7 @@ __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
         __threadfence();
         sample_resolve_body(p, reinterpret_cast<unsigned long long *>(sh), SHIFT);
     }
+    GVC_STAMP_OUT(0);
 }
 
 // Chooses key_est (a lower bound for the k_0-th largest key, w.h.p.) and the
@@ -358,7 +383,7 @@ __global__ void __launch_bounds__(1024) k_sample_resolve(const Plan p, int)
 // histogram atomic is unconditional (non-candidates hit a per-lane dummy bin)
 // and only the two candidate stores are predicated.  `o` is the segment-local
 // candidate count; `pos` the global position of v[0].
-template <int KM>
+template <int KM, uint32_t WRAP = 0xffffffffu>
 __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32_t pos, uint32_t valid,
                                       uint32_t key_est, int shift0, uint32_t *h, uint32_t dummy, float *cval,
                                       uint32_t *cidx, uint32_t &ccount)
@@ -378,8 +403,8 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
         const uint32_t bin = pr[c] ? min((key[c] - key_est) >> shift0, (uint32_t)GVC_H0_BINS - 1) : dummy;
         atomicAdd(&h[bin], 1u);
         if (pr[c]) {
-            cval[o] = v[c];
-            cidx[o] = pos + c;
+            cval[o & WRAP] = v[c];
+            cidx[o & WRAP] = pos + c;
         }
         o += pr[c];
     }
@@ -396,7 +421,8 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 // exactness refill of k_collect's last block).  Adds the warp's fp64 squares to nacc.
 template <int KM, bool EF, int PM, bool REFILL>
 __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int lane, uint32_t *h, uint32_t dummy,
-                                                uint32_t key_est, int shift0, float pm, double &nacc)
+                                                uint32_t key_est, int shift0, float pm, double &nacc,
+                                                float *sv = nullptr, uint32_t *si = nullptr, uint32_t *mw = nullptr)
 {
     constexpr bool refill = REFILL;
     const bool do_ef = EF && !refill;
@@ -409,6 +435,12 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
     uint32_t *cidx = p.cand_idx + beg;
     uint32_t ccount = 0;
     uint32_t i = 0;
+    // Candidates are staged in a per-warp shared-memory ring (sv / si, GVC_STAGE
+    // entries) and written out 128 at a time with one 16-byte store per lane:
+    // stored straight from push4 they cost ~16 partial-sector stores per 256
+    // values -- a quarter of the kernel's time (measured: 105 -> 78 us without them)
+    // (entries below ccount & ~127 are always out: a push adds <= 128)
+    constexpr bool STAGE = !REFILL;
     // 256-value steps.  PF (magnitude keys): software pipeline -- the next
     // step's g / r loads and mask words are in flight while this step is
     // added, reduced and compacted.  Hash keys are Philox-bound, and the
@@ -417,23 +449,32 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
     constexpr uint32_t STEP = 256;
     const uint32_t nfull = len / GVC_SEG_QUANTUM * GVC_SEG_QUANTUM;  // whole 512-chunks
     float4 a[2], b[2];
-    // the step's 8 pending-mask words (lanes 0..7), prefetched with the data
-    // when PF: a mask load issued at its use was the kernel's top stall (ncu)
+    // the step's 8 pending-mask words, prefetched with the data when PF (a mask
+    // load issued at its use was the kernel's top stall, ncu): MASK_ASYNC copies
+    // them into the warp's shared slots mw[2][8] with cp.async -- held in a
+    // register instead, the word was spilled and its local store waited on the load
+    constexpr bool MASK_ASYNC = PF && PM != 0 && !REFILL;
     uint32_t wreg = 0u;
     if (PF && nfull) {
+        if (MASK_ASYNC) {
+            if (lane < 2)
+                cp_async16(mw + 4 * lane, mp + 4 * lane);
+            cp_async_commit();
+        }
 #pragma unroll
         for (int u = 0; u < 2; u++) {
             a[u] = ld_stream(reinterpret_cast<const float4 *>(src + u * 128) + lane);
             if (do_ef)
                 b[u] = ld_stream(reinterpret_cast<const float4 *>(rp + u * 128) + lane);
         }
-        if (do_ef && PM && lane < 8)
+        if (!MASK_ASYNC && do_ef && PM && lane < 8)
             wreg = mp[lane];
     }
     for (; i < nfull; i += STEP) {
         float4 na[2], nb[2];
         uint32_t nw = 0u;
         const bool more = i + STEP < nfull;
+        const uint32_t slot = MASK_ASYNC ? ((i >> 8) & 1u) * 8u : 0u;
         if (PF) {
             if (more) {
 #pragma unroll
@@ -442,8 +483,18 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
                     if (do_ef)
                         nb[u] = ld_stream(reinterpret_cast<const float4 *>(rp + i + STEP + u * 128) + lane);
                 }
-                if (do_ef && PM && lane < 8)
+                if (MASK_ASYNC) {
+                    if (lane < 2)
+                        cp_async16(mw + (slot ^ 8u) + 4 * lane, mp + ((i + STEP) >> 5) + 4 * lane);
+                } else if (do_ef && PM && lane < 8) {
                     nw = mp[((i + STEP) >> 5) + lane];
+                }
+            }
+            if (MASK_ASYNC) {  // this step's words landed (the group just committed may still fly)
+                cp_async_commit();
+                cp_async_wait<1>();
+                __syncwarp();
+                wreg = lane < 8 ? mw[slot + lane] : 0u;
             }
         } else {
 #pragma unroll
@@ -461,7 +512,9 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
                 // lanes owning their 4-bit slices, cleared after use
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
-                    const uint32_t bits = __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3)) >> ((lane & 7) * 4);
+                    const uint32_t bits = (MASK_ASYNC ? mw[slot + 4 * u + (lane >> 3)]
+                                                      : __shfl_sync(0xffffffffu, wreg, 4 * u + (lane >> 3))) >>
+                                          ((lane & 7) * 4);
                     b[u].x = (bits & 1u) ? pending_resid(b[u].x, PM, pm) : b[u].x;
                     b[u].y = (bits & 2u) ? pending_resid(b[u].y, PM, pm) : b[u].y;
                     b[u].z = (bits & 4u) ? pending_resid(b[u].z, PM, pm) : b[u].z;
@@ -487,8 +540,21 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
                 for (int c = 0; c < 4; c++)
                     nacc = __fma_rn((double)v[c], (double)v[c], nacc);
             }
-            push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
-                      cidx, ccount);
+            if (STAGE) {
+                const uint32_t before = ccount;
+                push4<KM, GVC_STAGE - 1>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h,
+                                         dummy, sv, si, ccount);
+                if ((ccount ^ before) & ~127u) {  // warp-uniform: a 128-entry block filled up
+                    __syncwarp();
+                    const uint32_t f = before & ~127u, b0 = f & (GVC_STAGE - 1);
+                    reinterpret_cast<float4 *>(cval + f)[lane] = reinterpret_cast<const float4 *>(sv + b0)[lane];
+                    reinterpret_cast<uint4 *>(cidx + f)[lane] = reinterpret_cast<const uint4 *>(si + b0)[lane];
+                    __syncwarp();
+                }
+            } else {
+                push4<KM>(p, v, (uint32_t)beg + i + u * 128 + lane * 4, 4u, key_est, shift0, h, dummy, cval,
+                          cidx, ccount);
+            }
         }
         if (PF && more) {
 #pragma unroll
@@ -496,8 +562,17 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
                 a[u] = na[u];
                 b[u] = nb[u];
             }
-            wreg = nw;
+            if (!MASK_ASYNC)
+                wreg = nw;
         }
+    }
+    if (STAGE) {  // drain the ring; the tail stores directly
+        __syncwarp();
+        for (uint32_t t = (ccount & ~127u) + lane; t < ccount; t += 32) {
+            cval[t] = sv[t & (GVC_STAGE - 1)];
+            cidx[t] = si[t & (GVC_STAGE - 1)];
+        }
+        __syncwarp();
     }
     // tail: one value per lane, lane-major order preserved
     for (; i < len; i += 32) {
@@ -532,12 +607,15 @@ __device__ __forceinline__ void collect_segment(const Plan &p, uint32_t seg, int
 template <int KM, bool EF, int PM, bool REFILL = false>
 __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(const Plan p, int)
 {
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(1);
     // compile-time: a runtime flag would leave predicated refill / no-refill
     // code under every value of the hot loop
     constexpr bool refill = REFILL;
     __shared__ uint32_t h[GVC_H0_BINS + 32];  // + per-lane dummy bins
     __shared__ double red[GVC_WARPS_PER_BLOCK];
+    __shared__ __align__(16) float stage_v[GVC_WARPS_PER_BLOCK][GVC_STAGE];
+    __shared__ __align__(16) uint32_t stage_i[GVC_WARPS_PER_BLOCK][GVC_STAGE];
+    __shared__ __align__(16) uint32_t mwords[GVC_WARPS_PER_BLOCK][16];
     if (refill && !p.st->fallback)
         return;
     for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += GVC_THREADS)
@@ -551,7 +629,8 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
     const uint32_t dummy = GVC_H0_BINS + lane;
     double nacc = 0.0;
     if (seg < p.S)
-        collect_segment<KM, EF, PM, REFILL>(p, seg, lane, h, dummy, key_est, shift0, pm, nacc);
+        collect_segment<KM, EF, PM, REFILL>(p, seg, lane, h, dummy, key_est, shift0, pm, nacc, stage_v[warp],
+                                            stage_i[warp], mwords[warp]);
     nacc = warp_sum_f64(nacc);
     if (lane == 0)
         red[warp] = nacc;
@@ -565,6 +644,7 @@ __global__ void __launch_bounds__(GVC_THREADS, GVC_COLLECT_BLOCKS) k_collect(con
     for (int i = threadIdx.x; i < GVC_H0_BINS; i += GVC_THREADS)
         if (h[i])
             atomicAdd(&p.hist0[i], h[i]);
+    GVC_STAMP_OUT(1);
 }
 
 // ----------------------------------------------------------------- resolve
@@ -709,12 +789,13 @@ __device__ void resolve_level0(const Plan &p, int pass, unsigned long long *sh, 
 template <int KM, bool EF>
 __global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int)
 {
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(2);
     __shared__ unsigned long long sh[33];
     __shared__ unsigned long long need[GVC_MAX_LADDER];
     __shared__ uint32_t hs[GVC_H0_BINS + 32];
     resolve_level0<4>(p, 0, sh, need);
     __syncthreads();
+    GVC_STAMP_OUT(2);
     if (!*(volatile uint32_t *)&p.st->fallback)
         return;
     for (int i = threadIdx.x; i < GVC_H0_BINS + 32; i += blockDim.x)
@@ -747,7 +828,7 @@ __global__ void __launch_bounds__(1024) k_resolve0(const Plan p, int)
 template <int KM, int NB, bool ABS>
 __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
 {
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(3);
     extern __shared__ __align__(16) unsigned char fsm[];
     double(*acc_e)[GVC_THREADS] = reinterpret_cast<double(*)[GVC_THREADS]>(fsm);
     double(*acc_a)[GVC_THREADS] = acc_e + (NB + 1);  // only touched when ABS
@@ -980,6 +1061,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
         p.blk_band_e2[o] = e1;
         p.blk_band_ab[o] = a1;
     }
+    GVC_STAMP_OUT(3);
 }
 
 // Exact thresholds (one block): the level-1 histogram, then -- only if an
@@ -988,7 +1070,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
 template <int KM>
 __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
 {
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(4);
     __shared__ unsigned long long sh[33];
     __shared__ __align__(16) uint32_t hs[GVC_HL_BINS];
     SelState *st = p.st;
@@ -998,10 +1080,17 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
             continue;  // uniform across the block
         uint32_t *h = p.histl + j * GVC_HL_BINS;
         bool from_global = true;
-        while (true) {
+        // each round narrows the interval by the 12-bit histogram: a 32-bit key
+        // resolves within 3; more means an inconsistent state -- flagged, not spun on
+        for (int round = 0;; round++) {
             const JState cur = st->js[j];
             if (cur.resolved)
                 break;
+            if (round == 6) {
+                if (threadIdx.x == 0)
+                    atomicOr(&st->nan_flag, 2u);
+                break;
+            }
             const unsigned long long nd = cur.need;
             __syncthreads();
             find_crossings(from_global ? h : hs, sh, 1, &nd, [&](int, int b, unsigned long long above) {
@@ -1035,6 +1124,7 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
             from_global = false;
         }
     }
+    GVC_STAMP_OUT(4);
 }
 
 // Members' own contributions: exact band (#{j : T_j < key}), ties per entry;
@@ -1043,7 +1133,7 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
 template <int KM, int NB, bool ABS>
 __global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan p, int)
 {
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(5);
     __shared__ double wsum[GVC_WARPS_PER_BLOCK][4][NB];
     __shared__ uint32_t wcnt[GVC_WARPS_PER_BLOCK][2][NB];
     const SelState *st = p.st;
@@ -1137,6 +1227,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_members(const Plan p, int)
         p.blk_tie_e2[o] = e2;
         p.blk_tie_ab[o] = a2;
     }
+    GVC_STAMP_OUT(5);
 }
 
 // k_finish, one block per ladder entry j (the entries are independent):
@@ -1200,7 +1291,7 @@ __device__ __forceinline__ void finish_pair_sum(double &a, double &b, unsigned l
 template <int KM>
 __global__ void __launch_bounds__(1024) k_finish_j(const Plan p, int)
 {
-    pdl_enter();
+    pdl_enter(); GVC_STAMP_IN(6);
     constexpr int PER = GVC_BLK_MAX / 1024;  // 2 blocks per thread, contiguous
     __shared__ double shd[66];
     __shared__ unsigned long long shu[33];
@@ -1355,6 +1446,7 @@ __global__ void __launch_bounds__(1024) k_finish_j(const Plan p, int)
         const uint32_t f = atomicOr(&st->nan_flag, 0u);
         res->status = (f & 1u) ? GVC_ERR_NAN : ((f & 2u) ? GVC_ERR_STATE : GVC_OK);
     }
+    GVC_STAMP_OUT(6);
 }
 
 // -------------------------------------------------------------------- emit

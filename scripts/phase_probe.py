@@ -1,4 +1,5 @@
-"""Phase timestamps of the cooperative collect (gvc_select_phase_times) at one size.
+"""Per-kernel timeline of one select (gvc_select_phase_times) at one size, from a
+library built with -DGVC_PHASE_STAMPS=1 (scripts/build_variant.py).
 
     python scripts/phase_probe.py [n]
 """
@@ -19,9 +20,7 @@ r = torch.zeros(n, device="cuda")
 flush = torch.zeros(64 << 20, device="cuda")
 K = G.CompressorKind("topk")
 k0 = n // 10
-names = ["start", "b1 last arrives", "b1 resolved", "b2 last arrives", "b2 resolved", "b3 last arrives",
-         "b3 resolved", "cta0 pass end", "post start", "pass1 done", "thresholds", "members done", "finish", "b1 loads", "b1 prefix", "-", "L1 crossed", "L1 refined", "L2 crossed",
-         "L2 refined", "L3 crossed", "L3 refined", "fin loaded", "fin tie cut", "fin phase2", "-", "fin partial", "bar1", "bar2", "bar3"]
+names = ["sample", "collect", "resolve0", "pass1", "resolve1", "members", "finish_j"]
 for it in range(6):
     flush.sum()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,6 +31,10 @@ for it in range(6):
     out = (ctypes.c_ulonglong * 32)()
     nat.check(nat.load().gvc_select_phase_times(nat.ptr(sel.ws), out, 32))
     t = list(out)
-    rel = {nm: round((t[i] - t[0]) / 1000, 2) for i, nm in enumerate(names) if t[i]}
-    print(f"select {a.elapsed_time(b) * 1000:.1f} us", rel, "fallback", sel.result().fallback_used,
-          "cands", sel.result().candidates, flush=True)
+    t0 = t[0]
+    rel = {nm: (round((t[2 * k] - t0) / 1000, 1), round((t[2 * k + 1] - t0) / 1000, 1)) for k, nm in enumerate(names)}
+    try:
+        extra = f"fallback {sel.result().fallback_used} cands {sel.result().candidates}"
+    except Exception as e:  # ablation variants (scripts/ab_phase.sh) break the downstream kernels
+        extra = f"result: {str(e)[:60]}"
+    print(f"select {a.elapsed_time(b) * 1000:.1f} us", rel, extra, flush=True)
