@@ -323,6 +323,14 @@ GVC_API int gvc_select_phase_times(void *ws, unsigned long long *out, int n);
  * counter (pos_base + lo_j, stream), key seed. */
 GVC_API int gvc_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t rng_stream, uint64_t pos_base,
                            uint32_t *out_pos_dev, void *stream);
+/* The same sample, fused with its use (compressors.py:118-121): out[j] = the
+ * value at the j-th sampled position (as gvc_gather_ef: fl32(g + r_true) in EF
+ * mode, else values_dev), and bits_dev (u32[ceil(n/32)], overwritten) = the
+ * bitmap of the sampled positions, as gvc_select_args.dgc_sampled_dev wants it. */
+GVC_API int gvc_dgc_sample_gather(uint64_t n, uint64_t s, uint64_t seed, uint64_t rng_stream, uint64_t pos_base,
+                                  const float *values_dev, const float *g_dev, const float *resid_dev,
+                                  const uint32_t *pending_mask_dev, const float *pending_m_dev, int pending_mode,
+                                  float *out, uint32_t *bits_dev, void *stream);
 /* DGC helpers (compressors.py:110-137).
  * gvc_gather_ef: out[i] = values at pos[i]: fl32(g + r_true) in EF mode (g_dev and
  *   resid_dev, with the deferred mask of gvc_select_args applied), else values_dev[pos[i]].

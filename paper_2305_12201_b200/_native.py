@@ -30,7 +30,7 @@ EXPORTS = (
     "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
-    "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_select_phase_times", "gvc_dense_mean_peers",
+    "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
     "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
@@ -134,6 +134,8 @@ def load(build_if_missing: bool = False):
         L.gvc_aggregate_peers.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32, _vp, _vp]
         L.gvc_tile_bounds.argtypes = [_vp, _u64, _u64, _vp, _vp]
         L.gvc_dgc_sample.argtypes = [_u64, _u64, _u64, _u64, _u64, _vp, _vp]
+        L.gvc_dgc_sample_gather.argtypes = [_u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, ctypes.c_int,
+                                            _vp, _vp, _vp]
         L.gvc_dense_mean_peers.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _u64, _vp, ctypes.c_uint32, _vp, _vp]
         L.gvc_dense_collect.argtypes = [_vp, _vp, _u64, _vp, ctypes.c_int, ctypes.c_uint32, _vp, _vp]
         L.gvc_segmented_select_workspace_bytes.argtypes = [_u64, ctypes.c_int]

@@ -373,9 +373,14 @@ class _DgcStep:
                 # past ~4.6e8 values the emit ORs mask bits in global memory
                 # instead of writing every word from shared memory
                 self._mask1.zero_()
+            # (+ the decompress-average's tile boundaries of level 1, its emit's by-product)
+            nb = (self.n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1
+            bounds = torch.empty(nb, dtype=torch.int32, device=g.device)  # owned by the sent part
             idx, vals, sel1 = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
-                                         slot=slot + "a", want_result=True, sent_mask=self._mask1, check=False)
+                                         slot=slot + "a", want_result=True, sent_mask=self._mask1, check=False,
+                                         tile_bounds=bounds)
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
+            self.g_min._bounds = bounds
             self.norm = sel1.res_dev[:8].view(torch.float64)  # ||g_ef||^2 of the fused pass, on the device
             self._res.append(sel1.res_dev)
         if k2 < self.g_min.kept:
@@ -385,25 +390,33 @@ class _DgcStep:
             self._res.append(sel2.res_dev)
         else:
             self.g_c = self.g_min
-        # (E_min, E_c, ||g_ef||^2) as device scalars: every rank's row travels the same way in C2
-        norm_dev = squared_l2_norm_dev(store._resid).reshape(1) if self.norm is None else self.norm
-        self.stats = torch.cat([squared_l2_norm_dev(self.g_min.vals).reshape(1),
-                                squared_l2_norm_dev(self.g_c.vals).reshape(1), norm_dev.reshape(1)])
+        self.stats = None
+        if self.identity_level1:
+            # ||g_ef||^2 as a device scalar (every rank's row travels the same way in C2)
+            self.stats = squared_l2_norm_dev(store._resid).reshape(1)
+        # otherwise every number is in the selects' result records: ||g_ef||^2
+        # of the fused pass and each level's kept energy -- the fp64 sums of
+        # exactly the values sent (no separate norm kernels)
 
     def stats_dev(self) -> list[torch.Tensor]:
-        return [self.stats] + self._res
+        return ([self.stats] if self.stats is not None else []) + self._res
 
     def gains_from(self, raw: list[bytes], norm_host=None):
         import numpy as np
-        for b in raw[1:]:  # the DGC selects' statuses (NaN, consistency)
+        recs = []
+        for b in raw[1 if self.stats is not None else 0:]:  # the DGC selects' records
             r = nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES])
             if r.status == nat.GVC_ERR_NAN:
                 raise ValueError("NaN in gradient: compression order undefined")
             if r.status != nat.GVC_OK:
                 raise RuntimeError(f"selection consistency failure (status {r.status})")
-        e_min, e_c, norm = (float(x) for x in np.frombuffer(raw[0], dtype=np.float64))
+            recs.append(r)
         if self.identity_level1:  # theta_min == 1: the level-1 gain is exactly 1 (same sum)
-            e_min = norm
+            norm = float(np.frombuffer(raw[0], dtype=np.float64)[0])
+            e_c = float(recs[0].kept_sq[0]) if recs else norm
+            return norm, norm, e_c, []
+        norm, e_min = float(recs[0].ef_norm_sq), float(recs[0].kept_sq[0])
+        e_c = float(recs[1].kept_sq[0]) if len(recs) > 1 else e_min
         return norm, e_min, e_c, []
 
     def chosen_count(self, candidate: bool) -> int:

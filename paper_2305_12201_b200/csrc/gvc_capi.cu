@@ -325,6 +325,17 @@ int gvc_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t rng_stream, u
     return rc ? rc : check_launch("dgc_sample");
 }
 
+int gvc_dgc_sample_gather(uint64_t n, uint64_t s, uint64_t seed, uint64_t rng_stream, uint64_t pos_base,
+                          const float *values, const float *g, const float *resid, const uint32_t *pending_mask,
+                          const float *pending_m, int pending_mode, float *out, uint32_t *bits, void *stream)
+{
+    if (!out || !bits || (!values && (!g || !resid)) || (pending_mask && !g) || (pending_mode == 2 && !pending_m))
+        return set_error(GVC_ERR_ARG, "gvc_dgc_sample_gather: bad arguments");
+    int rc = dgc_sample_gather_run(n, s, seed, rng_stream, pos_base, values, g, resid, pending_mask, pending_m,
+                                   pending_mode, out, bits, STREAM(stream));
+    return rc ? rc : check_launch("dgc_sample_gather");
+}
+
 int gvc_tile_bounds(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, void *stream)
 {
     if (!idx || !bounds || n < 1 || k > n)

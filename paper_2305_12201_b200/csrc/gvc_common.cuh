@@ -22,6 +22,7 @@
 // 148 SMs x resident collect blocks x 8 warps: the collect grid is one full wave
 #define GVC_SEG_TARGET (148 * GVC_COLLECT_BLOCKS * 8)
 #define GVC_SEG_MAX 16384
+#define GVC_MEM_FLAT (1u << 22)  // flat member-key list of the level-1 refinement (16 MB)
 #define GVC_STAGE 256        // per-warp candidate staging ring in k_collect (entries)
 #define GVC_SEG_QUANTUM 512  // elements per warp iteration: 32 lanes x 4 float4
 #define GVC_H0_BINS 4096     // level-0 histogram (shared memory, 16 KB)

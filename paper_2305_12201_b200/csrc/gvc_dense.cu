@@ -188,21 +188,80 @@ int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const 
 // DGC's threshold sample: one position per stratum [j n / s, (j + 1) n / s),
 // offset = Philox word 0 at counter (pos_base + lo_j, stream) scaled to the
 // stratum width (the C-ABI header states the definition).
+// floor(j n / s) without a 64-bit integer division: with n < 2^32 and
+// j <= s <= n, j n fits 64 bits and the fp64 quotient is within 2^-20 of the
+// true one, so one correction step makes the floor exact
+__device__ __forceinline__ uint64_t stratum_lo(uint64_t j, uint64_t n, uint64_t s, double inv_s)
+{
+    const uint64_t a = j * n;
+    uint64_t q = (uint64_t)((double)a * inv_s);
+    if (q * s > a)
+        q--;
+    else if ((q + 1) * s <= a)
+        q++;
+    return q;
+}
+
+__device__ __forceinline__ uint32_t dgc_position(uint64_t j, uint64_t n, uint64_t s, double inv_s, uint64_t seed,
+                                                 uint64_t stream, uint64_t pos_base)
+{
+    const uint64_t lo = stratum_lo(j, n, s, inv_s), hi = stratum_lo(j + 1, n, s, inv_s);
+    const uint32_t h = philox_x0(pos_base + lo, stream, seed);
+    return (uint32_t)(lo + (((uint64_t)h * (hi - lo)) >> 32));
+}
+
 __global__ void k_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
                              uint32_t *__restrict__ out)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const double inv_s = 1.0 / (double)s;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < s; j += stride)
+        out[j] = dgc_position(j, n, s, inv_s, seed, stream, pos_base);
+}
+
+// gvc_dgc_sample + gvc_gather_ef + the sample's position bitmap in one pass
+// (bits zeroed by the caller's memset; strata are wider than 32 positions only
+// past s ~ n / 32, so two samples can share a word: atomicOr)
+__global__ void k_dgc_sample_gather(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
+                                    const float *__restrict__ values, const float *__restrict__ g,
+                                    const float *__restrict__ resid, const uint32_t *pmask, const float *pm_ptr,
+                                    int pmode, float *__restrict__ out, uint32_t *bits)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const double inv_s = 1.0 / (double)s;
+    const float pm = (pmask && pmode == 2) ? *pm_ptr : 0.f;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < s; j += stride) {
-        const uint64_t lo = j * n / s, hi = (j + 1) * n / s;
-        const uint32_t h = philox_x0(pos_base + lo, stream, seed);
-        out[j] = (uint32_t)(lo + (((uint64_t)h * (hi - lo)) >> 32));
+        const uint32_t q = dgc_position(j, n, s, inv_s, seed, stream, pos_base);
+        if (g) {
+            float r = resid[q];
+            if (pmask && ((pmask[q >> 5] >> (q & 31)) & 1u))
+                r = pending_resid(r, pmode, pm);
+            out[j] = __fadd_rn(g[q], r);
+        } else {
+            out[j] = values[q];
+        }
+        atomicOr(&bits[q >> 5], 1u << (q & 31));
     }
+}
+
+int dgc_sample_gather_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
+                          const float *values, const float *g, const float *resid, const uint32_t *pmask,
+                          const float *pm, int pmode, float *out, uint32_t *bits, cudaStream_t st)
+{
+    if (s < 1 || s > n || n > 0xffffffffull)
+        return set_error(GVC_ERR_ARG, "dgc_sample_gather: %llu samples of %llu positions", (unsigned long long)s,
+                         (unsigned long long)n);
+    cudaMemsetAsync(bits, 0, (n + 31) / 32 * 4, st);
+    count_launches(1);
+    k_dgc_sample_gather<<<grid_for(s, 256, 148 * 16), 256, 0, st>>>(n, s, seed, stream, pos_base, values, g, resid,
+                                                                    pmask, pm, pmode, out, bits);
+    return GVC_OK;
 }
 
 int dgc_sample_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base, uint32_t *out,
                    cudaStream_t st)
 {
-    if (s < 1 || s > n)
+    if (s < 1 || s > n || n > 0xffffffffull)
         return set_error(GVC_ERR_ARG, "dgc_sample: %llu samples of %llu positions", (unsigned long long)s,
                          (unsigned long long)n);
     count_launches(1);

@@ -52,6 +52,9 @@ int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *v
                                const gvc_peer_staging *sg, float *out, cudaStream_t s);
 int dgc_sample_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base, uint32_t *out,
                    cudaStream_t st);
+int dgc_sample_gather_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
+                          const float *values, const float *g, const float *resid, const uint32_t *pmask,
+                          const float *pm, int pmode, float *out, uint32_t *bits, cudaStream_t st);
 int tile_bounds_run(const uint32_t *idx, uint64_t k, uint64_t n, uint32_t *bounds, cudaStream_t s);
 int aggregate_run(const uint32_t *idx, const float *vals, const uint64_t *offs, const uint64_t *counts,
                   int nparts, uint64_t n, float *out, void *ws, size_t ws_bytes, const uint32_t *bounds,

@@ -63,6 +63,7 @@ struct SelState {
     float redsync_mean[GVC_MAX_LADDER];
     uint32_t fin_done;     // k_finish blocks done (the last one writes the status)
     uint32_t sample_done;  // k_sample blocks done (the last one resolves key_est)
+    uint32_t mem_flat;     // members appended to Plan::mem_key (may exceed its capacity)
     unsigned long long t_phase[32];  // %globaltimer at kernel boundaries (gvc_select_phase_times)
 };
 
@@ -87,6 +88,7 @@ struct Plan {
     int pmode;
     // sample
     uint64_t s_chunks, s_stride, s_target;
+    uint64_t s_target_lo;  // a count of sampled keys >= it says "k_0 keys are >= them" w.h.p.
     uint32_t hash_key_est;
     // workspace
     SelState *st;
@@ -94,6 +96,7 @@ struct Plan {
     uint32_t *seg_cnt;                     // [SEG_MAX] candidates per segment
     uint32_t *seg_mcnt;                    // [SEG_MAX] level-0 bin members per segment
     uint32_t *mem_idx;                     // [n_pad] members: segment-local candidate offsets
+    uint32_t *mem_key;                     // [GVC_MEM_FLAT] members' keys, flat, any order
     uint32_t *seg_band, *seg_tie;          // [L][SEG_MAX]
     double *blk_norm;                      // [BLK_MAX]
     uint32_t *blk_band_cnt, *blk_tie_cnt;  // [L][BLK_MAX]
@@ -133,10 +136,12 @@ static size_t carve(Plan *p, char *ws, uint64_t n)
     const size_t L = GVC_MAX_LADDER, SM = GVC_SEG_MAX, BM = GVC_BLK_MAX;
     Plan tmp;
     Plan *q = p ? p : &tmp;
+    // zeroed per select by ONE memset, st .. histl[n_ks] (adjacent, in this order)
     q->st = (SelState *)take(sizeof(SelState));
     q->hist0 = (uint32_t *)take(GVC_H0_BINS * 4);
-    q->histl = (uint32_t *)take(L * GVC_HL_BINS * 4);
     q->shist = (uint32_t *)take(GVC_SAMPLE_BINS * 4);
+    q->histl = (uint32_t *)take(L * GVC_HL_BINS * 4);
+    q->mem_key = (uint32_t *)take((size_t)GVC_MEM_FLAT * 4);
     q->seg_cnt = (uint32_t *)take(SM * 4);
     q->seg_mcnt = (uint32_t *)take(SM * 4);
     q->seg_band = (uint32_t *)take(L * SM * 4);
@@ -349,6 +354,12 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh, int s
     unsigned long long pre = block_excl_prefix(local, sh, &total);
     unsigned long long acc = total - pre - local;  // keys in bins above my range
     const unsigned long long target = p.s_target;
+    __shared__ unsigned long long s_flagged;  // DGC: sampled keys in the flagged half (bins >= 8192)
+    if (p.keymode == KEY_DGC) {
+        if (t == (1024 >> 1))
+            s_flagged = total - pre;
+        __syncthreads();
+    }
     if (total < target) {  // too few sampled values (e.g. NaN-only): exact path
         if (t == 0) {
             st->key_est = 0;
@@ -362,6 +373,12 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh, int s
             uint32_t est = (uint32_t)(t * PER + i) << shift;
             st->key_est = est;
             uint32_t mk = st->max_key;
+            // DGC composite keys, top-up branch (fewer than k_0 flagged keys,
+            // w.h.p.): the threshold is an unflagged key, i.e. a magnitude
+            // below thr, and every flagged key lies above it -- bins sized to
+            // the whole span put ~10^6 members in the threshold bin (measured)
+            if (p.keymode == KEY_DGC && est < 0x80000000u && mk >= 0x80000000u && s_flagged < p.s_target_lo)
+                mk = *p.dgc_thr;
             uint64_t span = mk > est ? (uint64_t)(mk - est) : 0;
             int shf = bitlen64(span) - 12;
             st->shift0 = shf < 0 ? 0 : shf;
@@ -921,8 +938,17 @@ __global__ void __launch_bounds__(GVC_THREADS) k_pass1(const Plan p, int)
                 acc_c[band][threadIdx.x] += 1u;
             }
             const uint32_t mbq = __ballot_sync(0xffffffffu, okq && in);
-            if (okq && in)
-                mem[mcount + __popc(mbq & lt)] = tq;
+            if (mbq) {  // + the flat key list of the level-1 refinement (k_resolve1)
+                uint32_t fb = 0;
+                if (lane == 0)
+                    fb = atomicAdd(&p.st->mem_flat, (uint32_t)__popc(mbq));
+                fb = __shfl_sync(0xffffffffu, fb, 0) + __popc(mbq & lt);
+                if (okq && in) {
+                    mem[mcount + __popc(mbq & lt)] = tq;
+                    if (fb < GVC_MEM_FLAT)
+                        p.mem_key[fb] = kq;
+                }
+            }
             mcount += __popc(mbq);
             __syncwarp();
         };
@@ -1100,8 +1126,6 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
                     hi = cur.hi;
                 set_jstate(st->js[j], lo, hi, cur.above + above, cur.need - above);
             });
-            if (from_global)
-                reinterpret_cast<uint4 *>(h)[threadIdx.x] = make_uint4(0, 0, 0, 0);
             __syncthreads();
             const JState nx = st->js[j];
             if (nx.resolved)
@@ -1110,15 +1134,38 @@ __global__ void __launch_bounds__(1024) k_resolve1(const Plan p, int)
             reinterpret_cast<uint4 *>(hs)[threadIdx.x] = make_uint4(0, 0, 0, 0);
             __syncthreads();
             const uint32_t lo = (uint32_t)nx.lo, wm1 = (uint32_t)(nx.hi - nx.lo - 1);
-            for (uint32_t sg = threadIdx.x; sg < p.S; sg += 1024) {
-                const uint64_t beg = (uint64_t)sg * p.seg_len;
-                const uint32_t mc = p.seg_mcnt[sg];
-                for (uint32_t i = 0; i < mc; i++) {
-                    const uint32_t t = p.mem_idx[beg + i];
-                    const float v = p.cand_val[beg + t];
-                    const uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + t]);
+            const uint32_t nflat = st->mem_flat;
+            if (nflat <= GVC_MEM_FLAT) {
+                // every entry's members, flat and coalesced (the per-segment
+                // walk below is a chain of dependent loads per thread: 95 us
+                // at 138M on DGC's composite keys, measured)
+                uint32_t f = threadIdx.x;
+                for (; f + 3 * 1024 < nflat; f += 4 * 1024) {
+                    uint32_t kk[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        kk[u] = p.mem_key[f + u * 1024];
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (kk[u] - lo <= wm1)
+                            atomicAdd(&hs[(kk[u] - lo) >> nx.shift], 1u);
+                }
+                for (; f < nflat; f += 1024) {
+                    const uint32_t key = p.mem_key[f];
                     if (key - lo <= wm1)
                         atomicAdd(&hs[(key - lo) >> nx.shift], 1u);
+                }
+            } else {  // more members than the flat list holds
+                for (uint32_t sg = threadIdx.x; sg < p.S; sg += 1024) {
+                    const uint64_t beg = (uint64_t)sg * p.seg_len;
+                    const uint32_t mc = p.seg_mcnt[sg];
+                    for (uint32_t i = 0; i < mc; i++) {
+                        const uint32_t t = p.mem_idx[beg + i];
+                        const float v = p.cand_val[beg + t];
+                        const uint32_t key = KM == KEY_MAG ? mag_key(v) : cand_key<KM>(p, v, p.cand_idx[beg + t]);
+                        if (key - lo <= wm1)
+                            atomicAdd(&hs[(key - lo) >> nx.shift], 1u);
+                    }
                 }
             }
             from_global = false;
@@ -1843,11 +1890,10 @@ static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *laun
 {
     if (gprobes)
         cudaEventRecordWithFlags(g_ev_mark[2], s, cudaEventRecordExternal);
-    cudaMemsetAsync(p.st, 0, sizeof(SelState), s);
-    cudaMemsetAsync(p.hist0, 0, GVC_H0_BINS * 4, s);
-    cudaMemsetAsync(p.histl, 0, GVC_MAX_LADDER * GVC_HL_BINS * 4, s);
-    if (p.keymode != KEY_HASH)
-        cudaMemsetAsync(p.shist, 0, GVC_SAMPLE_BINS * 4, s);
+    // SelState, hist0, shist and the level-1 histograms: one memset node, its
+    // size a function of the graph key (nb_for(n_ks), not n_ks: a cached graph
+    // serves every ladder length of its NB class)
+    cudaMemsetAsync(p.st, 0, (size_t)((char *)(p.histl + (size_t)nb_for(p.n_ks) * GVC_HL_BINS) - (char *)p.st), s);
     *launches = p.keymode == KEY_MAG   ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
                 : p.keymode == KEY_DGC ? launch_pipeline<KEY_DGC>(p, s, probes, gprobes)
                                        : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
@@ -1937,10 +1983,13 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
         p.s_stride = stride;
         if (sampled >= n) {
             p.s_target = k0;  // the sample is the whole vector: exact bin
+            p.s_target_lo = k0;
         } else {
             double mu = (double)k0 * (double)sampled / (double)n;
             double t = mu * 1.02 + 5.0 * sqrt(mu) + 32.0;
             p.s_target = t >= (double)sampled ? 0 : (uint64_t)ceil(t);
+            double tl = mu * 0.98 - 5.0 * sqrt(mu) - 32.0;
+            p.s_target_lo = tl <= 0.0 ? 0 : (uint64_t)floor(tl);
         }
     } else {
         double mu = (double)k0 + 8.0 * sqrt((double)k0) + 64.0;

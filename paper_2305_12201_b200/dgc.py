@@ -10,11 +10,11 @@ The reference:
 
 This build runs it with no host decision:
   * the sample is one counter-based (Philox) position per stratum of n / s
-    positions (gvc_dgc_sample; see DESIGN.md for why it replaces numpy's
-    choice), marked in a position bitmap;
-  * g_ef at the sampled positions is gathered (EF applied on the fly) and thr
-    is the exact rank-th largest sampled key (a Top-k select on s values,
-    threshold left on the device);
+    positions (see DESIGN.md for why it replaces numpy's choice); one pass
+    (gvc_dgc_sample_gather) gathers g_ef there (EF applied on the fly) and
+    marks the positions in a bitmap;
+  * thr is the exact rank-th largest sampled key (a Top-k select on s
+    values, threshold left on the device);
   * ONE fused selection over the composite key
         (|v| >= thr or sampled) ? 0x80000000 | |v| : |v|
     whose top-k is the DGC pick in both branches: when k entries reach thr,
@@ -31,30 +31,10 @@ import torch
 from . import _native as nat
 
 
-def _gather(pos: torch.Tensor, values=None, g=None, resid=None, pending=None) -> torch.Tensor:
-    dev = pos.device
-    out = torch.empty(pos.numel(), dtype=torch.float32, device=dev)
-    pm, pmk, mode = (None, None, 0) if pending is None else (pending[0], pending[1], int(pending[2]))
-    nat.check(nat.load().gvc_gather_ef(nat.ptr(pos), pos.numel(), nat.ptr(values), nat.ptr(g), nat.ptr(resid),
-                                       nat.ptr(pm), nat.ptr(pmk), mode, nat.ptr(out), nat.stream_ptr(dev)),
-              "gather_ef")
-    return out
-
-
-def _sample_bits(n: int, pos: torch.Tensor, slot: str) -> torch.Tensor:
-    """Bitmap of the sampled positions (u32[ceil(n / 32)]), a per-slot buffer."""
-    words = (n + 31) // 32
-    buf = nat.Workspace.get(pos.device, slot + "/bits", words * 4)[:words * 4].view(torch.int32).view(torch.uint32)
-    buf.zero_()
-    nat.check(nat.load().gvc_mark_sent(nat.ptr(pos), pos.numel(), nat.ptr(buf), nat.stream_ptr(pos.device)),
-              "mark_sent")
-    return buf
-
-
 def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0,
                idx_map: torch.Tensor | None = None, check: bool = True, *, g: torch.Tensor | None = None,
                resid: torch.Tensor | None = None, pending=None, slot: str = "dgc", want_result: bool = False,
-               sent_mask: torch.Tensor | None = None):
+               sent_mask: torch.Tensor | None = None, tile_bounds: torch.Tensor | None = None):
     """(ascending indices, values) of the DGC selection of k entries.
 
     Plain mode: ``values``.  EF mode: ``g`` + ``resid`` (+ ``pending``): g_ef is
@@ -62,6 +42,8 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
     also return the fused pass's Selection (its ``res_dev`` holds ||g_ef||^2
     and the status on the device).  ``sent_mask`` (level 1, no idx_map): also
     write the bit mask of the selected positions there, every word of it.
+    ``tile_bounds``: also write the aggregate's tile boundaries of the
+    selection (gvc_emit tile_bounds_dev), sparing the decompress its own pass.
     ``check``: read the status back (raises on NaN); the fused controller step
     leaves it on the device.
     """
@@ -74,11 +56,16 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
     if s >= n:  # full sample: threshold estimation degenerates to exact selection (:113-115)
         sel = Selection(topk, [k], values=values, g=g, resid=resid, pending=pending, slot=slot + "c")
     else:
-        P = torch.empty(s, dtype=torch.int32, device=dev).view(torch.uint32)
-        nat.check(nat.load().gvc_dgc_sample(n, s, rng.seed if rng is not None else 0,
-                                            rng.stream if rng is not None else 0, pos_base, nat.ptr(P),
-                                            nat.stream_ptr(dev)), "dgc_sample")
-        vP = _gather(P, values=values, g=g, resid=resid, pending=pending)
+        # the sample's values and position bitmap in one pass (gvc_dgc_sample_gather)
+        vP = torch.empty(s, dtype=torch.float32, device=dev)
+        words = (n + 31) // 32
+        bits = nat.Workspace.get(dev, slot + "/bits", words * 4)[:words * 4].view(torch.int32).view(torch.uint32)
+        pm, pmk, mode = (None, None, 0) if pending is None else (pending[0], pending[1], int(pending[2]))
+        nat.check(nat.load().gvc_dgc_sample_gather(n, s, rng.seed if rng is not None else 0,
+                                                   rng.stream if rng is not None else 0, pos_base,
+                                                   nat.ptr(values), nat.ptr(g), nat.ptr(resid), nat.ptr(pm),
+                                                   nat.ptr(pmk), mode, nat.ptr(vP), nat.ptr(bits),
+                                                   nat.stream_ptr(dev)), "dgc_sample_gather")
         rank = min(s, max(1, int(round(k * s / n))))
         if rank < s:
             sel_t = Selection(topk, [rank], values=vP, slot=slot + "t")
@@ -86,10 +73,9 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
             thr = sel_t.res_dev[off:off + 4].view(torch.int32)
         else:  # the threshold is the smallest sampled magnitude
             thr = (vP.view(torch.int32) & 0x7FFFFFFF).min().reshape(1)
-        bits = _sample_bits(n, P, slot)
         sel = Selection(topk, [k], values=values, g=g, resid=resid, pending=pending, slot=slot + "c",
                         dgc_thr=thr, dgc_bits=bits)
-    idx, vals = sel.emit(0, idx_map=idx_map, sent_mask=sent_mask)
+    idx, vals = sel.emit(0, idx_map=idx_map, sent_mask=sent_mask, tile_bounds=tile_bounds)
     if check:
         sel.result()  # raises ValueError on NaN
     return (idx, vals, sel) if want_result else (idx, vals)

@@ -390,6 +390,44 @@ def test_dgc_vs_oracle(G, n):
                 assert np.array_equal(bits(host(s.vals)), bits(ov)), (dist, cf, seed)
 
 
+@pytest.mark.parametrize("n,s", [(1000, 256), (300_001, 3_000), (138_000_000, 1_380_000), (4_000_000_000, 5_000)])
+def test_dgc_sample_gather_vs_oracle(G, n, s):
+    """gvc_dgc_sample_gather: the stratified sample positions (the oracle's
+    restatement), the values there (plain and EF with a deferred mask) and the
+    position bitmap, bit-exact; the large n exercise the fp64 stratum bounds."""
+    from paper_2305_12201_b200 import _native as nat
+    lib = nat.load()
+    want = O.dgc_sample_positions(n, s, 11, 22, 5).astype(np.int64)
+    pos = torch.empty(s, dtype=torch.int32, device="cuda")
+    nat.check(lib.gvc_dgc_sample(n, s, 11, 22, 5, nat.ptr(pos), None))
+    assert np.array_equal(host(pos).view(np.uint32).astype(np.int64), want)
+    if n > 200_000_000:
+        return  # positions only: no n-sized buffers
+    gen = torch.Generator(device="cuda").manual_seed(n)
+    g = torch.randn(n, device="cuda", generator=gen)
+    r = torch.randn(n, device="cuda", generator=gen)
+    words = (n + 31) // 32
+    mask = torch.randint(0, 2**31, (words,), device="cuda", generator=gen, dtype=torch.int64).to(torch.int32)
+    out = torch.empty(s, device="cuda")
+    bm = torch.full((words,), -1, dtype=torch.int32, device="cuda")
+    for mode, args in (("plain", (g, None, None, None, None, 0)), ("ef", (None, g, r, mask, None, 1))):
+        v, gg, rr, mk, pm, pmode = args
+        nat.check(lib.gvc_dgc_sample_gather(n, s, 11, 22, 5, nat.ptr(v), nat.ptr(gg), nat.ptr(rr), nat.ptr(mk),
+                                            nat.ptr(pm), pmode, nat.ptr(out), nat.ptr(bm), None))
+        gh = host(g)
+        if mode == "plain":
+            exp = gh[want]
+        else:
+            rh = host(r)[want].copy()
+            hit = (host(mask).view(np.uint32)[want >> 5] >> (want & 31).astype(np.uint32)) & 1
+            rh[hit == 1] = rh[hit == 1] - rh[hit == 1]  # pending mode 1: the sent entry's residual is zero
+            exp = (gh[want] + rh).astype(np.float32)
+        assert np.array_equal(bits(host(out)), bits(exp)), mode
+        b = np.zeros(words, dtype=np.uint32)
+        np.bitwise_or.at(b, want >> 5, (np.uint32(1) << (want & 31).astype(np.uint32)))
+        assert np.array_equal(host(bm).view(np.uint32), b), mode
+
+
 def test_dgc_overlap_distribution(G, golden):
     """Reference's test_compressors.py:88-96 as a distribution over 300 seeds."""
     d = golden("dgc_stats")
