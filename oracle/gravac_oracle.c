@@ -2,17 +2,34 @@
  * gravac_oracle.c -- CPU restatement of the GraVAC hot path (TEST INFRASTRUCTURE).
  * See gravac_oracle.h for scope, pinning and the "parity unpinned" note.
  *
- * Plain C99, single-threaded, deliberately simple: two-level radix counting
+ * Plain C99, deliberately simple: two-level radix counting
  * for the exact k-th key, then one ordered scan that keeps everything above
  * the threshold and the lowest-index ties.  That is the selection rule of
  * compressors.py:86-99 (np.partition kth, flatnonzero(mag > kth), first
  * `need` of flatnonzero(mag == kth)) without the partition.
+ *
+ * Threads: one by default -- the checker.  orc_set_threads(T > 1) (bench.py's
+ * CPU legs only) splits the O(n) passes over T OpenMP threads in index-ordered
+ * chunks: EF add, keys, counting, the ordered compaction (per-chunk counts,
+ * prefix, parallel write), residual update and aggregation give the same
+ * outputs; only the fp64 norm is then summed per chunk (a different rounding).
  */
 #include "gravac_oracle.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int g_threads = 1;
+
+void orc_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
+int orc_get_threads(void) { return g_threads; }
+
+/* [lo, hi) of chunk c of C over n */
+static inline uint64_t chunk_lo(uint64_t n, int c, int C) { return n * (uint64_t)c / (uint64_t)C; }
 
 /* |x| as an order-preserving integer key: clear the sign bit (-0 -> 0).
  * Monotone for every non-NaN float (compressors.py:174 np.abs + compare). */
@@ -57,6 +74,7 @@ uint32_t orc_position_hash(uint64_t seed, uint64_t stream, uint64_t i)
 /* ------------------------------------------------------------ dense pieces */
 void orc_ef_add(const float *g, const float *r, float *out, uint64_t n)
 {
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
     for (uint64_t i = 0; i < n; i++) {
         volatile float s = g[i] + r[i]; /* one IEEE fp32 rounding, no contraction */
         out[i] = s;
@@ -65,6 +83,23 @@ void orc_ef_add(const float *g, const float *r, float *out, uint64_t n)
 
 double orc_sq_norm(const float *x, uint64_t n)
 {
+    if (g_threads > 1 && n >= (1u << 20)) {
+        const int C = g_threads;
+        double part[256];
+#pragma omp parallel for num_threads(C) schedule(static, 1)
+        for (int c = 0; c < C; c++) {
+            double acc = 0.0;
+            for (uint64_t i = chunk_lo(n, c, C); i < chunk_lo(n, c + 1, C); i++) {
+                double v = (double)x[i];
+                acc += v * v;
+            }
+            part[c] = acc;
+        }
+        double acc = 0.0;
+        for (int c = 0; c < C; c++)
+            acc += part[c];
+        return acc;
+    }
     double acc = 0.0;
     for (uint64_t i = 0; i < n; i++) {
         double v = (double)x[i];
@@ -112,11 +147,41 @@ double orc_pairwise_sum_f64(const double *a, uint64_t n)
 /* ------------------------------------------------------- exact key select */
 /* Find the k-th largest key T and the tie quota q = k - #(key > T).
  * Two counting passes: top 16 bits, then low 16 bits inside the bin. */
+/* cnt[b] += #{i : keys[i] >> 16 == b} (hi) or #{i : keys[i] >> 16 == bin, keys[i] & 0xffff == b} */
+static void count_keys(const uint32_t *keys, uint64_t n, int hi, uint32_t bin, uint64_t *cnt)
+{
+    const int C = (g_threads > 1 && n >= (1u << 20)) ? g_threads : 1;
+    if (C == 1) {
+        for (uint64_t i = 0; i < n; i++) {
+            if (hi)
+                cnt[keys[i] >> 16]++;
+            else if ((keys[i] >> 16) == bin)
+                cnt[keys[i] & 0xffffu]++;
+        }
+        return;
+    }
+    uint32_t *loc = (uint32_t *)calloc((size_t)C * 65536, sizeof(uint32_t));
+#pragma omp parallel for num_threads(C) schedule(static, 1)
+    for (int c = 0; c < C; c++) {
+        uint32_t *h = loc + (size_t)c * 65536;
+        for (uint64_t i = chunk_lo(n, c, C); i < chunk_lo(n, c + 1, C); i++) {
+            if (hi)
+                h[keys[i] >> 16]++;
+            else if ((keys[i] >> 16) == bin)
+                h[keys[i] & 0xffffu]++;
+        }
+    }
+#pragma omp parallel for num_threads(C) schedule(static)
+    for (int b = 0; b < 65536; b++)
+        for (int c = 0; c < C; c++)
+            cnt[b] += loc[(size_t)c * 65536 + b];
+    free(loc);
+}
+
 static void kth_key(const uint32_t *keys, uint64_t n, uint64_t k, uint32_t *T, uint64_t *q)
 {
     uint64_t *cnt = (uint64_t *)calloc(65536, sizeof(uint64_t));
-    for (uint64_t i = 0; i < n; i++)
-        cnt[keys[i] >> 16]++;
+    count_keys(keys, n, 1, 0, cnt);
     uint64_t above = 0;
     int b = 65535;
     for (; b >= 0; b--) {
@@ -126,9 +191,7 @@ static void kth_key(const uint32_t *keys, uint64_t n, uint64_t k, uint32_t *T, u
     }
     uint64_t need = k - above;
     memset(cnt, 0, 65536 * sizeof(uint64_t));
-    for (uint64_t i = 0; i < n; i++)
-        if ((keys[i] >> 16) == (uint32_t)b)
-            cnt[keys[i] & 0xffffu]++;
+    count_keys(keys, n, 0, (uint32_t)b, cnt);
     uint64_t above2 = 0;
     int t = 65535;
     for (; t >= 0; t--) {
@@ -153,6 +216,42 @@ int orc_select_keys(const uint32_t *keys, uint64_t n, uint64_t k, uint32_t *out_
     uint32_t T;
     uint64_t q;
     kth_key(keys, n, k, &T, &q);
+    const int C = (g_threads > 1 && n >= (1u << 20)) ? g_threads : 1;
+    if (C > 1 && C <= 256) {
+        /* per-chunk (above, tie) counts, prefix, then every chunk writes its
+         * slice: the same ascending list as the scan below */
+        uint64_t ab[257], ti[257];
+#pragma omp parallel for num_threads(C) schedule(static, 1)
+        for (int c = 0; c < C; c++) {
+            uint64_t a = 0, t = 0;
+            for (uint64_t i = chunk_lo(n, c, C); i < chunk_lo(n, c + 1, C); i++) {
+                a += keys[i] > T;
+                t += keys[i] == T;
+            }
+            ab[c] = a;
+            ti[c] = t;
+        }
+        uint64_t o0[257], t0[257], oa = 0, ta = 0;
+        for (int c = 0; c < C; c++) {
+            o0[c] = oa;
+            t0[c] = ta;
+            const uint64_t take = ta >= q ? 0 : (q - ta < ti[c] ? q - ta : ti[c]);
+            oa += ab[c] + take;
+            ta += ti[c];
+        }
+        if (oa != k)
+            return ORC_ERR_ARG;
+#pragma omp parallel for num_threads(C) schedule(static, 1)
+        for (int c = 0; c < C; c++) {
+            uint64_t o = o0[c], ties = t0[c];
+            for (uint64_t i = chunk_lo(n, c, C); i < chunk_lo(n, c + 1, C); i++) {
+                uint32_t key = keys[i];
+                if (key > T || (key == T && ties++ < q))
+                    out_idx[o++] = (uint32_t)i;
+            }
+        }
+        return ORC_OK;
+    }
     uint64_t o = 0, ties = 0;
     for (uint64_t i = 0; i < n; i++) {
         uint32_t key = keys[i];
@@ -167,12 +266,14 @@ static uint32_t *mag_keys(const float *x, uint64_t n, int *nan_seen)
     uint32_t *keys = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
     if (!keys)
         return NULL;
-    *nan_seen = 0;
+    int nan = 0;
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static) reduction(|: nan)
     for (uint64_t i = 0; i < n; i++) {
         keys[i] = mag_key(x[i]);
         if (key_is_nan(keys[i]))
-            *nan_seen = 1;
+            nan = 1;
     }
+    *nan_seen = nan;
     return keys;
 }
 
@@ -390,16 +491,19 @@ int orc_aggregate(const uint32_t *idx, const float *vals, const uint64_t *counts
         return ORC_ERR_NOMEM;
     uint64_t off = 0;
     for (int p = 0; p < nparts; p++) {
-        for (uint64_t j = 0; j < counts[p]; j++) {
-            uint32_t i = idx[off + j];
-            if (i >= n) {
+        for (uint64_t j = 0; j < counts[p]; j++)
+            if (idx[off + j] >= n) {
                 free(acc);
                 return ORC_ERR_ARG;
             }
-            acc[i] += (double)vals[off + j];
-        }
+        /* a part's indices are distinct: its scatter splits over threads
+         * (parts in order, so every sum keeps the part order) */
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
+        for (uint64_t j = 0; j < counts[p]; j++)
+            acc[idx[off + j]] += (double)vals[off + j];
         off += counts[p];
     }
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
     for (uint64_t i = 0; i < n; i++)
         out[i] = (float)(acc[i] / (double)nparts);
     free(acc);
@@ -422,8 +526,12 @@ int orc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out)
 void orc_update_residual(const float *g_ef, const uint32_t *idx, const float *vals,
                          uint64_t k, uint64_t n, float *r_out)
 {
-    if (r_out != g_ef)
-        memcpy(r_out, g_ef, n * sizeof(float));
+    if (r_out != g_ef) {
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
+        for (uint64_t i = 0; i < n; i++)
+            r_out[i] = g_ef[i];
+    }
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
     for (uint64_t j = 0; j < k; j++) {
         volatile float d = r_out[idx[j]] - vals[j];
         r_out[idx[j]] = d;

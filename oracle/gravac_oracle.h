@@ -41,6 +41,11 @@ enum {
 enum { ORC_TOPK = 0, ORC_DGC = 1, ORC_REDSYNC = 2, ORC_RANDOMK = 3 };
 
 /* Philox4x32-10 (Salmon et al., SC'11): out = philox(ctr, key). */
+/* OpenMP threads of the O(n) passes (default 1: the checker's exact
+ * sequential semantics).  bench.py's CPU legs set the host's cores. */
+void orc_set_threads(int t);
+int orc_get_threads(void);
+
 void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 
 /* Counter-based position hash used by Random-k and the DGC sample:

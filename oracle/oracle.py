@@ -57,8 +57,20 @@ def lib():
         L.orc_aggregate_dense.argtypes = [vp, i32, u64, vp]
         L.orc_update_residual.argtypes = [vp, vp, vp, u64, u64, vp]
         L.orc_dgc_sample_positions.argtypes = [u64, u64, u64, u64, u64, vp]
+        L.orc_set_threads.argtypes = [i32]
+        L.orc_get_threads.restype = i32
         _lib = L
     return _lib
+
+
+def set_threads(t: int) -> int:
+    """OpenMP threads of the oracle's O(n) passes (1: the checker's exact
+    sequential semantics; bench.py's CPU legs use the host's cores).  Returns
+    the previous count."""
+    L = lib()
+    prev = int(L.orc_get_threads())
+    L.orc_set_threads(int(t))
+    return prev
 
 
 def _p(a: np.ndarray):

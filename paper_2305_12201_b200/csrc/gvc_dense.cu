@@ -7,6 +7,23 @@
 
 namespace gvc {
 
+// SMs of the current device (cached per device): grid caps are whole waves of
+// the part the kernel runs on, not of a hard-coded B200
+int device_sms()
+{
+    static int cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64)
+        return 148;
+    if (!cache[dev]) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = sms > 0 ? sms : 148;
+    }
+    return cache[dev];
+}
+
 static inline int grid_for(uint64_t work, int per_block, int cap)
 {
     uint64_t b = (work + per_block - 1) / per_block;
@@ -46,7 +63,7 @@ int ef_add_run(const float *g, const float *r, float *out, uint64_t n, cudaStrea
 {
     int vec = aligned16(g) && aligned16(r) && aligned16(out);
     count_launches(1);
-    k_ef_add<<<grid_for(n / 4 + 1, 256, 148 * 16), 256, 0, s>>>(g, r, out, n, vec);
+    k_ef_add<<<grid_for(n / 4 + 1, 256, device_sms() * 16), 256, 0, s>>>(g, r, out, n, vec);
     return GVC_OK;
 }
 
@@ -126,7 +143,7 @@ int update_residual_run(const float *ef, const uint32_t *idx, const float *vals,
         cudaMemcpyAsync(resid, ef, n * sizeof(float), cudaMemcpyDeviceToDevice, s);
     if (k)
         count_launches(1);
-    k_sub_scatter<<<grid_for(k, 256, 148 * 16), 256, 0, s>>>(idx, vals, k, resid);
+    k_sub_scatter<<<grid_for(k, 256, device_sms() * 16), 256, 0, s>>>(idx, vals, k, resid);
     return GVC_OK;
 }
 
@@ -152,7 +169,7 @@ int mark_sent_run(const uint32_t *idx, uint64_t k, uint32_t *mask, cudaStream_t 
 {
     if (k) {
         count_launches(1);
-        k_mark_sent<<<grid_for(k, 256, 148 * 16), 256, 0, s>>>(idx, k, mask);
+        k_mark_sent<<<grid_for(k, 256, device_sms() * 16), 256, 0, s>>>(idx, k, mask);
     }
     return GVC_OK;
 }
@@ -180,7 +197,7 @@ __global__ void k_apply_pending(float *resid, uint32_t *mask, uint64_t n, int mo
 int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const float *m, cudaStream_t s)
 {
     count_launches(1);
-    k_apply_pending<<<grid_for((n + 31) / 32, 256, 148 * 16), 256, 0, s>>>(resid, mask, n, mode, m);
+    k_apply_pending<<<grid_for((n + 31) / 32, 256, device_sms() * 16), 256, 0, s>>>(resid, mask, n, mode, m);
     return GVC_OK;
 }
 
@@ -253,7 +270,7 @@ int dgc_sample_gather_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream
                          (unsigned long long)n);
     cudaMemsetAsync(bits, 0, (n + 31) / 32 * 4, st);
     count_launches(1);
-    k_dgc_sample_gather<<<grid_for(s, 256, 148 * 16), 256, 0, st>>>(n, s, seed, stream, pos_base, values, g, resid,
+    k_dgc_sample_gather<<<grid_for(s, 256, device_sms() * 16), 256, 0, st>>>(n, s, seed, stream, pos_base, values, g, resid,
                                                                     pmask, pm, pmode, out, bits);
     return GVC_OK;
 }
@@ -265,7 +282,7 @@ int dgc_sample_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint6
         return set_error(GVC_ERR_ARG, "dgc_sample: %llu samples of %llu positions", (unsigned long long)s,
                          (unsigned long long)n);
     count_launches(1);
-    k_dgc_sample<<<grid_for(s, 256, 148 * 8), 256, 0, st>>>(n, s, seed, stream, pos_base, out);
+    k_dgc_sample<<<grid_for(s, 256, device_sms() * 8), 256, 0, st>>>(n, s, seed, stream, pos_base, out);
     return GVC_OK;
 }
 
@@ -293,7 +310,7 @@ int gather_ef_run(const uint32_t *pos, uint64_t k, const float *values, const fl
 {
     if (k) {
         count_launches(1);
-        k_gather_ef<<<grid_for(k, 256, 148 * 16), 256, 0, s>>>(pos, k, values, g, resid, pmask, pm, pmode, out);
+        k_gather_ef<<<grid_for(k, 256, device_sms() * 16), 256, 0, s>>>(pos, k, values, g, resid, pmask, pm, pmode, out);
     }
     return GVC_OK;
 }
@@ -328,7 +345,7 @@ int below_keys_run(const float *v, const uint32_t *pos, uint64_t n, const uint32
                    float *out, unsigned long long *count, cudaStream_t s)
 {
     count_launches(1);
-    k_below_keys<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(v, pos, n, thr, excl, out, count);
+    k_below_keys<<<grid_for(n, 256, device_sms() * 16), 256, 0, s>>>(v, pos, n, thr, excl, out, count);
     return GVC_OK;
 }
 
@@ -1158,7 +1175,7 @@ int aggregate_dense_run(const float *parts, int nparts, uint64_t n, float *out, 
     if (nparts < 1)
         return set_error(GVC_ERR_ARG, "aggregate_dense of zero parts");
     count_launches(1);
-    k_aggregate_dense<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(parts, nparts, n, out);
+    k_aggregate_dense<<<grid_for(n, 256, device_sms() * 16), 256, 0, s>>>(parts, nparts, n, out);
     return GVC_OK;
 }
 
@@ -1251,9 +1268,7 @@ int dense_mean_peers_run(float *const *bufs, int nranks, int rank, uint64_t n, c
     }
     const uint64_t n4 = (n + 3) / 4;  // the buffers hold n rounded up to 4 floats
     const uint64_t lo4 = n4 * rank / nranks, hi4 = n4 * (rank + 1) / nranks;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     count_launches(1);
     k_dense_mean_peers<<<grid_for(hi4 - lo4, 256, sms * 8), 256, 0, s>>>(P, nranks, lo4, hi4, flags, epoch, err);
     return GVC_OK;
@@ -1264,9 +1279,7 @@ int dense_collect_run(const float *own, float *out, uint64_t n, const uint32_t *
 {
     if (!own || !out || !flags || !err || nranks < 1 || nranks > GVC_MAX_PEERS)
         return set_error(GVC_ERR_ARG, "dense_collect: bad arguments");
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     count_launches(1);
     k_dense_collect<<<grid_for(n / 4 + 1, 256, sms * 8), 256, 0, s>>>(own, out, n, flags, nranks, epoch, err);
     return GVC_OK;
@@ -1282,7 +1295,7 @@ __global__ void k_iota(uint32_t *out, uint64_t n)
 int iota_run(uint32_t *out, uint64_t n, cudaStream_t s)
 {
     count_launches(1);
-    k_iota<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(out, n);
+    k_iota<<<grid_for(n, 256, device_sms() * 16), 256, 0, s>>>(out, n);
     return GVC_OK;
 }
 

@@ -1846,7 +1846,8 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
     int launches = 0;
     if (KM != KEY_HASH && p.force_exact == 0 && p.s_target > 0 && !p.key_est_dev) {
         uint64_t wb = (p.s_chunks + 31) / 32;
-        int sb = (int)(wb < 148 ? (wb ? wb : 1) : 148);
+        const uint64_t sms = (uint64_t)device_sms();
+        int sb = (int)(wb < sms ? (wb ? wb : 1) : sms);
         k_sample<KM><<<sb, 1024, GVC_SAMPLE_BINS * 4, s>>>(p, 0);  // its last block resolves key_est
         launches++;
     } else {

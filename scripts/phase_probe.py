@@ -20,7 +20,8 @@ r = torch.zeros(n, device="cuda")
 flush = torch.zeros(64 << 20, device="cuda")
 K = G.CompressorKind("topk")
 k0 = n // 10
-names = ["sample", "collect", "resolve0", "pass1", "resolve1", "members", "finish_j"]
+names = ["sample", "collect", "resolve0", "pass1", "resolve1", "members", "finish_j", "s:zero|loads", "s:merge|fin",
+         "s:resolve"]
 for it in range(6):
     flush.sum()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
