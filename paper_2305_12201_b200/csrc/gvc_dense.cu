@@ -478,13 +478,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p)
 }
 
 // Staged pull (C1 + K7 overlapped): the first `ncopy` CTAs of the merge grid
-// are copiers.  They wait for every peer's payload flag, then stream the
-// peers' (idx, vals) chunk by chunk over NVLink into local staging slots and
-// publish each chunk with a release store of the epoch into ready[chunk].
-// The remaining CTAs are the usual tiles; a tile waits only for the chunks
-// its entries fall in, so the merge trails the transfer instead of following
-// it.  Copiers have the lowest block indices: they are dispatched first, so a
-// spinning tile never holds the slot a copier needs.
+// to start (staged_ticket) are copiers.  They wait for every peer's payload
+// flag, then stream the peers' (idx, vals) chunk by chunk over NVLink into
+// local staging slots and publish each chunk with a release store of the
+// epoch into ready[chunk].  The remaining CTAs are the usual tiles; a tile
+// waits only for the chunks its entries fall in, so the merge trails the
+// transfer instead of following it.  Roles follow the start order, so a
+// spinning tile never holds the slot a copier still needs; every wait is
+// bounded besides (wait_epoch).
 struct Staged {
     int ncopy;           // copier CTAs (0: direct pull, no staging)
     int self;            // this rank's part (already local)
@@ -496,6 +497,7 @@ struct Staged {
     const float *src_val[GVC_MAX_PEERS];
     const uint32_t *src_bounds[GVC_MAX_PEERS];
     uint32_t *err;  // the flag area's error word (bounded waits)
+    uint32_t *ticket;    // dispatch-order CTA ticket (flags word GVC_FLAG_TICKET_WORD, reset by the last CTA)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p)
@@ -511,6 +513,7 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p)
 // stops waiting, so a dead peer costs seconds instead of a hung GPU.  The
 // host (exchange.PeerExchange) reads the word back every few exchanges.
 #define GVC_FLAG_ERR_WORD 63
+#define GVC_FLAG_TICKET_WORD 62  // staged merge: CTA roles in dispatch order
 __device__ __forceinline__ void wait_epoch(const uint32_t *word, uint32_t epoch, bool sys, uint32_t *err)
 {
     long long t0 = 0;
@@ -533,7 +536,7 @@ __device__ __forceinline__ uint32_t *flag_err(const uint32_t *flags)
 }
 
 __device__ void staged_copier(const Staged &st, const AggParts &parts, int nparts, const uint32_t *flags,
-                              uint32_t epoch)
+                              uint32_t epoch, uint32_t vb)
 {
     if (threadIdx.x < nparts && (int)threadIdx.x != st.self)
         wait_epoch(flags + threadIdx.x, epoch, true, st.err);
@@ -542,7 +545,7 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
     // chunks): copier b stages slice b of every remote part's bounds
     {
         const uint32_t per = (st.nb + st.ncopy - 1) / st.ncopy;
-        const uint32_t b0 = blockIdx.x * per, b1 = min(st.nb, b0 + per);
+        const uint32_t b0 = vb * per, b1 = min(st.nb, b0 + per);
         for (int q = 0; q < nparts; q++) {
             if (q == st.self)
                 continue;
@@ -553,10 +556,10 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0)
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + blockIdx.x), "r"(epoch) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + vb), "r"(epoch) : "memory");
     }
     constexpr int U = 4;
-    for (uint32_t c = blockIdx.x; c < st.nchunks; c += st.ncopy) {
+    for (uint32_t c = vb; c < st.nchunks; c += st.ncopy) {
         for (int q = 0; q < nparts; q++) {
             if (q == st.self)
                 continue;
@@ -596,6 +599,25 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
         if (threadIdx.x == 0)
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + st.ncopy + c), "r"(epoch) : "memory");
     }
+}
+
+// The CTA's role in the staged merge, from a ticket taken when it starts:
+// tickets 0 .. ncopy-1 copy, the rest merge tile (ticket - ncopy).  A tile
+// that waits for a chunk therefore runs only after every copier has started
+// -- block indices carry no such guarantee (CTAs may be dispatched in any
+// order, and SMs can be held by other work).  The last ticket resets the
+// counter for the next exchange (stream-ordered).
+__device__ __forceinline__ uint32_t staged_ticket(const Staged &st)
+{
+    __shared__ uint32_t s_vb;
+    if (threadIdx.x == 0) {
+        const uint32_t t = atomicAdd(st.ticket, 1u);
+        if (t == gridDim.x - 1)
+            atomicExch(st.ticket, 0u);
+        s_vb = t;
+    }
+    __syncthreads();
+    return s_vb;
 }
 
 // A tile's wait for the staged bound slices holding entries t and t + 1.
@@ -638,11 +660,12 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
     __shared__ __align__(16) double acc[MODE == 2 ? AGG_TILE : 2];
     __shared__ __align__(16) float accf[MODE == 2 ? 4 : AGG_TILE];
     __shared__ uint32_t s_a[NP], s_b[NP];
-    if (STAGED && (int)blockIdx.x < stg.ncopy) {
-        staged_copier(stg, parts, nparts, flags, epoch);
+    const uint32_t vb = STAGED ? staged_ticket(stg) : blockIdx.x;
+    if (STAGED && (int)vb < stg.ncopy) {
+        staged_copier(stg, parts, nparts, flags, epoch, vb);
         return;
     }
-    const uint32_t tile = STAGED ? blockIdx.x - stg.ncopy : blockIdx.x;
+    const uint32_t tile = STAGED ? vb - stg.ncopy : blockIdx.x;
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (MODE == 2) {
@@ -778,11 +801,12 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
     constexpr int U = NP >= 4 ? 2 : 4;
     extern __shared__ __align__(16) float tiles[];
     __shared__ uint32_t s_a[NP], s_b[NP];
-    if (STAGED && (int)blockIdx.x < stg.ncopy) {
-        staged_copier(stg, parts, nparts, flags, epoch);
+    const uint32_t vb = STAGED ? staged_ticket(stg) : blockIdx.x;
+    if (STAGED && (int)vb < stg.ncopy) {
+        staged_copier(stg, parts, nparts, flags, epoch, vb);
         return;
     }
-    const uint32_t tile = STAGED ? blockIdx.x - stg.ncopy : blockIdx.x;
+    const uint32_t tile = STAGED ? vb - stg.ncopy : blockIdx.x;
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (threadIdx.x < nparts) {
@@ -1127,6 +1151,7 @@ int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *v
     st.ch_log2 = (uint32_t)__builtin_ctz(ce);
     st.ready = sg->ready_dev;
     st.err = const_cast<uint32_t *>(flags) + GVC_FLAG_ERR_WORD;
+    st.ticket = const_cast<uint32_t *>(flags) + GVC_FLAG_TICKET_WORD;
     uint64_t kmax = 0;
     for (int p = 0; p < nparts; p++) {
         if (!idx[p] || !vals[p] || !bounds[p] || (p != sg->self && (!sg->src_idx_dev[p] || !sg->src_vals_dev[p])))
