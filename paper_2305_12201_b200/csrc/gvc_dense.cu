@@ -535,8 +535,11 @@ __device__ __forceinline__ uint32_t *flag_err(const uint32_t *flags)
     return const_cast<uint32_t *>(flags) + GVC_FLAG_ERR_WORD;
 }
 
+#ifndef GVC_COPIER_TMA
+#define GVC_COPIER_TMA 0
+#endif
 __device__ void staged_copier(const Staged &st, const AggParts &parts, int nparts, const uint32_t *flags,
-                              uint32_t epoch, uint32_t vb)
+                              uint32_t epoch, uint32_t vb, void *sbuf = nullptr, uint32_t sbytes = 0)
 {
     if (threadIdx.x < nparts && (int)threadIdx.x != st.self)
         wait_epoch(flags + threadIdx.x, epoch, true, st.err);
@@ -559,6 +562,91 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + vb), "r"(epoch) : "memory");
     }
     constexpr int U = 4;
+    if (GVC_COPIER_TMA && sbuf && nparts == 2 && (4u << st.ch_log2) <= sbytes / 2) {
+        // the TMA path (two parts: one remote): thread 0 moves the chunks
+        // through the CTA's (unused) tile buffer with bulk copies -- both
+        // arrays of a chunk in flight on two mbarriers, the next chunk's loads
+        // issued as soon as this chunk's stores have read shared memory, the
+        // chunk published once its stores completed
+        __shared__ __align__(8) uint64_t mbar[2];
+        if (threadIdx.x == 0) {
+            const int q = 1 - st.self;
+            const uint64_t k = parts.cnt[q];
+            const uint32_t half = sbytes / 2;  // one array of a chunk per half
+            const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sbuf);
+            const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            auto range = [&](uint32_t c, uint64_t &a, uint32_t &bytes) {
+                const uint64_t lo = (uint64_t)c << st.ch_log2;
+                const uint64_t hi = min((unsigned long long)k, (unsigned long long)(lo + (1ull << st.ch_log2)));
+                a = lo & ~3ull;
+                bytes = lo >= hi ? 0u : (uint32_t)((((hi + 3) & ~3ull) - a) * 4);  // padded slots
+            };
+            auto load = [&](uint32_t c) {
+                uint64_t a;
+                uint32_t bytes;
+                range(c, a, bytes);
+                if (!bytes)
+                    return;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb0), "r"(bytes) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(sb), "l"(st.src_idx[q] + a), "r"(bytes), "r"(mb0) : "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb0 + 8), "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(sb + half), "l"(st.src_val[q] + a), "r"(bytes), "r"(mb0 + 8) : "memory");
+            };
+            auto wait = [&](uint32_t mb, uint32_t phase) {
+                const long long t0 = clock64();
+                for (;;) {
+                    uint32_t done;
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                                 "selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done)
+                                 : "r"(mb), "r"(phase)
+                                 : "memory");
+                    if (done || clock64() - t0 > (1ll << 33)) {
+                        if (!done)
+                            atomicOr(st.err, 4u);
+                        return;
+                    }
+                }
+            };
+            uint32_t phase = 0;
+            if (vb < st.nchunks)
+                load(vb);
+            for (uint32_t c = vb; c < st.nchunks; c += st.ncopy) {
+                uint64_t a;
+                uint32_t bytes;
+                range(c, a, bytes);
+                if (bytes) {
+                    wait(mb0, phase);
+                    wait(mb0 + 8, phase);
+                    phase ^= 1u;
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     const_cast<uint32_t *>(parts.idx[q]) + a),
+                                 "r"(sb), "r"(bytes)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     const_cast<float *>(parts.vals[q]) + a),
+                                 "r"(sb + half), "r"(bytes)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+                if (c + st.ncopy < st.nchunks)
+                    load(c + st.ncopy);
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + st.ncopy + c), "r"(epoch)
+                             : "memory");
+            }
+        }
+        return;
+    }
     for (uint32_t c = vb; c < st.nchunks; c += st.ncopy) {
         for (int q = 0; q < nparts; q++) {
             if (q == st.self)
@@ -662,7 +750,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
     __shared__ uint32_t s_a[NP], s_b[NP];
     const uint32_t vb = STAGED ? staged_ticket(stg) : blockIdx.x;
     if (STAGED && (int)vb < stg.ncopy) {
-        staged_copier(stg, parts, nparts, flags, epoch, vb);
+        staged_copier(stg, parts, nparts, flags, epoch, vb, MODE == 2 ? (void *)acc : (void *)accf,
+                      MODE == 2 ? (uint32_t)sizeof(acc) : (uint32_t)sizeof(accf));
         return;
     }
     const uint32_t tile = STAGED ? vb - stg.ncopy : blockIdx.x;
@@ -803,7 +892,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
     __shared__ uint32_t s_a[NP], s_b[NP];
     const uint32_t vb = STAGED ? staged_ticket(stg) : blockIdx.x;
     if (STAGED && (int)vb < stg.ncopy) {
-        staged_copier(stg, parts, nparts, flags, epoch, vb);
+        staged_copier(stg, parts, nparts, flags, epoch, vb, tiles, (uint32_t)(nparts * AGG_TILE * 4));
         return;
     }
     const uint32_t tile = STAGED ? vb - stg.ncopy : blockIdx.x;
