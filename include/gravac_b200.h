@@ -309,6 +309,10 @@ GVC_API int gvc_aggregate_dense(const float *parts_dev, int nparts, uint64_t n, 
  * 3 aggregate) and resets.  gvc_launch_count is a running count of every
  * kernel this library launched. */
 GVC_API void gvc_prof_enable(int on);
+/* Probe only the selects / emits of vectors of at least n values (default 0:
+ * all) -- a step with several selects (DGC's sample, the level-2 select) then
+ * reports the full-size one alone. */
+GVC_API void gvc_prof_min_n(uint64_t n);
 GVC_API int gvc_prof_read(double *ms, unsigned long long *counts, int ncat);
 GVC_API unsigned long long gvc_launch_count(void);
 

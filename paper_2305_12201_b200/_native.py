@@ -27,7 +27,7 @@ EXPORTS = (
     "gvc_last_error", "gvc_abi_version", "gvc_select_workspace_bytes", "gvc_select", "gvc_emit",
     "gvc_ef_add", "gvc_sq_norm_workspace_bytes", "gvc_sq_norm", "gvc_update_residual",
     "gvc_decompress", "gvc_aggregate", "gvc_aggregate_workspace_bytes", "gvc_aggregate_dense",
-    "gvc_iota", "gvc_prof_enable", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
+    "gvc_iota", "gvc_prof_enable", "gvc_prof_min_n", "gvc_prof_read", "gvc_launch_count", "gvc_mark_sent", "gvc_apply_pending",
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
     "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
@@ -148,6 +148,8 @@ def load(build_if_missing: bool = False):
                                         ctypes.POINTER(EmitMirrors), _vp]
         L.gvc_prof_enable.argtypes = [ctypes.c_int]
         L.gvc_prof_enable.restype = None
+        L.gvc_prof_min_n.argtypes = [_u64]
+        L.gvc_prof_min_n.restype = None
         L.gvc_prof_read.argtypes = [_vp, _vp, ctypes.c_int]
         L.gvc_launch_count.restype = ctypes.c_ulonglong
         if hasattr(L, "gvc_select_phase_times"):  # diagnostic

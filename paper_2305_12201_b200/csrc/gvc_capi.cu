@@ -27,6 +27,7 @@ int set_error(int code, const char *fmt, ...)
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;     // mode 1: direct launches bracketed by events
 static bool g_prof_graph = false;  // mode 2: event-record nodes around k_collect inside the select graph
+static uint64_t g_prof_min_n = 0;  // only selects / emits of at least this many values are probed
 static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_pending;
 static std::vector<cudaEvent_t> g_prof_free;
 static double g_prof_ms[PROF_NCAT];
@@ -74,6 +75,12 @@ bool prof_enabled()
     return g_prof_on;
 }
 
+bool prof_wants(uint64_t n)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    return n >= g_prof_min_n;
+}
+
 bool prof_graph_enabled()
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -107,6 +114,12 @@ extern "C" {
 const char *gvc_last_error(void) { return g_err; }
 
 int gvc_abi_version(void) { return GVC_ABI_VERSION; }
+
+void gvc_prof_min_n(uint64_t n)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_min_n = n;
+}
 
 void gvc_prof_enable(int on)
 {

@@ -23,6 +23,7 @@ struct ProfScope {
 void count_launches(int n);
 bool prof_enabled();
 bool prof_graph_enabled();
+bool prof_wants(uint64_t n);  // the select / emit of an n-value vector is probed (gvc_prof_min_n)
 void prof_graph_pair(int cat, cudaEvent_t *a, cudaEvent_t *b);
 
 size_t select_workspace_bytes(int kind, uint64_t n);

@@ -2004,11 +2004,12 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     }
     set_attributes();
     int launches = 0;
-    if (prof_enabled()) {
+    const bool probe_this = prof_wants(p.n);
+    if (prof_enabled() && probe_this) {
         // measurement mode: direct launches bracketed by CUDA events (bench.py roofline)
         enqueue_select(p, s, true, &launches);
     } else {
-        const bool gprobes = prof_graph_enabled();
+        const bool gprobes = prof_graph_enabled() && probe_this;
         const std::string key = graph_key(p, ws) + (gprobes ? "|ev" : "");
         std::lock_guard<std::mutex> glk(g_mu);
         auto it = g_graphs.find(key);
@@ -2128,7 +2129,7 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
     if (j < 0 || j >= p.n_ks)
         return set_error(GVC_ERR_ARG, "gvc_emit: ladder index %d out of range [0, %d)", j, p.n_ks);
     const int blocks = (int)p.B;
-    ProfScope pe(PROF_EMIT, s);
+    ProfScope pe(prof_wants(p.n) ? PROF_EMIT : -1, s);
     count_launches(stats ? 2 : 1);
     const size_t mbytes = (size_t)GVC_WARPS_PER_BLOCK * (p.seg_len >> 5) * 4;
     const bool smem_mask = smask && !idx_map && mbytes <= 96 * 1024;
