@@ -474,12 +474,22 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     chosen.clear()
     for key in STATS:
         STATS[key] = 0
-    def raw_state():
+    def raw_state(into=None):
         """The store's raw buffers (residual, deferred sent mask, Redsync mean, mode): copies,
-        so the step itself runs unchanged (reading .residual would apply the mask)."""
-        return (store._resid.clone(), None if store._mask is None else store._mask.clone(),
-                None if store._pm is None else store._pm.clone(), int(store._pmode))
+        so the step itself runs unchanged (reading .residual would apply the mask).  ``into``:
+        preallocated buffers (the timed loop must not grow the allocator: a cudaMalloc there
+        stalls the host between the step's events)."""
+        src = (store._resid, store._mask, store._pm)
+        if into is None:
+            out = tuple(None if t is None else t.clone() for t in src)
+        else:
+            out = tuple(None if t is None else (t.clone() if d is None else d.copy_(t)) for t, d in zip(src, into))
+        return out + (int(store._pmode),)
 
+    # the last timed step's inputs are snapshotted into buffers allocated here
+    snap_bufs = (torch.empty_like(store._resid), torch.empty_like(store._mask) if store._mask is not None else None,
+                 torch.empty_like(store._pm) if store._pm is not None else None)
+    g_snap = torch.empty_like(gbuf)
     launches0 = nat.launch_count()
     clocks.mark("t0")
     snap_in = None
@@ -487,7 +497,7 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
         g = fresh()
         if s == args.steps - 1:  # inputs of the last timed step, for the oracle re-check (untimed)
             launches_snap = nat.launch_count()
-            snap_in = (g.clone(),) + raw_state()
+            snap_in = (g_snap.copy_(g),) + raw_state(snap_bufs)
             launches0 += nat.launch_count() - launches_snap
         cool()  # evict L2 (outside the timed events)
         ev[s][0].record()

@@ -240,10 +240,19 @@ GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, u
  * lower index; out = the segments' (global index, value) lists concatenated
  * in segment order (sum seg_k entries; a segment with seg_k >= its length
  * keeps everything).  seg_offsets / seg_k are HOST arrays.  Every segment is
- * resolved by the same 11 launches (4 radix passes of 8 key bits over all
- * segments at once, counts, one scan, an ordered compaction) however many
- * segments there are.  *status_dev |= 1 on a NaN magnitude. */
+ * resolved by the same 12 launches (a state init, 4 radix passes of 8 key
+ * bits over all segments at once, per-slice counts, one scan, an ordered
+ * compaction) however many segments there are.  *status_dev |= 1 on a NaN
+ * magnitude.  The layout's work-item tables live in the workspace and are
+ * uploaded only when (n, kind, seg_offsets, seg_k) differ from the previous
+ * call on the same workspace address -- as with gvc_select's cached graphs,
+ * a workspace is identified by its address: a new buffer must not reuse a
+ * freed workspace's address while the library holds state for it (or call
+ * gvc_workspace_forget first). */
 GVC_API size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg);
+/* Drop every per-workspace cache entry (select graphs and plans, segment
+ * tables) for `ws` before its memory is freed or reused. */
+GVC_API int gvc_workspace_forget(void *ws);
 GVC_API int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                                  const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream,
                                  uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev, size_t ws_bytes,

@@ -31,7 +31,7 @@ EXPORTS = (
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
     "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
-    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select",
+    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -140,6 +140,7 @@ def load(build_if_missing: bool = False):
         L.gvc_dense_collect.argtypes = [_vp, _vp, _u64, _vp, ctypes.c_int, ctypes.c_uint32, _vp, _vp]
         L.gvc_segmented_select_workspace_bytes.argtypes = [_u64, ctypes.c_int]
         L.gvc_segmented_select_workspace_bytes.restype = _sz
+        L.gvc_workspace_forget.argtypes = [_vp]
         L.gvc_segmented_select.argtypes = [ctypes.c_int, _vp, _u64, _vp, _vp, ctypes.c_int, _u64, _u64, _vp, _vp,
                                            _vp, _sz, _vp, _vp]
         L.gvc_aggregate_peers_staged.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32,
@@ -204,6 +205,8 @@ class Workspace:
         key = (device.index if device.index is not None else torch.cuda.current_device(), slot)
         buf = cls._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
+            if buf is not None:  # the library's per-workspace caches name the old address
+                load().gvc_workspace_forget(ctypes.c_void_p(buf.data_ptr()))
             buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
             cls._bufs[key] = buf
         return buf

@@ -236,6 +236,9 @@ def _select(kind: CompressorKind, values: torch.Tensor, k: int, rng: SeededRng |
     return out
 
 
+_LAYOUTS: dict = {}
+
+
 def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf: float, rng):
     """compressors.py:204-217: per segment keep_count(len, cf) by the kind's
     rule, indices offset by the segment start, concatenated in order.  Top-k
@@ -243,21 +246,27 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
     (gvc_segmented_select); DGC and Redsync: one selection per segment,
     enqueued back to back, statuses read once at the end."""
     n = values.numel()
-    bounds = [sl for sl in g.layer_slices() if sl.stop > sl.start]
-    ks = [keep_count(sl.stop - sl.start, cf) for sl in bounds]
     if kind.name in (RANDOMK, DGC) and rng is None:
         raise ValueError(f"{kind.name} compression requires an rng")
     dev = values.device
     lib = nat.load()
-    if kind.name in (TOPK, RANDOMK):
+    # the layout's segment table (bounds, keep counts, the C arrays): built once
+    # per (offsets, length, cf) -- a training loop passes the same layout every step
+    key = (g.layer_offsets, n, float(cf))
+    lay = _LAYOUTS.get(key)
+    if lay is None:
+        bounds = [sl for sl in g.layer_slices() if sl.stop > sl.start]
+        ks = [keep_count(sl.stop - sl.start, cf) for sl in bounds]
         total = sum(min(k, sl.stop - sl.start) for k, sl in zip(ks, bounds))
-        offs = (ctypes.c_uint64 * (len(bounds) + 1))()
+        offs = (ctypes.c_uint64 * (len(bounds) + 1))(*[sl.start for sl in bounds], bounds[-1].stop)
         kk = (ctypes.c_uint64 * len(bounds))(*ks)
-        for q, sl in enumerate(bounds):
-            offs[q] = sl.start
-        offs[len(bounds)] = bounds[-1].stop
         # (segments are contiguous in GradientVector: each starts where the previous ended)
         contiguous = all(bounds[q].stop == bounds[q + 1].start for q in range(len(bounds) - 1))
+        lay = _LAYOUTS[key] = (bounds, ks, total, offs, kk, contiguous)
+        if len(_LAYOUTS) > 64:
+            _LAYOUTS.pop(next(iter(_LAYOUTS)))
+    bounds, ks, total, offs, kk, contiguous = lay
+    if kind.name in (TOPK, RANDOMK):
         if contiguous:
             idx = torch.empty(total, dtype=torch.int32, device=dev).view(torch.uint32)
             vals = torch.empty(total, dtype=torch.float32, device=dev)
@@ -267,7 +276,7 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
                                                rng.seed if rng is not None else 0, rng.stream if rng is not None else 0,
                                                nat.ptr(idx), nat.ptr(vals), nat.ptr(ws), ws.numel(), nat.ptr(status),
                                                nat.stream_ptr(dev)), "segmented_select")
-            if int(status.item()) & 1:
+            if nat.d2h_bytes(status)[0] & 1:  # (event spin: no scheduler-quantum wake-up)
                 raise ValueError("NaN in gradient: compression order undefined")
             return idx, vals
     idx_parts, val_parts, checks = [], [], []

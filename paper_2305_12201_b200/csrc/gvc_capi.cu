@@ -367,6 +367,15 @@ int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, 
 
 size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg) { return segsel_workspace_bytes(n, nseg); }
 
+int gvc_workspace_forget(void *ws)
+{
+    if (!ws)
+        return set_error(GVC_ERR_ARG, "gvc_workspace_forget: null workspace");
+    select_forget(ws);
+    segsel_forget(ws);
+    return GVC_OK;
+}
+
 int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                          const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream, uint32_t *out_idx_dev,
                          float *out_val_dev, void *ws_dev, size_t ws_bytes, uint32_t *status_dev, void *stream)

@@ -68,6 +68,8 @@ int dense_collect_run(const float *own, float *out, uint64_t n, const uint32_t *
                       uint32_t *err, cudaStream_t s);
 int iota_run(uint32_t *out, uint64_t n, cudaStream_t s);
 size_t segsel_workspace_bytes(uint64_t n, int nseg);
+void select_forget(const void *ws);
+void segsel_forget(const void *ws);
 int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
                uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
                uint32_t *status, cudaStream_t s);

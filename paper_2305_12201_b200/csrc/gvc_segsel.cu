@@ -20,6 +20,9 @@
 // Keys: 31-bit |v| (Top-k) or the Philox position hash of the global
 // position (Random-k, the counter-based sampler with pos_base = segment start,
 // DESIGN.md).  11 launches whatever the number of segments.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "gvc_common.cuh"
@@ -29,7 +32,6 @@ namespace gvc {
 
 #define SS_CHUNK 16384
 #define SS_THREADS 256
-#define SS_PER (SS_CHUNK / SS_THREADS)  // values per thread in a chunk, contiguous
 
 struct SegState {
     uint32_t prefix;     // resolved key bits (most significant first)
@@ -42,7 +44,7 @@ struct SegPlan {
     uint64_t n;
     int nseg, nitems, keymode;
     uint64_t seed, stream;
-    const uint64_t *seg_lo;   // [nseg]
+    const uint64_t *seg_lo;   // [nseg + 1] segment offsets
     const uint64_t *seg_k;    // [nseg]
     const uint32_t *item_seg;  // [nitems]
     const uint64_t *item_lo;   // [nitems] global start of the item
@@ -50,6 +52,7 @@ struct SegPlan {
     SegState *seg;             // [nseg]
     uint32_t *hist;            // [4][nseg][256]
     uint32_t *item_gt, *item_eq;  // [nitems]
+    uint32_t *warp_gt, *warp_eq;  // [nitems][SS_THREADS / 32]: the same counts per k_ss_write warp slice
     uint32_t *item_take;          // [nitems] ties this item keeps
     unsigned long long *item_out; // [nitems] output offset
     unsigned long long *item_E;   // [nitems] exclusive scan of the == counts
@@ -57,12 +60,16 @@ struct SegPlan {
     uint32_t *status;             // bit 1: NaN
 };
 
+// (the key mode is a template parameter of every pass: a runtime test per
+// value cost the compaction pass ~20% of its issue slots)
+template <int KM>
 __device__ __forceinline__ uint32_t ss_key(const SegPlan &P, float v, uint64_t pos)
 {
-    return P.keymode == KEY_HASH ? hash_key(pos, P.stream, P.seed) : mag_key(v);
+    return KM == KEY_HASH ? hash_key(pos, P.stream, P.seed) : mag_key(v);
 }
 
 // Pass d: histogram of digit d of the keys matching the segment's prefix.
+template <int KM>
 __global__ void __launch_bounds__(SS_THREADS) k_ss_hist(SegPlan P, int d)
 {
     __shared__ uint32_t h[256];
@@ -80,8 +87,8 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_hist(SegPlan P, int d)
         uint32_t nan = 0;
         for (uint32_t i = threadIdx.x; i < len; i += SS_THREADS) {
             const float v = P.values[lo + i];
-            const uint32_t key = ss_key(P, v, lo + i);
-            if (d == 0 && P.keymode == KEY_MAG)
+            const uint32_t key = ss_key<KM>(P, v, lo + i);
+            if (d == 0 && KM == KEY_MAG)
                 nan |= key > 0x7f800000u;
             if ((key & pmask) == st.prefix)
                 atomicAdd(&h[(key >> shift) & 255u], 1u);
@@ -140,20 +147,45 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_resolve(SegPlan P, int d)
     }
 }
 
-// Per item: keys above the threshold and equal to it.
+// The slice of an item that warp w of k_ss_count / k_ss_write owns (contiguous,
+// a multiple of 32 values).
+__device__ __forceinline__ void ss_slice(uint32_t len, int warp, uint32_t &wb, uint32_t &we)
+{
+    constexpr int W = SS_THREADS / 32;
+    const uint32_t per = ((len + W - 1) / W + 31) & ~31u;
+    wb = min(len, warp * per);
+    we = min(len, wb + per);
+}
+
+// Segment states from the (cached) tables: nothing to copy per call.
+__global__ void k_ss_init(SegPlan P)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P.nseg)
+        return;
+    const uint64_t len = P.seg_lo[q + 1] - P.seg_lo[q], k = P.seg_k[q];
+    SegState st;
+    st.prefix = 0;
+    st.all = len == 0 || k >= len;
+    st.need = k;
+    P.seg[q] = st;
+}
+
+// Per item and per warp slice: keys above the threshold and equal to it.
+template <int KM>
 __global__ void __launch_bounds__(SS_THREADS) k_ss_count(SegPlan P)
 {
-    __shared__ uint32_t sgt, seq;
+    constexpr int W = SS_THREADS / 32;
+    __shared__ uint32_t s_gt[W], s_eq[W];
     const int it = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const SegState st = P.seg[P.item_seg[it]];
-    if (threadIdx.x == 0)
-        sgt = seq = 0;
-    __syncthreads();
     const uint64_t lo = P.item_lo[it];
-    const uint32_t len = P.item_len[it];
+    uint32_t wb, we;
+    ss_slice(P.item_len[it], warp, wb, we);
     uint32_t gt = 0, eq = 0;
-    for (uint32_t i = threadIdx.x; i < len; i += SS_THREADS) {
-        const uint32_t key = ss_key(P, P.values[lo + i], lo + i);
+    for (uint32_t i = wb + lane; i < we; i += 32) {
+        const uint32_t key = ss_key<KM>(P, P.values[lo + i], lo + i);
         gt += st.all || key > st.prefix;
         eq += !st.all && key == st.prefix;
     }
@@ -162,14 +194,21 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_count(SegPlan P)
         gt += __shfl_xor_sync(0xffffffffu, gt, o);
         eq += __shfl_xor_sync(0xffffffffu, eq, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&sgt, gt);
-        atomicAdd(&seq, eq);
+    if (lane == 0) {
+        s_gt[warp] = gt;
+        s_eq[warp] = eq;
+        P.warp_gt[it * W + warp] = gt;
+        P.warp_eq[it * W + warp] = eq;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        P.item_gt[it] = sgt;
-        P.item_eq[it] = seq;
+        uint32_t a = 0, b = 0;
+        for (int w = 0; w < W; w++) {
+            a += s_gt[w];
+            b += s_eq[w];
+        }
+        P.item_gt[it] = a;
+        P.item_eq[it] = b;
     }
 }
 
@@ -224,41 +263,85 @@ __global__ void __launch_bounds__(1024) k_ss_scan(SegPlan P)
     }
 }
 
-// Ordered compaction of one item: thread t owns values [t*PER, (t+1)*PER) of
-// the chunk; kept = key > T, or key == T among the item's first take ties.
+// Ordered compaction of one item, warp-cooperative: warp w owns a contiguous
+// slice of the item and walks it 32 values at a time (coalesced loads, ballot
+// compaction, coalesced stores); kept = key > T, or key == T among the item's
+// first `take` ties.  k_ss_count's per-slice counts give each warp its output
+// offset and its first tie rank.  (Thread-contiguous slices read and wrote
+// with a 256-byte stride across the warp: 368 us at 44.5M, measured; with a
+// counting pass of its own, 117 us.)
+template <int KM>
 __global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *out_idx, float *out_val)
 {
-    __shared__ unsigned long long sh[33];
+    constexpr int W = SS_THREADS / 32;
     const int it = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const SegState st = P.seg[P.item_seg[it]];
-    const uint64_t lo = P.item_lo[it];
-    const uint32_t len = P.item_len[it];
+    const uint32_t lo = (uint32_t)P.item_lo[it];  // n < 2^32 (gvc_segmented_select checks)
     const uint32_t take = P.item_take[it];
-    const uint32_t b = threadIdx.x * SS_PER, e = min(len, b + SS_PER);
-    uint32_t gt = 0, eq = 0;
-    for (uint32_t i = b; i < e; i++) {
-        const uint32_t key = ss_key(P, P.values[lo + i], lo + i);
-        gt += st.all || key > st.prefix;
-        eq += !st.all && key == st.prefix;
-    }
-    const unsigned long long eq_pre = block_excl_prefix(eq, sh);
-    // ties this thread keeps: the item's first `take` ties
-    const uint32_t tk = eq_pre >= take ? 0u : min((uint32_t)(take - eq_pre), eq);
-    unsigned long long o = P.item_out[it] + block_excl_prefix(gt + tk, sh);
+    uint32_t wb, we;
+    ss_slice(P.item_len[it], warp, wb, we);
+    // this warp's first tie rank and output offset within the item
     uint32_t ties = 0;
-    for (uint32_t i = b; i < e; i++) {
-        const float v = P.values[lo + i];
-        const uint32_t key = ss_key(P, v, lo + i);
-        bool keep = st.all || key > st.prefix;
-        if (!st.all && key == st.prefix) {
-            keep = ties < tk;
-            ties++;
+    uint32_t o = (uint32_t)P.item_out[it];
+    for (int w = 0; w < warp; w++) {
+        const uint32_t e = P.warp_eq[it * W + w];
+        const uint32_t tk = ties >= take ? 0u : min(take - ties, e);
+        o += P.warp_gt[it * W + w] + tk;
+        ties += e;
+    }
+    const uint32_t lt = lanemask_lt();
+    // kept entries go through a per-warp shared ring and leave 128 at a time
+    // in whole 128-byte rows (stored straight from the ballot, every row of 32
+    // values cost two partial-sector stores)
+    __shared__ uint32_t ring_i[W][256];
+    __shared__ float ring_v[W][256];
+    uint32_t cnt = 0, flushed = 0;
+    // U rows of 32 loaded before any is compacted
+    constexpr int U = 8;
+    for (uint32_t base = wb; base < we; base += 32 * U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t i = base + u * 32 + lane;
+            v[u] = i < we ? P.values[lo + i] : 0.f;
         }
-        if (keep) {
-            out_idx[o] = (uint32_t)(lo + i);
-            out_val[o] = v;
-            o++;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t i = base + u * 32 + lane;
+            const bool ok = i < we;
+            const uint32_t key = ok ? ss_key<KM>(P, v[u], lo + i) : 0u;
+            const bool iseq = ok && !st.all && key == st.prefix;
+            bool keep = ok && (st.all || key > st.prefix);
+            const uint32_t em = __ballot_sync(0xffffffffu, iseq);
+            if (em) {  // warp-uniform: ties in this row (rare)
+                keep |= iseq && ties + __popc(em & lt) < take;
+                ties += __popc(em);
+            }
+            const uint32_t km = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const uint32_t r = (cnt + __popc(km & lt)) & 255u;
+                ring_i[warp][r] = (uint32_t)(lo + i);
+                ring_v[warp][r] = v[u];
+            }
+            cnt += __popc(km);
+            if (cnt - flushed >= 128) {  // warp-uniform; the ring never holds more than 159
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t e = flushed + q * 32 + lane;
+                    out_idx[o + e] = ring_i[warp][e & 255u];
+                    out_val[o + e] = ring_v[warp][e & 255u];
+                }
+                flushed += 128;
+                __syncwarp();
+            }
         }
+    }
+    __syncwarp();
+    for (uint32_t e = flushed + lane; e < cnt; e += 32) {
+        out_idx[o + e] = ring_i[warp][e & 255u];
+        out_val[o + e] = ring_v[warp][e & 255u];
     }
 }
 
@@ -267,42 +350,64 @@ static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t segsel_workspace_bytes(uint64_t n, int nseg)
 {
     const uint64_t items = n / SS_CHUNK + (uint64_t)nseg + 1;
-    return al256(nseg * sizeof(SegState)) + al256((size_t)4 * nseg * 256 * 4) + al256(nseg * 8) * 2 +
-           al256(nseg * 4) + al256(items * 4) * 6 + al256(items * 8) * 3 + 256;
+    return al256(nseg * sizeof(SegState)) + al256((size_t)4 * nseg * 256 * 4) + al256((nseg + 1) * 8) * 2 +
+           al256(nseg * 4) + al256(items * 4) * 6 + al256(items * 8) * 3 + al256(items * (SS_THREADS / 32) * 4) * 2 +
+           256;
+}
+
+// The work-item tables of a segment layout, uploaded once per (workspace,
+// layout): a steady training loop calls with the same layer offsets and keep
+// counts every step, and then only the launches are issued.
+struct SegLayout {
+    uint64_t n = 0;
+    int kind = -1;
+    std::vector<uint64_t> off, k;
+    int nitems = 0;
+};
+static std::mutex g_seg_mu;
+static std::unordered_map<const void *, SegLayout> g_seg_layouts;
+
+void segsel_forget(const void *ws)
+{
+    std::lock_guard<std::mutex> lk(g_seg_mu);
+    g_seg_layouts.erase(ws);
 }
 
 int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
                uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
                uint32_t *status, cudaStream_t s)
 {
-    // host: the work items and the segment table
-    std::vector<uint32_t> iseg, ilen, sfirst(nseg, 0);
-    std::vector<uint64_t> ilo, slo(nseg), sk(nseg);
-    std::vector<SegState> sst(nseg);
     for (int q = 0; q < nseg; q++) {
         const uint64_t a = seg_off[q], b = seg_off[q + 1];
         if (b < a || b > n)
             return set_error(GVC_ERR_ARG, "segmented select: segment %d [%llu, %llu) outside [0, %llu)", q,
                              (unsigned long long)a, (unsigned long long)b, (unsigned long long)n);
-        slo[q] = a;
-        sk[q] = seg_k[q];
-        sst[q].prefix = 0;
-        sst[q].all = (b - a == 0) || seg_k[q] >= b - a;
-        sst[q].need = seg_k[q];
         if (b - a && seg_k[q] < 1)
             return set_error(GVC_ERR_ARG, "segmented select: keep count 0 in segment %d", q);
-        sfirst[q] = (uint32_t)iseg.size();
-        for (uint64_t c = a; c < b; c += SS_CHUNK) {
-            iseg.push_back((uint32_t)q);
-            ilo.push_back(c);
-            ilen.push_back((uint32_t)(b - c < SS_CHUNK ? b - c : SS_CHUNK));
-        }
     }
-    const int nitems = (int)iseg.size();
-    if (nitems == 0)
-        return GVC_OK;
     if (segsel_workspace_bytes(n, nseg) > ws_bytes)
         return set_error(GVC_ERR_WORKSPACE, "segmented select workspace too small");
+    std::lock_guard<std::mutex> lk(g_seg_mu);
+    SegLayout &L = g_seg_layouts[ws];
+    const bool same = L.n == n && L.kind == kind && (int)L.k.size() == nseg &&
+                      std::equal(L.off.begin(), L.off.end(), seg_off) && std::equal(L.k.begin(), L.k.end(), seg_k);
+    int nitems = L.nitems;
+    std::vector<uint32_t> iseg, ilen, sfirst;
+    std::vector<uint64_t> ilo;
+    if (!same) {
+        sfirst.assign(nseg, 0);
+        for (int q = 0; q < nseg; q++) {
+            sfirst[q] = (uint32_t)iseg.size();
+            for (uint64_t c = seg_off[q]; c < seg_off[q + 1]; c += SS_CHUNK) {
+                iseg.push_back((uint32_t)q);
+                ilo.push_back(c);
+                ilen.push_back((uint32_t)(seg_off[q + 1] - c < SS_CHUNK ? seg_off[q + 1] - c : SS_CHUNK));
+            }
+        }
+        nitems = (int)iseg.size();
+    }
+    if (nitems == 0)
+        return GVC_OK;
     char *w = (char *)ws;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -320,8 +425,8 @@ int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_of
     P.stream = stream;
     P.seg = (SegState *)take(nseg * sizeof(SegState));
     P.hist = (uint32_t *)take((size_t)4 * nseg * 256 * 4);
-    P.seg_lo = (const uint64_t *)take(nseg * 8);
-    P.seg_k = (const uint64_t *)take(nseg * 8);
+    P.seg_lo = (const uint64_t *)take((nseg + 1) * 8);
+    P.seg_k = (const uint64_t *)take((nseg + 1) * 8);
     P.item_seg = (const uint32_t *)take(nitems * 4);
     P.item_len = (const uint32_t *)take(nitems * 4);
     P.item_gt = (uint32_t *)take(nitems * 4);
@@ -331,25 +436,44 @@ int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_of
     P.item_out = (unsigned long long *)take(nitems * 8);
     P.item_E = (unsigned long long *)take(nitems * 8);
     P.seg_first = (const uint32_t *)take(nseg * 4);
+    P.warp_gt = (uint32_t *)take((size_t)nitems * (SS_THREADS / 32) * 4);
+    P.warp_eq = (uint32_t *)take((size_t)nitems * (SS_THREADS / 32) * 4);
     P.status = status;
-    cudaMemcpyAsync(P.seg, sst.data(), nseg * sizeof(SegState), cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync((void *)P.seg_lo, slo.data(), nseg * 8, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync((void *)P.seg_k, sk.data(), nseg * 8, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync((void *)P.item_seg, iseg.data(), nitems * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync((void *)P.item_len, ilen.data(), nitems * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync((void *)P.item_lo, ilo.data(), nitems * 8, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync((void *)P.seg_first, sfirst.data(), nseg * 4, cudaMemcpyHostToDevice, s);
+    if (!same) {
+        // (pageable host vectors: the copies complete before the calls return)
+        cudaMemcpyAsync((void *)P.seg_lo, seg_off, (nseg + 1) * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync((void *)P.seg_k, seg_k, nseg * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync((void *)P.item_seg, iseg.data(), nitems * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync((void *)P.item_len, ilen.data(), nitems * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync((void *)P.item_lo, ilo.data(), nitems * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync((void *)P.seg_first, sfirst.data(), nseg * 4, cudaMemcpyHostToDevice, s);
+        L.n = n;
+        L.kind = kind;
+        L.off.assign(seg_off, seg_off + nseg + 1);
+        L.k.assign(seg_k, seg_k + nseg);
+        L.nitems = nitems;
+    }
     cudaMemsetAsync(P.hist, 0, (size_t)4 * nseg * 256 * 4, s);
-    // (the host vectors are pageable: the copies complete before the calls return)
+    k_ss_init<<<(nseg + 255) / 256, 256, 0, s>>>(P);
     const int rgrid = (nseg + SS_THREADS / 32 - 1) / (SS_THREADS / 32);
+    const bool hash = P.keymode == KEY_HASH;
     for (int d = 0; d < 4; d++) {
-        k_ss_hist<<<nitems, SS_THREADS, 0, s>>>(P, d);
+        if (hash)
+            k_ss_hist<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P, d);
+        else
+            k_ss_hist<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P, d);
         k_ss_resolve<<<rgrid, SS_THREADS, 0, s>>>(P, d);
     }
-    k_ss_count<<<nitems, SS_THREADS, 0, s>>>(P);
+    if (hash)
+        k_ss_count<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P);
+    else
+        k_ss_count<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P);
     k_ss_scan<<<1, 1024, 0, s>>>(P);
-    k_ss_write<<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
-    count_launches(11);
+    if (hash)
+        k_ss_write<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
+    else
+        k_ss_write<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
+    count_launches(12);
     return GVC_OK;
 }
 

@@ -1918,6 +1918,7 @@ struct GraphEntry {
     int launches;
     Plan last;  // the plan the nodes currently hold
     bool has_last = false;
+    const void *ws = nullptr;  // the workspace the graph's plans point into
 };
 static std::unordered_map<std::string, GraphEntry> g_graphs;
 
@@ -2057,6 +2058,7 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
             }
             ce = cudaGraphInstantiate(&ge.exec, graph, 0);
             ge.graph = graph;  // kept alive: the exec-node updates name its nodes
+            ge.ws = ws;
             if (ce != cudaSuccess)
                 return set_error(GVC_ERR_CUDA, "select graph instantiate: %s", cudaGetErrorString(ce));
             it = g_graphs.emplace(key, std::move(ge)).first;
@@ -2091,6 +2093,22 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     std::lock_guard<std::mutex> lk(g_mu);
     g_plans[ws] = p;
     return GVC_OK;
+}
+
+// gvc_workspace_forget: the select's per-workspace state (graphs, plan)
+void select_forget(const void *ws)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_plans.erase(ws);
+    for (auto it = g_graphs.begin(); it != g_graphs.end();) {
+        if (it->second.ws == ws) {
+            cudaGraphExecDestroy(it->second.exec);
+            cudaGraphDestroy(it->second.graph);
+            it = g_graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
 }
 
 int select_phase_times(void *ws, unsigned long long *out, int n)
