@@ -82,7 +82,10 @@ typedef struct {
     float *resid_dev;             /* EF mode residual in, g_ef out                          */
     uint64_t ks[GVC_MAX_LADDER];  /* keep counts, non-increasing, each in [1, n)            */
     uint64_t seed;                /* SeededRng.seed   (gradcore.py:139-142)                 */
-    uint64_t rng_stream;          /* SeededRng.stream (after split)                         */
+    uint64_t rng_stream;          /* SeededRng.stream (after split).  Random-k keeps the k
+                                     positions i with the smallest hash h(i) = word (i & 3)
+                                     of Philox4x32-10 at counter (i >> 2, rng_stream), key
+                                     seed (i = pos_base + position), ties to the lower index */
     uint64_t pos_base;            /* hash counter offset (layerwise segments)               */
     double dgc_sample_fraction;   /* CompressorKind.dgc_sample_fraction (compressors.py:36) */
     int32_t force_exact;          /* 1: skip the threshold estimate (every value is a candidate);
@@ -236,7 +239,8 @@ GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, u
 /* ---- layerwise compression (compressors.py:204-217) as one segmented selection ----
  * Segment q = [seg_offsets[q], seg_offsets[q + 1]) keeps seg_k[q] entries
  * (keep_count of its length) by the compressor's key -- |v| for Top-k, the
- * Philox position hash of the global position for Random-k -- ties to the
+ * Philox position hash h(i) of the global position for Random-k (as in
+ * gvc_select_args.rng_stream) -- ties to the
  * lower index; out = the segments' (global index, value) lists concatenated
  * in segment order (sum seg_k entries; a segment with seg_k >= its length
  * keeps everything).  seg_offsets / seg_k are HOST arrays.  Every segment is

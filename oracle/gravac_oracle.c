@@ -62,6 +62,16 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
+uint32_t orc_randomk_hash(uint64_t seed, uint64_t stream, uint64_t i)
+{
+    uint64_t q = i >> 2;
+    uint32_t ctr[4] = {(uint32_t)q, (uint32_t)(q >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    orc_philox4x32_10(ctr, key, out);
+    return out[i & 3];
+}
+
 uint32_t orc_position_hash(uint64_t seed, uint64_t stream, uint64_t i)
 {
     uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(i >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
@@ -440,7 +450,7 @@ int orc_select(int kind, const float *values, uint64_t n, uint64_t k,
         if (!hk)
             return ORC_ERR_NOMEM;
         for (uint64_t i = 0; i < n; i++)
-            hk[i] = ~orc_position_hash(seed, stream, pos_base + i);
+            hk[i] = ~orc_randomk_hash(seed, stream, pos_base + i);
         rc = orc_select_keys(hk, n, k, out_idx);
         free(hk);
     } else {

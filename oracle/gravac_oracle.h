@@ -48,8 +48,11 @@ int orc_get_threads(void);
 
 void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 
-/* Counter-based position hash used by Random-k and the DGC sample:
- * ctr = (lo(i), hi(i), lo(stream), hi(stream)), key = (lo(seed), hi(seed)) -> out[0]. */
+/* Counter-based position hash of the DGC sample:
+ * ctr = (lo(i), hi(i), lo(stream), hi(stream)), key = (lo(seed), hi(seed)) -> out[0].
+ * Random-k's key of position i: out[i & 3] at ctr = (lo(i >> 2), hi(i >> 2), lo(stream),
+ * hi(stream)) -- one Philox evaluation per four consecutive positions. */
+uint32_t orc_randomk_hash(uint64_t seed, uint64_t stream, uint64_t i);
 void orc_dgc_sample_positions(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
                               uint32_t *out);
 uint32_t orc_position_hash(uint64_t seed, uint64_t stream, uint64_t i);

@@ -45,6 +45,8 @@ def lib():
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_position_hash.argtypes = [u64, u64, u64]
         L.orc_position_hash.restype = ctypes.c_uint32
+        L.orc_randomk_hash.argtypes = [u64, u64, u64]
+        L.orc_randomk_hash.restype = ctypes.c_uint32
         L.orc_ef_add.argtypes = [vp, vp, vp, u64]
         L.orc_sq_norm.argtypes = [vp, u64]
         L.orc_sq_norm.restype = dbl
@@ -117,7 +119,13 @@ def philox4x32_10(ctr, key) -> np.ndarray:
 
 
 def position_hash(seed: int, stream: int, i: int) -> int:
+    """Philox4x32-10 word 0 at counter (i, stream): the DGC sample's draw."""
     return int(lib().orc_position_hash(seed & _MASK64, stream & _MASK64, i))
+
+
+def randomk_hash(seed: int, stream: int, i: int) -> int:
+    """Random-k's hash of position i: word (i & 3) of Philox4x32-10 at counter (i >> 2, stream)."""
+    return int(lib().orc_randomk_hash(seed & _MASK64, stream & _MASK64, i))
 
 
 # ------------------------------------------------------------------- dense

@@ -76,11 +76,45 @@ __device__ __forceinline__ uint32_t philox_x0(uint64_t i, uint64_t stream, uint6
     return c0;
 }
 
-// Random-k / DGC-sample selection key: the k SMALLEST hashes win, so the key
-// (larger wins) is the bitwise complement.
+// All four output words of Philox4x32-10 at counter (lo i, hi i, lo stream,
+// hi stream).
+__device__ __forceinline__ uint4 philox4(uint64_t i, uint64_t stream, uint64_t seed)
+{
+    uint32_t c0 = (uint32_t)i, c1 = (uint32_t)(i >> 32), c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        if (r > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// Random-k selection key of position pos: word (pos & 3) of Philox4x32-10 at
+// counter (pos >> 2, stream) -- one Philox evaluation serves four consecutive
+// positions.  The k SMALLEST hashes win, so the key (larger wins) is the
+// bitwise complement.
 __device__ __forceinline__ uint32_t hash_key(uint64_t pos, uint64_t stream, uint64_t seed)
 {
-    return ~philox_x0(pos, stream, seed);
+    const uint4 h = philox4(pos >> 2, stream, seed);
+    const uint32_t w = (uint32_t)pos & 3u;
+    return ~(w == 0 ? h.x : w == 1 ? h.y : w == 2 ? h.z : h.w);
+}
+
+// The keys of positions 4q .. 4q + 3 from one evaluation.
+__device__ __forceinline__ uint4 hash_key4(uint64_t pos4, uint64_t stream, uint64_t seed)
+{
+    const uint4 h = philox4(pos4 >> 2, stream, seed);
+    return make_uint4(~h.x, ~h.y, ~h.z, ~h.w);
 }
 
 __device__ __forceinline__ double warp_sum_f64(double v)

@@ -407,9 +407,20 @@ __device__ __forceinline__ void push4(const Plan &p, const float (&v)[4], uint32
 {
     uint32_t key[4], m[4];
     bool pr[4];
+    if (KM == KEY_HASH && valid == 4u && ((p.pos_base + pos) & 3u) == 0) {
+        // four consecutive positions: one Philox evaluation (hash_key4)
+        const uint4 h = hash_key4(p.pos_base + pos, p.stream, p.seed);
+        key[0] = h.x;
+        key[1] = h.y;
+        key[2] = h.z;
+        key[3] = h.w;
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+            key[c] = cand_key<KM>(p, v[c], pos + c);
+    }
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-        key[c] = cand_key<KM>(p, v[c], pos + c);
         pr[c] = ((uint32_t)c < valid) & (key[c] >= key_est);
         m[c] = __ballot_sync(0xffffffffu, pr[c]);
     }

@@ -149,7 +149,7 @@ def test_randomk_properties():
     assert a.size == 100 and np.array_equal(a, b) and not np.array_equal(a, c)
     assert np.array_equal(va, x[a])
     # the sampler is exactly "k smallest position hashes, ties to the lower index"
-    h = np.array([O.position_hash(5, 0, i) for i in range(1000)], dtype=np.uint64)
+    h = np.array([O.randomk_hash(5, 0, i) for i in range(1000)], dtype=np.uint64)
     order = np.lexsort((np.arange(1000), h))[:100]
     assert np.array_equal(np.sort(order).astype(np.uint32), a)
 
