@@ -478,14 +478,12 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p)
 }
 
 // Staged pull (C1 + K7 overlapped): the first `ncopy` CTAs of the merge grid
-// to start (staged_ticket) are copiers.  They wait for every peer's payload
+// (by block index, or by start order with GVC_STAGED_TICKET) are copiers.  They wait for every peer's payload
 // flag, then stream the peers' (idx, vals) chunk by chunk over NVLink into
 // local staging slots and publish each chunk with a release store of the
 // epoch into ready[chunk].  The remaining CTAs are the usual tiles; a tile
 // waits only for the chunks its entries fall in, so the merge trails the
-// transfer instead of following it.  Roles follow the start order, so a
-// spinning tile never holds the slot a copier still needs; every wait is
-// bounded besides (wait_epoch).
+// transfer instead of following it.  Every wait is bounded (wait_epoch).
 struct Staged {
     int ncopy;           // copier CTAs (0: direct pull, no staging)
     int self;            // this rank's part (already local)
@@ -695,8 +693,19 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
 // -- block indices carry no such guarantee (CTAs may be dispatched in any
 // order, and SMs can be held by other work).  The last ticket resets the
 // counter for the next exchange (stream-ordered).
+// GVC_STAGED_TICKET=1: roles by the dispatch-order ticket.  Measured at N = 4
+// (ResNet101 44.5M, scripts/ab_n4.sh): median step 0.425 ms vs 0.390 with
+// block-index roles, and tail steps up to 0.9 ms -- ~11K CTAs take the same
+// atomic -- so the default keeps block-index roles: the low-index copiers are
+// dispatched first in practice, and every wait is bounded, so an unlucky
+// schedule costs a timeout error, not a hung GPU.
+#ifndef GVC_STAGED_TICKET
+#define GVC_STAGED_TICKET 0
+#endif
 __device__ __forceinline__ uint32_t staged_ticket(const Staged &st)
 {
+    if (!GVC_STAGED_TICKET)
+        return blockIdx.x;
     __shared__ uint32_t s_vb;
     if (threadIdx.x == 0) {
         const uint32_t t = atomicAdd(st.ticket, 1u);

@@ -2172,12 +2172,20 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
             cudaFuncSetAttribute(k_emit<KEY_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_DGC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_MAG, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(k_emit<KEY_DGC, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(k_emit<KEY_HASH, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         }
         lk.unlock();
         const bool lean = !idx_map && !resid && mir.n == 0 && !stats && p.kind != GVC_REDSYNC;
         if (p.keymode == KEY_MAG && lean)
             k_emit<KEY_MAG, true, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
                                                                              smask, sm_out, tile_b, mir, 0);
+        else if (p.keymode == KEY_DGC && lean)
+            k_emit<KEY_DGC, true, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
+                                                                             smask, sm_out, tile_b, mir, 0);
+        else if (p.keymode == KEY_HASH && lean)
+            k_emit<KEY_HASH, true, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
+                                                                              smask, sm_out, tile_b, mir, 0);
         else if (p.keymode == KEY_MAG)
             k_emit<KEY_MAG, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
                                                                        sm_out, tile_b, mir, stats != nullptr);
