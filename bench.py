@@ -342,9 +342,14 @@ def north_star(args, G, nat, O, dev):
     def step():
         return G.run_iteration(state, G.GradientVector._wrap(gbuf), store, cost, rng, extra_cfs=extra,
                                average=True, average_out=avg)
-    for _ in range(3):
+    snap_bufs = None
+    for w in range(3):
         gbuf.normal_(generator=gen)
         step()
+        if w == 0:  # snapshot buffers taken during warm-up (see run_ours)
+            snap_bufs = [torch.empty_like(gbuf), torch.empty_like(store._resid),
+                         None if store._mask is None else torch.empty_like(store._mask),
+                         None if store._pm is None else torch.empty_like(store._pm)]
     torch.cuda.synchronize()
     # select / collect: CUDA event-record nodes inside the real step's select graph
     nat.load().gvc_prof_enable(2)
@@ -358,8 +363,9 @@ def north_star(args, G, nat, O, dev):
     for s in range(n):
         gbuf.normal_(generator=gen)
         if s == n - 1:
-            snap_in = (gbuf.clone(), store._resid.clone(), None if store._mask is None else store._mask.clone(),
-                       None if store._pm is None else store._pm.clone(), int(store._pmode))
+            src = (gbuf, store._resid, store._mask, store._pm)
+            snap_in = tuple(None if t is None else (t.clone() if d is None else d.copy_(t))
+                            for t, d in zip(src, snap_bufs)) + (int(store._pmode),)
         torch.sum(flush, dim=0, out=flush_out)
         ev[s][0].record()
         res = step()
@@ -459,10 +465,20 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region (re-enabled right after)
     res = None
+    snap_bufs = g_snap = None
     for w in range(args.warmup):
         g = fresh()
         cool()
         res, _ = step(g)
+        if w == 0:
+            # the last timed step's inputs are snapshotted into buffers allocated
+            # here, during warm-up: allocated after it, they took blocks the next
+            # step's outputs needed, and that step paid a cudaMalloc (~0.7 ms
+            # stall at 11.7M, measured)
+            snap_bufs = (torch.empty_like(store._resid),
+                         torch.empty_like(store._mask) if store._mask is not None else None,
+                         torch.empty_like(store._pm) if store._pm is not None else None)
+            g_snap = torch.empty_like(gbuf)
     torch.cuda.synchronize()
     if pg is not None:
         dist.barrier()
@@ -486,10 +502,6 @@ def run_ours(args, M, theta_min, theta_s, extra, desc):
             out = tuple(None if t is None else (t.clone() if d is None else d.copy_(t)) for t, d in zip(src, into))
         return out + (int(store._pmode),)
 
-    # the last timed step's inputs are snapshotted into buffers allocated here
-    snap_bufs = (torch.empty_like(store._resid), torch.empty_like(store._mask) if store._mask is not None else None,
-                 torch.empty_like(store._pm) if store._pm is not None else None)
-    g_snap = torch.empty_like(gbuf)
     launches0 = nat.launch_count()
     clocks.mark("t0")
     snap_in = None

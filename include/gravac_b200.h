@@ -257,6 +257,15 @@ GVC_API size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg);
 /* Drop every per-workspace cache entry (select graphs and plans, segment
  * tables) for `ws` before its memory is freed or reused. */
 GVC_API int gvc_workspace_forget(void *ws);
+
+/* The controller's one read-back per step, started without host stream
+ * bookkeeping: once `stream` reaches this point, copy `bytes` from dev_src to
+ * (pinned) host_dst on side_stream.  events[2] (ready, done) are created on
+ * first use and reused; gvc_event_done(events[1]) polls completion (1 done,
+ * 0 not yet, < 0 error). */
+GVC_API int gvc_read_async(void *host_dst, const void *dev_src, size_t bytes, void *stream, void *side_stream,
+                           void **events);
+GVC_API int gvc_event_done(void *event);
 GVC_API int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                                  const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream,
                                  uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev, size_t ws_bytes,

@@ -31,7 +31,7 @@ EXPORTS = (
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
     "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
-    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget",
+    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget", "gvc_read_async", "gvc_event_done",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -141,6 +141,8 @@ def load(build_if_missing: bool = False):
         L.gvc_segmented_select_workspace_bytes.argtypes = [_u64, ctypes.c_int]
         L.gvc_segmented_select_workspace_bytes.restype = _sz
         L.gvc_workspace_forget.argtypes = [_vp]
+        L.gvc_read_async.argtypes = [_vp, _vp, _sz, _vp, _vp, _vp]
+        L.gvc_event_done.argtypes = [_vp]
         L.gvc_segmented_select.argtypes = [ctypes.c_int, _vp, _u64, _vp, _vp, ctypes.c_int, _u64, _u64, _vp, _vp,
                                            _vp, _sz, _vp, _vp]
         L.gvc_aggregate_peers_staged.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32,
@@ -287,8 +289,12 @@ class PendingRead:
         self.host, self.ev, self.src = host, ev, src
 
     def wait(self) -> bytes:
-        while not self.ev.query():
-            pass
+        done = load().gvc_event_done
+        while True:
+            r = done(self.ev)
+            if r:
+                break
+        check(r if r < 0 else 0, "read-back")
         self.src = None
         return self.host.numpy().tobytes()
 
@@ -302,23 +308,18 @@ def d2h_start(t: torch.Tensor, ready: "torch.cuda.Event | None" = None) -> Pendi
     key = ("async", t.device.index, nb)
     buf = _pinned.get(key)
     if buf is None:
-        buf = (torch.empty(nb, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+        # (ready, done) events, created by the library on first use
+        buf = (torch.empty(nb, dtype=torch.uint8, pin_memory=True), (ctypes.c_void_p * 2)())
         _pinned[key] = buf
-    host, ev = buf
+    host, evs = buf
     side = side_stream(t.device)
-    if ready is None:
-        # one reusable marker per device: the side stream's wait on it is
-        # enqueued before the next record can happen
-        rkey = ("ready", t.device.index)
-        ready = _pinned.get(rkey)
-        if ready is None:
-            ready = _pinned[rkey] = torch.cuda.Event()
-        ready.record()
-    side.wait_event(ready)
-    with torch.cuda.stream(side):
-        host.copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
-        ev.record()
-    return PendingRead(host, ev, t)
+    if ready is not None:
+        side.wait_event(ready)
+    # one C call: no torch stream bookkeeping (tens of microseconds of host time
+    # per torch stream / event call in this build)
+    check(load().gvc_read_async(ctypes.c_void_p(host.data_ptr()), ctypes.c_void_p(t.data_ptr()), nb,
+                                stream_ptr(t.device), ctypes.c_void_p(side.cuda_stream), evs), "read_async")
+    return PendingRead(host, ctypes.c_void_p(evs[1]), t)
 
 
 def read_result(res_dev: torch.Tensor) -> SelectResult:

@@ -583,6 +583,7 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
             rows = allgather_stats(flat.cpu(), group)
     else:
         pending = nat.d2h_start(flat)
+    _mark("stats_started")
 
     # ---- speculative emit: enqueue the previous step's choice right behind the
     # select so the GPU keeps working while the host reads the gains back; a

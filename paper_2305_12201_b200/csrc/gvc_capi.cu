@@ -367,6 +367,31 @@ int gvc_aggregate_dense(const float *parts, int nparts, uint64_t n, float *out, 
 
 size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg) { return segsel_workspace_bytes(n, nseg); }
 
+int gvc_read_async(void *host_dst, const void *dev_src, size_t bytes, void *stream, void *side_stream,
+                   void **events)
+{
+    if (!host_dst || !dev_src || !events || !side_stream)
+        return set_error(GVC_ERR_ARG, "gvc_read_async: bad arguments");
+    for (int e = 0; e < 2; e++)
+        if (!events[e] && cudaEventCreateWithFlags((cudaEvent_t *)&events[e], cudaEventDisableTiming) != cudaSuccess)
+            return set_error(GVC_ERR_CUDA, "gvc_read_async: event create");
+    cudaEventRecord((cudaEvent_t)events[0], STREAM(stream));
+    cudaStreamWaitEvent(STREAM(side_stream), (cudaEvent_t)events[0], 0);
+    cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, STREAM(side_stream));
+    cudaEventRecord((cudaEvent_t)events[1], STREAM(side_stream));
+    return check_launch("read_async");
+}
+
+int gvc_event_done(void *event)
+{
+    const cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+    if (e == cudaSuccess)
+        return 1;
+    if (e == cudaErrorNotReady)
+        return 0;
+    return set_error(GVC_ERR_CUDA, "gvc_event_done: %s", cudaGetErrorString(e));
+}
+
 int gvc_workspace_forget(void *ws)
 {
     if (!ws)
