@@ -256,14 +256,15 @@ def d2h_bytes(t: torch.Tensor) -> bytes:
     key = (t.device.index, nb)
     buf = _pinned.get(key)
     if buf is None:
-        buf = (torch.empty(nb, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+        buf = (torch.empty(nb, dtype=torch.uint8, pin_memory=True), (ctypes.c_void_p * 2)())
         _pinned[key] = buf
-    host, ev = buf
-    host.copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
-    ev.record()
-    while not ev.query():
-        pass
-    return host.numpy().tobytes()
+    host, evs = buf
+    if not t.is_contiguous():
+        t = t.contiguous()
+    s = stream_ptr(t.device)  # copied on the current stream itself
+    check(load().gvc_read_async(ctypes.c_void_p(host.data_ptr()), ctypes.c_void_p(t.data_ptr()), nb, s, s, evs),
+          "read")
+    return PendingRead(host, ctypes.c_void_p(evs[1]), t).wait()
 
 
 _side: dict = {}
@@ -312,6 +313,8 @@ def d2h_start(t: torch.Tensor, ready: "torch.cuda.Event | None" = None) -> Pendi
         buf = (torch.empty(nb, dtype=torch.uint8, pin_memory=True), (ctypes.c_void_p * 2)())
         _pinned[key] = buf
     host, evs = buf
+    if not t.is_contiguous():
+        t = t.contiguous()
     side = side_stream(t.device)
     if ready is not None:
         side.wait_event(ready)

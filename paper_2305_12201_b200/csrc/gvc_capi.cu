@@ -370,7 +370,7 @@ size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg) { return segse
 int gvc_read_async(void *host_dst, const void *dev_src, size_t bytes, void *stream, void *side_stream,
                    void **events)
 {
-    if (!host_dst || !dev_src || !events || !side_stream)
+    if (!host_dst || !dev_src || !events)  // (a NULL stream is the legacy default stream)
         return set_error(GVC_ERR_ARG, "gvc_read_async: bad arguments");
     for (int e = 0; e < 2; e++)
         if (!events[e] && cudaEventCreateWithFlags((cudaEvent_t *)&events[e], cudaEventDisableTiming) != cudaSuccess)
