@@ -276,3 +276,42 @@ def test_layerwise_edge_segments(G, kind):
             np.testing.assert_allclose(host(s.vals), ov, rtol=RTOL)
         else:
             assert np.array_equal(bits(host(s.vals)), bits(ov)), (kind, cf)
+
+
+def test_layerwise_layout_changes_on_one_workspace(G):
+    """The segmented select caches a layout's work tables per workspace: a
+    different layout of the same length and segment count, then the first one
+    again, then a workspace forgotten (gvc_workspace_forget) -- every call
+    bit-exact against the oracle."""
+    from paper_2305_12201_b200 import _native as nat
+    x = _gauss(300_007, 21)
+    layouts = [(0, 1000, 50_000, 200_000), (0, 7, 150_000, 250_000), (0, 1000, 50_000, 200_000)]
+    rng = G.SeededRng(2)
+    for q, offs in enumerate(layouts + layouts[:1]):
+        if q == 3:
+            ws = nat.Workspace.get(torch.device("cuda", 0), "segsel", 1)
+            nat.check(nat.load().gvc_workspace_forget(nat.ptr(ws)))
+        g = G.GradientVector(x, offs)
+        for kind in ("topk", "randomk"):
+            s, _ = G.compress(G.CompressorKind(kind), g, 10.0, rng, layerwise=True)
+            oi, ov, _ = O.compress(kind, x, 10.0, seed=rng.seed, stream=rng.stream, layer_offsets=offs,
+                                   layerwise=True)
+            assert np.array_equal(host(s.indices), oi), (q, kind)
+            assert np.array_equal(bits(host(s.vals)), bits(ov)), (q, kind)
+
+
+def test_select_after_workspace_forget(G):
+    """gvc_workspace_forget drops the select graphs and plan of a workspace;
+    the next select on it captures afresh and stays exact."""
+    from paper_2305_12201_b200 import _native as nat
+    from paper_2305_12201_b200.compressors import Selection
+    x = _gauss(1_000_003, 5)
+    xd = torch.from_numpy(x).cuda()
+    K = G.CompressorKind("topk")
+    for rep in range(3):
+        sel = Selection(K, [100_000, 10_000], values=xd, slot="forget")
+        for j, k in enumerate((100_000, 10_000)):
+            idx, vals = sel.emit(j)
+            oi = O.topk_indices(x, k)
+            assert np.array_equal(host(idx), oi), (rep, j)
+        nat.check(nat.load().gvc_workspace_forget(nat.ptr(sel.ws)))
