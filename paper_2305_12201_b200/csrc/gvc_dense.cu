@@ -536,9 +536,6 @@ __device__ __forceinline__ uint32_t *flag_err(const uint32_t *flags)
 #ifndef GVC_COPIER_TMA
 #define GVC_COPIER_TMA 0
 #endif
-#ifndef GVC_COPIER_PREFETCH
-#define GVC_COPIER_PREFETCH 0
-#endif
 __device__ void staged_copier(const Staged &st, const AggParts &parts, int nparts, const uint32_t *flags,
                               uint32_t epoch, uint32_t vb, void *sbuf = nullptr, uint32_t sbytes = 0)
 {
@@ -648,75 +645,6 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
         }
         return;
     }
-#if GVC_COPIER_PREFETCH
-    if (U * AGG_THREADS * 4 >= (1 << st.ch_log2)) {
-        // every (chunk, part) item is at most one U-row per thread: the next
-        // item's NVLink loads are issued before this chunk's fence, barrier and
-        // release, so the link stays busy across the publication
-        auto item = [&](uint32_t c, int q, uint32_t &lo4, uint32_t &hi4) -> bool {
-            const uint64_t lo = (uint64_t)c << st.ch_log2;
-            const uint64_t hi = min((unsigned long long)parts.cnt[q], (unsigned long long)(lo + (1ull << st.ch_log2)));
-            lo4 = (uint32_t)(lo >> 2);
-            hi4 = (uint32_t)((hi + 3) >> 2);
-            return q != st.self && lo < hi;
-        };
-        auto load = [&](uint32_t c, int q, int4 (&a)[U], int4 (&b)[U]) {
-            uint32_t lo4, hi4;
-            item(c, q, lo4, hi4);
-            const int4 *si = reinterpret_cast<const int4 *>(st.src_idx[q]);
-            const int4 *sv = reinterpret_cast<const int4 *>(st.src_val[q]);
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t i = lo4 + threadIdx.x + u * AGG_THREADS;
-                if (i < hi4) {
-                    a[u] = __ldcg(si + i);
-                    b[u] = __ldcg(sv + i);
-                }
-            }
-        };
-        // the first item at or after (c, q) in (chunk, part) order
-        auto next = [&](uint32_t &c, int &q) -> bool {
-            uint32_t lo4, hi4;
-            for (; c < st.nchunks; c += st.ncopy, q = 0)
-                for (; q < nparts; q++)
-                    if (item(c, q, lo4, hi4))
-                        return true;
-            return false;
-        };
-        int4 a[U], b[U];
-        uint32_t nc = vb;
-        int nq = 0;
-        bool have = next(nc, nq);
-        if (have)
-            load(nc, nq, a, b);
-        for (uint32_t c = vb; c < st.nchunks; c += st.ncopy) {
-            while (have && nc == c) {
-                uint32_t lo4, hi4;
-                item(nc, nq, lo4, hi4);
-                int4 *di = reinterpret_cast<int4 *>(const_cast<uint32_t *>(parts.idx[nq]));
-                int4 *dv = reinterpret_cast<int4 *>(const_cast<float *>(parts.vals[nq]));
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const uint32_t i = lo4 + threadIdx.x + u * AGG_THREADS;
-                    if (i < hi4) {
-                        __stcg(di + i, a[u]);
-                        __stcg(dv + i, b[u]);
-                    }
-                }
-                nq++;
-                have = next(nc, nq);
-                if (have)
-                    load(nc, nq, a, b);  // in flight across the publication below
-            }
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0)
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + st.ncopy + c), "r"(epoch)
-                             : "memory");
-        }
-        return;
-    }
-#endif
     for (uint32_t c = vb; c < st.nchunks; c += st.ncopy) {
         for (int q = 0; q < nparts; q++) {
             if (q == st.self)
