@@ -266,6 +266,10 @@ GVC_API int gvc_workspace_forget(void *ws);
 GVC_API int gvc_read_async(void *host_dst, const void *dev_src, size_t bytes, void *stream, void *side_stream,
                            void **events);
 GVC_API int gvc_event_done(void *event);
+/* Stream ordering without host-side stream objects: record *event (created on
+ * first use) on `stream`; make `stream` wait for `event`. */
+GVC_API int gvc_event_record(void **event, void *stream);
+GVC_API int gvc_stream_wait_event(void *stream, void *event);
 GVC_API int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                                  const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream,
                                  uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev, size_t ws_bytes,

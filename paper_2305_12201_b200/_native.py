@@ -31,7 +31,7 @@ EXPORTS = (
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
     "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
-    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget", "gvc_read_async", "gvc_event_done",
+    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget", "gvc_read_async", "gvc_event_done", "gvc_event_record", "gvc_stream_wait_event",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -143,6 +143,8 @@ def load(build_if_missing: bool = False):
         L.gvc_workspace_forget.argtypes = [_vp]
         L.gvc_read_async.argtypes = [_vp, _vp, _sz, _vp, _vp, _vp]
         L.gvc_event_done.argtypes = [_vp]
+        L.gvc_event_record.argtypes = [_vp, _vp]
+        L.gvc_stream_wait_event.argtypes = [_vp, _vp]
         L.gvc_segmented_select.argtypes = [ctypes.c_int, _vp, _u64, _vp, _vp, ctypes.c_int, _u64, _u64, _vp, _vp,
                                            _vp, _sz, _vp, _vp]
         L.gvc_aggregate_peers_staged.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32,
@@ -268,6 +270,17 @@ def d2h_bytes(t: torch.Tensor) -> bytes:
 
 
 _side: dict = {}
+_events: dict = {}
+
+
+def event_slot(device, name: str):
+    """A per-(device, name) slot holding a library-created cudaEvent_t
+    (gvc_event_record creates it on first use)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    slot = _events.get((idx, name))
+    if slot is None:
+        slot = _events[(idx, name)] = (ctypes.c_void_p * 1)()
+    return slot
 
 
 def side_stream(device) -> torch.cuda.Stream:

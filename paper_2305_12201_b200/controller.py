@@ -12,6 +12,8 @@ writes the chosen (index, value) list and leaves g_ef - sent in the residual.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -557,20 +559,17 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     flat = stats[0].reshape(-1).view(torch.uint8) if len(stats) == 1 else \
         torch.cat([t.reshape(-1).view(torch.uint8) for t in stats])
     pending = rows = None
+    c2_ready = None
     if group is not None:
         import torch.distributed as dist
         if dist.get_backend(group) == "nccl" and peer is not None:
-            # C2 on a side stream: the peer-memory exchange issues no other NCCL
-            # work this step, so the collective cannot be reordered against one
-            ready = torch.cuda.Event()
-            ready.record()
-            side = nat.side_stream(dev)
-            side.wait_event(ready)
-            with torch.cuda.stream(side):
-                gathered = torch.empty((dist.get_world_size(group), flat.numel()), dtype=torch.uint8, device=dev)
-                dist.all_gather_into_tensor(gathered, flat, group=group)
-                pending = nat.d2h_start(gathered)
-                _mark("c2_read", side)
+            # C2 on a side stream (the peer-memory exchange issues no other NCCL
+            # work this step, so the collective cannot be reordered against
+            # one), ordered after the select by an event recorded here; its host
+            # setup (~0.1 ms of torch / NCCL calls) is done after the speculative
+            # emit and exchange are enqueued, so the GPU never waits for it
+            c2_ready = nat.event_slot(dev, "c2_ready")
+            nat.check(nat.load().gvc_event_record(c2_ready, nat.stream_ptr(dev)), "event_record")
         elif dist.get_backend(group) == "nccl":
             # NCCL exchange: every collective of this communicator on one stream
             # (collectives on two streams may execute in different orders on
@@ -606,6 +605,14 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
     _mark("spec_emitted")
     spec_avg = _average(spec_parts, group, average_out, peer) if (average and spec_parts is not None) else None
     _mark("spec_averaged")
+    if c2_ready is not None:
+        side = nat.side_stream(dev)
+        nat.check(nat.load().gvc_stream_wait_event(ctypes.c_void_p(side.cuda_stream), c2_ready[0]), "stream_wait")
+        with torch.cuda.stream(side):
+            gathered = torch.empty((dist.get_world_size(group), flat.numel()), dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(gathered, flat, group=group)
+            pending = nat.d2h_start(gathered)
+            _mark("c2_read", side)
 
     if pending is not None:
         raw_all = pending.wait()

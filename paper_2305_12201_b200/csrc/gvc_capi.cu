@@ -382,6 +382,24 @@ int gvc_read_async(void *host_dst, const void *dev_src, size_t bytes, void *stre
     return check_launch("read_async");
 }
 
+int gvc_event_record(void **event, void *stream)
+{
+    if (!event)
+        return set_error(GVC_ERR_ARG, "gvc_event_record: null slot");
+    if (!*event && cudaEventCreateWithFlags((cudaEvent_t *)event, cudaEventDisableTiming) != cudaSuccess)
+        return set_error(GVC_ERR_CUDA, "gvc_event_record: event create");
+    cudaEventRecord((cudaEvent_t)*event, STREAM(stream));
+    return check_launch("event_record");
+}
+
+int gvc_stream_wait_event(void *stream, void *event)
+{
+    if (!event)
+        return set_error(GVC_ERR_ARG, "gvc_stream_wait_event: null event");
+    cudaStreamWaitEvent(STREAM(stream), (cudaEvent_t)event, 0);
+    return check_launch("stream_wait_event");
+}
+
 int gvc_event_done(void *event)
 {
     const cudaError_t e = cudaEventQuery((cudaEvent_t)event);
