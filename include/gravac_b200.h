@@ -270,6 +270,9 @@ GVC_API int gvc_event_done(void *event);
  * first use) on `stream`; make `stream` wait for `event`. */
 GVC_API int gvc_event_record(void **event, void *stream);
 GVC_API int gvc_stream_wait_event(void *stream, void *event);
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): a caller's
+ * host->device gradient upload without host-side stream objects. */
+GVC_API int gvc_copy_async(void *dst, const void *src, size_t bytes, void *stream);
 GVC_API int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                                  const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream,
                                  uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev, size_t ws_bytes,

@@ -392,6 +392,14 @@ int gvc_event_record(void **event, void *stream)
     return check_launch("event_record");
 }
 
+int gvc_copy_async(void *dst, const void *src, size_t bytes, void *stream)
+{
+    if (!dst || !src)
+        return set_error(GVC_ERR_ARG, "gvc_copy_async: null pointer");
+    cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, STREAM(stream));
+    return check_launch("copy_async");
+}
+
 int gvc_stream_wait_event(void *stream, void *event)
 {
     if (!event)
