@@ -103,7 +103,11 @@ typedef struct {
     int32_t allow_short;          /* with key_est_dev: if fewer than ks[0] candidates exist, keep
                                      them ALL (DGC overshoot, compressors.py:126-128) and report
                                      the shortfall in gvc_select_result.shortfall              */
-    int32_t reserved2;
+    /* 1: every nonzero |value| is the same (a Redsync level-1 output, ±m or
+     * 0: compressors.py:226-246 then orders by position alone) -- the order is
+     * "nonzero first, then the lower index", one pass without the tie path.
+     * Plain mode, one ladder entry, Top-k or Redsync, n + pos_base < 2^31. */
+    int32_t equal_magnitudes;
     /* DGC in one selection, both branches of compressors.py:123-137 (no host
      * decision): with dgc_thr_dev (the sampled threshold key, device u32) and
      * dgc_sampled_dev (bit i set = position i is in the threshold sample,

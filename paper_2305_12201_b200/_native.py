@@ -47,7 +47,7 @@ class SelectArgs(ctypes.Structure):
         ("dgc_sample_fraction", _f64),
         ("force_exact", _i32), ("pending_mode", _i32),
         ("pending_mask_dev", _vp), ("pending_m_dev", _vp),
-        ("key_est_dev", _vp), ("allow_short", _i32), ("reserved2", _i32),
+        ("key_est_dev", _vp), ("allow_short", _i32), ("equal_magnitudes", _i32),
         ("dgc_thr_dev", _vp), ("dgc_sampled_dev", _vp),
     ]
 

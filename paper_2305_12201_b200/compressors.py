@@ -130,7 +130,8 @@ class Selection:
                  rng: SeededRng | None = None, pos_base: int = 0, slot: str = "sel0",
                  force_exact: int = 0, pending=None, key_est: torch.Tensor | None = None,
                  allow_short: bool = False, persist_res: bool = False,
-                 dgc_thr: torch.Tensor | None = None, dgc_bits: torch.Tensor | None = None):
+                 dgc_thr: torch.Tensor | None = None, dgc_bits: torch.Tensor | None = None,
+                 equal_magnitudes: bool = False):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -157,6 +158,7 @@ class Selection:
         a.pos_base = pos_base
         a.dgc_sample_fraction = kind.dgc_sample_fraction
         a.force_exact = int(force_exact)
+        a.equal_magnitudes = 1 if equal_magnitudes else 0  # every nonzero |v| equal: position order
         if key_est is not None:  # forced candidate threshold (DGC), a device u32/i32 scalar
             a.key_est_dev = key_est.data_ptr()
             a.allow_short = 1 if allow_short else 0

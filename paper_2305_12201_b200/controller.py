@@ -246,7 +246,12 @@ class _WorkerStep:
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
             self._bounds1 = bounds
             if k2 < k1:
-                self.sel2 = Selection(kind, [k2], values=vals, rng=rng1, slot=slot + "b")
+                # a Redsync level 1 sends sign(v) * m: every nonzero level-1 value
+                # has magnitude m, so level 2 (compressors.py:226-246) orders by
+                # position alone -- equal_magnitudes skips the all-ties path
+                # (152 us of k_pass1 + 86 us of tie handling at 66M, measured)
+                self.sel2 = Selection(kind, [k2], values=vals, rng=rng1, slot=slot + "b",
+                                      equal_magnitudes=kind.name == "redsync")
 
     def stats_dev(self) -> list[torch.Tensor]:
         """Device tensors whose bytes the host reads once per iteration."""

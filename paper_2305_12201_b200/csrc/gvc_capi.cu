@@ -181,6 +181,11 @@ int gvc_select(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     if (a->dgc_thr_dev && (!a->dgc_sampled_dev || a->n_ks != 1 || a->key_est_dev || a->force_exact ||
                            a->kind == GVC_RANDOMK || a->kind == GVC_REDSYNC))
         return set_error(GVC_ERR_ARG, "dgc_thr_dev needs dgc_sampled_dev, one ladder entry and no forced threshold");
+    if (a->equal_magnitudes &&
+        (a->n_ks != 1 || !a->values_dev || a->g_dev || a->dgc_thr_dev || a->key_est_dev || a->pending_mask_dev ||
+         (a->kind != GVC_TOPK && a->kind != GVC_REDSYNC) || a->n + a->pos_base >= (1ull << 31) - 1))
+        return set_error(GVC_ERR_ARG, "equal_magnitudes needs plain mode, one ladder entry, Top-k or Redsync and "
+                                      "n + pos_base < 2^31 - 1");
     if (a->allow_short && (!a->key_est_dev || a->n_ks != 1 || a->kind != GVC_TOPK))
         return set_error(GVC_ERR_ARG, "allow_short needs key_est_dev, one ladder entry and magnitude keys");
     if (a->n < 1 || a->n >= (1ull << 32))

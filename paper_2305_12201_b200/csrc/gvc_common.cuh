@@ -36,7 +36,9 @@ namespace gvc {
 
 // KEY_MAG: 31-bit |v|; KEY_HASH: Philox position hash (Random-k); KEY_DGC:
 // DGC's composite key (gvc_select_args.dgc_thr_dev), 32-bit.
-enum KeyMode { KEY_MAG = 0, KEY_HASH = 1, KEY_DGC = 2 };
+// KEY_POS: equal nonzero magnitudes (a Redsync level-1 output): nonzero first,
+// then lower position -- the magnitude order with its ties already broken
+enum KeyMode { KEY_MAG = 0, KEY_HASH = 1, KEY_DGC = 2, KEY_POS = 3 };
 
 // |x| as an order-preserving integer: clear the sign bit (-0 -> 0).  Monotone
 // for every non-NaN float; NaN keys are > 0x7f800000.

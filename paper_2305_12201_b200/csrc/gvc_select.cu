@@ -179,6 +179,8 @@ __device__ __forceinline__ uint32_t cand_key(const Plan &p, float v, uint32_t po
         const bool hi = m >= __ldg(p.dgc_thr) || ((__ldg(p.dgc_bits + (pos >> 5)) >> (pos & 31)) & 1u);
         return hi ? (0x80000000u | m) : m;
     }
+    if (KM == KEY_POS)  // equal nonzero magnitudes: nonzero first by position; zeros tie at key 0
+        return v != 0.f ? 0x80000000u | (0x7fffffffu - (uint32_t)(p.pos_base + pos)) : 0u;
     return hash_key(p.pos_base + pos, p.stream, p.seed);
 }
 
@@ -186,7 +188,7 @@ __device__ __forceinline__ uint32_t cand_key(const Plan &p, float v, uint32_t po
 template <int KM>
 __device__ __forceinline__ bool key_nan(uint32_t key)
 {
-    return KM != KEY_HASH && (key & 0x7fffffffu) > 0x7f800000u;
+    return KM != KEY_HASH && KM != KEY_POS && (key & 0x7fffffffu) > 0x7f800000u;
 }
 
 // Development probe (-DGVC_PHASE_STAMPS=1, scripts/phase_probe.py): per select
@@ -221,7 +223,7 @@ __device__ void sample_resolve_body(const Plan &p, unsigned long long *sh, int s
 template <int KM>
 __global__ void __launch_bounds__(1024) k_sample(const Plan p, int)
 {
-    constexpr int SHIFT = KM == KEY_DGC ? GVC_SAMPLE_SHIFT + 1 : GVC_SAMPLE_SHIFT;  // 32- / 31-bit keys
+    constexpr int SHIFT = (KM == KEY_DGC || KM == KEY_POS) ? GVC_SAMPLE_SHIFT + 1 : GVC_SAMPLE_SHIFT;  // 32- / 31-bit keys
     pdl_enter(); GVC_STAMP_IN(0);
     extern __shared__ uint32_t sh[];
     for (int i = threadIdx.x; i < GVC_SAMPLE_BINS; i += 1024)
@@ -1797,6 +1799,11 @@ static void launch_tail(const Plan &p, cudaStream_t s, bool pdl)
 {
     if constexpr (KM == KEY_DGC) {  // DGC picks one keep count at a time
         launch_tail_nb<KM, 1, false>(p, s, pdl);
+    } else if constexpr (KM == KEY_POS) {  // one keep count (a level-2 Redsync / Top-k pick)
+        if (p.kind == GVC_REDSYNC)
+            launch_tail_nb<KM, 1, true>(p, s, pdl);
+        else
+            launch_tail_nb<KM, 1, false>(p, s, pdl);
     } else {
         const bool abs_sums = p.kind == GVC_REDSYNC;
         switch (nb_for(p.n_ks)) {
@@ -1831,6 +1838,7 @@ static void set_attributes()
     done.push_back(dev);
     cudaFuncSetAttribute(k_sample<KEY_MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
     cudaFuncSetAttribute(k_sample<KEY_DGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
+    cudaFuncSetAttribute(k_sample<KEY_POS>, cudaFuncAttributeMaxDynamicSharedMemorySize, GVC_SAMPLE_BINS * 4);
 #define GVC_PASS1_ATTR(KM, NB, ABS)                                                                          \
     cudaFuncSetAttribute(k_pass1<KM, NB, ABS>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
                          (int)((NB + 1) * GVC_THREADS * (8 + (ABS ? 8 : 0) + 4)));
@@ -1842,6 +1850,8 @@ static void set_attributes()
     GVC_PASS1_ATTR_KM(KEY_MAG)
     GVC_PASS1_ATTR_KM(KEY_HASH)
     GVC_PASS1_ATTR(KEY_DGC, 1, false)
+    GVC_PASS1_ATTR(KEY_POS, 1, false)
+    GVC_PASS1_ATTR(KEY_POS, 1, true)
 }
 
 // The select pipeline on stream s; every kernel takes the plan by value (its
@@ -1870,7 +1880,7 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[0], s, cudaEventRecordExternal);
         const bool cpdl = pdl && !gprobes;
-        if (!p.ef)
+        if (KM == KEY_POS || !p.ef)  // (KEY_POS selections are plain mode: gvc_select checks)
             launch_k(k_collect<KM, false, 0>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
         else if (!p.pmask)
             launch_k(k_collect<KM, true, 0>, dim3(blocks), dim3(GVC_THREADS), 0, s, cpdl, p, 0);
@@ -1881,7 +1891,7 @@ static int launch_pipeline(const Plan &p, cudaStream_t s, bool probes, bool gpro
         if (gprobes)
             cudaEventRecordWithFlags(g_ev_mark[1], s, cudaEventRecordExternal);
     }
-    if (p.ef)
+    if (KM != KEY_POS && p.ef)
         launch_k(k_resolve0<KM, true>, dim3(1), dim3(1024), 0, s, pdl && !gprobes, p, 0);
     else
         launch_k(k_resolve0<KM, false>, dim3(1), dim3(1024), 0, s, pdl && !gprobes, p, 0);
@@ -1908,6 +1918,7 @@ static void enqueue_select(const Plan &p, cudaStream_t s, bool probes, int *laun
     cudaMemsetAsync(p.st, 0, (size_t)((char *)(p.histl + (size_t)nb_for(p.n_ks) * GVC_HL_BINS) - (char *)p.st), s);
     *launches = p.keymode == KEY_MAG   ? launch_pipeline<KEY_MAG>(p, s, probes, gprobes)
                 : p.keymode == KEY_DGC ? launch_pipeline<KEY_DGC>(p, s, probes, gprobes)
+                : p.keymode == KEY_POS ? launch_pipeline<KEY_POS>(p, s, probes, gprobes)
                                        : launch_pipeline<KEY_HASH>(p, s, probes, gprobes);
     if (gprobes)
         cudaEventRecordWithFlags(g_ev_mark[3], s, cudaEventRecordExternal);
@@ -1954,7 +1965,10 @@ int select_run(const gvc_select_args *a, void *ws, size_t ws_bytes, gvc_select_r
     p.n = a->n;
     p.n_ks = a->n_ks;
     p.kind = a->kind;
-    p.keymode = a->kind == GVC_RANDOMK ? KEY_HASH : (a->dgc_thr_dev ? KEY_DGC : KEY_MAG);
+    p.keymode = a->kind == GVC_RANDOMK ? KEY_HASH
+                : a->dgc_thr_dev         ? KEY_DGC
+                : a->equal_magnitudes    ? KEY_POS
+                                         : KEY_MAG;
     p.dgc_thr = a->dgc_thr_dev;
     p.dgc_bits = a->dgc_sampled_dev;
     p.ef = a->g_dev != nullptr;
@@ -2173,6 +2187,7 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
             cudaFuncSetAttribute(k_emit<KEY_DGC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_MAG, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_DGC, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(k_emit<KEY_POS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(k_emit<KEY_HASH, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         }
         lk.unlock();
@@ -2192,6 +2207,9 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
         else if (p.keymode == KEY_DGC)
             k_emit<KEY_DGC, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
                                                                        sm_out, tile_b, mir, stats != nullptr);
+        else if (p.keymode == KEY_POS)
+            k_emit<KEY_POS, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                       sm_out, tile_b, mir, stats != nullptr);
         else
             k_emit<KEY_HASH, true><<<blocks, GVC_THREADS, mbytes, s>>>(p, j, idx_map, out_idx, out_val, resid,
                                                                         smask, sm_out, tile_b, mir, stats != nullptr);
@@ -2201,6 +2219,9 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
                                                                    sm_out, tile_b, mir, stats != nullptr);
         else if (p.keymode == KEY_DGC)
             k_emit<KEY_DGC, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
+                                                                   sm_out, tile_b, mir, stats != nullptr);
+        else if (p.keymode == KEY_POS)
+            k_emit<KEY_POS, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,
                                                                    sm_out, tile_b, mir, stats != nullptr);
         else
             k_emit<KEY_HASH, false><<<blocks, GVC_THREADS, 0, s>>>(p, j, idx_map, out_idx, out_val, resid, smask,

@@ -608,3 +608,32 @@ def test_redsync_ladder_vs_oracle(G, dist, ladder):
         idx, vals = sel.emit(j)
         assert np.array_equal(host(idx), oi), (j, k)
         np.testing.assert_allclose(host(vals), ov, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("n", [1000, 300_007, 6_600_000])
+def test_equal_magnitudes_select_vs_oracle(G, n):
+    """gvc_select_args.equal_magnitudes (the level-2 pick over a Redsync level-1
+    output, +-m or 0): the same entries, values and gains as the magnitude
+    select, with zeros kept when fewer than k values are nonzero."""
+    from paper_2305_12201_b200.compressors import Selection
+    rs = np.random.default_rng(n)
+    m = np.float32(0.8125)
+    for zeros in (0.0, 0.3, 0.95):
+        x = np.where(rs.random(n) < 0.5, m, -m).astype(np.float32)
+        x[rs.random(n) < zeros] = 0.0
+        xd = torch.from_numpy(x).cuda()
+        for kind in ("redsync", "topk"):
+            for cf in (2.0, 10.0, 100.0):
+                k = G.keep_count(n, cf)
+                sel = Selection(G.CompressorKind(kind), [k], values=xd, slot="eqm", equal_magnitudes=True)
+                res = sel.result()
+                idx, vals = sel.emit(0)
+                oi, ov = O.select(kind, x, k)
+                assert np.array_equal(host(idx), oi), (kind, zeros, cf)
+                if kind == "redsync":
+                    np.testing.assert_allclose(host(vals), ov, rtol=GAIN_RTOL)
+                else:
+                    assert np.array_equal(bits(host(vals)), bits(ov)), (zeros, cf)
+                want_e = O.sq_norm(ov)
+                assert res.kept_sq[0] == pytest.approx(want_e, rel=GAIN_RTOL, abs=1e-30), (kind, zeros, cf)
+                assert res.kept_nonzero[0] == int(np.count_nonzero(ov)), (kind, zeros, cf)
