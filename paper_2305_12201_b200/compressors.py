@@ -131,7 +131,7 @@ class Selection:
                  force_exact: int = 0, pending=None, key_est: torch.Tensor | None = None,
                  allow_short: bool = False, persist_res: bool = False,
                  dgc_thr: torch.Tensor | None = None, dgc_bits: torch.Tensor | None = None,
-                 equal_magnitudes: bool = False):
+                 equal_magnitudes: bool = False, res_dev: torch.Tensor | None = None):
         src = values if values is not None else g
         nat.require_cuda(src)
         self.kind = kind
@@ -142,7 +142,9 @@ class Selection:
         self.ws = nat.select_workspace(self.device, slot, kind.kind_id, self.n)
         # persist_res: the slot's result buffer is reused (the controller reads
         # it back within the step), so an unchanged plan needs no graph update
-        self.res_dev = (nat.Workspace.get(self.device, slot + "/res", nat.RESULT_BYTES)[:nat.RESULT_BYTES]
+        # (res_dev: a caller's buffer, e.g. one of two adjacent records read back together)
+        self.res_dev = (res_dev if res_dev is not None else
+                        nat.Workspace.get(self.device, slot + "/res", nat.RESULT_BYTES)[:nat.RESULT_BYTES]
                         if persist_res else torch.empty(nat.RESULT_BYTES, dtype=torch.uint8, device=self.device))
         a = nat.SelectArgs()
         a.kind = kind.kind_id

@@ -234,7 +234,11 @@ class _WorkerStep:
                                   pending=pending, persist_res=True)
         else:
             self.ladder = [k1]
-            self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a", pending=pending)
+            # both levels' result records side by side: one read-back, no concatenation
+            rb = nat.RESULT_BYTES
+            self._res12 = nat.Workspace.get(g.device, slot + "/res12", 2 * rb)[:2 * rb]
+            self.sel1 = Selection(kind, [k1], g=g, resid=resid, rng=rng0, slot=slot + "a", pending=pending,
+                                  res_dev=self._res12[:rb])
             # the level-1 emit also builds its sent mask (every word, in the spare
             # buffer), the Redsync mean and the K7 tile bounds; taken if level 1 is sent
             self._mask1 = store._spare_buf()
@@ -251,11 +255,13 @@ class _WorkerStep:
                 # position alone -- equal_magnitudes skips the all-ties path
                 # (152 us of k_pass1 + 86 us of tie handling at 66M, measured)
                 self.sel2 = Selection(kind, [k2], values=vals, rng=rng1, slot=slot + "b",
-                                      equal_magnitudes=kind.name == "redsync")
+                                      equal_magnitudes=kind.name == "redsync", res_dev=self._res12[rb:])
 
     def stats_dev(self) -> list[torch.Tensor]:
         """Device tensors whose bytes the host reads once per iteration."""
         out = [self._norm_dev.reshape(1)] if self.identity1 else []
+        if self.sel1 is not None and self.sel2 is not None and getattr(self, "_res12", None) is not None:
+            return out + [self._res12]  # the two records, adjacent
         if self.sel1 is not None:
             out.append(self.sel1.res_dev)
         if self.sel2 is not None:
@@ -268,7 +274,8 @@ class _WorkerStep:
             import numpy as np
             norm_host = float(np.frombuffer(raw[0], dtype=np.float64)[0])
             raw = raw[1:]
-        results = [nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES]) for b in raw]
+        rb = nat.RESULT_BYTES
+        results = [nat.SelectResult.from_buffer_copy(b[o:o + rb]) for b in raw for o in range(0, len(b), rb)]
         STATS["fallbacks"] += sum(int(r.fallback_used) for r in results)
         r1 = results[0] if self.sel1 is not None else None
         r2 = results[-1] if self.sel2 is not None else None
