@@ -3,7 +3,8 @@ over NVLink, in ONE process (so ncu can replay it; a multi-rank job cannot be
 profiled).  GPU 0 merges its own part with the parts of GPUs 1..W-1, read
 through peer mappings; the peers' flags are pre-posted, so no kernel waits.
 
-    python scripts/nvlink_probe.py [W] [n] [cf]        (needs W GPUs)
+    python scripts/nvlink_probe.py [W] [n] [cf] [G]   (W parts on G GPUs, default G = W;
+                                                       parts 1.. round-robin over GPUs 1..G-1)
 
 Prints CUDA-event times of the direct pull and the staged pull (copier CTAs
 + trailing merge) and checks both against the C oracle's aggregate().
@@ -24,9 +25,16 @@ from paper_2305_12201_b200.exchange import Payload  # noqa: E402
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 44_500_000
 cf = float(sys.argv[3]) if len(sys.argv) > 3 else 10.0
+NG = int(sys.argv[4]) if len(sys.argv) > 4 else W
 k = int(n // cf)
 lib = nat.load()
-for d in range(1, W):
+
+
+def gpu_of(r):
+    return 0 if r == 0 else 1 + (r - 1) % (NG - 1)
+
+
+for d in range(1, NG):
     cudart.cudaSetDevice(0)
     cudart.cudaDeviceEnablePeerAccess(d, 0)
 torch.cuda.set_device(0)
@@ -36,7 +44,7 @@ for r in range(W):
     idx = np.sort(rs.choice(n, k, replace=False)).astype(np.uint32)
     vals = rs.standard_normal(k).astype(np.float32)
     parts.append((idx, vals))
-    dev = torch.device("cuda", r)
+    dev = torch.device("cuda", gpu_of(r))
     pl = Payload(k, n, dev, with_bounds=True)
     pl.idx[:k].copy_(torch.from_numpy(idx.view(np.int32)).to(dev).view(torch.uint32))
     pl.vals[:k].copy_(torch.from_numpy(vals).to(dev))
