@@ -197,7 +197,10 @@ def _gain_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gain_exchange_gloo_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_gain_exchange_gloo(world):
+    """C2 on gloo: every rank gets every rank's row in rank order and forms the
+    same worker-ordered mean (controller.py:284-288)."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s:
@@ -205,11 +208,14 @@ def test_gain_exchange_gloo_world2():
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gain_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gain_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(60)
-    assert out[0][1] == out[1][1] == [[10.0, 4.0, 1.0, 0.0], [11.0, 5.0, 2.0, 0.5]]
-    assert out[0][2] == out[1][2] == (0.4 + 5.0 / 11.0) / 2
+    want_rows = [[10.0 + r, 4.0 + r, 1.0 + r, 0.5 * r] for r in range(world)]
+    want_mean = sum(min(1.0, (4.0 + r) / (10.0 + r)) for r in range(world)) / world
+    for r in range(world):
+        assert out[r][1] == want_rows
+        assert out[r][2] == want_mean
