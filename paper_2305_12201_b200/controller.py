@@ -368,6 +368,7 @@ class _DgcStep:
         self.n = g.numel()
         self.identity1 = False
         self._res = []
+        self._res12 = None
         rng0 = rng.split(i, w, _STAGE_MIN)
         rng1 = rng.split(i, w, _STAGE_STEP)
         slot = f"dgc{w}"
@@ -390,16 +391,20 @@ class _DgcStep:
             # (+ the decompress-average's tile boundaries of level 1, its emit's by-product)
             nb = (self.n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1
             bounds = torch.empty(nb, dtype=torch.int32, device=g.device)  # owned by the sent part
+            # both levels' result records side by side: one read-back, no concatenation
+            rb = nat.RESULT_BYTES
+            self._res12 = nat.Workspace.get(g.device, slot + "/res12", 2 * rb)[:2 * rb]
             idx, vals, sel1 = dgc_select(kind, None, k1, rng0, g=g, resid=store._resid, pending=pending,
                                          slot=slot + "a", want_result=True, sent_mask=self._mask1, check=False,
-                                         tile_bounds=bounds)
+                                         tile_bounds=bounds, res_dev=self._res12[:rb])
             self.g_min = SparseGradient._wrap(idx, vals, self.n, self.n / k1)
             self.g_min._bounds = bounds
             self.norm = sel1.res_dev[:8].view(torch.float64)  # ||g_ef||^2 of the fused pass, on the device
             self._res.append(sel1.res_dev)
         if k2 < self.g_min.kept:
+            res2 = self._res12[nat.RESULT_BYTES:] if self._res12 is not None else None
             idx2, vals2, sel2 = dgc_select(kind, self.g_min.vals, k2, rng1, idx_map=self.g_min.indices,
-                                           slot=slot + "b", want_result=True, check=False)
+                                           slot=slot + "b", want_result=True, check=False, res_dev=res2)
             self.g_c = SparseGradient._wrap(idx2, vals2, self.n, self.n / k2)
             self._res.append(sel2.res_dev)
         else:
@@ -413,13 +418,17 @@ class _DgcStep:
         # exactly the values sent (no separate norm kernels)
 
     def stats_dev(self) -> list[torch.Tensor]:
+        if self.stats is None and len(self._res) == 2 and self._res12 is not None:
+            return [self._res12]  # the two levels' records, adjacent
         return ([self.stats] if self.stats is not None else []) + self._res
 
     def gains_from(self, raw: list[bytes], norm_host=None):
         import numpy as np
         recs = []
-        for b in raw[1 if self.stats is not None else 0:]:  # the DGC selects' records
-            r = nat.SelectResult.from_buffer_copy(b[:nat.RESULT_BYTES])
+        rb = nat.RESULT_BYTES
+        chunks = [b[o:o + rb] for b in raw[1 if self.stats is not None else 0:] for o in range(0, len(b), rb)]
+        for b in chunks:  # the DGC selects' records
+            r = nat.SelectResult.from_buffer_copy(b)
             if r.status == nat.GVC_ERR_NAN:
                 raise ValueError("NaN in gradient: compression order undefined")
             if r.status != nat.GVC_OK:

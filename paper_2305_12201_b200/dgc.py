@@ -34,7 +34,8 @@ from . import _native as nat
 def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0,
                idx_map: torch.Tensor | None = None, check: bool = True, *, g: torch.Tensor | None = None,
                resid: torch.Tensor | None = None, pending=None, slot: str = "dgc", want_result: bool = False,
-               sent_mask: torch.Tensor | None = None, tile_bounds: torch.Tensor | None = None):
+               sent_mask: torch.Tensor | None = None, tile_bounds: torch.Tensor | None = None,
+               res_dev: torch.Tensor | None = None):
     """(ascending indices, values) of the DGC selection of k entries.
 
     Plain mode: ``values``.  EF mode: ``g`` + ``resid`` (+ ``pending``): g_ef is
@@ -54,7 +55,8 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
     topk = CompressorKind("topk")
     s = min(n, max(256, int(round(kind.dgc_sample_fraction * n))))
     if s >= n:  # full sample: threshold estimation degenerates to exact selection (:113-115)
-        sel = Selection(topk, [k], values=values, g=g, resid=resid, pending=pending, slot=slot + "c")
+        sel = Selection(topk, [k], values=values, g=g, resid=resid, pending=pending, slot=slot + "c",
+                        res_dev=res_dev)
     else:
         # the sample's values and position bitmap in one pass (gvc_dgc_sample_gather)
         vP = torch.empty(s, dtype=torch.float32, device=dev)
@@ -74,7 +76,7 @@ def dgc_select(kind, values: torch.Tensor | None, k: int, rng, pos_base: int = 0
         else:  # the threshold is the smallest sampled magnitude
             thr = (vP.view(torch.int32) & 0x7FFFFFFF).min().reshape(1)
         sel = Selection(topk, [k], values=values, g=g, resid=resid, pending=pending, slot=slot + "c",
-                        dgc_thr=thr, dgc_bits=bits)
+                        dgc_thr=thr, dgc_bits=bits, res_dev=res_dev)
     idx, vals = sel.emit(0, idx_map=idx_map, sent_mask=sent_mask, tile_bounds=tile_bounds)
     if check:
         sel.result()  # raises ValueError on NaN
