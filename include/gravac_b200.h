@@ -258,6 +258,16 @@ GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, u
  * freed workspace's address while the library holds state for it (or call
  * gvc_workspace_forget first). */
 GVC_API size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg);
+/* Layerwise Redsync: after gvc_segmented_select in Top-k mode (the support),
+ * replace segment q's kept values vals_dev[out_off[q] .. out_off[q+1]) by
+ * sign(v) * fl32(mean_f64 |v|) of that segment (compressors.py:140-161,
+ * :187-189); a segment whose count reaches its length (seg_len[q]) is an
+ * identity pass-through (:172-173).  out_off: u64[nseg + 1] and seg_len:
+ * u64[nseg] are HOST arrays; the work is cut into 16384-entry items, two
+ * launches however unequal the segments. */
+GVC_API size_t gvc_segmented_redsync_workspace_bytes(uint64_t total_kept, int nseg);
+GVC_API int gvc_segmented_redsync_values(float *vals_dev, const uint64_t *out_off, const uint64_t *seg_len, int nseg,
+                                         void *ws_dev, size_t ws_bytes, void *stream);
 /* Drop every per-workspace cache entry (select graphs and plans, segment
  * tables) for `ws` before its memory is freed or reused. */
 GVC_API int gvc_workspace_forget(void *ws);

@@ -247,8 +247,10 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
     """compressors.py:204-217: per segment keep_count(len, cf) by the kind's
     rule, indices offset by the segment start, concatenated in order.  Top-k
     and Random-k: one segmented selection over every segment
-    (gvc_segmented_select); DGC and Redsync: one selection per segment,
-    enqueued back to back, statuses read once at the end."""
+    (gvc_segmented_select); Redsync: the same segmented Top-k support (F1)
+    then each segment's mean substitution (gvc_segmented_redsync_values);
+    DGC: one selection per segment, enqueued back to back, statuses read once
+    at the end."""
     n = values.numel()
     if kind.name in (RANDOMK, DGC) and rng is None:
         raise ValueError(f"{kind.name} compression requires an rng")
@@ -266,20 +268,29 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
         kk = (ctypes.c_uint64 * len(bounds))(*ks)
         # (segments are contiguous in GradientVector: each starts where the previous ended)
         contiguous = all(bounds[q].stop == bounds[q + 1].start for q in range(len(bounds) - 1))
-        lay = _LAYOUTS[key] = (bounds, ks, total, offs, kk, contiguous)
+        # per-segment output offsets and lengths (layerwise Redsync; host arrays)
+        cnt = [min(k, sl.stop - sl.start) for k, sl in zip(ks, bounds)]
+        out_off = (ctypes.c_uint64 * (len(bounds) + 1))(0, *[int(c) for c in np.cumsum(cnt)])
+        seg_len = (ctypes.c_uint64 * len(bounds))(*[sl.stop - sl.start for sl in bounds])
+        lay = _LAYOUTS[key] = (bounds, ks, total, offs, kk, contiguous, out_off, seg_len)
         if len(_LAYOUTS) > 64:
             _LAYOUTS.pop(next(iter(_LAYOUTS)))
-    bounds, ks, total, offs, kk, contiguous = lay
-    if kind.name in (TOPK, RANDOMK):
+    bounds, ks, total, offs, kk, contiguous, out_off, seg_len = lay
+    if kind.name in (TOPK, RANDOMK, "redsync"):
         if contiguous:
             idx = torch.empty(total, dtype=torch.int32, device=dev).view(torch.uint32)
             vals = torch.empty(total, dtype=torch.float32, device=dev)
             ws = nat.Workspace.get(dev, "segsel", int(lib.gvc_segmented_select_workspace_bytes(n, len(bounds))))
             status = torch.zeros(1, dtype=torch.int32, device=dev)
-            nat.check(lib.gvc_segmented_select(kind.kind_id, nat.ptr(values), n, offs, kk, len(bounds),
+            sel_kind = kind.kind_id if kind.name != "redsync" else CompressorKind(TOPK).kind_id
+            nat.check(lib.gvc_segmented_select(sel_kind, nat.ptr(values), n, offs, kk, len(bounds),
                                                rng.seed if rng is not None else 0, rng.stream if rng is not None else 0,
                                                nat.ptr(idx), nat.ptr(vals), nat.ptr(ws), ws.numel(), nat.ptr(status),
                                                nat.stream_ptr(dev)), "segmented_select")
+            if kind.name == "redsync":
+                rws = nat.Workspace.get(dev, "segrs", int(lib.gvc_segmented_redsync_workspace_bytes(total, len(bounds))))
+                nat.check(lib.gvc_segmented_redsync_values(nat.ptr(vals), out_off, seg_len, len(bounds), nat.ptr(rws),
+                                                           rws.numel(), nat.stream_ptr(dev)), "segmented_redsync")
             if nat.d2h_bytes(status)[0] & 1:  # (event spin: no scheduler-quantum wake-up)
                 raise ValueError("NaN in gradient: compression order undefined")
             return idx, vals

@@ -423,6 +423,20 @@ int gvc_event_done(void *event)
     return set_error(GVC_ERR_CUDA, "gvc_event_done: %s", cudaGetErrorString(e));
 }
 
+size_t gvc_segmented_redsync_workspace_bytes(uint64_t total, int nseg)
+{
+    return seg_redsync_workspace_bytes(total, nseg);
+}
+
+int gvc_segmented_redsync_values(float *vals_dev, const uint64_t *out_off, const uint64_t *seg_len, int nseg,
+                                 void *ws_dev, size_t ws_bytes, void *stream)
+{
+    if (!vals_dev || !out_off || !seg_len || nseg < 1 || !ws_dev)
+        return set_error(GVC_ERR_ARG, "gvc_segmented_redsync_values: bad arguments");
+    int rc = seg_redsync_run(vals_dev, out_off, seg_len, nseg, ws_dev, ws_bytes, STREAM(stream));
+    return rc ? rc : check_launch("segmented_redsync_values");
+}
+
 int gvc_workspace_forget(void *ws)
 {
     if (!ws)

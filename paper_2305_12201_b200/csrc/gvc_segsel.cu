@@ -345,6 +345,120 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *ou
     }
 }
 
+// Layerwise Redsync (compressors.py:140-161, :187-189, per segment): the
+// segmented Top-k support is Redsync's support; each segment's
+// kept values become sign(v) * fl32(mean_f64 |v|) of that segment.  The kept
+// values are cut into 16384-entry items (a segment's items are consecutive);
+// pass 1 sums |v| per item (fixed-order block sum), pass 2 adds a segment's
+// item sums in item order and substitutes the item's values -- every item in
+// parallel, however unequal the segments (VGG16's first fc layer keeps 10.3M
+// of the 13.8M).  A segment that keeps all its values passes through
+// unchanged (compressors.py:172-173): it has no items.
+#define RS_ITEM 16384
+static size_t al256x(size_t x) { return (x + 255) & ~(size_t)255; }
+struct RsPlan {
+    float *vals;
+    const uint32_t *item_seg;   // [nitems]
+    const uint64_t *item_lo;    // [nitems] output range [lo, hi)
+    const uint64_t *item_hi;
+    const uint32_t *seg_first;  // [nseg] first item of the segment
+    const uint32_t *seg_items;  // [nseg] its item count
+    const uint64_t *seg_k;      // [nseg] kept count
+    double *partial;            // [nitems]
+};
+
+__global__ void __launch_bounds__(256) k_rs_sum(RsPlan P)
+{
+    __shared__ double sh[33];
+    const int it = blockIdx.x;
+    double acc = 0.0;
+    for (uint64_t i = P.item_lo[it] + threadIdx.x; i < P.item_hi[it]; i += blockDim.x)
+        acc += fabs((double)P.vals[i]);
+    const double s = block_sum_f64(acc, sh);
+    if (threadIdx.x == 0)
+        P.partial[it] = s;
+}
+
+__global__ void __launch_bounds__(256) k_rs_substitute(RsPlan P)
+{
+    __shared__ float s_m;
+    const int it = blockIdx.x;
+    const uint32_t q = P.item_seg[it];
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (uint32_t j = 0; j < P.seg_items[q]; j++)
+            sum += P.partial[P.seg_first[q] + j];
+        s_m = (float)(sum / (double)P.seg_k[q]);
+    }
+    __syncthreads();
+    const float m = s_m;
+    for (uint64_t i = P.item_lo[it] + threadIdx.x; i < P.item_hi[it]; i += blockDim.x) {
+        const float v = P.vals[i];
+        const float sg = v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f);
+        P.vals[i] = __fmul_rn(sg, m);
+    }
+}
+
+size_t seg_redsync_workspace_bytes(uint64_t total, int nseg)
+{
+    const uint64_t items = total / RS_ITEM + (uint64_t)nseg + 1;
+    return al256x(items * 4) + al256x(items * 8) * 3 + al256x((size_t)nseg * 4) * 2 + al256x((size_t)nseg * 8) + 256;
+}
+
+int seg_redsync_run(float *vals, const uint64_t *out_off, const uint64_t *seg_len, int nseg, void *ws,
+                    size_t ws_bytes, cudaStream_t s)
+{
+    std::vector<uint32_t> iseg, sfirst(nseg), sitems(nseg);
+    std::vector<uint64_t> ilo, ihi, sk(nseg);
+    for (int q = 0; q < nseg; q++) {
+        const uint64_t a = out_off[q], b = out_off[q + 1];
+        if (b < a)
+            return set_error(GVC_ERR_ARG, "segmented redsync: segment %d output range reversed", q);
+        sk[q] = b - a;
+        sfirst[q] = (uint32_t)iseg.size();
+        if (b - a == 0 || b - a >= seg_len[q])
+            continue;  // identity pass-through
+        for (uint64_t c = a; c < b; c += RS_ITEM) {
+            iseg.push_back((uint32_t)q);
+            ilo.push_back(c);
+            ihi.push_back(c + RS_ITEM < b ? c + RS_ITEM : b);
+        }
+        sitems[q] = (uint32_t)iseg.size() - sfirst[q];
+    }
+    const int nitems = (int)iseg.size();
+    if (nitems == 0)
+        return GVC_OK;
+    if (seg_redsync_workspace_bytes(out_off[nseg], nseg) > ws_bytes)
+        return set_error(GVC_ERR_WORKSPACE, "segmented redsync workspace too small");
+    char *w = (char *)ws;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *q = w + off;
+        off += al256x(bytes);
+        return q;
+    };
+    RsPlan P;
+    P.vals = vals;
+    P.item_seg = (const uint32_t *)take(nitems * 4);
+    P.item_lo = (const uint64_t *)take(nitems * 8);
+    P.item_hi = (const uint64_t *)take(nitems * 8);
+    P.partial = (double *)take(nitems * 8);
+    P.seg_first = (const uint32_t *)take(nseg * 4);
+    P.seg_items = (const uint32_t *)take(nseg * 4);
+    P.seg_k = (const uint64_t *)take(nseg * 8);
+    // (pageable host vectors: the copies complete before the calls return)
+    cudaMemcpyAsync((void *)P.item_seg, iseg.data(), nitems * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.item_lo, ilo.data(), nitems * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.item_hi, ihi.data(), nitems * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.seg_first, sfirst.data(), nseg * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.seg_items, sitems.data(), nseg * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync((void *)P.seg_k, sk.data(), nseg * 8, cudaMemcpyHostToDevice, s);
+    count_launches(2);
+    k_rs_sum<<<nitems, 256, 0, s>>>(P);
+    k_rs_substitute<<<nitems, 256, 0, s>>>(P);
+    return GVC_OK;
+}
+
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t segsel_workspace_bytes(uint64_t n, int nseg)

@@ -238,7 +238,7 @@ def _resnet101_offsets():
     return offs, int(np.sum(sizes))
 
 
-@pytest.mark.parametrize("kind", ["topk", "randomk"])
+@pytest.mark.parametrize("kind", ["topk", "randomk", "redsync"])
 def test_layerwise_resnet101_segments(G, kind):
     """compressors.py:204-217 on ResNet-101's ~314 layer segments (44.5M values)
     as one segmented selection: every segment's keep count, order and values
@@ -255,7 +255,10 @@ def test_layerwise_resnet101_segments(G, kind):
         s, _ = G.compress(G.CompressorKind(kind), g, cf, rng, layerwise=True)
         oi, ov, _ = O.compress(kind, x, cf, seed=rng.seed, stream=rng.stream, layer_offsets=offs, layerwise=True)
         assert np.array_equal(host(s.indices), oi), cf
-        assert np.array_equal(bits(host(s.vals)), bits(ov)), cf
+        if kind == "redsync":  # each segment's mean: an fp64 sum in another order
+            np.testing.assert_allclose(host(s.vals), ov, rtol=RTOL)
+        else:
+            assert np.array_equal(bits(host(s.vals)), bits(ov)), cf
 
 
 @pytest.mark.parametrize("kind", ["topk", "randomk", "redsync", "dgc"])
