@@ -294,7 +294,11 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
             if nat.d2h_bytes(status)[0] & 1:  # (event spin: no scheduler-quantum wake-up)
                 raise ValueError("NaN in gradient: compression order undefined")
             return idx, vals
-    idx_parts, val_parts, checks = [], [], []
+    idx_parts, val_parts = [], []
+    # every segment's result record in one buffer: ONE read-back at the end
+    rb = nat.RESULT_BYTES
+    recs = nat.Workspace.get(dev, "lw/res", rb * len(bounds))
+    nrec = 0
     for sl, k in zip(bounds, ks):
         seg = values[sl.start:sl.stop]
         if seg.data_ptr() % 16:
@@ -304,16 +308,24 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
             i, v = _iota(m, dev), seg.clone()
         elif kind.name == DGC:
             from .dgc import dgc_select
-            i, v, sel = dgc_select(kind, seg, k, rng, pos_base=sl.start, check=False, want_result=True)
-            checks.append(sel)
+            i, v, sel = dgc_select(kind, seg, k, rng, pos_base=sl.start, check=False, want_result=True,
+                                   res_dev=recs[nrec * rb:(nrec + 1) * rb])
+            nrec += 1
         else:
-            sel = Selection(kind, [k], values=seg, rng=rng, pos_base=sl.start)
+            sel = Selection(kind, [k], values=seg, rng=rng, pos_base=sl.start,
+                            res_dev=recs[nrec * rb:(nrec + 1) * rb])
             i, v = sel.emit(0)
-            checks.append(sel)
+            nrec += 1
         idx_parts.append(i.to(torch.int64) + sl.start)
         val_parts.append(v)
-    for sel in checks:  # one read-back each, after every segment was enqueued
-        sel.result()
+    if nrec:
+        raw = nat.d2h_bytes(recs[:nrec * rb])
+        for q in range(nrec):
+            r = nat.SelectResult.from_buffer_copy(raw[q * rb:(q + 1) * rb])
+            if r.status == nat.GVC_ERR_NAN:
+                raise ValueError("NaN in gradient: compression order undefined")
+            if r.status != nat.GVC_OK:
+                raise RuntimeError(f"selection consistency failure (status {r.status})")
     return torch.cat(idx_parts).to(torch.uint32), torch.cat(val_parts)
 
 
