@@ -316,7 +316,7 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
                             res_dev=recs[nrec * rb:(nrec + 1) * rb])
             i, v = sel.emit(0)
             nrec += 1
-        idx_parts.append(i.to(torch.int64) + sl.start)
+        idx_parts.append(i.view(torch.int32))  # segment-local positions (< 2^31)
         val_parts.append(v)
     if nrec:
         raw = nat.d2h_bytes(recs[:nrec * rb])
@@ -326,7 +326,13 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
                 raise ValueError("NaN in gradient: compression order undefined")
             if r.status != nat.GVC_OK:
                 raise RuntimeError(f"selection consistency failure (status {r.status})")
-    return torch.cat(idx_parts).to(torch.uint32), torch.cat(val_parts)
+    # global indices in three launches for all segments (two small torch ops
+    # per segment cost ~10 us of host time each)
+    cnt = [int(t.numel()) for t in idx_parts]
+    starts = torch.tensor([sl.start for sl in bounds], dtype=torch.int64).to(dev, non_blocking=True)
+    counts = torch.tensor(cnt, dtype=torch.int64).to(dev, non_blocking=True)
+    idx = torch.cat(idx_parts).to(torch.int64) + torch.repeat_interleave(starts, counts, output_size=sum(cnt))
+    return idx.to(torch.uint32), torch.cat(val_parts)
 
 
 def compress(kind: CompressorKind, g: GradientVector, cf: float, rng: SeededRng | None = None,
