@@ -268,6 +268,12 @@ GVC_API size_t gvc_segmented_select_workspace_bytes(uint64_t n, int nseg);
 GVC_API size_t gvc_segmented_redsync_workspace_bytes(uint64_t total_kept, int nseg);
 GVC_API int gvc_segmented_redsync_values(float *vals_dev, const uint64_t *out_off, const uint64_t *seg_len, int nseg,
                                          void *ws_dev, size_t ws_bytes, void *stream);
+/* Layerwise (compressors.py:211-213): idx_dev[j] += starts_dev[q] for the
+ * segment q whose outputs out_off_dev[q] <= j < out_off_dev[q + 1] hold j --
+ * segment-local positions to global indices in one launch.  Device arrays;
+ * 1 <= nseg <= 6000. */
+GVC_API int gvc_add_segment_offsets(uint32_t *idx_dev, uint64_t total, const uint64_t *out_off_dev,
+                                    const uint64_t *starts_dev, int nseg, void *stream);
 /* Drop every per-workspace cache entry (select graphs and plans, segment
  * tables) for `ws` before its memory is freed or reused. */
 GVC_API int gvc_workspace_forget(void *ws);

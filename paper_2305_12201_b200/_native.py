@@ -31,7 +31,7 @@ EXPORTS = (
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
     "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
-    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget", "gvc_segmented_redsync_values", "gvc_segmented_redsync_workspace_bytes", "gvc_read_async", "gvc_event_done", "gvc_event_record", "gvc_stream_wait_event", "gvc_copy_async",
+    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget", "gvc_segmented_redsync_values", "gvc_segmented_redsync_workspace_bytes", "gvc_add_segment_offsets", "gvc_read_async", "gvc_event_done", "gvc_event_record", "gvc_stream_wait_event", "gvc_copy_async",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -141,6 +141,7 @@ def load(build_if_missing: bool = False):
         L.gvc_segmented_select_workspace_bytes.argtypes = [_u64, ctypes.c_int]
         L.gvc_segmented_select_workspace_bytes.restype = _sz
         L.gvc_workspace_forget.argtypes = [_vp]
+        L.gvc_add_segment_offsets.argtypes = [_vp, _u64, _vp, _vp, ctypes.c_int, _vp]
         L.gvc_segmented_redsync_values.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _sz, _vp]
         L.gvc_segmented_redsync_workspace_bytes.argtypes = [_u64, ctypes.c_int]
         L.gvc_segmented_redsync_workspace_bytes.restype = _sz

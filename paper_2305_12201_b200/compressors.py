@@ -272,10 +272,13 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
         cnt = [min(k, sl.stop - sl.start) for k, sl in zip(ks, bounds)]
         out_off = (ctypes.c_uint64 * (len(bounds) + 1))(0, *[int(c) for c in np.cumsum(cnt)])
         seg_len = (ctypes.c_uint64 * len(bounds))(*[sl.stop - sl.start for sl in bounds])
-        lay = _LAYOUTS[key] = (bounds, ks, total, offs, kk, contiguous, out_off, seg_len)
+        # (segment starts and kept counts on the device: the per-segment path's index offsets)
+        starts_dev = torch.tensor([sl.start for sl in bounds], dtype=torch.int64).to(dev)
+        out_off_dev = torch.tensor(list(out_off), dtype=torch.int64).to(dev)
+        lay = _LAYOUTS[key] = (bounds, ks, total, offs, kk, contiguous, out_off, seg_len, starts_dev, out_off_dev)
         if len(_LAYOUTS) > 64:
             _LAYOUTS.pop(next(iter(_LAYOUTS)))
-    bounds, ks, total, offs, kk, contiguous, out_off, seg_len = lay
+    bounds, ks, total, offs, kk, contiguous, out_off, seg_len, starts_dev, out_off_dev = lay
     if kind.name in (TOPK, RANDOMK, "redsync"):
         if contiguous:
             idx = torch.empty(total, dtype=torch.int32, device=dev).view(torch.uint32)
@@ -316,7 +319,7 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
                             res_dev=recs[nrec * rb:(nrec + 1) * rb])
             i, v = sel.emit(0)
             nrec += 1
-        idx_parts.append(i.view(torch.int32))  # segment-local positions (< 2^31)
+        idx_parts.append(i)  # segment-local positions
         val_parts.append(v)
     if nrec:
         raw = nat.d2h_bytes(recs[:nrec * rb])
@@ -327,12 +330,13 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
             if r.status != nat.GVC_OK:
                 raise RuntimeError(f"selection consistency failure (status {r.status})")
     # global indices in three launches for all segments (two small torch ops
-    # per segment cost ~10 us of host time each)
-    cnt = [int(t.numel()) for t in idx_parts]
-    starts = torch.tensor([sl.start for sl in bounds], dtype=torch.int64).to(dev, non_blocking=True)
-    counts = torch.tensor(cnt, dtype=torch.int64).to(dev, non_blocking=True)
-    idx = torch.cat(idx_parts).to(torch.int64) + torch.repeat_interleave(starts, counts, output_size=sum(cnt))
-    return idx.to(torch.uint32), torch.cat(val_parts)
+    # per segment cost ~10 us of host time each; the layout's starts and counts
+    # live on the device -- a pageable upload here would synchronise the stream)
+    # segment-local -> global indices, every segment in one launch
+    idx = torch.cat([t.view(torch.int32) for t in idx_parts]).view(torch.uint32)
+    nat.check(lib.gvc_add_segment_offsets(nat.ptr(idx), total, nat.ptr(out_off_dev), nat.ptr(starts_dev), len(bounds),
+                                          nat.stream_ptr(dev)), "add_segment_offsets")
+    return idx, torch.cat(val_parts)
 
 
 def compress(kind: CompressorKind, g: GradientVector, cf: float, rng: SeededRng | None = None,

@@ -437,6 +437,13 @@ int gvc_segmented_redsync_values(float *vals_dev, const uint64_t *out_off, const
     return rc ? rc : check_launch("segmented_redsync_values");
 }
 
+int gvc_add_segment_offsets(uint32_t *idx_dev, uint64_t total, const uint64_t *out_off_dev,
+                            const uint64_t *starts_dev, int nseg, void *stream)
+{
+    int rc = add_seg_offsets_run(idx_dev, total, out_off_dev, starts_dev, nseg, STREAM(stream));
+    return rc ? rc : check_launch("add_segment_offsets");
+}
+
 int gvc_workspace_forget(void *ws)
 {
     if (!ws)

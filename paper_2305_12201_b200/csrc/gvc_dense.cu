@@ -1408,6 +1408,46 @@ int dense_collect_run(const float *own, float *out, uint64_t n, const uint32_t *
     return GVC_OK;
 }
 
+// Layerwise per-segment path: segment-local output positions -> global
+// indices (idx[j] += start of the segment whose outputs hold j), one launch
+// for every segment; the segment of j by binary search over the output
+// offsets staged in shared memory.
+__global__ void k_add_seg_offsets(uint32_t *idx, uint64_t total, const uint64_t *out_off, const uint64_t *starts,
+                                  int nseg)
+{
+    extern __shared__ uint64_t so[];  // [nseg + 1] offsets, then [nseg] starts
+    for (int q = threadIdx.x; q <= nseg; q += blockDim.x)
+        so[q] = out_off[q];
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x)
+        so[nseg + 1 + q] = starts[q];
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride) {
+        int lo = 0, hi = nseg - 1;  // last q with so[q] <= j
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (so[mid] <= j)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        idx[j] += (uint32_t)so[nseg + 1 + lo];
+    }
+}
+
+int add_seg_offsets_run(uint32_t *idx, uint64_t total, const uint64_t *out_off, const uint64_t *starts, int nseg,
+                        cudaStream_t s)
+{
+    if (nseg < 1 || nseg > 6000 || !idx || !out_off || !starts)
+        return set_error(GVC_ERR_ARG, "add_seg_offsets: %d segments", nseg);
+    if (!total)
+        return GVC_OK;
+    const size_t smem = (size_t)(2 * nseg + 1) * 8;
+    count_launches(1);
+    k_add_seg_offsets<<<grid_for(total, 256, device_sms() * 8), 256, smem, s>>>(idx, total, out_off, starts, nseg);
+    return GVC_OK;
+}
+
 __global__ void k_iota(uint32_t *out, uint64_t n)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

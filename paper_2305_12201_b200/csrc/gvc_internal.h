@@ -51,7 +51,9 @@ int aggregate_peers_run(const uint32_t *const *idx, const float *const *vals, co
 int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *vals, const uint32_t *const *bounds,
                                const uint64_t *counts, int nparts, uint64_t n, const uint32_t *flags, uint32_t epoch,
                                const gvc_peer_staging *sg, float *out, cudaStream_t s);
-int device_sms();  // SM count of the current device (cached)
+int device_sms();
+int add_seg_offsets_run(uint32_t *idx, uint64_t total, const uint64_t *out_off, const uint64_t *starts, int nseg,
+                        cudaStream_t s);  // SM count of the current device (cached)
 int dgc_sample_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base, uint32_t *out,
                    cudaStream_t st);
 int dgc_sample_gather_run(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
