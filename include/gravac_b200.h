@@ -271,7 +271,7 @@ GVC_API int gvc_segmented_redsync_values(float *vals_dev, const uint64_t *out_of
 /* Layerwise (compressors.py:211-213): idx_dev[j] += starts_dev[q] for the
  * segment q whose outputs out_off_dev[q] <= j < out_off_dev[q + 1] hold j --
  * segment-local positions to global indices in one launch.  Device arrays;
- * 1 <= nseg <= 6000. */
+ * 1 <= nseg <= 3000. */
 GVC_API int gvc_add_segment_offsets(uint32_t *idx_dev, uint64_t total, const uint64_t *out_off_dev,
                                     const uint64_t *starts_dev, int nseg, void *stream);
 /* Drop every per-workspace cache entry (select graphs and plans, segment

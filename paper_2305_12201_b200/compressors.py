@@ -333,6 +333,9 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
     # per segment cost ~10 us of host time each; the layout's starts and counts
     # live on the device -- a pageable upload here would synchronise the stream)
     # segment-local -> global indices, every segment in one launch
+    if len(bounds) > 3000:  # (the kernel stages the offsets in 48 KB of shared memory)
+        idx = torch.cat([t.to(torch.int64) + sl.start for t, sl in zip(idx_parts, bounds)]).to(torch.uint32)
+        return idx, torch.cat(val_parts)
     idx = torch.cat([t.view(torch.int32) for t in idx_parts]).view(torch.uint32)
     nat.check(lib.gvc_add_segment_offsets(nat.ptr(idx), total, nat.ptr(out_off_dev), nat.ptr(starts_dev), len(bounds),
                                           nat.stream_ptr(dev)), "add_segment_offsets")

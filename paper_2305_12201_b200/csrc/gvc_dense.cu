@@ -1438,7 +1438,7 @@ __global__ void k_add_seg_offsets(uint32_t *idx, uint64_t total, const uint64_t 
 int add_seg_offsets_run(uint32_t *idx, uint64_t total, const uint64_t *out_off, const uint64_t *starts, int nseg,
                         cudaStream_t s)
 {
-    if (nseg < 1 || nseg > 6000 || !idx || !out_off || !starts)
+    if (nseg < 1 || nseg > 3000 || !idx || !out_off || !starts)  // (<= 48 KB of shared memory)
         return set_error(GVC_ERR_ARG, "add_seg_offsets: %d segments", nseg);
     if (!total)
         return GVC_OK;
