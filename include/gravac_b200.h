@@ -293,6 +293,22 @@ GVC_API int gvc_stream_wait_event(void *stream, void *event);
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): a caller's
  * host->device gradient upload without host-side stream objects. */
 GVC_API int gvc_copy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* Layerwise DGC (compressors.py:204-217 with the DGC rule of :110-137 in every
+ * segment; replaces the per-segment gvc_dgc_sample_gather + threshold select
+ * + composite-key gvc_select sequence): segment q draws
+ * s_q = min(len, max(256, round(sample_fraction * len))) stratified positions
+ * (the gvc_dgc_sample definition with pos_base = the segment start), its
+ * threshold is the rank_q-th largest sampled |v| (rank_q = min(s_q, max(1,
+ * round(seg_k[q] s_q / len)))), and it keeps the top seg_k[q] of the DGC
+ * composite key -- the same picks as the per-segment sequence, for every
+ * segment at once (one sample launch + 9 + 12 segmented-selection launches).
+ * A segment with s_q = len takes the exact top-k.  Host seg_offsets /
+ * seg_k as in gvc_segmented_select; *status_dev |= 1 on a NaN. */
+GVC_API size_t gvc_segmented_dgc_workspace_bytes(uint64_t n, int nseg, double sample_fraction);
+GVC_API int gvc_segmented_dgc_select(const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
+                                     const uint64_t *seg_k, int nseg, double sample_fraction, uint64_t seed,
+                                     uint64_t rng_stream, uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev,
+                                     size_t ws_bytes, uint32_t *status_dev, void *stream);
 GVC_API int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                                  const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream,
                                  uint32_t *out_idx_dev, float *out_val_dev, void *ws_dev, size_t ws_bytes,

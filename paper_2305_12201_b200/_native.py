@@ -31,7 +31,7 @@ EXPORTS = (
     "gvc_gather_ef", "gvc_below_keys", "gvc_compact_workspace_bytes", "gvc_compact_mask",
     "gvc_peer_signal", "gvc_aggregate_peers", "gvc_tile_bounds", "gvc_emit_mirrored",
     "gvc_aggregate_peers_staged", "gvc_dgc_sample", "gvc_dgc_sample_gather", "gvc_select_phase_times", "gvc_dense_mean_peers",
-    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_workspace_forget", "gvc_segmented_redsync_values", "gvc_segmented_redsync_workspace_bytes", "gvc_add_segment_offsets", "gvc_read_async", "gvc_event_done", "gvc_event_record", "gvc_stream_wait_event", "gvc_copy_async",
+    "gvc_dense_collect", "gvc_segmented_select_workspace_bytes", "gvc_segmented_select", "gvc_segmented_dgc_workspace_bytes", "gvc_segmented_dgc_select", "gvc_workspace_forget", "gvc_segmented_redsync_values", "gvc_segmented_redsync_workspace_bytes", "gvc_add_segment_offsets", "gvc_read_async", "gvc_event_done", "gvc_event_record", "gvc_stream_wait_event", "gvc_copy_async",
 )
 MAX_PEERS = 8  # GVC_MAX_PEERS
 
@@ -150,6 +150,10 @@ def load(build_if_missing: bool = False):
         L.gvc_event_record.argtypes = [_vp, _vp]
         L.gvc_stream_wait_event.argtypes = [_vp, _vp]
         L.gvc_copy_async.argtypes = [_vp, _vp, _sz, _vp]
+        L.gvc_segmented_dgc_workspace_bytes.argtypes = [_u64, ctypes.c_int, ctypes.c_double]
+        L.gvc_segmented_dgc_workspace_bytes.restype = _sz
+        L.gvc_segmented_dgc_select.argtypes = [_vp, _u64, _vp, _vp, ctypes.c_int, ctypes.c_double, _u64, _u64, _vp,
+                                               _vp, _vp, _sz, _vp, _vp]
         L.gvc_segmented_select.argtypes = [ctypes.c_int, _vp, _u64, _vp, _vp, ctypes.c_int, _u64, _u64, _vp, _vp,
                                            _vp, _sz, _vp, _vp]
         L.gvc_aggregate_peers_staged.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, _u64, _vp, ctypes.c_uint32,

@@ -249,8 +249,9 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
     and Random-k: one segmented selection over every segment
     (gvc_segmented_select); Redsync: the same segmented Top-k support (F1)
     then each segment's mean substitution (gvc_segmented_redsync_values);
-    DGC: one selection per segment, enqueued back to back, statuses read once
-    at the end."""
+    DGC: every segment's sample, threshold and composite-key selection at
+    once (gvc_segmented_dgc_select).  Non-contiguous layouts: one selection
+    per segment, enqueued back to back, statuses read once at the end."""
     n = values.numel()
     if kind.name in (RANDOMK, DGC) and rng is None:
         raise ValueError(f"{kind.name} compression requires an rng")
@@ -297,6 +298,19 @@ def _layerwise(kind: CompressorKind, values: torch.Tensor, g: GradientVector, cf
             if nat.d2h_bytes(status)[0] & 1:  # (event spin: no scheduler-quantum wake-up)
                 raise ValueError("NaN in gradient: compression order undefined")
             return idx, vals
+    if kind.name == DGC and contiguous:
+        # every segment's sample, threshold and composite-key selection at once
+        idx = torch.empty(total, dtype=torch.int32, device=dev).view(torch.uint32)
+        vals = torch.empty(total, dtype=torch.float32, device=dev)
+        frac = float(kind.dgc_sample_fraction)
+        ws = nat.Workspace.get(dev, "segdgc", int(lib.gvc_segmented_dgc_workspace_bytes(n, len(bounds), frac)))
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        nat.check(lib.gvc_segmented_dgc_select(nat.ptr(values), n, offs, kk, len(bounds), frac, rng.seed, rng.stream,
+                                               nat.ptr(idx), nat.ptr(vals), nat.ptr(ws), ws.numel(), nat.ptr(status),
+                                               nat.stream_ptr(dev)), "segmented_dgc_select")
+        if nat.d2h_bytes(status)[0] & 1:
+            raise ValueError("NaN in gradient: compression order undefined")
+        return idx, vals
     idx_parts, val_parts = [], []
     # every segment's result record in one buffer: ONE read-back at the end
     rb = nat.RESULT_BYTES

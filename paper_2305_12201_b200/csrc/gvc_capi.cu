@@ -453,6 +453,24 @@ int gvc_workspace_forget(void *ws)
     return GVC_OK;
 }
 
+size_t gvc_segmented_dgc_workspace_bytes(uint64_t n, int nseg, double sample_fraction)
+{
+    return seg_dgc_workspace_bytes(n, nseg, sample_fraction);
+}
+
+int gvc_segmented_dgc_select(const float *values_dev, uint64_t n, const uint64_t *seg_offsets, const uint64_t *seg_k,
+                             int nseg, double sample_fraction, uint64_t seed, uint64_t rng_stream, uint32_t *out_idx_dev,
+                             float *out_val_dev, void *ws_dev, size_t ws_bytes, uint32_t *status_dev, void *stream)
+{
+    if (!values_dev || !seg_offsets || !seg_k || nseg < 1 || !out_idx_dev || !out_val_dev || !ws_dev || !status_dev)
+        return set_error(GVC_ERR_ARG, "segmented DGC: null argument or no segment");
+    if (n >= (1ull << 32))
+        return set_error(GVC_ERR_ARG, "segmented DGC: length %llu >= 2^32", (unsigned long long)n);
+    int rc = seg_dgc_run(values_dev, n, seg_offsets, seg_k, nseg, sample_fraction, seed, rng_stream, out_idx_dev,
+                         out_val_dev, ws_dev, ws_bytes, status_dev, STREAM(stream));
+    return rc ? rc : check_launch("segmented_dgc_select");
+}
+
 int gvc_segmented_select(int kind, const float *values_dev, uint64_t n, const uint64_t *seg_offsets,
                          const uint64_t *seg_k, int nseg, uint64_t seed, uint64_t rng_stream, uint32_t *out_idx_dev,
                          float *out_val_dev, void *ws_dev, size_t ws_bytes, uint32_t *status_dev, void *stream)

@@ -202,31 +202,7 @@ int apply_pending_run(float *resid, uint32_t *mask, uint64_t n, int mode, const 
 }
 
 // ------------------------------------------------------------ DGC helpers
-// DGC's threshold sample: one position per stratum [j n / s, (j + 1) n / s),
-// offset = Philox word 0 at counter (pos_base + lo_j, stream) scaled to the
-// stratum width (the C-ABI header states the definition).
-// floor(j n / s) without a 64-bit integer division: with n < 2^32 and
-// j <= s <= n, j n fits 64 bits and the fp64 quotient is within 2^-20 of the
-// true one, so one correction step makes the floor exact
-__device__ __forceinline__ uint64_t stratum_lo(uint64_t j, uint64_t n, uint64_t s, double inv_s)
-{
-    const uint64_t a = j * n;
-    uint64_t q = (uint64_t)((double)a * inv_s);
-    if (q * s > a)
-        q--;
-    else if ((q + 1) * s <= a)
-        q++;
-    return q;
-}
-
-__device__ __forceinline__ uint32_t dgc_position(uint64_t j, uint64_t n, uint64_t s, double inv_s, uint64_t seed,
-                                                 uint64_t stream, uint64_t pos_base)
-{
-    const uint64_t lo = stratum_lo(j, n, s, inv_s), hi = stratum_lo(j + 1, n, s, inv_s);
-    const uint32_t h = philox_x0(pos_base + lo, stream, seed);
-    return (uint32_t)(lo + (((uint64_t)h * (hi - lo)) >> 32));
-}
-
+// (stratum_lo / dgc_position: gvc_common.cuh, shared with the layerwise DGC)
 __global__ void k_dgc_sample(uint64_t n, uint64_t s, uint64_t seed, uint64_t stream, uint64_t pos_base,
                              uint32_t *__restrict__ out)
 {

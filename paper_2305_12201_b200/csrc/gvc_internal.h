@@ -75,6 +75,10 @@ void segsel_forget(const void *ws);
 size_t seg_redsync_workspace_bytes(uint64_t total, int nseg);
 int seg_redsync_run(float *vals, const uint64_t *out_off, const uint64_t *seg_len, int nseg, void *ws,
                     size_t ws_bytes, cudaStream_t s);
+size_t seg_dgc_workspace_bytes(uint64_t n, int nseg, double frac);
+int seg_dgc_run(const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg, double frac,
+                uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
+                uint32_t *status, cudaStream_t s);
 int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
                uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
                uint32_t *status, cudaStream_t s);

@@ -21,6 +21,7 @@
 // position (Random-k, the counter-based sampler with pos_base = segment start,
 // DESIGN.md).  11 launches whatever the number of segments.
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -58,14 +59,31 @@ struct SegPlan {
     unsigned long long *item_E;   // [nitems] exclusive scan of the == counts
     const uint32_t *seg_first;    // [nseg] first item of the segment
     uint32_t *status;             // bit 1: NaN
+    // KEY_DGC (layerwise DGC): segment q's sampled threshold key is
+    // dgc_seg[q].prefix (the sample selection's states); dgc_bits = the
+    // samples' global position bitmap
+    const SegState *dgc_seg;
+    const uint32_t *dgc_bits;
+    int thr_only;  // the sample selection: k = len resolves the minimum key too
 };
 
 // (the key mode is a template parameter of every pass: a runtime test per
 // value cost the compaction pass ~20% of its issue slots)
 template <int KM>
-__device__ __forceinline__ uint32_t ss_key(const SegPlan &P, float v, uint64_t pos)
+__device__ __forceinline__ uint32_t ss_key(const SegPlan &P, float v, uint64_t pos, uint32_t thr)
 {
+    if (KM == KEY_DGC) {  // the composite key of gvc_select's KEY_DGC, per segment
+        const uint32_t m = mag_key(v);
+        const bool hi = m >= thr || ((__ldg(P.dgc_bits + (pos >> 5)) >> (pos & 31)) & 1u);
+        return hi ? (0x80000000u | m) : m;
+    }
     return KM == KEY_HASH ? hash_key(pos, P.stream, P.seed) : mag_key(v);
+}
+
+template <int KM>
+__device__ __forceinline__ uint32_t ss_thr(const SegPlan &P, uint32_t s)
+{
+    return KM == KEY_DGC ? P.dgc_seg[s].prefix : 0u;
 }
 
 // Pass d: histogram of digit d of the keys matching the segment's prefix.
@@ -84,12 +102,13 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_hist(SegPlan P, int d)
         const uint32_t len = P.item_len[it];
         const int shift = 24 - 8 * d;
         const uint32_t pmask = d ? (0xffffffffu << (32 - 8 * d)) : 0u;
+        const uint32_t thr = ss_thr<KM>(P, s);
         uint32_t nan = 0;
         for (uint32_t i = threadIdx.x; i < len; i += SS_THREADS) {
             const float v = P.values[lo + i];
-            const uint32_t key = ss_key<KM>(P, v, lo + i);
-            if (d == 0 && KM == KEY_MAG)
-                nan |= key > 0x7f800000u;
+            const uint32_t key = ss_key<KM>(P, v, lo + i, thr);
+            if (d == 0 && KM != KEY_HASH)
+                nan |= (key & 0x7fffffffu) > 0x7f800000u;
             if ((key & pmask) == st.prefix)
                 atomicAdd(&h[(key >> shift) & 255u], 1u);
         }
@@ -166,7 +185,7 @@ __global__ void k_ss_init(SegPlan P)
     const uint64_t len = P.seg_lo[q + 1] - P.seg_lo[q], k = P.seg_k[q];
     SegState st;
     st.prefix = 0;
-    st.all = len == 0 || k >= len;
+    st.all = len == 0 || (!P.thr_only && k >= len);
     st.need = k;
     P.seg[q] = st;
 }
@@ -180,12 +199,13 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_count(SegPlan P)
     const int it = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const SegState st = P.seg[P.item_seg[it]];
+    const uint32_t thr = ss_thr<KM>(P, P.item_seg[it]);
     const uint64_t lo = P.item_lo[it];
     uint32_t wb, we;
     ss_slice(P.item_len[it], warp, wb, we);
     uint32_t gt = 0, eq = 0;
     for (uint32_t i = wb + lane; i < we; i += 32) {
-        const uint32_t key = ss_key<KM>(P, P.values[lo + i], lo + i);
+        const uint32_t key = ss_key<KM>(P, P.values[lo + i], lo + i, thr);
         gt += st.all || key > st.prefix;
         eq += !st.all && key == st.prefix;
     }
@@ -277,6 +297,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *ou
     const int it = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const SegState st = P.seg[P.item_seg[it]];
+    const uint32_t thr = ss_thr<KM>(P, P.item_seg[it]);
     const uint32_t lo = (uint32_t)P.item_lo[it];  // n < 2^32 (gvc_segmented_select checks)
     const uint32_t take = P.item_take[it];
     uint32_t wb, we;
@@ -310,7 +331,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *ou
         for (int u = 0; u < U; u++) {
             const uint32_t i = base + u * 32 + lane;
             const bool ok = i < we;
-            const uint32_t key = ok ? ss_key<KM>(P, v[u], lo + i) : 0u;
+            const uint32_t key = ok ? ss_key<KM>(P, v[u], lo + i, thr) : 0u;
             const bool iseq = ok && !st.all && key == st.prefix;
             bool keep = ok && (st.all || key > st.prefix);
             const uint32_t em = __ballot_sync(0xffffffffu, iseq);
@@ -480,23 +501,34 @@ struct SegLayout {
 };
 static std::mutex g_seg_mu;
 static std::unordered_map<const void *, SegLayout> g_seg_layouts;
+static std::unordered_map<const void *, const void *> g_seg_alias;  // layerwise DGC: its sample selection's tables
 
 void segsel_forget(const void *ws)
 {
     std::lock_guard<std::mutex> lk(g_seg_mu);
     g_seg_layouts.erase(ws);
+    auto a = g_seg_alias.find(ws);
+    if (a != g_seg_alias.end()) {
+        g_seg_layouts.erase(a->second);
+        g_seg_alias.erase(a);
+    }
 }
 
-int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
-               uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
-               uint32_t *status, cudaStream_t s)
+// One segmented selection.  keymode KEY_MAG / KEY_HASH / KEY_DGC (dgc_seg,
+// dgc_bits); thr_only: stop after the radix passes (each segment's threshold
+// key left in its state; k = len resolves the minimum).
+static int segsel_launch(int keymode, int thr_only, const SegState *dgc_seg, const uint32_t *dgc_bits,
+                         const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
+                         uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws,
+                         size_t ws_bytes, uint32_t *status, cudaStream_t s)
 {
+    const int kind = keymode * 2 + thr_only;  // (the cached layout's tag)
     for (int q = 0; q < nseg; q++) {
         const uint64_t a = seg_off[q], b = seg_off[q + 1];
         if (b < a || b > n)
             return set_error(GVC_ERR_ARG, "segmented select: segment %d [%llu, %llu) outside [0, %llu)", q,
                              (unsigned long long)a, (unsigned long long)b, (unsigned long long)n);
-        if (b - a && seg_k[q] < 1)
+        if (b - a && seg_k[q] < 1 && !thr_only)
             return set_error(GVC_ERR_ARG, "segmented select: keep count 0 in segment %d", q);
     }
     if (segsel_workspace_bytes(n, nseg) > ws_bytes)
@@ -534,7 +566,10 @@ int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_of
     P.n = n;
     P.nseg = nseg;
     P.nitems = nitems;
-    P.keymode = kind == GVC_RANDOMK ? KEY_HASH : KEY_MAG;
+    P.keymode = keymode;
+    P.thr_only = thr_only;
+    P.dgc_seg = dgc_seg;
+    P.dgc_bits = dgc_bits;
     P.seed = seed;
     P.stream = stream;
     P.seg = (SegState *)take(nseg * sizeof(SegState));
@@ -570,25 +605,166 @@ int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_of
     cudaMemsetAsync(P.hist, 0, (size_t)4 * nseg * 256 * 4, s);
     k_ss_init<<<(nseg + 255) / 256, 256, 0, s>>>(P);
     const int rgrid = (nseg + SS_THREADS / 32 - 1) / (SS_THREADS / 32);
-    const bool hash = P.keymode == KEY_HASH;
     for (int d = 0; d < 4; d++) {
-        if (hash)
+        if (keymode == KEY_HASH)
             k_ss_hist<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P, d);
+        else if (keymode == KEY_DGC)
+            k_ss_hist<KEY_DGC><<<nitems, SS_THREADS, 0, s>>>(P, d);
         else
             k_ss_hist<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P, d);
         k_ss_resolve<<<rgrid, SS_THREADS, 0, s>>>(P, d);
     }
-    if (hash)
+    if (thr_only) {
+        count_launches(9);
+        return GVC_OK;
+    }
+    if (keymode == KEY_HASH)
         k_ss_count<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P);
+    else if (keymode == KEY_DGC)
+        k_ss_count<KEY_DGC><<<nitems, SS_THREADS, 0, s>>>(P);
     else
         k_ss_count<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P);
     k_ss_scan<<<1, 1024, 0, s>>>(P);
-    if (hash)
+    if (keymode == KEY_HASH)
         k_ss_write<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
+    else if (keymode == KEY_DGC)
+        k_ss_write<KEY_DGC><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
     else
         k_ss_write<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
     count_launches(12);
     return GVC_OK;
+}
+
+int segsel_run(int kind, const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg,
+               uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
+               uint32_t *status, cudaStream_t s)
+{
+    return segsel_launch(kind == GVC_RANDOMK ? KEY_HASH : KEY_MAG, 0, nullptr, nullptr, values, n, seg_off, seg_k,
+                         nseg, seed, stream, out_idx, out_val, ws, ws_bytes, status, s);
+}
+
+// ------------------------------------------------------------ layerwise DGC
+// compressors.py:204-217 with the DGC rule (:110-137) inside every segment,
+// as three steps over all segments at once:
+//   1. k_sdgc_sample: segment q draws s_q = min(len, max(256, round(f len)))
+//      stratified positions (dgc_position with pos_base = the segment start,
+//      as the per-segment selection draws them), gathers their values into
+//      the segment's run of the sample vector and marks them in a global
+//      position bitmap;
+//   2. a threshold-only segmented selection over the samples: segment q's
+//      rank_q-th largest sampled |v|, rank_q = min(s_q, max(1, round(k s / len)))
+//      (rank_q = s_q: the minimum); segments sampled in full (s_q = len, exact
+//      top-k) have no samples and threshold 0, under which every key is in
+//      the upper half -- plain top-k;
+//   3. the segmented selection over gvc_select's DGC composite key
+//      ((|v| >= T_q or sampled) ? 2^31 | |v| : |v|) with segment q's T_q.
+__global__ void __launch_bounds__(256) k_sdgc_sample(const float *__restrict__ values, uint64_t seed, uint64_t stream,
+                                                     const uint64_t *__restrict__ seg_off,
+                                                     const uint64_t *__restrict__ samp_off, int nseg,
+                                                     float *__restrict__ vP, uint32_t *bits)
+{
+    const uint64_t S = samp_off[nseg];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t J = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; J < S; J += stride) {
+        int a = 0, b = nseg - 1;  // the segment q with samp_off[q] <= J < samp_off[q + 1]
+        while (a < b) {
+            const int m = (a + b + 1) >> 1;
+            if (__ldg(samp_off + m) <= J)
+                a = m;
+            else
+                b = m - 1;
+        }
+        const uint64_t s0 = samp_off[a], sq = samp_off[a + 1] - s0;
+        const uint64_t base = seg_off[a], len = seg_off[a + 1] - base;
+        const uint64_t q = base + dgc_position(J - s0, len, sq, 1.0 / (double)sq, seed, stream, base);
+        vP[J] = values[q];
+        atomicOr(&bits[q >> 5], 1u << (q & 31));
+    }
+}
+
+// the per-segment sample sizes and ranks (host; compressors.py:112, :119-121)
+static void sdgc_counts(const uint64_t *seg_off, const uint64_t *seg_k, int nseg, double frac,
+                        std::vector<uint64_t> &samp_off, std::vector<uint64_t> &rank)
+{
+    samp_off.assign(nseg + 1, 0);
+    rank.assign(nseg, 0);
+    for (int q = 0; q < nseg; q++) {
+        const uint64_t len = seg_off[q + 1] - seg_off[q], k = seg_k[q];
+        uint64_t sq = 0;
+        if (len && k < len) {
+            const double r = std::nearbyint(frac * (double)len);  // Python round(): ties to even
+            sq = std::min<uint64_t>(len, std::max<uint64_t>(256, (uint64_t)r));
+            if (sq >= len)
+                sq = 0;  // the full sample: exact top-k (:113-115)
+            else {
+                // k s / len correctly rounded (k s < 2^53 for any n < 2^32 here:
+                // s <= ~n / 100 + 256), then round half to even
+                const double x = (double)(k * sq) / (double)len;
+                rank[q] = std::min<uint64_t>(sq, std::max<uint64_t>(1, (uint64_t)std::nearbyint(x)));
+            }
+        }
+        samp_off[q + 1] = samp_off[q] + sq;
+    }
+}
+
+static uint64_t sdgc_sample_bound(uint64_t n, int nseg, double frac)
+{
+    const double b = std::ceil(frac * (double)n) + 258.0 * nseg;
+    return std::min<uint64_t>(n, (uint64_t)b);
+}
+
+size_t seg_dgc_workspace_bytes(uint64_t n, int nseg, double frac)
+{
+    const uint64_t S = sdgc_sample_bound(n, nseg, frac);
+    return segsel_workspace_bytes(n, nseg) + segsel_workspace_bytes(S, nseg) + al256(S * 4) + al256((n + 31) / 32 * 4) +
+           al256((size_t)(nseg + 1) * 8) * 2 + 256;
+}
+
+int seg_dgc_run(const float *values, uint64_t n, const uint64_t *seg_off, const uint64_t *seg_k, int nseg, double frac,
+                uint64_t seed, uint64_t stream, uint32_t *out_idx, float *out_val, void *ws, size_t ws_bytes,
+                uint32_t *status, cudaStream_t s)
+{
+    if (!(frac > 0.0 && frac <= 1.0))
+        return set_error(GVC_ERR_ARG, "segmented DGC: sample fraction %g outside (0, 1]", frac);
+    for (int q = 0; q < nseg; q++)
+        if (seg_off[q + 1] < seg_off[q] || seg_off[q + 1] > n)
+            return set_error(GVC_ERR_ARG, "segmented DGC: segment %d outside [0, %llu)", q, (unsigned long long)n);
+    if (seg_dgc_workspace_bytes(n, nseg, frac) > ws_bytes)
+        return set_error(GVC_ERR_WORKSPACE, "segmented DGC workspace too small");
+    std::vector<uint64_t> samp_off, rank;
+    sdgc_counts(seg_off, seg_k, nseg, frac, samp_off, rank);
+    const uint64_t S = samp_off[nseg];
+    char *w = (char *)ws;
+    char *ws_main = w;
+    char *ws_samp = ws_main + segsel_workspace_bytes(n, nseg);
+    float *vP = (float *)(ws_samp + segsel_workspace_bytes(sdgc_sample_bound(n, nseg, frac), nseg));
+    uint32_t *bits = (uint32_t *)((char *)vP + al256(sdgc_sample_bound(n, nseg, frac) * 4));
+    uint64_t *d_seg_off = (uint64_t *)((char *)bits + al256((n + 31) / 32 * 4));
+    uint64_t *d_samp_off = (uint64_t *)((char *)d_seg_off + al256((size_t)(nseg + 1) * 8));
+    // (pageable host arrays: the copies complete before the calls return)
+    cudaMemcpyAsync(d_seg_off, seg_off, (nseg + 1) * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_samp_off, samp_off.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(bits, 0, (n + 31) / 32 * 4, s);
+    {
+        std::lock_guard<std::mutex> lk(g_seg_mu);
+        g_seg_alias[ws] = ws_samp;
+    }
+    if (!S)  // every segment exact or kept whole: thresholds 0 (no sample selection runs)
+        cudaMemsetAsync(ws_samp, 0, nseg * sizeof(SegState), s);
+    else {
+        count_launches(1);
+        const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)device_sms() * 8);
+        k_sdgc_sample<<<blocks, 256, 0, s>>>(values, seed, stream, d_seg_off, d_samp_off,
+                                                                          nseg, vP, bits);
+    }
+    // the sample selection's states are at the start of its workspace (segsel_launch's carve)
+    int rc = segsel_launch(KEY_MAG, 1, nullptr, nullptr, vP, S, samp_off.data(), rank.data(), nseg, seed, stream,
+                           nullptr, nullptr, ws_samp, segsel_workspace_bytes(sdgc_sample_bound(n, nseg, frac), nseg),
+                           status, s);
+    if (rc)
+        return rc;
+    return segsel_launch(KEY_DGC, 0, (const SegState *)ws_samp, bits, values, n, seg_off, seg_k, nseg, seed, stream,
+                         out_idx, out_val, ws_main, segsel_workspace_bytes(n, nseg), status, s);
 }
 
 }  // namespace gvc

@@ -238,7 +238,7 @@ def _resnet101_offsets():
     return offs, int(np.sum(sizes))
 
 
-@pytest.mark.parametrize("kind", ["topk", "randomk", "redsync"])
+@pytest.mark.parametrize("kind", ["topk", "randomk", "redsync", "dgc"])
 def test_layerwise_resnet101_segments(G, kind):
     """compressors.py:204-217 on ResNet-101's ~314 layer segments (44.5M values)
     as one segmented selection: every segment's keep count, order and values
@@ -281,6 +281,29 @@ def test_layerwise_edge_segments(G, kind):
             assert np.array_equal(bits(host(s.vals)), bits(ov)), (kind, cf)
 
 
+@pytest.mark.parametrize("frac", [0.003, 0.01, 0.05, 1.0])
+def test_layerwise_dgc_sample_fractions(G, frac):
+    """Layerwise DGC (gvc_segmented_dgc_select) at several sample fractions:
+    segments sampled at 256 (the floor), at f * len, in full (exact top-k),
+    a rank that reaches the whole sample (cf ~ 1: the minimum sampled |v|),
+    tie-only and scaled segments -- bit-exact against the oracle's
+    per-segment DGC."""
+    x = _gauss(400_003, 8)
+    x[1000:3000] = 0.25
+    x[3000:90_000] *= np.float32(1e-3)
+    x[90_000:90_600] = np.round(x[90_000:90_600])
+    offs = (0, 1000, 3000, 90_000, 90_600, 91_600, 300_000)
+    K = G.CompressorKind("dgc", dgc_sample_fraction=frac)
+    rng = G.SeededRng(31).split(3)
+    for cf in (1.001, 2.0, 10.0, 300.0):
+        g = G.GradientVector(x, offs)
+        s, _ = G.compress(K, g, cf, rng, layerwise=True)
+        oi, ov, _ = O.compress("dgc", x, cf, seed=rng.seed, stream=rng.stream, layer_offsets=offs, layerwise=True,
+                               dgc_sample_fraction=frac)
+        assert np.array_equal(host(s.indices), oi), (frac, cf)
+        assert np.array_equal(bits(host(s.vals)), bits(ov)), (frac, cf)
+
+
 def test_layerwise_layout_changes_on_one_workspace(G):
     """The segmented select caches a layout's work tables per workspace: a
     different layout of the same length and segment count, then the first one
@@ -295,7 +318,7 @@ def test_layerwise_layout_changes_on_one_workspace(G):
             ws = nat.Workspace.get(torch.device("cuda", 0), "segsel", 1)
             nat.check(nat.load().gvc_workspace_forget(nat.ptr(ws)))
         g = G.GradientVector(x, offs)
-        for kind in ("topk", "randomk"):
+        for kind in ("topk", "randomk", "dgc"):
             s, _ = G.compress(G.CompressorKind(kind), g, 10.0, rng, layerwise=True)
             oi, ov, _ = O.compress(kind, x, 10.0, seed=rng.seed, stream=rng.stream, layer_offsets=offs,
                                    layerwise=True)
