@@ -7,11 +7,11 @@
 // ResNet-101 gradient has ~300 segments; instead of one selection pipeline per
 // segment, every segment is resolved at once:
 //   * work items = (segment, chunk of <= SS_CHUNK values), one CTA each;
-//   * 4 radix passes of 8 key bits, most significant first: every CTA
+//   * 3 radix passes of 11 / 11 / 10 key bits, most significant first: every CTA
 //     histograms the keys of its chunk that match its segment's resolved
-//     prefix (256 shared-memory bins, merged into the segment's global bins);
+//     prefix (2048 shared-memory bins, merged into the segment's global bins);
 //     one warp per segment then picks the digit where the count from the top
-//     reaches the segment's remaining rank -> after 4 passes each segment has
+//     reaches the segment's remaining rank -> after 3 passes each segment has
 //     its exact threshold key T_s and tie quota q_s;
 //   * counts per item (> T, == T), one CTA scans them into per-item output
 //     offsets and tie quotas (the segments' outputs are contiguous and in
@@ -19,7 +19,7 @@
 //   * an ordered compaction writes (global index, value) per item.
 // Keys: 31-bit |v| (Top-k) or the Philox position hash of the global
 // position (Random-k, the counter-based sampler with pos_base = segment start,
-// DESIGN.md).  11 launches whatever the number of segments.
+// DESIGN.md).  10 launches whatever the number of segments.
 #include <algorithm>
 #include <cmath>
 #include <mutex>
@@ -51,7 +51,7 @@ struct SegPlan {
     const uint64_t *item_lo;   // [nitems] global start of the item
     const uint32_t *item_len;  // [nitems]
     SegState *seg;             // [nseg]
-    uint32_t *hist;            // [4][nseg][256]
+    uint32_t *hist;            // [SS_PASSES][nseg][SS_BINS]
     uint32_t *item_gt, *item_eq;  // [nitems]
     uint32_t *warp_gt, *warp_eq;  // [nitems][SS_THREADS / 32]: the same counts per k_ss_write warp slice
     uint32_t *item_take;          // [nitems] ties this item keeps
@@ -86,77 +86,107 @@ __device__ __forceinline__ uint32_t ss_thr(const SegPlan &P, uint32_t s)
     return KM == KEY_DGC ? P.dgc_seg[s].prefix : 0u;
 }
 
+// Radix digits, most significant first: 11 + 11 + 10 bits (3 passes; 8-bit
+// digits took 4 passes of ~44 us each over a 44.5M gradient).
+#define SS_PASSES 3
+#define SS_BINS 2048
+__host__ __device__ __forceinline__ int ss_shift(int d) { return d == 0 ? 21 : (d == 1 ? 10 : 0); }
+__host__ __device__ __forceinline__ int ss_nbins(int d) { return d == 2 ? 1024 : 2048; }
+__host__ __device__ __forceinline__ uint32_t ss_pmask(int d) { return d == 0 ? 0u : (d == 1 ? 0xffe00000u : 0xfffffc00u); }
+
 // Pass d: histogram of digit d of the keys matching the segment's prefix.
+// The item is read 16 bytes per load (scalar head and tail to the 16-byte
+// boundary), four loads in flight per thread.
 template <int KM>
 __global__ void __launch_bounds__(SS_THREADS) k_ss_hist(SegPlan P, int d)
 {
-    __shared__ uint32_t h[256];
+    __shared__ uint32_t h[SS_BINS];
     const int it = blockIdx.x;
     const uint32_t s = P.item_seg[it];
     const SegState st = P.seg[s];
-    for (int i = threadIdx.x; i < 256; i += SS_THREADS)
+    const int nb = ss_nbins(d);
+    for (int i = threadIdx.x; i < nb; i += SS_THREADS)
         h[i] = 0;
     __syncthreads();
     if (!st.all) {
         const uint64_t lo = P.item_lo[it];
         const uint32_t len = P.item_len[it];
-        const int shift = 24 - 8 * d;
-        const uint32_t pmask = d ? (0xffffffffu << (32 - 8 * d)) : 0u;
+        const int shift = ss_shift(d);
+        const uint32_t dmask = (uint32_t)nb - 1u;
+        const uint32_t pmask = ss_pmask(d);
         const uint32_t thr = ss_thr<KM>(P, s);
         uint32_t nan = 0;
-        for (uint32_t i = threadIdx.x; i < len; i += SS_THREADS) {
-            const float v = P.values[lo + i];
-            const uint32_t key = ss_key<KM>(P, v, lo + i, thr);
+        auto one = [&](float v, uint64_t pos) {
+            const uint32_t key = ss_key<KM>(P, v, pos, thr);
             if (d == 0 && KM != KEY_HASH)
                 nan |= (key & 0x7fffffffu) > 0x7f800000u;
             if ((key & pmask) == st.prefix)
-                atomicAdd(&h[(key >> shift) & 255u], 1u);
+                atomicAdd(&h[(key >> shift) & dmask], 1u);
+        };
+        // 16-byte aligned body [head, head + 4 * nv)
+        uint32_t head = (uint32_t)((4 - ((reinterpret_cast<uintptr_t>(P.values + lo) >> 2) & 3)) & 3);
+        if (head > len)
+            head = len;
+        const uint32_t nv = (len - head) >> 2;
+        for (uint32_t i = threadIdx.x; i < head; i += SS_THREADS)
+            one(P.values[lo + i], lo + i);
+        const float4 *v4 = reinterpret_cast<const float4 *>(P.values + lo + head);
+        for (uint32_t b = threadIdx.x; b < nv; b += 4 * SS_THREADS) {
+            float4 q[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (b + u * SS_THREADS < nv)
+                    q[u] = v4[b + u * SS_THREADS];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t e = b + u * SS_THREADS;
+                if (e < nv) {
+                    const uint64_t pos = lo + head + 4ull * e;
+                    one(q[u].x, pos);
+                    one(q[u].y, pos + 1);
+                    one(q[u].z, pos + 2);
+                    one(q[u].w, pos + 3);
+                }
+            }
         }
+        for (uint32_t i = head + 4 * nv + threadIdx.x; i < len; i += SS_THREADS)
+            one(P.values[lo + i], lo + i);
         if (d == 0 && __any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0)
             atomicOr(P.status, 1u);
     }
     __syncthreads();
-    uint32_t *g = P.hist + ((size_t)d * P.nseg + s) * 256;
-    for (int i = threadIdx.x; i < 256; i += SS_THREADS)
+    uint32_t *g = P.hist + ((size_t)d * P.nseg + s) * SS_BINS;
+    for (int i = threadIdx.x; i < nb; i += SS_THREADS)
         if (h[i])
             atomicAdd(&g[i], h[i]);
 }
 
-// One warp per segment: the digit where the count from the top reaches `need`.
+// One CTA per segment: the digit where the count from the top reaches `need`
+// (thread t holds nb / 256 consecutive descending digits; a block scan).
 __global__ void __launch_bounds__(SS_THREADS) k_ss_resolve(SegPlan P, int d)
 {
-    const int lane = threadIdx.x & 31;
-    const int s = blockIdx.x * (SS_THREADS / 32) + (threadIdx.x >> 5);
-    if (s >= P.nseg)
-        return;
+    __shared__ unsigned long long sh[33];
+    const int s = blockIdx.x;
     SegState st = P.seg[s];
     if (st.all)
-        return;
-    const uint32_t *g = P.hist + ((size_t)d * P.nseg + s) * 256;
-    // lane l holds bins 255 - 8l .. 248 - 8l (descending digits)
-    uint32_t c[8];
+        return;  // (uniform over the block)
+    const int nb = ss_nbins(d), per = nb / SS_THREADS;
+    const uint32_t *g = P.hist + ((size_t)d * P.nseg + s) * SS_BINS;
+    const int top = nb - 1 - per * (int)threadIdx.x;
+    uint32_t c[SS_BINS / SS_THREADS];
     unsigned long long local = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        c[i] = g[255 - 8 * lane - i];
+    for (int i = 0; i < SS_BINS / SS_THREADS; i++) {
+        c[i] = i < per ? g[top - i] : 0u;
         local += c[i];
     }
-    unsigned long long incl = local;  // inclusive prefix over lanes (from the top digit)
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o)
-            incl += y;
-    }
-    const unsigned long long before = incl - local;
+    const unsigned long long before = block_excl_prefix(local, sh);
     const unsigned long long nd = st.need;
-    const bool here = before < nd && nd <= incl;
-    if (here) {
+    if (before < nd && nd <= before + local) {
         unsigned long long acc = before;
-        for (int i = 0; i < 8; i++) {
+        for (int i = 0; i < per; i++) {
             if (acc + c[i] >= nd) {
-                const uint32_t digit = 255u - 8u * lane - i;
-                st.prefix |= digit << (24 - 8 * d);
+                st.prefix |= (uint32_t)(top - i) << ss_shift(d);
                 st.need = nd - acc;
                 P.seg[s] = st;
                 break;
@@ -485,7 +515,7 @@ static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t segsel_workspace_bytes(uint64_t n, int nseg)
 {
     const uint64_t items = n / SS_CHUNK + (uint64_t)nseg + 1;
-    return al256(nseg * sizeof(SegState)) + al256((size_t)4 * nseg * 256 * 4) + al256((nseg + 1) * 8) * 2 +
+    return al256(nseg * sizeof(SegState)) + al256((size_t)SS_PASSES * nseg * SS_BINS * 4) + al256((nseg + 1) * 8) * 2 +
            al256(nseg * 4) + al256(items * 4) * 6 + al256(items * 8) * 3 + al256(items * (SS_THREADS / 32) * 4) * 2 +
            256;
 }
@@ -573,7 +603,7 @@ static int segsel_launch(int keymode, int thr_only, const SegState *dgc_seg, con
     P.seed = seed;
     P.stream = stream;
     P.seg = (SegState *)take(nseg * sizeof(SegState));
-    P.hist = (uint32_t *)take((size_t)4 * nseg * 256 * 4);
+    P.hist = (uint32_t *)take((size_t)SS_PASSES * nseg * SS_BINS * 4);
     P.seg_lo = (const uint64_t *)take((nseg + 1) * 8);
     P.seg_k = (const uint64_t *)take((nseg + 1) * 8);
     P.item_seg = (const uint32_t *)take(nitems * 4);
@@ -602,10 +632,10 @@ static int segsel_launch(int keymode, int thr_only, const SegState *dgc_seg, con
         L.k.assign(seg_k, seg_k + nseg);
         L.nitems = nitems;
     }
-    cudaMemsetAsync(P.hist, 0, (size_t)4 * nseg * 256 * 4, s);
+    cudaMemsetAsync(P.hist, 0, (size_t)SS_PASSES * nseg * SS_BINS * 4, s);
     k_ss_init<<<(nseg + 255) / 256, 256, 0, s>>>(P);
-    const int rgrid = (nseg + SS_THREADS / 32 - 1) / (SS_THREADS / 32);
-    for (int d = 0; d < 4; d++) {
+    const int rgrid = nseg;
+    for (int d = 0; d < SS_PASSES; d++) {
         if (keymode == KEY_HASH)
             k_ss_hist<KEY_HASH><<<nitems, SS_THREADS, 0, s>>>(P, d);
         else if (keymode == KEY_DGC)
@@ -615,7 +645,7 @@ static int segsel_launch(int keymode, int thr_only, const SegState *dgc_seg, con
         k_ss_resolve<<<rgrid, SS_THREADS, 0, s>>>(P, d);
     }
     if (thr_only) {
-        count_launches(9);
+        count_launches(1 + 2 * SS_PASSES);
         return GVC_OK;
     }
     if (keymode == KEY_HASH)
@@ -631,7 +661,7 @@ static int segsel_launch(int keymode, int thr_only, const SegState *dgc_seg, con
         k_ss_write<KEY_DGC><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
     else
         k_ss_write<KEY_MAG><<<nitems, SS_THREADS, 0, s>>>(P, out_idx, out_val);
-    count_launches(12);
+    count_launches(4 + 2 * SS_PASSES);
     return GVC_OK;
 }
 
