@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -234,11 +235,26 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_count(SegPlan P)
     uint32_t wb, we;
     ss_slice(P.item_len[it], warp, wb, we);
     uint32_t gt = 0, eq = 0;
-    for (uint32_t i = wb + lane; i < we; i += 32) {
-        const uint32_t key = ss_key<KM>(P, P.values[lo + i], lo + i, thr);
-        gt += st.all || key > st.prefix;
-        eq += !st.all && key == st.prefix;
+    uint32_t base = st.all ? we : wb;  // (a segment kept whole is not read)
+    for (; base + 256 <= we; base += 256) {  // full trips: 8 loads in flight per lane, no bounds checks
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            v[u] = P.values[lo + base + u * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const uint32_t key = ss_key<KM>(P, v[u], lo + base + u * 32 + lane, thr);
+            gt += key > st.prefix;
+            eq += key == st.prefix;
+        }
     }
+    for (uint32_t i = base + lane; i < we; i += 32) {
+        const uint32_t key = ss_key<KM>(P, P.values[lo + i], lo + i, thr);
+        gt += key > st.prefix;
+        eq += key == st.prefix;
+    }
+    if (st.all && lane == 0)  // every value kept, no ties
+        gt = we - wb;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         gt += __shfl_xor_sync(0xffffffffu, gt, o);
@@ -348,26 +364,33 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *ou
     __shared__ uint32_t ring_i[W][256];
     __shared__ float ring_v[W][256];
     uint32_t cnt = 0, flushed = 0;
-    // U rows of 32 loaded before any is compacted
-    constexpr int U = 8;
-    for (uint32_t base = wb; base < we; base += 32 * U) {
+    // the tie logic only where k_ss_count saw a tie in this warp's slice, the
+    // bounds checks only in the last partial trip (the row loop is
+    // instruction-bound: ~54 instructions per 32 values with both)
+    const bool ties_here = !st.all && P.warp_eq[it * W + warp] != 0;
+    auto trip = [&](uint32_t base, auto ties_t, auto full_t) {
+        constexpr bool TIES = decltype(ties_t)::value, FULL = decltype(full_t)::value;
+        // U rows of 32 loaded before any is compacted
+        constexpr int U = 8;
         float v[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t i = base + u * 32 + lane;
-            v[u] = i < we ? P.values[lo + i] : 0.f;
+            v[u] = (FULL || i < we) ? P.values[lo + i] : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t i = base + u * 32 + lane;
-            const bool ok = i < we;
-            const uint32_t key = ok ? ss_key<KM>(P, v[u], lo + i, thr) : 0u;
-            const bool iseq = ok && !st.all && key == st.prefix;
+            const bool ok = FULL || i < we;
+            const uint32_t key = ss_key<KM>(P, v[u], lo + i, thr);
             bool keep = ok && (st.all || key > st.prefix);
-            const uint32_t em = __ballot_sync(0xffffffffu, iseq);
-            if (em) {  // warp-uniform: ties in this row (rare)
-                keep |= iseq && ties + __popc(em & lt) < take;
-                ties += __popc(em);
+            if (TIES) {
+                const bool iseq = ok && !st.all && key == st.prefix;
+                const uint32_t em = __ballot_sync(0xffffffffu, iseq);
+                if (em) {  // warp-uniform: ties in this row (rare)
+                    keep |= iseq && ties + __popc(em & lt) < take;
+                    ties += __popc(em);
+                }
             }
             const uint32_t km = __ballot_sync(0xffffffffu, keep);
             if (keep) {
@@ -388,6 +411,20 @@ __global__ void __launch_bounds__(SS_THREADS) k_ss_write(SegPlan P, uint32_t *ou
                 __syncwarp();
             }
         }
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    uint32_t base = wb;
+    if (ties_here) {
+        for (; base + 256 <= we; base += 256)
+            trip(base, T_(), T_());
+        if (base < we)
+            trip(base, T_(), F_());
+    } else {
+        for (; base + 256 <= we; base += 256)
+            trip(base, F_(), T_());
+        if (base < we)
+            trip(base, F_(), F_());
     }
     __syncwarp();
     for (uint32_t e = flushed + lane; e < cnt; e += 32) {
