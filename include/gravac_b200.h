@@ -35,7 +35,7 @@ extern "C" {
 #define GVC_API
 #endif
 
-#define GVC_ABI_VERSION 1
+#define GVC_ABI_VERSION 2
 #define GVC_MAX_LADDER 16
 #define GVC_AGG_TILE 4096 /* outputs per CTA of the decompress-average */
 
@@ -232,6 +232,10 @@ typedef struct gvc_emit_mirrors {
     uint32_t *idx_dev[GVC_MAX_PEERS];
     float *vals_dev[GVC_MAX_PEERS];
     uint32_t *bounds_dev[GVC_MAX_PEERS];
+    /* the staged exchange's 16-bit wire index (idx mod GVC_AGG_TILE; the
+     * tile bounds say which tile an entry lies in), written beside out_idx
+     * into this rank's own slot; NULL = none.  count may be 0 for this alone. */
+    uint16_t *off16_dev;
 } gvc_emit_mirrors;
 /* gvc_emit plus mirrors (NULL mirrors == gvc_emit). */
 GVC_API int gvc_emit_mirrored(void *ws_dev, size_t ws_bytes, int j, const uint32_t *idx_map_dev,
@@ -248,9 +252,10 @@ GVC_API int gvc_peer_signal(uint32_t *const *peer_flags, int nranks, int rank, u
  * lower index; out = the segments' (global index, value) lists concatenated
  * in segment order (sum seg_k entries; a segment with seg_k >= its length
  * keeps everything).  seg_offsets / seg_k are HOST arrays.  Every segment is
- * resolved by the same 12 launches (a state init, 4 radix passes of 8 key
- * bits over all segments at once, per-slice counts, one scan, an ordered
- * compaction) however many segments there are.  *status_dev |= 1 on a NaN
+ * resolved by the same 10 launches (a state init, 3 radix passes of 11 / 11
+ * / 10 key bits over all segments at once -- a histogram and a resolve each --,
+ * per-slice counts, one scan, an ordered compaction) however many segments
+ * there are.  *status_dev |= 1 on a NaN
  * magnitude.  The layout's work-item tables live in the workspace and are
  * uploaded only when (n, kind, seg_offsets, seg_k) differ from the previous
  * call on the same workspace address -- as with gvc_select's cached graphs,
@@ -351,6 +356,12 @@ typedef struct gvc_peer_staging {
     const uint32_t *src_idx_dev[GVC_MAX_PEERS];
     const float *src_vals_dev[GVC_MAX_PEERS];
     const uint32_t *src_bounds_dev[GVC_MAX_PEERS];
+    /* 16-bit wire indices (gvc_emit_mirrors.off16_dev): when every part has
+     * them, the copiers move (u16 offset, f32 value) -- 6 bytes per entry over
+     * NVLink instead of 8 -- and the tiles read offsets, not idx: src_off16_dev[p]
+     * peer p's (remote), off16_dev[p] the local slot (p == self: this rank's own). */
+    const uint16_t *src_off16_dev[GVC_MAX_PEERS];
+    uint16_t *off16_dev[GVC_MAX_PEERS];
 } gvc_peer_staging;
 GVC_API int gvc_aggregate_peers_staged(const uint32_t *const *idx_dev, const float *const *vals_dev,
                         const uint32_t *const *bounds_dev, const uint64_t *counts, int nparts, uint64_t n,

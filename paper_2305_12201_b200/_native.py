@@ -77,13 +77,15 @@ class PeerStaging(ctypes.Structure):
     """gvc_peer_staging: the staged-pull exchange (copier CTAs + merge tiles)."""
     _fields_ = [("self_rank", _i32), ("copy_blocks", _i32), ("chunk_entries", ctypes.c_uint32),
                 ("reserved", ctypes.c_uint32), ("ready_dev", _vp), ("src_idx_dev", _vp * 8),
-                ("src_vals_dev", _vp * 8), ("src_bounds_dev", _vp * 8)]
+                ("src_vals_dev", _vp * 8), ("src_bounds_dev", _vp * 8), ("src_off16_dev", _vp * 8),
+                ("off16_dev", _vp * 8)]
 
 
 class EmitMirrors(ctypes.Structure):
-    """gvc_emit_mirrors: peer destinations the emit also writes (push exchange)."""
+    """gvc_emit_mirrors: peer destinations the emit also writes (push exchange),
+    and the staged exchange's 16-bit wire indices (off16_dev)."""
     _fields_ = [("count", _i32), ("reserved", _i32), ("idx_dev", _vp * 8), ("vals_dev", _vp * 8),
-                ("bounds_dev", _vp * 8)]
+                ("bounds_dev", _vp * 8), ("off16_dev", _vp)]
 
 _lib = None
 _lock = threading.Lock()
@@ -168,7 +170,7 @@ def load(build_if_missing: bool = False):
         L.gvc_launch_count.restype = ctypes.c_ulonglong
         if hasattr(L, "gvc_select_phase_times"):  # diagnostic
             L.gvc_select_phase_times.argtypes = [_vp, _vp, ctypes.c_int]
-        if L.gvc_abi_version() != 1:
+        if L.gvc_abi_version() != 2:
             raise ImportError("libgravac_b200 ABI version mismatch")
         _lib = L
         return L

@@ -198,7 +198,8 @@ class Selection:
                                             nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),
                                             nat.ptr(tile_bounds), nat.ptr(stats), ctypes.byref(mirrors),
                                             nat.stream_ptr(self.device)), "gvc_emit")
-            payload.pushed = tile_bounds is not None and count is None
+            payload.pushed = mirrors.count > 0 and tile_bounds is not None and count is None
+            payload.wire16 = bool(mirrors.off16_dev) and count is None
         else:
             nat.check(lib.gvc_emit(nat.ptr(self.ws), self.ws.numel(), j, nat.ptr(idx_map), nat.ptr(out_idx),
                                    nat.ptr(out_val), nat.ptr(resid), nat.ptr(sent_mask), nat.ptr(sent_m),

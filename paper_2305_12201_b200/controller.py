@@ -613,7 +613,11 @@ def run_iteration(state: ControllerState, gradients, residuals, cost: CostModelP
 
     def wire(s, c, bnd):
         if peer is not None:
-            return peer.slot(s.chosen_count(c), length, push=bnd and xmode == "push")
+            # staged pull: the emit writes the tile bounds (level-1 Top-k) and the
+            # 16-bit wire indices into the slot, so the exchange launches no
+            # bounds pass and moves 6 bytes per entry over NVLink
+            return peer.slot(s.chosen_count(c), length, push=bnd and xmode == "push", bounds=bnd,
+                             off16=xmode == "staged")
         from .exchange import new_payload
         return new_payload(s.chosen_count(c), dev, n=length if bnd else None)
 

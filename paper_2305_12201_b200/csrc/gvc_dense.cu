@@ -470,6 +470,12 @@ struct Staged {
     const uint32_t *src_idx[GVC_MAX_PEERS];  // peer p's payload (remote)
     const float *src_val[GVC_MAX_PEERS];
     const uint32_t *src_bounds[GVC_MAX_PEERS];
+    // 16-bit wire indices (all parts or none): the copiers move src_off
+    // instead of src_idx into off[p], and the tiles read off[p] (own part's
+    // included) -- 6 bytes per entry over NVLink instead of 8
+    int use_off;
+    const uint16_t *src_off[GVC_MAX_PEERS];
+    const uint16_t *off[GVC_MAX_PEERS];
     uint32_t *err;  // the flag area's error word (bounded waits)
     uint32_t *ticket;    // dispatch-order CTA ticket (flags word GVC_FLAG_TICKET_WORD, reset by the last CTA)
 };
@@ -512,6 +518,7 @@ __device__ __forceinline__ uint32_t *flag_err(const uint32_t *flags)
 #ifndef GVC_COPIER_TMA
 #define GVC_COPIER_TMA 0
 #endif
+template <bool OFF>
 __device__ void staged_copier(const Staged &st, const AggParts &parts, int nparts, const uint32_t *flags,
                               uint32_t epoch, uint32_t vb, void *sbuf = nullptr, uint32_t sbytes = 0)
 {
@@ -536,7 +543,7 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(st.ready + vb), "r"(epoch) : "memory");
     }
     constexpr int U = 4;
-    if (GVC_COPIER_TMA && sbuf && nparts == 2 && (4u << st.ch_log2) <= sbytes / 2) {
+    if (GVC_COPIER_TMA && !OFF && sbuf && nparts == 2 && (4u << st.ch_log2) <= sbytes / 2) {
         // the TMA path (two parts: one remote): thread 0 moves the chunks
         // through the CTA's (unused) tile buffer with bulk copies -- both
         // arrays of a chunk in flight on two mbarriers, the next chunk's loads
@@ -630,12 +637,43 @@ __device__ void staged_copier(const Staged &st, const AggParts &parts, int npart
             const uint64_t hi = min((unsigned long long)k, (unsigned long long)(lo + (1ull << st.ch_log2)));
             if (lo >= hi)
                 continue;
+            const int4 *sv = reinterpret_cast<const int4 *>(st.src_val[q]);
+            int4 *dv = reinterpret_cast<int4 *>(const_cast<float *>(parts.vals[q]));
+            if (OFF) {
+                // (u16 offset, f32 value): offsets in int4 granules of 8 (the
+                // offset area is padded to 8 entries), values in granules of 4
+                const uint32_t lo8 = (uint32_t)(lo >> 3), hi8 = (uint32_t)((hi + 7) >> 3);
+                const uint32_t lo4 = (uint32_t)(lo >> 2), hi4 = (uint32_t)((hi + 3) >> 2);
+                const int4 *so = reinterpret_cast<const int4 *>(st.src_off[q]);
+                int4 *dO = reinterpret_cast<int4 *>(const_cast<uint16_t *>(st.off[q]));
+                const uint32_t n8 = hi8 - lo8, n4 = hi4 - lo4;  // n8 <= (n4 + 1) / 2
+                // value granule i and offset granule i in flight together: a
+                // 4096-entry chunk in one round trip over NVLink, as the u32 path
+                for (uint32_t i0 = threadIdx.x; i0 < n4; i0 += U * AGG_THREADS) {
+                    int4 a[U], b[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const uint32_t i = i0 + u * AGG_THREADS;
+                        if (i < n8)
+                            a[u] = __ldcg(so + lo8 + i);
+                        if (i < n4)
+                            b[u] = __ldcg(sv + lo4 + i);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const uint32_t i = i0 + u * AGG_THREADS;
+                        if (i < n8)
+                            __stcg(dO + lo8 + i, a[u]);
+                        if (i < n4)
+                            __stcg(dv + lo4 + i, b[u]);
+                    }
+                }
+                continue;
+            }
             // int4 granules; the slots are padded to 4 entries, so rounding up is safe
             const uint32_t lo4 = (uint32_t)(lo >> 2), hi4 = (uint32_t)((hi + 3) >> 2);
             const int4 *si = reinterpret_cast<const int4 *>(st.src_idx[q]);
-            const int4 *sv = reinterpret_cast<const int4 *>(st.src_val[q]);
             int4 *di = reinterpret_cast<int4 *>(const_cast<uint32_t *>(parts.idx[q]));
-            int4 *dv = reinterpret_cast<int4 *>(const_cast<float *>(parts.vals[q]));
             for (uint32_t i0 = lo4 + threadIdx.x; i0 < hi4; i0 += U * AGG_THREADS) {
                 int4 a[U], b[U];
 #pragma unroll
@@ -724,7 +762,7 @@ __device__ __forceinline__ void staged_wait(const Staged &st, int q, uint32_t a,
 // waits until peer p has posted `epoch` into flags[p] (its payload is
 // complete), and all part reads bypass L1 (ld.global.cg), so no stale line of
 // an earlier exchange through the same slot can be hit.
-template <int MODE, bool WAIT, int NP, bool STAGED = false>
+template <int MODE, bool WAIT, int NP, bool STAGED = false, bool OFF = false>
 __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int nparts, uint64_t n,
                                                             float *__restrict__ out, const uint32_t *flags,
                                                             uint32_t epoch, Staged stg)
@@ -735,11 +773,12 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
     __shared__ uint32_t s_a[NP], s_b[NP];
     const uint32_t vb = STAGED ? staged_ticket(stg) : blockIdx.x;
     if (STAGED && (int)vb < stg.ncopy) {
-        staged_copier(stg, parts, nparts, flags, epoch, vb, MODE == 2 ? (void *)acc : (void *)accf,
+        staged_copier<OFF>(stg, parts, nparts, flags, epoch, vb, MODE == 2 ? (void *)acc : (void *)accf,
                       MODE == 2 ? (uint32_t)sizeof(acc) : (uint32_t)sizeof(accf));
         return;
     }
     const uint32_t tile = STAGED ? vb - stg.ncopy : blockIdx.x;
+    constexpr bool use_off = STAGED && OFF;  // 16-bit wire indices: tile offsets directly
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (MODE == 2) {
@@ -785,11 +824,13 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
                     const uint32_t a = s_a[q] + threadIdx.x;
                     left[q] = (int)s_b[q] - (int)a;
                     const uint32_t *pi = parts.idx[p0 + q] + a;
+                    const uint16_t *po = use_off ? stg.off[p0 + q] + a : nullptr;
                     const float *pv = parts.vals[p0 + q] + a;
 #pragma unroll
                     for (int u = 0; u < U; u++) {
                         if (u * AGG_THREADS < left[q]) {
-                            r[q][u] = __ldcg(pi + u * AGG_THREADS) - (uint32_t)lo;
+                            r[q][u] = use_off ? (uint32_t)__ldcg(po + u * AGG_THREADS)
+                                              : __ldcg(pi + u * AGG_THREADS) - (uint32_t)lo;
                             v[q][u] = __ldcg(pv + u * AGG_THREADS);
                         }
                     }
@@ -809,6 +850,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
         } else {
             for (int q = 0; q < np; q++) {
                 const uint32_t *pi = parts.idx[p0 + q];
+                const uint16_t *po = use_off ? stg.off[p0 + q] : nullptr;
                 const float *pv = parts.vals[p0 + q];
                 const uint32_t b = s_b[q];
                 for (uint32_t t0 = s_a[q] + threadIdx.x; t0 < b; t0 += U * AGG_THREADS) {
@@ -817,7 +859,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
 #pragma unroll
                     for (int u = 0; u < U; u++) {
                         if (t0 + u * AGG_THREADS < b) {
-                            r[u] = __ldcg(pi + t0 + u * AGG_THREADS) - (uint32_t)lo;
+                            r[u] = use_off ? (uint32_t)__ldcg(po + t0 + u * AGG_THREADS)
+                                           : __ldcg(pi + t0 + u * AGG_THREADS) - (uint32_t)lo;
                             v[u] = __ldcg(pv + t0 + u * AGG_THREADS);
                         }
                     }
@@ -867,7 +910,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_merge(AggParts parts, int 
 // contributes +0.0, which leaves any fp64 sum starting from +0.0 unchanged
 // (it can never be -0.0).  MODE 0: decompress (one part, fp32 copy, -0.0
 // kept); MODE 1: average.  Dynamic shared memory: NP * AGG_TILE floats.
-template <int MODE, bool WAIT, int NP, bool STAGED = false>
+template <int MODE, bool WAIT, int NP, bool STAGED = false, bool OFF = false>
 __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int nparts, uint64_t n,
                                                            float *__restrict__ out, const uint32_t *flags,
                                                            uint32_t epoch, Staged stg)
@@ -877,10 +920,11 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
     __shared__ uint32_t s_a[NP], s_b[NP];
     const uint32_t vb = STAGED ? staged_ticket(stg) : blockIdx.x;
     if (STAGED && (int)vb < stg.ncopy) {
-        staged_copier(stg, parts, nparts, flags, epoch, vb, tiles, (uint32_t)(nparts * AGG_TILE * 4));
+        staged_copier<OFF>(stg, parts, nparts, flags, epoch, vb, tiles, (uint32_t)(nparts * AGG_TILE * 4));
         return;
     }
     const uint32_t tile = STAGED ? vb - stg.ncopy : blockIdx.x;
+    constexpr bool use_off = STAGED && OFF;  // 16-bit wire indices: tile offsets directly
     const uint64_t lo = (uint64_t)tile * AGG_TILE;
     const uint32_t width = (uint32_t)min((uint64_t)AGG_TILE, n - lo);
     if (threadIdx.x < nparts) {
@@ -916,11 +960,13 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
                 const uint32_t a = s_a[q] + threadIdx.x;
                 left[q] = (int)s_b[q] - (int)a;
                 const uint32_t *pi = parts.idx[q] + a;
+                const uint16_t *po = use_off ? stg.off[q] + a : nullptr;
                 const float *pv = parts.vals[q] + a;
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     if (u * AGG_THREADS < left[q]) {
-                        r[q][u] = __ldcg(pi + u * AGG_THREADS) - (uint32_t)lo;
+                        r[q][u] = use_off ? (uint32_t)__ldcg(po + u * AGG_THREADS)
+                                          : __ldcg(pi + u * AGG_THREADS) - (uint32_t)lo;
                         v[q][u] = __ldcg(pv + u * AGG_THREADS);
                     }
                 }
@@ -937,6 +983,7 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
     } else {
         for (int q = 0; q < nparts; q++) {
             const uint32_t *pi = parts.idx[q];
+            const uint16_t *po = use_off ? stg.off[q] : nullptr;
             const float *pv = parts.vals[q];
             const uint32_t b = s_b[q];
             for (uint32_t t0 = s_a[q] + threadIdx.x; t0 < b; t0 += U * AGG_THREADS) {
@@ -945,7 +992,8 @@ __global__ void __launch_bounds__(AGG_THREADS) k_tile_part(AggParts parts, int n
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     if (t0 + u * AGG_THREADS < b) {
-                        r[u] = __ldcg(pi + t0 + u * AGG_THREADS) - (uint32_t)lo;
+                        r[u] = use_off ? (uint32_t)__ldcg(po + t0 + u * AGG_THREADS)
+                                       : __ldcg(pi + t0 + u * AGG_THREADS) - (uint32_t)lo;
                         v[u] = __ldcg(pv + t0 + u * AGG_THREADS);
                     }
                 }
@@ -1101,7 +1149,15 @@ static int tile_merge_run(bool avg, AggParts &P, int nparts, uint64_t n, float *
     memset(&none, 0, sizeof(none));
     const Staged &st = staged ? *staged : none;
     const unsigned gs = g + (unsigned)st.ncopy;
-    if (staged) {
+    if (staged && st.use_off) {  // 16-bit wire indices
+        if (nparts <= 2)
+            k_tile_part<1, true, 2, true, true><<<gs, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch,
+                                                                                     st);
+        else if (nparts <= 4)
+            k_tile_merge<2, true, 4, true, true><<<gs, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch, st);
+        else
+            k_tile_merge<2, true, 8, true, true><<<gs, AGG_THREADS, 0, s>>>(P, nparts, n, out, flags, epoch, st);
+    } else if (staged) {
         if (nparts <= 2)
             k_tile_part<1, true, 2, true><<<gs, AGG_THREADS, nparts * sm1, s>>>(P, nparts, n, out, flags, epoch, st);
         else if (nparts <= 4)
@@ -1237,10 +1293,17 @@ int aggregate_peers_staged_run(const uint32_t *const *idx, const float *const *v
         st.src_idx[p] = sg->src_idx_dev[p];
         st.src_val[p] = sg->src_vals_dev[p];
         st.src_bounds[p] = sg->src_bounds_dev[p];
+        st.src_off[p] = sg->src_off16_dev[p];
+        st.off[p] = sg->off16_dev[p];
         if (p != sg->self && !sg->src_bounds_dev[p])
             return set_error(GVC_ERR_ARG, "aggregate_peers_staged: part %d has no source bounds", p);
         kmax = counts[p] > kmax ? counts[p] : kmax;
     }
+    // 16-bit wire indices only when every part has them (local and remote)
+    st.use_off = 1;
+    for (int p = 0; p < nparts; p++)
+        if (!st.off[p] || (p != sg->self && !st.src_off[p]))
+            st.use_off = 0;
     st.nchunks = (uint32_t)((kmax + ce - 1) / ce);
     st.nb = (uint32_t)((n + AGG_TILE - 1) / AGG_TILE + 1);
     return tile_merge_run(true, P, nparts, n, out, nullptr, 0, flags, epoch, s, &st);

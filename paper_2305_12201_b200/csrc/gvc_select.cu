@@ -1525,6 +1525,7 @@ struct Mirrors {
     uint32_t *idx[GVC_MAX_PEERS];
     float *val[GVC_MAX_PEERS];
     uint32_t *tb[GVC_MAX_PEERS];
+    uint16_t *off;  // this rank's 16-bit wire indices (idx mod GVC_AGG_TILE), or null
 };
 
 // LEAN: the hot level-1 emit (no idx_map, no direct residual, no Redsync
@@ -1538,7 +1539,7 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
     if (LEAN) {
         idx_map = nullptr;
         resid = nullptr;
-        mir.n = 0;
+        mir.n = 0;  // (mir.off stays: the staged exchange's wire indices)
         want_stats = 0;
     }
     __shared__ double wst[GVC_WARPS_PER_BLOCK][2];
@@ -1663,6 +1664,8 @@ __global__ void __launch_bounds__(GVC_THREADS) k_emit(Plan p, int j, const uint3
                     const uint32_t gi = idx_map ? idx_map[pos[c]] : pos[c];
                     out_idx[w] = gi;
                     out_val[w] = sv;
+                    if (mir.off)
+                        mir.off[w] = (uint16_t)(gi & (GVC_AGG_TILE - 1));
                     if (!LEAN) {
                         for (int q = 0; q < mir.n; q++) {
                             mir.idx[q][w] = gi;
@@ -2154,6 +2157,7 @@ int emit_run(void *ws, size_t ws_bytes, int j, const uint32_t *idx_map, uint32_t
     memset(&mir, 0, sizeof(mir));
     if (mirrors) {
         mir.n = mirrors->count;
+        mir.off = mirrors->off16_dev;
         for (int q = 0; q < mir.n; q++) {
             mir.idx[q] = mirrors->idx_dev[q];
             mir.val[q] = mirrors->vals_dev[q];

@@ -48,23 +48,31 @@ def allgather_stats(flat: torch.Tensor, group=None) -> "np.ndarray":
 
 
 class Payload:
-    """Flat int32 wire buffer of one rank: [idx (kpad) | vals (kpad) | tile bounds (bpad)].
+    """Flat int32 wire buffer of one rank:
+    [idx (kpad) | vals (kpad) | tile bounds (bpad) | 16-bit wire indices (opad, optional)].
 
-    kpad/bpad round to 4 words so every section stays 16-byte aligned.  The
+    kpad/bpad/opad round to 4 words so every section stays 16-byte aligned.  The
     tile bounds (gvc_emit tile_bounds_dev) let K7 skip its boundary pass on the
     gathered parts; every rank uses the same layout (same kind, same k, n).
+    The 16-bit wire indices (idx mod GVC_AGG_TILE, written by the emit beside
+    idx) are what the staged exchange moves over NVLink instead of idx: 6
+    bytes per entry instead of 8.
     """
 
-    __slots__ = ("buf", "k", "kpad", "nb", "bpad", "idx", "vals", "bounds", "bounds_area", "peer", "mirrors",
-                 "pushed")
+    __slots__ = ("buf", "k", "kpad", "nb", "bpad", "opad", "idx", "vals", "bounds", "bounds_area", "peer",
+                 "mirrors", "pushed", "off_word", "wire16")
 
-    def __init__(self, k: int, n: int, device, with_bounds: bool = True, buf: torch.Tensor | None = None):
+    def __init__(self, k: int, n: int, device, with_bounds: bool = True, buf: torch.Tensor | None = None,
+                 off16: bool = False):
         self.k = k
         self.kpad = (k + 3) & ~3
         self.nb = (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1 if (with_bounds or buf is not None) else 0
         self.bpad = (self.nb + 3) & ~3
+        self.opad = ((self.kpad + 7) & ~7) // 2 if off16 else 0  # u16 entries padded to 8 (int4 granules)
+        self.off_word = 2 * self.kpad + self.bpad
+        self.wire16 = False  # set by the emit once it wrote the 16-bit wire indices
         if buf is None:
-            buf = torch.empty(2 * self.kpad + self.bpad, dtype=torch.int32, device=device)
+            buf = torch.empty(2 * self.kpad + self.bpad + self.opad, dtype=torch.int32, device=device)
         self.buf = buf
         self.idx = self.buf[:self.kpad].view(torch.uint32)
         self.vals = self.buf[self.kpad:2 * self.kpad].view(torch.float32)
@@ -76,9 +84,14 @@ class Payload:
         self.pushed = False  # set by the emit once the mirrors hold the full payload
 
     @staticmethod
-    def words_for(k: int, n: int) -> int:
+    def words_for(k: int, n: int, off16: bool = False) -> int:
         nb = (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1
-        return 2 * ((k + 3) & ~3) + ((nb + 3) & ~3)
+        kpad = (k + 3) & ~3
+        return 2 * kpad + ((nb + 3) & ~3) + (((kpad + 7) & ~7) // 2 if off16 else 0)
+
+    @property
+    def off16_ptr(self) -> int:
+        return self.buf.data_ptr() + 4 * self.off_word
 
     @property
     def words(self) -> int:
@@ -244,17 +257,26 @@ class PeerExchange:
             ev.record()
             self._err_check = (host, ev)
 
-    def slot(self, k: int, n: int, push: bool = True) -> Payload:
+    def slot(self, k: int, n: int, push: bool = True, bounds: bool | None = None, off16: bool = False) -> Payload:
         """This rank's payload slot of the next exchange.  With ``push`` (a
         level-1 Top-k emit, which writes the tile bounds) the emit also writes
-        the same slot of every peer; otherwise the bounds are computed at the
-        exchange and the peers pull."""
-        words = Payload.words_for(k, n)
+        the same slot of every peer; otherwise the peers pull.  ``bounds``
+        (default: ``push``): the emit writes the tile bounds into the slot
+        (a level-1 Top-k emit), else the exchange computes them.  ``off16``
+        (staged pull): the emit also writes the 16-bit wire indices, which the
+        copiers move instead of the u32 indices."""
+        words = Payload.words_for(k, n, off16)
         self._ensure(words)
         e = self.epoch + 1
         base = self._slot_word(e % 2, self.rank)
-        pl = Payload(k, n, self.device, with_bounds=push, buf=self.buf[base:base + words])
+        pl = Payload(k, n, self.device, with_bounds=push if bounds is None else bounds,
+                     buf=self.buf[base:base + words], off16=off16)
         pl.peer = (self, e, base)
+        if off16 and not push:
+            m = nat.EmitMirrors()
+            m.count = 0
+            m.off16_dev = pl.off16_ptr
+            pl.mirrors = m
         if push and self.world > 1:
             m = nat.EmitMirrors()
             m.count = self.world - 1
@@ -309,6 +331,9 @@ class PeerExchange:
                 sg.src_idx_dev[p] = peer_slot[p]
                 sg.src_vals_dev[p] = peer_slot[p] + 4 * pl.kpad
                 sg.src_bounds_dev[p] = peer_slot[p] + 8 * pl.kpad
+                if pl.wire16:  # every rank's emit wrote them (identical decisions, identical path)
+                    sg.src_off16_dev[p] = peer_slot[p] + 4 * pl.off_word
+                    sg.off16_dev[p] = own_slot[p] + 4 * pl.off_word
             idx = (ctypes.c_void_p * W)(*own_slot)
             vals = (ctypes.c_void_p * W)(*[b + 4 * pl.kpad for b in own_slot])
             bnd = (ctypes.c_void_p * W)(*[b + 8 * pl.kpad for b in own_slot])

@@ -32,7 +32,7 @@ def test_library_exports_every_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (gvc_\w+)", out))
     assert set(declared()) <= exported
-    assert lib.gvc_abi_version() == 1
+    assert lib.gvc_abi_version() == 2
 
 
 def test_struct_layout_matches_c():

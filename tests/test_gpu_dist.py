@@ -40,8 +40,9 @@ def _worker(rank, world, port, kind, q, exchange="auto"):
                                         vals[r * part.kept:(r + 1) * part.kept], n, part.achieved_cf)
                  for r in range(world)]
         ref = G.aggregate(parts)
+        wire16 = bool(getattr(getattr(part, "_payload", None), "wire16", False))
         out.append((res.decision.choice, res.decision.cf, res.gain_min_raw, res.gain_c_raw,
-                    bool(torch.equal(avg.values.view(torch.int32), ref.values.view(torch.int32)))))
+                    bool(torch.equal(avg.values.view(torch.int32), ref.values.view(torch.int32))), wire16))
     q.put((rank, out))
     dist.destroy_process_group()
 
@@ -92,6 +93,9 @@ def test_multi_rank_step(kind, exchange):
     for r in range(1, world):
         assert res[r] == res[0]  # identical decisions and gains on every rank
     assert all(r[4] for r in res[0])  # exchange == aggregate() bit for bit
+    if exchange == "staged" and kind == "topk":
+        # the emitted payloads carried the 16-bit wire indices (6 bytes per entry over NVLink)
+        assert all(r[5] for r in res[0] if r[0] != "dense")
 
 
 def _step_worker(rank, world, port, kind, exchange, q):
@@ -121,13 +125,18 @@ def _peer_worker(rank, world, port, q):
             if e == 3:
                 vals[::7] = -0.0
             parts.append((idx, vals))
-        pl = px.slot(k, n, push=False)
+        staged = e % 2 == 0
+        pl = px.slot(k, n, push=False, off16=staged)
         pl.idx[:k].copy_(torch.from_numpy(parts[rank][0].view(np.int32)).to(dev).view(torch.uint32))
+        if staged:  # the 16-bit wire indices (what an emit writes beside idx): idx mod GVC_AGG_TILE
+            wire = (parts[rank][0] % 4096).astype(np.int16)
+            pl.buf[pl.off_word:pl.off_word + pl.opad].view(torch.int16)[:k].copy_(torch.from_numpy(wire).to(dev))
+            pl.wire16 = True
         pl.vals[:k].copy_(torch.from_numpy(parts[rank][1]).to(dev))
         pl.bounds = None  # not written by an emit: the exchange computes them
         part = G.SparseGradient._wrap(pl.idx[:k], pl.vals[:k], n, n / k)
         part._payload = pl
-        out = px.aggregate(part, staged=e % 2 == 0).cpu().numpy()
+        out = px.aggregate(part, staged=staged).cpu().numpy()
         ref = O.aggregate(parts, n)
         ok.append(bool(np.array_equal(out.view(np.int32), ref.view(np.int32))))
     q.put((rank, ok))
