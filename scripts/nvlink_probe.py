@@ -45,8 +45,11 @@ for r in range(W):
     vals = rs.standard_normal(k).astype(np.float32)
     parts.append((idx, vals))
     dev = torch.device("cuda", gpu_of(r))
-    pl = Payload(k, n, dev, with_bounds=True)
+    pl = Payload(k, n, dev, with_bounds=True, off16=True)
     pl.idx[:k].copy_(torch.from_numpy(idx.view(np.int32)).to(dev).view(torch.uint32))
+    # the 16-bit wire indices an emit writes beside idx (idx mod GVC_AGG_TILE)
+    pl.buf[pl.off_word:pl.off_word + pl.opad].view(torch.int16)[:k].copy_(
+        torch.from_numpy((idx % 4096).astype(np.int16)).to(dev))
     pl.vals[:k].copy_(torch.from_numpy(vals).to(dev))
     with torch.cuda.device(dev):
         nat.check(lib.gvc_tile_bounds(nat.ptr(pl.idx), k, n, nat.ptr(pl.bounds_area), nat.stream_ptr(dev)))
@@ -70,12 +73,12 @@ def direct():
 
 
 # staged: local copies of the remote parts on GPU 0 are the merge's inputs; the copiers fill them
-local = [pls[0]] + [Payload(k, n, dev0, with_bounds=True) for _ in range(1, W)]
+local = [pls[0]] + [Payload(k, n, dev0, with_bounds=True, off16=True) for _ in range(1, W)]
 ready = torch.zeros(74 + (k + 4095) // 4096 + 2, dtype=torch.int32, device=dev0)
 epoch = [1]
 
 
-def staged():
+def staged(wire16=False):
     sg = nat.PeerStaging()
     sg.self_rank = 0
     sg.copy_blocks = 74
@@ -85,6 +88,9 @@ def staged():
         sg.src_idx_dev[p] = pls[p].idx.data_ptr()
         sg.src_vals_dev[p] = pls[p].vals.data_ptr()
         sg.src_bounds_dev[p] = pls[p].bounds_area.data_ptr()
+        if wire16:
+            sg.src_off16_dev[p] = pls[p].off16_ptr
+            sg.off16_dev[p] = local[p].off16_ptr
     li = (ctypes.c_void_p * W)(*[p.idx.data_ptr() for p in local])
     lv = (ctypes.c_void_p * W)(*[p.vals.data_ptr() for p in local])
     lb = (ctypes.c_void_p * W)(*[p.bounds_area.data_ptr() for p in local])
@@ -92,10 +98,10 @@ def staged():
                                              nat.ptr(out), nat.stream_ptr(dev0)), "aggregate_peers_staged")
 
 
-for name, fn in (("direct pull", direct), ("staged pull", staged)):
+for name, fn in (("direct pull", direct), ("staged pull", staged), ("staged pull 16-bit wire", lambda: staged(True))):
     ms = []
     for it in range(8):
-        if name == "staged pull":  # every run is a new exchange for the readiness epochs
+        if name.startswith("staged pull"):  # every run is a new exchange for the readiness epochs
             epoch[0] = it + 1
             flags[:W] = epoch[0]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -105,7 +111,7 @@ for name, fn in (("direct pull", direct), ("staged pull", staged)):
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
     ok = np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
-    recv = (W - 1) * 8 * k
+    recv = (W - 1) * (6 if "16-bit" in name else 8) * k
     t = float(np.median(ms[2:]))
     print(f"{name}: W={W} n={n} k={k} {t * 1e3:.1f} us, {recv / (t * 1e-3) / 1e9:.0f} GB/s received "
           f"({recv / 1e6:.1f} MB over NVLink), oracle {'ok' if ok else 'MISMATCH'}", flush=True)
