@@ -1,6 +1,6 @@
 #!/bin/bash
 # staged-exchange copier count / chunk sweep at N GPUs (ResNet101 44.5M and VGG16 138M)
-for cfg in ${CFGS:-"74 4096" "148 4096" "37 4096" "74 8192" "148 2048"}; do
+for cfg in "74 4096" "148 4096" "37 4096" "74 8192" "148 8192" "74 2048"; do
   set -- $cfg
   for W in resnet101 vgg16; do
     P=$((29500 + RANDOM % 1000))
