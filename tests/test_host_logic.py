@@ -219,3 +219,22 @@ def test_gain_exchange_gloo(world):
     for r in range(world):
         assert out[r][1] == want_rows
         assert out[r][2] == want_mean
+
+
+def test_wire_payload_layout():
+    """exchange.Payload with the 16-bit wire indices (staged exchange): every
+    section 16-byte aligned, the offset area holds k entries padded to the
+    copier's 8-entry granules, and words_for matches the buffer the slot carves."""
+    from paper_2305_12201_b200 import _native as nat
+    from paper_2305_12201_b200.exchange import Payload
+    for k in (1, 3, 4, 5, 7, 8, 9, 4095, 4096, 4097, 4_450_000):
+        for n in (k, 44_500_000):
+            pl = Payload(k, n, "cpu", with_bounds=True, off16=True)
+            assert pl.buf.numel() == Payload.words_for(k, n, True)
+            assert pl.kpad % 4 == 0 and pl.bpad % 4 == 0 and pl.opad % 4 == 0 and pl.off_word % 4 == 0
+            assert 2 * pl.opad >= ((k + 7) & ~7)  # u16 entries, padded to int4 granules
+            assert pl.off_word == 2 * pl.kpad + pl.bpad
+            assert pl.nb == (n + nat.AGG_TILE - 1) // nat.AGG_TILE + 1
+            plain = Payload(k, n, "cpu", with_bounds=True)
+            assert plain.opad == 0 and plain.buf.numel() == Payload.words_for(k, n)
+            assert not pl.wire16  # set only by the emit that writes the offsets
